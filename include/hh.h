@@ -1,0 +1,157 @@
+/*
+ * hh.h — C ABI of the B200 hot path of arXiv 2104.01439 ("PAPER"):
+ * FGMRES on the Q1 finite-element Helmholtz system A_0, right-preconditioned
+ * by one two-grid V(nu,nu) cycle on the complex-shifted operator A_eps.
+ *
+ *   A(k, eps) = K - M(k, eps) - i B(k)                (Eq. sys_matrix)
+ *   A_0 = A(k, 0), A_eps = A(k, eps), eps_e = beta * k_e^sigma
+ *   V-cycle: Alg. 1, L = 2, damped Jacobi, I^T / I
+ *   transfers, exact coarse solve factored once
+ *   FGMRES: right-preconditioned, flexible
+ *
+ * Conventions (all entry points):
+ *  - Every call returns hh_status; HH_OK = 0.  No C++ exception crosses the
+ *    ABI.  On a non-OK status hh_last_error() returns a thread-local message.
+ *  - Vectors are caller-owned DEVICE pointers to complex128 stored as
+ *    interleaved (re, im) doubles — the layout of torch.complex128 — of
+ *    length (n+1)^dim (fine) or (n/2+1)^dim (coarse), nodes ordered
+ *    lexicographically with x fastest: node (i, j[, l]) -> i + (n+1) j [+ (n+1)^2 l].
+ *    They must be 16-byte aligned.  Host pointers are accepted only where
+ *    stated (hh_problem_desc.k_elem*, hh_fgmres_solve_host).
+ *  - The library owns everything else (coefficients, coarse factor, Krylov
+ *    bases, scratch).  It allocates in hh_setup_problem / hh_sweep and
+ *    frees in hh_destroy_problem; hot calls (apply_op, vcycle,
+ *    fgmres_solve) never allocate.
+ *  - One handle per thread/stream; handles are not thread-safe.  Calls
+ *    marked "async" are enqueued on the handle's stream and return without
+ *    synchronising; calls marked "blocks" synchronise that stream.
+ *  - Non-convergence is a RESULT (report.converged = 0), not an error.
+ */
+#ifndef HH_H_
+#define HH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HH_OK = 0,
+  HH_E_ARG = 1,        /* NULL pointer / invalid enum                                   */
+  HH_E_CONFIG = 2,     /* dim not in {2,3}, n odd or < 4, omega not in (0,1], nu < 1 ... */
+  HH_E_DIM = 3,        /* size mismatch                                                 */
+  HH_E_CUDA = 4,       /* CUDA runtime error (message has the CUDA error string)        */
+  HH_E_NCCL = 5,       /* reserved: NCCL error (slab decomposition)                     */
+  HH_E_OOM = 6,        /* device allocation failed                                      */
+  HH_E_SINGULAR = 7,   /* zero Jacobi diagonal or zero coarse pivot (message has k, eps, h) */
+  HH_E_BREAKDOWN = 8,  /* Arnoldi breakdown with a residual above tolerance             */
+  HH_E_DIVERGED = 9,   /* NaN/Inf in the Krylov recurrence                              */
+  HH_E_STATE = 10      /* call not valid in the handle's state                          */
+} hh_status;
+
+typedef struct hh_problem hh_problem;   /* opaque */
+
+/* operator selector for hh_apply_op */
+enum { HH_OP_A0 = 0, HH_OP_AEPS = 1, HH_OP_AEPS_COARSE = 2 };
+
+/* coarse direct solver (Alg. 1 line 3) */
+enum { HH_COARSE_AUTO = 0, HH_COARSE_ND = 1 };
+
+typedef struct {
+  int32_t dim;                  /* 2 | 3                                                    */
+  int32_t n_cells;              /* fine cells per side, even, >= 4; Omega=(0,1)^dim, h=1/n   */
+  double  k_const;              /* wavenumber, used iff k_elem == NULL                      */
+  const double* k_elem;         /* optional per-fine-element k_e, n^dim, x fastest (HOST)    */
+  const double* k_elem_coarse;  /* required iff k_elem != NULL: (n/2)^dim (HOST)             */
+  double  beta, sigma;          /* eps_e = beta * k_e^sigma; beta = 0 gives eps = 0          */
+  int32_t nu_pre, nu_post;      /* Jacobi steps (BASELINE: 2, 2), 1..4                       */
+  double  omega;                /* Jacobi damping (BASELINE: 0.6), in (0, 1]                 */
+  int32_t coarse_solver;        /* HH_COARSE_*                                              */
+  int32_t device;               /* CUDA device ordinal                                      */
+  void*   stream;               /* cudaStream_t for every async call on this handle (NULL = legacy default) */
+  int32_t max_restart;          /* Krylov workspace: largest FGMRES restart length (m) this handle will run */
+} hh_problem_desc;
+
+typedef struct {
+  int32_t restart;              /* m (<= desc.max_restart)                                  */
+  int32_t max_iters;            /* total preconditioner applications cap (BASELINE reading: 500) */
+  int32_t fixed_iters;          /* > 0: run exactly this many Arnoldi steps (parity at threshold) */
+  double  rtol;                 /* stop when |g_{j+1}| <= rtol * ||b||                      */
+  int32_t check_every;          /* host reads the device convergence flag every this many steps (>=1) */
+} hh_fgmres_opts;
+
+typedef struct {
+  int32_t iterations;           /* preconditioner applications                              */
+  int32_t restarts;
+  int32_t converged;
+  double  rel_res_lsq;          /* |g_{j+1}| / ||b|| at exit                               */
+  double  rel_res_true;         /* ||b - A_0 x|| / ||b|| recomputed at exit */
+  double  rho;                  /* (rel_res_true)^(1/iterations)             */
+  double  setup_s;              /* handle setup incl. coarse factorisation (s)              */
+  double  solve_s;              /* this solve (s, device events)                            */
+} hh_fgmres_report;
+
+typedef struct {
+  int64_t id;
+  int32_t n_cells;              /* 2D, constant k                                          */
+  double  k, beta, sigma;
+} hh_sample;
+
+typedef struct {
+  int64_t id;
+  int32_t status, iterations, converged;
+  double  rel_res_true, rho, setup_s, solve_s;
+} hh_sample_result;
+
+/* Build a problem: coefficients, coarse operator A_eps^{(1)} (rediscretised on
+ * the 2h mesh) and its factorisation, Krylov workspace.  blocks. */
+hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out);
+
+/* Node counts of the fine and coarse level.                                    */
+hh_status hh_layout(const hh_problem* p, int64_t* n_fine_nodes, int64_t* n_coarse_nodes);
+
+/* y = A x with A = A_0 | A_eps (fine, matrix-free) | A_eps^{(1)} (coarse).
+ * x, y: device complex128, distinct.  async. (PAPER.md:387-396 semi matrix-free) */
+hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void* y);
+
+/* z = P_eps^{-1} f: one V(nu_pre, nu_post) cycle from a zero initial guess
+ * (Alg. 1).  f, z: device complex128 fine vectors. async. */
+hh_status hh_vcycle(hh_problem* p, const void* f, void* z);
+
+/* Coarse direct solve e = (A_eps^{(1)})^{-1} r (coarse device vectors). async. */
+hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e);
+
+/* FGMRES(m) on A_0 x = b with right preconditioner one V-cycle
+ * (PAPER.md:357-360).  b: device; x: device, in: ignored (x0 = 0), out:
+ * solution.  res_hist: optional HOST array of max_iters+1 doubles receiving
+ * |g_{j+1}|/||b|| per iteration (entry 0 = 1).  blocks. */
+hh_status hh_fgmres_solve(hh_problem* p, const void* b, void* x, const hh_fgmres_opts* o,
+                          hh_fgmres_report* r, double* res_hist);
+
+/* Same, with HOST b and x (complex128): the host<->device copies are part of
+ * the call (end-to-end path).  blocks. */
+hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, void* x_host,
+                               const hh_fgmres_opts* o, hh_fgmres_report* r);
+
+/* Sweep: for each 2D constant-k sample, set up, factor and solve with a unit
+ * point source at the centre node (BASELINE configs[1]); common carries dim,
+ * nu, omega, device, stream.  s, out: HOST arrays of n entries.  blocks. */
+hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                   const hh_sample* s, int32_t n, hh_sample_result* out);
+
+hh_status hh_destroy_problem(hh_problem* p);
+
+/* Device time (ms) of the last call's phases, for the bench roofline:
+ * [0] total V-cycle fine kernels, [1] coarse solve, [2] Krylov kernels,
+ * [3] A_0 apply; accumulated since the last hh_reset_timers. */
+hh_status hh_reset_timers(hh_problem* p, int32_t enable);
+hh_status hh_read_timers(hh_problem* p, double* ms4, int64_t* launches);
+
+const char* hh_last_error(void);
+const char* hh_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HH_H_ */

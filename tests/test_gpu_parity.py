@@ -1,0 +1,139 @@
+"""GPU <-> oracle parity through the C ABI (-m gpu).
+
+Bars (BASELINE.json north_star): operator apply and V-cycle <= 1e-10 relative
+2-norm; FGMRES iteration counts equal or +-1; solution <= 1e-8 relative (at
+equal iteration counts, reading C12)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import fem
+from oracle.solve import OracleProblem, coefficients
+from oracle.twogrid import CoarseSolver
+from workloads import config_spec, sweep_samples
+from workloads.configs import ProblemSpec, sweep_sample_spec
+
+pytestmark = pytest.mark.gpu
+
+hh = pytest.importorskip("paper_2104_01439_b200.hh") if torch.cuda.is_available() else None
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).cuda()
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def _rand(n, seed):
+    r = np.random.default_rng(seed)
+    return r.standard_normal(n) + 1j * r.standard_normal(n)
+
+
+SPECS = [
+    ("cfg0", lambda: config_spec("cfg0")),
+    ("cfg0_n4", lambda: config_spec("cfg0", n=4)),
+    ("cfg0_n6", lambda: config_spec("cfg0", n=6)),
+    ("cfg0_n70", lambda: config_spec("cfg0", n=70)),            # ragged tiles
+    ("cfg2_n64", lambda: config_spec("cfg2", n=64)),            # heterogeneous
+    ("cfg2_n130", lambda: config_spec("cfg2", n=130)),
+    ("sweep_k160_kh06", lambda: sweep_sample_spec(
+        {"id": 0, "n": 268, "k": 160.0, "beta": 0.1, "sigma": 1.0, "kh_target": 0.6})),
+]
+
+
+@pytest.fixture(scope="module", params=SPECS, ids=[s[0] for s in SPECS])
+def pair(request):
+    spec = request.param[1]()
+    orc = OracleProblem(spec)
+    gp = hh.Problem.from_spec(spec)
+    yield spec, orc, gp
+    gp.close()
+
+
+def test_apply_op_parity(pair):
+    spec, orc, gp = pair
+    x = _rand(spec.n_nodes, 1)
+    for op in (hh.HH_OP_A0, hh.HH_OP_AEPS):
+        y = _host(gp.apply_op(op, _dev(x)))
+        assert _rel(y, orc.apply(op, x)) <= 1e-10, op
+    xc = _rand(spec.n_coarse_nodes, 2)
+    yc = _host(gp.apply_op(hh.HH_OP_AEPS_COARSE, _dev(xc)))
+    assert _rel(yc, orc.apply(2, xc)) <= 1e-10
+
+
+def test_coarse_solve_parity(pair):
+    spec, orc, gp = pair
+    r = _rand(spec.n_coarse_nodes, 3)
+    e = _host(gp.coarse_solve(_dev(r)))
+    assert _rel(e, orc.tg.coarse.solve(r)) <= 1e-10
+    assert _rel(orc.tg.Ac @ e, r) <= 1e-11
+
+
+def test_vcycle_parity(pair):
+    spec, orc, gp = pair
+    for seed in (4, 5):
+        f = _rand(spec.n_nodes, seed)
+        z = _host(gp.vcycle(_dev(f)))
+        assert _rel(z, orc.vcycle(f)) <= 1e-10
+
+
+def test_fgmres_parity(pair):
+    spec, orc, gp = pair
+    b = spec.rhs()
+    xo, ro = orc.solve(b)
+    o = hh.opts(restart=spec.restart, rtol=spec.rtol, max_iters=spec.max_iters)
+    xg, rg = gp.fgmres_solve(_dev(b), o=o, history=True)
+    assert abs(rg["iterations"] - ro.iterations) <= 1, (rg, ro)
+    assert rg["converged"] == 1
+    assert rg["rel_res_true"] <= 1.01 * spec.rtol
+    if rg["iterations"] != ro.iterations:   # reading C12: compare at equal counts
+        o2 = hh.opts(restart=spec.restart, rtol=spec.rtol, max_iters=spec.max_iters,
+                     fixed_iters=ro.iterations)
+        xg, rg = gp.fgmres_solve(_dev(b), o=o2)
+    assert _rel(_host(xg), xo) <= 1e-8
+    h = rg.get("history")
+    if h:
+        assert all(h[i + 1] <= h[i] * (1 + 1e-12) for i in range(len(h) - 1))
+
+
+def test_fgmres_host_entry_point():
+    spec = config_spec("cfg0")
+    gp = hh.Problem.from_spec(spec)
+    b = spec.rhs()
+    x = np.zeros_like(b)
+    rep = gp.fgmres_solve_host(b, x, hh.opts(restart=100, rtol=1e-6))
+    xo, ro = OracleProblem(spec).solve(b)
+    assert abs(rep["iterations"] - ro.iterations) <= 1
+    if rep["iterations"] == ro.iterations:
+        assert _rel(x, xo) <= 1e-8
+    gp.close()
+
+
+def test_errors_are_reported():
+    with pytest.raises(hh.HHError) as e:
+        hh.Problem(2, 7, k_const=10.0)          # odd n
+    assert e.value.status == 2
+    with pytest.raises(hh.HHError):
+        hh.Problem(2, 8, k_const=10.0, omega=1.5)
+    gp = hh.Problem(2, 8, k_const=10.0)
+    with pytest.raises(ValueError):
+        gp.apply_op(0, torch.zeros(5, dtype=torch.complex128, device="cuda"))
+    gp.close()
+
+
+def test_sweep_subset_matches_oracle():
+    """hh_sweep on a strided subset of the cfg1 sweep: iteration counts +-1."""
+    samples = sweep_samples()[::97][:24]
+    res = hh.sweep(samples)
+    for s, r in zip(samples, res):
+        assert r["status"] == 0
+        _, ro = OracleProblem(sweep_sample_spec(s)).solve()
+        assert abs(r["iterations"] - ro.iterations) <= 1, (s, r, ro.iterations)
+        assert r["converged"] == int(ro.converged)
