@@ -142,11 +142,18 @@ hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
 
 hh_status hh_destroy_problem(hh_problem* p);
 
-/* Device time (ms) of the last call's phases, for the bench roofline:
- * [0] total V-cycle fine kernels, [1] coarse solve, [2] Krylov kernels,
- * [3] A_0 apply; accumulated since the last hh_reset_timers. */
+/* Phase instrumentation for the bench roofline (device events around each
+ * phase of every FGMRES iteration; enabling it adds one host sync per
+ * iteration).  st12 = [ms x4, algorithmic HBM bytes x4, phase launches x4]
+ * for the phases [pre-smooth+restrict, coarse solve, prolong+post-smooth+A_0,
+ * Krylov (multi-dot + update)], accumulated since the last reset. */
 hh_status hh_reset_timers(hh_problem* p, int32_t enable);
-hh_status hh_read_timers(hh_problem* p, double* ms4, int64_t* launches);
+hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launches);
+
+/* Sweep-wide phase instrumentation (same st12 layout as hh_read_timers) and
+ * kernel-launch count since the last reset; reset_enable >= 0 resets and sets
+ * timing on (1) / off (0); -1 only reads. */
+hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches);
 
 const char* hh_last_error(void);
 const char* hh_version(void);

@@ -7,23 +7,26 @@
 //    Front(t) = sep(t) (eliminated at t) + halo(t) (1-ring of box(t), clipped).
 //  * multifrontal elimination WITHOUT pivoting (reading C18: the Hermitian part
 //    of i*A_eps is eps*M + k*B, positive definite for eps > 0, so every
-//    principal submatrix is non-singular), all fronts of one tree level in one
-//    batched launch.  Each front is "swept" on its separator block by partial
-//    Gauss-Jordan (block size NB): afterwards the dense front holds
+//    principal submatrix is non-singular); all fronts of one tree level of all
+//    B samples of a batch in one launch.  Each front is "swept" on its
+//    separator block by partial Gauss-Jordan (block size NB): afterwards the
+//    dense front holds
 //        [ X = F_ss^{-1}      H = F_ss^{-1} F_su ]
 //        [ -H^T               S = F_uu - F_us X F_su ]
 //    and S is extend-added into the parent front.
 //  * solve = two sweeps of batched GEMVs over the stored blocks (explicit
 //    inverses, no triangular recurrences):
-//        forward (leaves -> root):  z_s = r[sep] + sum_children-of-halo contributions,
+//        forward (leaves -> root):  z_s = r[sep] + sum of descendant contributions,
 //                                   contribution_t = -H^T z_s  (gathered, no atomics)
 //        backward (root -> leaves): x[sep] = X z_s - H x[halo]
 //    Bytes streamed per solve ~ 16 * sum_t (s_t f_t + u_t s_t), the same as a
 //    triangular LDL^T solve; every launch is fully parallel.
+// The tree (NDPlan) depends only on (dim, m) and is shared by all samples.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
-#include <unordered_map>
 #include "hh_internal.cuh"
 
 namespace {
@@ -34,8 +37,7 @@ struct FrontMeta {          // device-visible per-front data
   int s, u, f, level;
   int64_t Foff;             // offset (complex entries) of the f x f front
   int64_t sepOff, haloOff;  // into sep / halo index arrays
-  int64_t zsOff, outOff;    // into the solve work vectors
-  int64_t gptrOff;          // into gptr (s+1 entries)
+  int64_t zsOff, outOff;    // into the solve work vector (zs part / out part)
   int64_t eaOff;            // into extend-add map (u entries)
   int parent;
   int pad;
@@ -44,15 +46,17 @@ struct FrontMeta {          // device-visible per-front data
 struct LevelInfo {
   int begin, count;         // fronts [begin, begin+count)
   int max_s, max_u, max_f;
-  int64_t asmBegin, asmCount;       // assembly entries
+  int64_t asmBegin, asmCount;        // assembly entries
+  int64_t Fbegin, Fcount;            // F entries of the level
   int ea_count[2];                   // children per slot
   int64_t ea_list_off[2];            // offsets into eaList
 };
 }  // namespace
 
-struct NDFactor {
+struct NDPlan {
   int dim = 2, m = 0;            // coarse grid nodes per side
   int64_t N = 0;                 // coarse nodes
+  int S = 9;                     // stencil entries per node
   std::vector<FrontMeta> fronts; // host copy
   std::vector<LevelInfo> levels;
   FrontMeta* d_fronts = nullptr;
@@ -62,33 +66,48 @@ struct NDFactor {
   int* d_eamap = nullptr;        // child halo pos -> parent front pos
   int* d_eaList = nullptr;       // child front ids grouped by (level, slot)
   int64_t* d_gptr = nullptr;     // CSR over all separator entries
-  int64_t* d_gidx = nullptr;     // index into out buffer
-  cplx* d_F = nullptr;           // all fronts
-  cplx* d_C = nullptr;           // saved column block (per level, f x NB per front)
-  int64_t* d_Coff = nullptr;     // per front offset into d_C (level-local)
-  cplx* d_zs = nullptr;          // forward solve values per separator entry
-  cplx* d_out = nullptr;         // forward contributions per halo entry
-  int* d_flag = nullptr;         // zero-pivot flag
-  int64_t F_entries = 0, zs_entries = 0, out_entries = 0;
+  int64_t* d_gidx = nullptr;     // index into the out part of the work vector
+  int64_t* d_Coff = nullptr;     // per front offset into the pivot column buffer (level-local)
+  int64_t F_entries = 0, zs_entries = 0, out_entries = 0, C_entries = 0;
   int64_t stream_bytes = 0;
+  // bottom-subtree decompositions, one per candidate cut level L (fronts of level <= L)
+  std::vector<int> sub_cnt;          // number of subtrees for cut L
+  std::vector<int64_t> sub_off;      // offset of cut L's ptr array in d_sub_ptr
+  std::vector<int64_t> list_off;     // offset of cut L's front list in d_sub_list
+  std::vector<double> sub_cost_us;   // estimated cost of the slowest subtree (one CTA)
+  std::vector<int> sub_maxf;
+  int* d_sub_ptr = nullptr;
+  int* d_sub_list = nullptr;
+  std::mutex cut_mu;
+  std::vector<std::pair<int, int>> cut_cache;   // (B, L)
 };
 
 // ============================================================ device kernels
 namespace {
 
+__global__ void k_nd_zero(cplx* __restrict__ F, int64_t FE, int64_t begin, int64_t count) {
+  cplx* p = F + (int64_t)blockIdx.y * FE + begin;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = cmake(0, 0);
+}
+
 __global__ void k_nd_assemble(const int4* __restrict__ e, int64_t cnt,
                               const FrontMeta* __restrict__ fr, const cplx* __restrict__ st,
-                              cplx* __restrict__ F) {
+                              int64_t stS, cplx* __restrict__ F, int64_t FE) {
+  const int b = blockIdx.y;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cnt) return;
   const int4 v = e[i];
   const FrontMeta m = fr[v.x];
-  F[m.Foff + (int64_t)v.y * m.f + v.z] = st[v.w];
+  F[(int64_t)b * FE + m.Foff + (int64_t)v.y * m.f + v.z] = st[(int64_t)b * stS + v.w];
 }
 
 // extend-add of the child update matrices S_c into the parents (one child per parent per launch)
 __global__ void k_nd_extend_add(const int* __restrict__ list, const FrontMeta* __restrict__ fr,
-                                const int* __restrict__ eamap, cplx* __restrict__ F) {
+                                const int* __restrict__ eamap, cplx* __restrict__ Fall,
+                                int64_t FE) {
+  cplx* F = Fall + (int64_t)blockIdx.z * FE;
   const int c = list[blockIdx.x];
   const FrontMeta mc = fr[c];
   const FrontMeta mp = fr[mc.parent];
@@ -97,7 +116,7 @@ __global__ void k_nd_extend_add(const int* __restrict__ list, const FrontMeta* _
     const cplx* src = F + mc.Foff + (int64_t)(mc.s + a) * mc.f + mc.s;
     cplx* dst = F + mp.Foff + (int64_t)map[a] * mp.f;
     for (int b = threadIdx.x; b < mc.u; b += blockDim.x) {
-      cplx v = src[b];
+      const cplx v = src[b];
       cplx& d = dst[map[b]];
       d.x += v.x;
       d.y += v.y;
@@ -107,37 +126,37 @@ __global__ void k_nd_extend_add(const int* __restrict__ list, const FrontMeta* _
 
 // pivot step: P = F[K,K]^{-1}; save column block C = F[:,K]; rows K <- P F[K,:], F[K,K] <- P
 __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr, int begin,
-                                                int kb, cplx* __restrict__ F,
-                                                cplx* __restrict__ Cbuf,
+                                                int kb, cplx* __restrict__ Fall, int64_t FE,
+                                                cplx* __restrict__ Call, int64_t CE,
                                                 const int64_t* __restrict__ Coff,
                                                 int* __restrict__ flag) {
   const int t = begin + blockIdx.x;
+  const int b = blockIdx.y;
   const FrontMeta m = fr[t];
   if (kb >= m.s) return;
   const int nb = min(NB, m.s - kb);
   const int f = m.f;
-  cplx* A = F + m.Foff;
-  cplx* C = Cbuf + Coff[blockIdx.x];
+  cplx* A = Fall + (int64_t)b * FE + m.Foff;
+  cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.x];
   __shared__ cplx P[NB][NB + 1];
   const int ti = threadIdx.x / NB, tj = threadIdx.x % NB;   // 16 x 16
   if (ti < nb && tj < nb) P[ti][tj] = A[(int64_t)(kb + ti) * f + kb + tj];
   // save column block (rows outside K only are used later)
-  for (int idx = threadIdx.x; idx < f * nb; idx += blockDim.x) {
-    const int i = idx / nb, k = idx % nb;
-    C[(int64_t)i * NB + k] = A[(int64_t)i * f + kb + k];
+  for (int i = threadIdx.x / NB; i < f; i += 256 / NB) {
+    const int k = threadIdx.x % NB;
+    if (k < nb) C[(int64_t)i * NB + k] = A[(int64_t)i * f + kb + k];
   }
   __syncthreads();
   // in-place Gauss-Jordan inversion of the nb x nb pivot block (sweep operator)
   for (int p = 0; p < nb; ++p) {
     const cplx piv = P[p][p];
-    if (cabs2(piv) == 0.0) {
-      if (threadIdx.x == 0) atomicExch(flag, 1);
-    }
+    if (cabs2(piv) == 0.0 && threadIdx.x == 0) atomicExch(flag + b, 1);
     const cplx pinv = cinv(piv);
     __syncthreads();
-    cplx rowp = (ti == p && tj < nb && tj != p) ? cmul(P[p][tj], pinv) : cmake(0, 0);
+    const bool inrow = (ti == p && tj < nb && tj != p);
+    const cplx rowp = inrow ? cmul(P[p][tj], pinv) : cmake(0, 0);
     __syncthreads();
-    if (ti == p && tj < nb && tj != p) P[p][tj] = rowp;
+    if (inrow) P[p][tj] = rowp;
     __syncthreads();
     cplx newv = cmake(0, 0);
     bool wr = false;
@@ -182,18 +201,19 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
 //   F[i][j] <- (j in K ? 0 : F[i][j]) - sum_k C[i][k] * F[kb+k][j]
 constexpr int UT = 32;   // update tile (UT x UT outputs per CTA, 256 threads)
 __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
-                                                int kb, cplx* __restrict__ F,
-                                                const cplx* __restrict__ Cbuf,
-                                                const int64_t* __restrict__ Coff) {
-  const int t = begin + blockIdx.z;
+                                                int kb, int tiles, cplx* __restrict__ Fall,
+                                                int64_t FE, const cplx* __restrict__ Call,
+                                                int64_t CE, const int64_t* __restrict__ Coff) {
+  const int t = begin + blockIdx.y;
+  const int b = blockIdx.z;
   const FrontMeta m = fr[t];
   if (kb >= m.s) return;
   const int f = m.f;
-  const int i0 = blockIdx.y * UT, j0 = blockIdx.x * UT;
+  const int i0 = (blockIdx.x / tiles) * UT, j0 = (blockIdx.x % tiles) * UT;
   if (i0 >= f || j0 >= f) return;
   const int nb = min(NB, m.s - kb);
-  cplx* A = F + m.Foff;
-  const cplx* C = Cbuf + Coff[blockIdx.z];
+  cplx* A = Fall + (int64_t)b * FE + m.Foff;
+  const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
   __shared__ cplx Cs[UT][NB + 1];
   __shared__ cplx Rs[NB][UT + 1];
   for (int idx = threadIdx.x; idx < UT * NB; idx += 256) {
@@ -221,25 +241,9 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   }
 }
 
-// forward: gather z_s = r[sep] + sum of descendant contributions
-__global__ void k_nd_gather(const FrontMeta* __restrict__ fr, int begin,
-                            const int* __restrict__ sep, const int64_t* __restrict__ gptr,
-                            const int64_t* __restrict__ gidx, const cplx* __restrict__ rhs,
-                            const cplx* __restrict__ out, cplx* __restrict__ zs) {
-  const FrontMeta m = fr[begin + blockIdx.x];
-  for (int a = threadIdx.x + blockIdx.y * blockDim.x; a < m.s; a += blockDim.x * gridDim.y) {
-    cplx v = rhs[sep[m.sepOff + a]];
-    const int64_t p0 = gptr[m.gptrOff + a], p1 = gptr[m.gptrOff + a + 1];
-    for (int64_t p = p0; p < p1; ++p) {
-      const cplx c = out[gidx[p]];
-      v.x += c.x;
-      v.y += c.y;
-    }
-    zs[m.zsOff + a] = v;
-  }
-}
+// ------------------------------------------------------------------ solve
+constexpr int VMAX = 4096;   // front vectors up to this length are staged in shared memory
 
-// warp-per-row GEMV helpers
 __device__ __forceinline__ cplx warp_sum(cplx v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -249,41 +253,170 @@ __device__ __forceinline__ cplx warp_sum(cplx v) {
   return v;
 }
 
-// forward contributions out[b] = sum_a F[s+b][a] zs[a]   (F[u][s] = -H^T)
-__global__ void __launch_bounds__(256) k_nd_fwd(const FrontMeta* __restrict__ fr, int begin,
-                                                const cplx* __restrict__ F,
-                                                const cplx* __restrict__ zs,
-                                                cplx* __restrict__ out) {
-  const FrontMeta m = fr[begin + blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const cplx* z = zs + m.zsOff;
-  for (int b = blockIdx.y * 8 + warp; b < m.u; b += gridDim.y * 8) {
-    const cplx* row = F + m.Foff + (int64_t)(m.s + b) * m.f;
-    cplx acc = cmake(0, 0);
-    for (int a = lane; a < m.s; a += 32) cfma(acc, row[a], z[a]);
-    acc = warp_sum(acc);
-    if (lane == 0) out[m.outOff + b] = acc;
+// lane-strided dot of a front row with v (2 independent accumulators)
+__device__ __forceinline__ cplx row_dot(const cplx* __restrict__ row, const cplx* v, int len, int lane) {
+  cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
+  int c = lane;
+  for (; c + 32 < len; c += 64) {
+    const cplx r0 = __ldg(&row[c]), r1 = __ldg(&row[c + 32]);
+    cfma(a0, r0, v[c]);
+    cfma(a1, r1, v[c + 32]);
+  }
+  if (c < len) cfma(a0, __ldg(&row[c]), v[c]);
+  return warp_sum(cadd(a0, a1));
+}
+
+struct SolveArgs {
+  const FrontMeta* fr;
+  const int* st;
+  const int* sep;
+  const int* halo;
+  const int64_t* gptr;
+  const int64_t* gidx;
+  const cplx* F; int64_t FE;
+  cplx* work; int64_t WE, zsE;
+  VArg rhs, x;
+};
+
+// z_s[a] = r[sep[a]] + sum of descendant contributions, a = a0 + team_rank (stride team)
+__device__ __forceinline__ void front_gather(const SolveArgs& A, const FrontMeta& m, int b, cplx* dst,
+                                             cplx* dst2, int a0, int stride) {
+  const cplx* r = A.rhs.at(b);
+  const cplx* out = A.work + (int64_t)b * A.WE + A.zsE;
+  for (int a = a0; a < m.s; a += stride) {
+    cplx v = __ldg(&r[A.sep[m.sepOff + a]]);
+    const int64_t p0 = A.gptr[m.sepOff + a], p1 = A.gptr[m.sepOff + a + 1];
+    for (int64_t p = p0; p < p1; ++p) {
+      const cplx c = out[A.gidx[p]];
+      v.x += c.x;
+      v.y += c.y;
+    }
+    dst[a] = v;
+    if (dst2) dst2[a] = v;
   }
 }
 
-// backward: x[sep[a]] = sum_b F[a][b] v[b],  v = [z_s ; -x[halo]]
-__global__ void __launch_bounds__(256) k_nd_bwd(const FrontMeta* __restrict__ fr, int begin,
-                                                const cplx* __restrict__ F,
-                                                const cplx* __restrict__ zs,
-                                                const int* __restrict__ sep,
-                                                const int* __restrict__ halo,
-                                                cplx* __restrict__ x) {
-  const FrontMeta m = fr[begin + blockIdx.x];
+// forward rows b = r0.. (step) : out[b] = F[s+b][0:s] . z
+__device__ __forceinline__ void front_fwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
+                                               const cplx* z, int r0, int step, int lane) {
+  const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
+  cplx* out = A.work + (int64_t)bs * A.WE + A.zsE + m.outOff;
+  for (int b = r0; b < m.u; b += step) {
+    const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, z, m.s, lane);
+    if (lane == 0) out[b] = acc;
+  }
+}
+
+// backward rows a: x[sep[a]] = F[a][0:f] . v,  v = [z_s ; -x[halo]] (staged)
+__device__ __forceinline__ void front_bwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
+                                               const cplx* v, int r0, int step, int lane) {
+  const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
+  cplx* x = A.x.at(bs);
+  for (int a = r0; a < m.s; a += step) {
+    const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
+    if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+  }
+}
+
+__device__ __forceinline__ void stage_bwd(const SolveArgs& A, const FrontMeta& m, int bs, cplx* v) {
+  const cplx* zs = A.work + (int64_t)bs * A.WE + m.zsOff;
+  const cplx* x = A.x.at(bs);
+  for (int c = threadIdx.x; c < m.f; c += blockDim.x) {
+    if (c < m.s) v[c] = zs[c];
+    else {
+      const cplx t = x[A.halo[m.haloOff + c - m.s]];
+      v[c] = cmake(-t.x, -t.y);
+    }
+  }
+}
+
+// large fronts only: gather z_s to global (separate pass)
+__global__ void k_nd_gather(SolveArgs A, int begin) {
+  const int b = blockIdx.z;
+  if (A.st && A.st[b]) return;
+  const FrontMeta m = A.fr[begin + blockIdx.x];
+  cplx* zs = A.work + (int64_t)b * A.WE + m.zsOff;
+  front_gather(A, m, b, zs, nullptr, threadIdx.x + blockIdx.y * blockDim.x, blockDim.x * gridDim.y);
+}
+
+// one tree level, forward: (gather into smem +) contribution GEMV rows
+__global__ void __launch_bounds__(256) k_nd_fwd(SolveArgs A, int begin) {
+  extern __shared__ double4 smem_raw[];
+  cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
+  const int b = blockIdx.z;
+  if (A.st && A.st[b]) return;
+  const FrontMeta m = A.fr[begin + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const cplx* z = zs + m.zsOff;
-  const int* hl = halo + m.haloOff;
-  for (int a = blockIdx.y * 8 + warp; a < m.s; a += gridDim.y * 8) {
-    const cplx* row = F + m.Foff + (int64_t)a * m.f;
-    cplx acc = cmake(0, 0);
-    for (int b = lane; b < m.s; b += 32) cfma(acc, row[b], z[b]);
-    for (int b = lane; b < m.u; b += 32) cfms(acc, row[m.s + b], x[hl[b]]);
-    acc = warp_sum(acc);
-    if (lane == 0) x[sep[m.sepOff + a]] = acc;
+  const cplx* z;
+  if (m.s <= VMAX) {
+    front_gather(A, m, b, zsh, blockIdx.y == 0 ? A.work + (int64_t)b * A.WE + m.zsOff : nullptr,
+                 threadIdx.x, blockDim.x);
+    __syncthreads();
+    z = zsh;
+  } else {
+    z = A.work + (int64_t)b * A.WE + m.zsOff;   // gathered by k_nd_gather
+  }
+  front_fwd_rows(A, m, b, z, blockIdx.y * 8 + warp, gridDim.y * 8, lane);
+}
+
+// one tree level, backward
+__global__ void __launch_bounds__(256) k_nd_bwd(SolveArgs A, int begin) {
+  extern __shared__ double4 smem_raw[];
+  cplx* v = reinterpret_cast<cplx*>(smem_raw);
+  const int b = blockIdx.z;
+  if (A.st && A.st[b]) return;
+  const FrontMeta m = A.fr[begin + blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (m.f <= VMAX) {
+    stage_bwd(A, m, b, v);
+    __syncthreads();
+    front_bwd_rows(A, m, b, v, blockIdx.y * 8 + warp, gridDim.y * 8, lane);
+  } else {   // huge fronts: operands straight from global memory
+    const cplx* F = A.F + (int64_t)b * A.FE + m.Foff;
+    const cplx* z = A.work + (int64_t)b * A.WE + m.zsOff;
+    const int* hl = A.halo + m.haloOff;
+    cplx* x = A.x.at(b);
+    for (int a = blockIdx.y * 8 + warp; a < m.s; a += gridDim.y * 8) {
+      const cplx* row = F + (int64_t)a * m.f;
+      cplx acc = row_dot(row, z, m.s, lane);
+      cplx acc2 = cmake(0, 0);
+      for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
+      acc = cadd(acc, warp_sum(acc2));
+      if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+    }
+  }
+}
+
+// bottom subtrees: one CTA walks all fronts of one subtree (bottom-up / top-down)
+__global__ void __launch_bounds__(256) k_nd_fwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+                                                    const int* __restrict__ sub_list) {
+  extern __shared__ double4 smem_raw[];
+  cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
+  const int b = blockIdx.y;
+  if (A.st && A.st[b]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = sub_ptr[blockIdx.x]; k < sub_ptr[blockIdx.x + 1]; ++k) {
+    const FrontMeta m = A.fr[sub_list[k]];
+    front_gather(A, m, b, zsh, A.work + (int64_t)b * A.WE + m.zsOff, threadIdx.x, blockDim.x);
+    __syncthreads();
+    front_fwd_rows(A, m, b, zsh, warp, 8, lane);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_nd_bwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+                                                    const int* __restrict__ sub_list) {
+  extern __shared__ double4 smem_raw[];
+  cplx* v = reinterpret_cast<cplx*>(smem_raw);
+  const int b = blockIdx.y;
+  if (A.st && A.st[b]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = sub_ptr[blockIdx.x + 1] - 1; k >= sub_ptr[blockIdx.x]; --k) {
+    const FrontMeta m = A.fr[sub_list[k]];
+    stage_bwd(A, m, b, v);
+    __syncthreads();
+    front_bwd_rows(A, m, b, v, warp, 8, lane);
+    __syncthreads();
   }
 }
 
@@ -304,6 +437,17 @@ int64_t box_count(const Box& b, int dim) {
   return c;
 }
 
+void push_box_nodes(const Box& b, int dim, int m, std::vector<int>& out) {
+  int c[3] = {0, 0, 0};
+  for (c[2] = (dim > 2 ? b.lo[2] : 0); c[2] < (dim > 2 ? b.hi[2] : 1); ++c[2])
+    for (c[1] = b.lo[1]; c[1] < b.hi[1]; ++c[1])
+      for (c[0] = b.lo[0]; c[0] < b.hi[0]; ++c[0]) {
+        int64_t g = 0, st = 1;
+        for (int d = 0; d < dim; ++d) { g += c[d] * st; st *= m; }
+        out.push_back((int)g);
+      }
+}
+
 void build_tree(const Box& b, int dim, int m, int parent, std::vector<HostFront>& out) {
   const int id = (int)out.size();
   out.push_back(HostFront());
@@ -313,28 +457,13 @@ void build_tree(const Box& b, int dim, int m, int parent, std::vector<HostFront>
   for (int d = 1; d < dim; ++d)
     if (b.hi[d] - b.lo[d] > b.hi[ax] - b.lo[ax]) ax = d;
   const int ext = b.hi[ax] - b.lo[ax];
-  const int64_t cnt = box_count(b, dim);
-  auto idx = [&](const int* c) {
-    int64_t g = 0, st = 1;
-    for (int d = 0; d < dim; ++d) { g += c[d] * st; st *= m; }
-    return (int)g;
-  };
-  if (cnt <= LEAF || ext < 3) {
-    // leaf: all nodes, lexicographic
-    int c[3] = {0, 0, 0};
-    for (c[2] = (dim > 2 ? b.lo[2] : 0); c[2] < (dim > 2 ? b.hi[2] : 1); ++c[2])
-      for (c[1] = b.lo[1]; c[1] < b.hi[1]; ++c[1])
-        for (c[0] = b.lo[0]; c[0] < b.hi[0]; ++c[0]) out[id].sep.push_back(idx(c));
+  if (box_count(b, dim) <= LEAF || ext < 3) {   // leaf: all nodes, lexicographic
+    push_box_nodes(b, dim, m, out[id].sep);
     return;
   }
   const int mid = (b.lo[ax] + b.hi[ax]) / 2;
   Box s = b; s.lo[ax] = mid; s.hi[ax] = mid + 1;
-  {
-    int c[3] = {0, 0, 0};
-    for (c[2] = (dim > 2 ? s.lo[2] : 0); c[2] < (dim > 2 ? s.hi[2] : 1); ++c[2])
-      for (c[1] = s.lo[1]; c[1] < s.hi[1]; ++c[1])
-        for (c[0] = s.lo[0]; c[0] < s.hi[0]; ++c[0]) out[id].sep.push_back(idx(c));
-  }
+  push_box_nodes(s, dim, m, out[id].sep);
   Box l = b; l.hi[ax] = mid;
   Box r = b; r.lo[ax] = mid + 1;
   const int lid = (int)out.size();
@@ -348,17 +477,18 @@ void build_tree(const Box& b, int dim, int m, int parent, std::vector<HostFront>
 }  // namespace
 
 // ============================================================ host API
-hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
-  (void)s;
-  NDFactor* nd = new NDFactor();
-  const int dim = C.dim, m = C.n + 1;
-  nd->dim = dim; nd->m = m; nd->N = C.nodes;
+hh_status nd_plan_create(int dim, int m, NDPlan** out) {
+  NDPlan* nd = new NDPlan();
+  nd->dim = dim; nd->m = m;
+  nd->N = 1;
+  for (int d = 0; d < dim; ++d) nd->N *= m;
+  nd->S = dim == 2 ? 9 : 27;
   std::vector<HostFront> tf;
   Box root;
   for (int d = 0; d < 3; ++d) { root.lo[d] = 0; root.hi[d] = (d < dim) ? m : 1; }
   build_tree(root, dim, m, -1, tf);
   const int nf = (int)tf.size();
-  // halo rings + levels (height)
+  // halo rings + levels (height above the leaves)
   for (int t = nf - 1; t >= 0; --t) {
     int lv = 0;
     for (int c : tf[t].children) lv = std::max(lv, tf[c].level + 1);
@@ -399,9 +529,8 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
   std::vector<int> sepAll, haloAll, eamap;
   std::vector<int4> asmE;
   int64_t Foff = 0, zsOff = 0, outOff = 0, eaOff = 0;
-  const int S = (dim == 2) ? 9 : 27;
+  const int S = nd->S;
   std::vector<int> loc(nd->N, -1);
-  // assembly entries grouped per level: collect per front then concatenate (fronts ordered by level)
   for (int i = 0; i < nf; ++i) {
     const HostFront& h = tf[order[i]];
     FrontMeta& fm = nd->fronts[i];
@@ -412,7 +541,7 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
     fm.zsOff = zsOff; zsOff += fm.s;
     fm.outOff = outOff; outOff += fm.u;
     fm.parent = h.parent >= 0 ? newid[h.parent] : -1;
-    // local map
+    fm.pad = 0;
     for (int a = 0; a < fm.s; ++a) loc[h.sep[a]] = a;
     for (int b = 0; b < fm.u; ++b) loc[h.halo[b]] = fm.s + b;
     for (int a = 0; a < fm.s; ++a) {
@@ -421,15 +550,14 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
       int64_t r = g;
       for (int d = 0; d < dim; ++d) { c[d] = (int)(r % m); r /= m; }
       for (int o = 0; o < S; ++o) {
-        int nb[3] = {0, 0, 0};
         bool ok = true;
         int oo = o;
         int64_t gj = 0, st = 1;
         for (int d = 0; d < dim; ++d) {
-          const int dd = oo % 3 - 1; oo /= 3;
-          nb[d] = c[d] + dd;
-          ok = ok && nb[d] >= 0 && nb[d] < m;
-          gj += nb[d] * st; st *= m;
+          const int nbd = c[d] + oo % 3 - 1;
+          oo /= 3;
+          ok = ok && nbd >= 0 && nbd < m;
+          gj += nbd * st; st *= m;
         }
         if (!ok) continue;
         const int lj = loc[gj];
@@ -461,28 +589,28 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
     for (size_t b = 0; b < hp.halo.size(); ++b) loc[hp.halo[b]] = -1;
   }
   // gather CSR: for every separator entry (front t, a): contributions (front d, halo pos b)
-  std::vector<std::vector<int64_t>> contrib(sepAll.size());
+  std::vector<int> cnt(sepAll.size() + 1, 0);
+  for (int d = 0; d < nf; ++d) {
+    const HostFront& h = tf[order[d]];
+    for (int g : h.halo) cnt[nd->fronts[owner[g]].sepOff + ownpos[g] + 1]++;
+  }
+  std::vector<int64_t> gptr(sepAll.size() + 1, 0);
+  for (size_t e = 0; e < sepAll.size(); ++e) gptr[e + 1] = gptr[e] + cnt[e + 1];
+  std::vector<int64_t> gidx(gptr.back()), fill(gptr.begin(), gptr.end() - 1);
   for (int d = 0; d < nf; ++d) {
     const FrontMeta& fm = nd->fronts[d];
     const HostFront& h = tf[order[d]];
     for (int b = 0; b < fm.u; ++b) {
       const int g = h.halo[b];
-      const int t = owner[g];
-      contrib[nd->fronts[t].sepOff + ownpos[g]].push_back(fm.outOff + b);
+      gidx[fill[nd->fronts[owner[g]].sepOff + ownpos[g]]++] = fm.outOff + b;
     }
   }
-  std::vector<int64_t> gptr(sepAll.size() + 1, 0), gidx;
-  for (size_t e = 0; e < sepAll.size(); ++e) {
-    gptr[e + 1] = gptr[e] + (int64_t)contrib[e].size();
-    gidx.insert(gidx.end(), contrib[e].begin(), contrib[e].end());
-  }
-  for (int i = 0; i < nf; ++i) nd->fronts[i].gptrOff = nd->fronts[i].sepOff;   // gptr indexed per sep entry
   // levels
   nd->levels.resize(nlev);
+  std::vector<int> eaList;
   {
     int i = 0;
     int64_t ai = 0;
-    std::vector<int> eaList;
     for (int L = 0; L < nlev; ++L) {
       LevelInfo& li = nd->levels[L];
       li.begin = i; li.count = 0; li.max_s = li.max_u = li.max_f = 0;
@@ -492,6 +620,10 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
         li.max_f = std::max(li.max_f, nd->fronts[i].f);
         ++li.count; ++i;
       }
+      const FrontMeta& f0 = nd->fronts[li.begin];
+      const FrontMeta& fl = nd->fronts[li.begin + li.count - 1];
+      li.Fbegin = f0.Foff;
+      li.Fcount = fl.Foff + (int64_t)fl.f * fl.f - f0.Foff;
       li.asmBegin = ai;
       while (ai < (int64_t)asmE.size() && nd->fronts[asmE[ai].x].level == L) ++ai;
       li.asmCount = ai - li.asmBegin;
@@ -507,115 +639,208 @@ hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s) {
         }
       }
     }
-    HH_CUDA_TRY(cudaMalloc(&nd->d_eaList, std::max<size_t>(1, eaList.size()) * sizeof(int)));
-    HH_CUDA_TRY(cudaMemcpy(nd->d_eaList, eaList.data(), eaList.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
-  // C buffer offsets (level-local)
+  // pivot column buffer offsets (level-local, indexed by front id)
   int64_t Cmax = 0;
   std::vector<int64_t> Coff(nf);
   for (auto& li : nd->levels) {
     int64_t o = 0;
-    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t - li.begin + li.begin] = o; o += (int64_t)nd->fronts[t].f * NB; }
+    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB; }
     Cmax = std::max(Cmax, o);
   }
-  // device Coff array indexed by blockIdx (level-local): store per front, pass pointer at level begin
-  nd->F_entries = Foff; nd->zs_entries = zsOff; nd->out_entries = outOff;
+  nd->F_entries = Foff; nd->zs_entries = zsOff; nd->out_entries = outOff; nd->C_entries = Cmax;
   int64_t sb = 0;
   for (auto& fm : nd->fronts) sb += (int64_t)fm.s * fm.f + (int64_t)fm.u * fm.s;
   nd->stream_bytes = sb * (int64_t)sizeof(cplx);
 
+  // bottom-subtree decompositions for every cut level
+  std::vector<int> sptr_all, slist_all;
+  {
+    std::vector<std::vector<int>> kids(nf);
+    for (int i = 0; i < nf; ++i)
+      if (nd->fronts[i].parent >= 0) kids[nd->fronts[i].parent].push_back(i);
+    for (int L = 0; L < nlev; ++L) {
+      nd->sub_off.push_back((int64_t)sptr_all.size());
+      nd->list_off.push_back((int64_t)slist_all.size());
+      int cnt = 0, maxf = 0;
+      double worst = 0;
+      const int base = (int)slist_all.size();
+      for (int r = 0; r < nf; ++r) {
+        const FrontMeta& fm = nd->fronts[r];
+        if (fm.level > L) continue;
+        if (fm.parent >= 0 && nd->fronts[fm.parent].level <= L) continue;
+        // subtree of r in bottom-up order: BFS then reverse
+        std::vector<int> order_sub{r};
+        for (size_t q = 0; q < order_sub.size(); ++q)
+          for (int c : kids[order_sub[q]]) order_sub.push_back(c);
+        std::reverse(order_sub.begin(), order_sub.end());
+        sptr_all.push_back((int)slist_all.size() - base);
+        double cost = 0;
+        for (int t : order_sub) {
+          const FrontMeta& ft = nd->fronts[t];
+          maxf = std::max(maxf, ft.f);
+          // measured on B200: ~5 us of dependent-load latency per front + ~40 GB/s per CTA
+          cost += 5.0 + ((double)ft.s * ft.f + (double)ft.u * ft.s) * 16.0 / 4.0e4;
+          slist_all.push_back(t);
+        }
+        worst = std::max(worst, cost);
+        ++cnt;
+      }
+      sptr_all.push_back((int)slist_all.size() - base);
+      nd->sub_cnt.push_back(cnt);
+      nd->sub_cost_us.push_back(worst);
+      nd->sub_maxf.push_back(maxf);
+    }
+  }
   auto up = [&](auto** dptr, const auto& vec) -> hh_status {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
     const size_t bytes = std::max<size_t>(1, vec.size()) * sizeof(T);
-    if (cudaMalloc((void**)dptr, bytes) != cudaSuccess) { hh_set_error("nd: cudaMalloc %zu B failed", bytes); return HH_E_OOM; }
+    if (cudaMalloc((void**)dptr, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      hh_set_error("nd: cudaMalloc %zu B failed", bytes);
+      return HH_E_OOM;
+    }
     if (!vec.empty()) HH_CUDA_TRY(cudaMemcpy(*dptr, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
     return HH_OK;
   };
-  HH_TRY(up(&nd->d_fronts, nd->fronts));
-  HH_TRY(up(&nd->d_sep, sepAll));
-  HH_TRY(up(&nd->d_halo, haloAll));
-  HH_TRY(up(&nd->d_asm, asmE));
-  HH_TRY(up(&nd->d_eamap, eamap));
-  HH_TRY(up(&nd->d_gptr, gptr));
-  HH_TRY(up(&nd->d_gidx, gidx));
-  HH_TRY(up(&nd->d_Coff, Coff));
-  if (cudaMalloc(&nd->d_F, std::max<int64_t>(1, Foff) * sizeof(cplx)) != cudaSuccess) {
-    hh_set_error("nd: cannot allocate %.3f GB of fronts", Foff * 16.0 / 1e9);
-    return HH_E_OOM;
-  }
-  if (cudaMalloc(&nd->d_C, std::max<int64_t>(1, Cmax) * sizeof(cplx)) != cudaSuccess) return HH_E_OOM;
-  HH_CUDA_TRY(cudaMalloc(&nd->d_zs, std::max<int64_t>(1, zsOff) * sizeof(cplx)));
-  HH_CUDA_TRY(cudaMalloc(&nd->d_out, std::max<int64_t>(1, outOff) * sizeof(cplx)));
-  HH_CUDA_TRY(cudaMalloc(&nd->d_flag, sizeof(int)));
+  hh_status st = HH_OK;
+  if (st == HH_OK) st = up(&nd->d_fronts, nd->fronts);
+  if (st == HH_OK) st = up(&nd->d_sep, sepAll);
+  if (st == HH_OK) st = up(&nd->d_halo, haloAll);
+  if (st == HH_OK) st = up(&nd->d_asm, asmE);
+  if (st == HH_OK) st = up(&nd->d_eamap, eamap);
+  if (st == HH_OK) st = up(&nd->d_eaList, eaList);
+  if (st == HH_OK) st = up(&nd->d_gptr, gptr);
+  if (st == HH_OK) st = up(&nd->d_gidx, gidx);
+  if (st == HH_OK) st = up(&nd->d_Coff, Coff);
+  if (st == HH_OK) st = up(&nd->d_sub_ptr, sptr_all);
+  if (st == HH_OK) st = up(&nd->d_sub_list, slist_all);
+  if (st != HH_OK) { nd_plan_destroy(nd); return st; }
   *out = nd;
   return HH_OK;
 }
 
-hh_status nd_factor(NDFactor* nd, const cplx* st, cudaStream_t s) {
-  HH_CUDA_TRY(cudaMemsetAsync(nd->d_flag, 0, sizeof(int), s));
+void nd_plan_destroy(NDPlan* nd) {
+  if (!nd) return;
+  cudaFree(nd->d_fronts); cudaFree(nd->d_sep); cudaFree(nd->d_halo); cudaFree(nd->d_asm);
+  cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gptr); cudaFree(nd->d_gidx);
+  cudaFree(nd->d_Coff); cudaFree(nd->d_sub_ptr); cudaFree(nd->d_sub_list);
+  delete nd;
+}
+
+int64_t nd_front_entries(const NDPlan* p) { return p->F_entries; }
+int64_t nd_stream_bytes(const NDPlan* p) { return p->stream_bytes; }
+int nd_levels(const NDPlan* p) { return (int)p->levels.size(); }
+int64_t nd_work_entries(const NDPlan* p) { return p->zs_entries + p->out_entries; }
+int64_t nd_cbuf_entries(const NDPlan* p) { return std::max<int64_t>(1, p->C_entries); }
+
+hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
+                    cudaStream_t s) {
+  const int64_t FE = nd->F_entries, CE = nd_cbuf_entries(nd);
+  const int64_t stS = nd->N * nd->S;
+  HH_CUDA_TRY(cudaMemsetAsync(flag, 0, B * sizeof(int), s));
   for (size_t L = 0; L < nd->levels.size(); ++L) {
     const LevelInfo& li = nd->levels[L];
-    const FrontMeta& f0 = nd->fronts[li.begin];
-    const FrontMeta& fl = nd->fronts[li.begin + li.count - 1];
-    const int64_t lvEntries = fl.Foff + (int64_t)fl.f * fl.f - f0.Foff;
-    HH_CUDA_TRY(cudaMemsetAsync(nd->d_F + f0.Foff, 0, lvEntries * sizeof(cplx), s));
+    {
+      const unsigned gx = (unsigned)std::min<int64_t>(4096, (li.Fcount + 255) / 256);
+      k_nd_zero<<<dim3(gx, B), 256, 0, s>>>(F, FE, li.Fbegin, li.Fcount);
+    }
     if (li.asmCount) {
       const int bs = 256;
-      k_nd_assemble<<<(unsigned)((li.asmCount + bs - 1) / bs), bs, 0, s>>>(
-          nd->d_asm + li.asmBegin, li.asmCount, nd->d_fronts, st, nd->d_F);
+      k_nd_assemble<<<dim3((unsigned)((li.asmCount + bs - 1) / bs), B), bs, 0, s>>>(
+          nd->d_asm + li.asmBegin, li.asmCount, nd->d_fronts, st, stS, F, FE);
     }
     for (int slot = 0; slot < 2; ++slot) {
       if (!li.ea_count[slot]) continue;
-      dim3 g(li.ea_count[slot], std::min(64, std::max(1, nd->levels[0].max_u)));
+      dim3 g(li.ea_count[slot], 32, B);
       k_nd_extend_add<<<g, 128, 0, s>>>(nd->d_eaList + li.ea_list_off[slot], nd->d_fronts,
-                                        nd->d_eamap, nd->d_F);
+                                        nd->d_eamap, F, FE);
     }
+    const int tiles = (li.max_f + UT - 1) / UT;
     for (int kb = 0; kb < li.max_s; kb += NB) {
-      k_nd_piv<<<li.count, 256, 0, s>>>(nd->d_fronts, li.begin, kb, nd->d_F, nd->d_C,
-                                        nd->d_Coff + li.begin, nd->d_flag);
-      const int tiles = (li.max_f + UT - 1) / UT;
-      dim3 g(tiles, tiles, li.count);
-      k_nd_upd<<<g, 256, 0, s>>>(nd->d_fronts, li.begin, kb, nd->d_F, nd->d_C,
-                                 nd->d_Coff + li.begin);
+      k_nd_piv<<<dim3(li.count, B), 256, 0, s>>>(nd->d_fronts, li.begin, kb, F, FE, cbuf, CE,
+                                                  nd->d_Coff + li.begin, flag);
+      k_nd_upd<<<dim3(tiles * tiles, li.count, B), 256, 0, s>>>(nd->d_fronts, li.begin, kb, tiles,
+                                                                 F, FE, cbuf, CE,
+                                                                 nd->d_Coff + li.begin);
     }
     HH_CUDA_TRY(cudaGetLastError());
   }
-  int flag = 0;
-  HH_CUDA_TRY(cudaMemcpyAsync(&flag, nd->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  HH_CUDA_TRY(cudaStreamSynchronize(s));
-  if (flag) { hh_set_error("nd: zero pivot in the coarse factorisation"); return HH_E_SINGULAR; }
   return HH_OK;
 }
 
-hh_status nd_solve(NDFactor* nd, const cplx* rhs, cplx* x, cudaStream_t s) {
-  const int nlev = (int)nd->levels.size();
-  for (int L = 0; L < nlev; ++L) {
-    const LevelInfo& li = nd->levels[L];
-    dim3 gg(li.count, std::max(1, std::min(32, (li.max_s + 255) / 256)));
-    k_nd_gather<<<gg, 256, 0, s>>>(nd->d_fronts, li.begin, nd->d_sep, nd->d_gptr, nd->d_gidx,
-                                   rhs, nd->d_out, nd->d_zs);
-    if (li.max_u > 0) {
-      dim3 g(li.count, std::max(1, std::min(1024, (li.max_u + 7) / 8)));
-      k_nd_fwd<<<g, 256, 0, s>>>(nd->d_fronts, li.begin, nd->d_F, nd->d_zs, nd->d_out);
-    }
+// cut level for a batch of B samples: levels <= L run as one-CTA subtrees, the rest per level
+static int choose_cut(NDPlan* nd, int B) {
+  if (const char* e = getenv("HH_ND_CUT")) {   // experiment override: -1 = per-level only
+    const int c = atoi(e);
+    return std::min<int>(c, (int)nd->levels.size() - 1);
   }
-  for (int L = nlev - 1; L >= 0; --L) {
+  {
+    std::lock_guard<std::mutex> lk(nd->cut_mu);
+    for (auto& c : nd->cut_cache) if (c.first == B) return c.second;
+  }
+  const int nlev = (int)nd->levels.size();
+  const double launch_us = 10.0;   // measured per-level kernel (fwd or bwd) on small fronts
+  const int slots = 148 * 4;
+  int best = -1;
+  double best_t = 2.0 * nlev * launch_us;
+  for (int L = 0; L < nlev; ++L) {
+    if (nd->sub_maxf[L] > 1024) break;
+    const int64_t ctas = (int64_t)nd->sub_cnt[L] * B;
+    const double waves = std::ceil((double)ctas / slots);
+    const double t = 2.0 * (launch_us + nd->sub_cost_us[L] * waves) + 2.0 * (nlev - 1 - L) * launch_us;
+    if (t < best_t) { best_t = t; best = L; }
+  }
+  std::lock_guard<std::mutex> lk(nd->cut_mu);
+  nd->cut_cache.push_back({B, best});
+  return best;
+}
+
+hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
+                   VArg x, cudaStream_t s) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  const int nlev = (int)nd->levels.size();
+  SolveArgs A;
+  A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo;
+  A.gptr = nd->d_gptr; A.gidx = nd->d_gidx; A.F = F; A.FE = nd->F_entries;
+  A.work = work; A.WE = nd_work_entries(nd); A.zsE = nd->zs_entries; A.rhs = rhs; A.x = x;
+  const int cut = choose_cut(nd, B);
+  if (cut >= 0) {
+    const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
+    k_nd_fwd_sub<<<dim3(nd->sub_cnt[cut], B), 256, sm, s>>>(A, nd->d_sub_ptr + nd->sub_off[cut],
+                                                            nd->d_sub_list + nd->list_off[cut]);
+  }
+  for (int L = cut + 1; L < nlev; ++L) {
     const LevelInfo& li = nd->levels[L];
-    dim3 g(li.count, std::max(1, std::min(1024, (li.max_s + 7) / 8)));
-    k_nd_bwd<<<g, 256, 0, s>>>(nd->d_fronts, li.begin, nd->d_F, nd->d_zs, nd->d_sep, nd->d_halo, x);
+    if (li.max_s > VMAX) {
+      dim3 gg(li.count, std::max(1, std::min(64, (li.max_s + 255) / 256)), B);
+      k_nd_gather<<<gg, 256, 0, s>>>(A, li.begin);
+    }
+    const size_t sm = (size_t)std::min(li.max_s, VMAX) * sizeof(cplx);
+    if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dim3 g(li.count, std::max(1, std::min(1024, (li.max_u + 7) / 8)), B);
+    k_nd_fwd<<<g, 256, sm, s>>>(A, li.begin);
+  }
+  for (int L = nlev - 1; L > cut; --L) {
+    const LevelInfo& li = nd->levels[L];
+    const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
+    if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    dim3 g(li.count, std::max(1, std::min(1024, (li.max_s + 7) / 8)), B);
+    k_nd_bwd<<<g, 256, sm, s>>>(A, li.begin);
+  }
+  if (cut >= 0) {
+    const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
+    k_nd_bwd_sub<<<dim3(nd->sub_cnt[cut], B), 256, sm, s>>>(A, nd->d_sub_ptr + nd->sub_off[cut],
+                                                            nd->d_sub_list + nd->list_off[cut]);
   }
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
-void nd_destroy(NDFactor* nd) {
-  if (!nd) return;
-  cudaFree(nd->d_fronts); cudaFree(nd->d_sep); cudaFree(nd->d_halo); cudaFree(nd->d_asm);
-  cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gptr); cudaFree(nd->d_gidx);
-  cudaFree(nd->d_F); cudaFree(nd->d_C); cudaFree(nd->d_Coff); cudaFree(nd->d_zs);
-  cudaFree(nd->d_out); cudaFree(nd->d_flag);
-  delete nd;
+int nd_solve_launches(const NDPlan* ndc, int B) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  const int cut = choose_cut(nd, B);
+  int n = (cut >= 0 ? 2 : 0) + 2 * ((int)nd->levels.size() - 1 - cut);
+  for (int L = cut + 1; L < (int)nd->levels.size(); ++L) n += nd->levels[L].max_s > VMAX;
+  return n;
 }
-
-int64_t nd_factor_bytes(const NDFactor* nd) { return nd ? nd->stream_bytes : 0; }
-int nd_levels(const NDFactor* nd) { return nd ? (int)nd->levels.size() : 0; }

@@ -1,24 +1,26 @@
-// 2D fine-level kernels: matrix-free Q1 operator apply, fused damped-Jacobi
-// pre-smoothing + residual restriction, fused prolongation + correction +
-// post-smoothing (+ A_0 apply of the result), coarse stencil assembly.
+// 2D fine-level kernels (batched): matrix-free Q1 operator apply, fused
+// damped-Jacobi pre-smoothing + residual restriction, fused prolongation +
+// correction + post-smoothing (+ A_0 apply of the result), coarse stencil.
 //
 // Operator (Eq. sys_matrix; 2D stencils PAPER.md:124-129):
 //   A(k,eps) = K - M(k,eps) - i B(k),  element-constant lambda_e = k_e^2 + i eps_e
-//   (reading C1), boundary faces weighted by the adjacent element's k_e (C3).
+//   (reading C1), boundary edges weighted by the adjacent element's k_e (C3).
 // Per element e with the node at one corner and its element neighbours
 // xh (along x), xv (along y), xd (diagonal):
 //   K^e row  = 2/3 xp - 1/6 (xh + xv) - 1/3 xd
 //   M^e row  = h^2/36 (4 xp + 2 (xh + xv) + xd)
 //   B^f row  = h/6 (2 xp + x_other)                 (boundary edge f)
+// Interior nodes use the assembled 9-point form: K = (1/3)[-1 -1 -1; -1 8 -1; -1 -1 -1]
+// plus sum_q lambda_q M^{e_q} (constant k: the printed mass stencil).
 // Jacobi: u <- u + omega D^{-1} (f - A_eps u), D = diag(A_eps) incl. -i k B
 // (reading C6).  Transfers: I^T with weights
 // 1, 1/2, 1/4 (reading C5) and bilinear I.
 //
-// Design (B200): one CTA computes a TX x TY tile of fine nodes; the inputs
-// of the whole multi-step sequence are staged once in shared memory with a
-// halo of R = nu + 1 nodes and every intermediate Jacobi iterate lives in
-// shared memory (halo recompute / temporal blocking), so a V-cycle touches
-// HBM twice per fine vector instead of once per smoothing step.
+// B200 design: one CTA computes a TX x TY tile of fine nodes of one sample
+// (blockIdx.z); every input of the multi-step sequence is staged once in
+// shared memory with a halo of R = nu + 1 nodes, and every intermediate Jacobi
+// iterate lives in shared memory (halo recompute / temporal blocking), so a
+// whole V-cycle reads each fine input once and writes each output once.
 #include "hh_internal.cuh"
 
 namespace {
@@ -33,92 +35,119 @@ struct Tile {
   __device__ __forceinline__ int gy(int sy) const { return Y0 - R + sy; }
 };
 
-// element coefficient (k, eps) of element (ex, ey); the smem copy covers the
-// (SX+1) x (SY+1) elements starting at (X0-R-1, Y0-R-1) so that the diagonal
-// of every node of the region is available.
+// element coefficient (k, eps): the smem copy covers (SX+1) x (SY+1) elements
+// starting at (X0-R-1, Y0-R-1) so the diagonal of every region node is available.
 template <bool HET>
 __device__ __forceinline__ double2 elem_coef(const double2* sE, const Tile& t, int ex, int ey,
-                                             double kc, double ec) {
+                                             double2 kc) {
   if (HET) return sE[(ex - (t.X0 - t.R - 1)) + (ey - (t.Y0 - t.R - 1)) * (t.SX + 1)];
-  return make_double2(kc, ec);
+  return kc;
 }
 
-// (A x)_p and optionally D_p at the node held in smem slot si (coords gx, gy).
-// EPS: use lambda = k^2 + i eps (A_eps) if true, k^2 (A_0) otherwise.
-template <bool HET, bool EPS, bool WANT_D>
-__device__ __forceinline__ void node_op(const cplx* __restrict__ X, int si, const Tile& t, int gx,
-                                        int gy, int n, double h, const double2* sE, double kc,
-                                        double ec, cplx& ax, cplx& dg) {
+// generic (boundary-safe) row of A x at smem slot si: quadrant loop + boundary edges
+template <bool HET, bool EPS>
+__device__ __noinline__ cplx node_op_generic(const cplx* __restrict__ X, int si, const Tile& t,
+                                             int gx, int gy, int n, double h, const double2* sE,
+                                             double2 kc) {
   const int SX = t.SX;
   const double h2 = h * h * (1.0 / 36.0);
   const cplx xp = X[si];
-  ax = cmake(0, 0);
-  dg = cmake(0, 0);
-  cplx ksum = cmake(0, 0), msum = cmake(0, 0);
-  int nq = 0;
-#pragma unroll
+  cplx ax = cmake(0, 0);
   for (int q = 0; q < 4; ++q) {
     const int dx = (q & 1) ? 1 : -1, dy = (q & 2) ? 1 : -1;
     const int ex = gx + (dx < 0 ? -1 : 0), ey = gy + (dy < 0 ? -1 : 0);
     if (ex < 0 || ex >= n || ey < 0 || ey >= n) continue;
     const cplx xh = X[si + dx], xv = X[si + dy * SX], xd = X[si + dx + dy * SX];
     const cplx hv = cadd(xh, xv);
-    cplx kp = cmake((2.0 / 3.0) * xp.x - (1.0 / 6.0) * hv.x - (1.0 / 3.0) * xd.x,
-                    (2.0 / 3.0) * xp.y - (1.0 / 6.0) * hv.y - (1.0 / 3.0) * xd.y);
-    cplx mp = cmake(h2 * (4.0 * xp.x + 2.0 * hv.x + xd.x), h2 * (4.0 * xp.y + 2.0 * hv.y + xd.y));
-    if (HET) {
-      const double2 c = elem_coef<true>(sE, t, ex, ey, kc, ec);
-      const cplx lam = cmake(c.x * c.x, EPS ? c.y : 0.0);
-      ax = cadd(ax, kp);
-      cfms(ax, lam, mp);
-      if (WANT_D) { dg.x += 2.0 / 3.0 - lam.x * 4.0 * h2; dg.y -= lam.y * 4.0 * h2; }
-    } else {
-      ksum = cadd(ksum, kp);
-      msum = cadd(msum, mp);
-      ++nq;
-    }
+    const cplx kp = cmake((2.0 / 3.0) * xp.x - (1.0 / 6.0) * hv.x - (1.0 / 3.0) * xd.x,
+                          (2.0 / 3.0) * xp.y - (1.0 / 6.0) * hv.y - (1.0 / 3.0) * xd.y);
+    const cplx mp = cmake(h2 * (4.0 * xp.x + 2.0 * hv.x + xd.x), h2 * (4.0 * xp.y + 2.0 * hv.y + xd.y));
+    const double2 c = elem_coef<HET>(sE, t, ex, ey, kc);
+    const cplx lam = cmake(c.x * c.x, EPS ? c.y : 0.0);
+    ax = cadd(ax, kp);
+    cfms(ax, lam, mp);
   }
-  if (!HET) {
-    const cplx lam = cmake(kc * kc, EPS ? ec : 0.0);
-    ax = ksum;
-    cfms(ax, lam, msum);
-    if (WANT_D) { dg.x = nq * (2.0 / 3.0 - lam.x * 4.0 * h2); dg.y = -nq * lam.y * 4.0 * h2; }
+  const double h6 = h * (1.0 / 6.0);
+  auto edge = [&](int ex, int ey, cplx xo) {
+    const double k = elem_coef<HET>(sE, t, ex, ey, kc).x;
+    const cplx s = cmake(2.0 * xp.x + xo.x, 2.0 * xp.y + xo.y);
+    ax.x += k * h6 * s.y;      // -i k h/6 s
+    ax.y -= k * h6 * s.x;
+  };
+  if (gx == 0 || gx == n) {
+    const int ex = (gx == 0) ? 0 : n - 1;
+    if (gy > 0) edge(ex, gy - 1, X[si - SX]);
+    if (gy < n) edge(ex, gy, X[si + SX]);
   }
-  // boundary edges: -i k_e h/6 (2 xp + x_other)
-  if (gx == 0 || gx == n || gy == 0 || gy == n) {
-    const double h6 = h * (1.0 / 6.0);
-    auto edge = [&](int ex, int ey, cplx xo) {
-      const double k = elem_coef<HET>(sE, t, ex, ey, kc, ec).x;
-      const cplx s = cmake(2.0 * xp.x + xo.x, 2.0 * xp.y + xo.y);
-      ax.x += k * h6 * s.y;
-      ax.y -= k * h6 * s.x;
-      if (WANT_D) dg.y -= k * 2.0 * h6;
-    };
-    if (gx == 0 || gx == n) {
-      const int ex = (gx == 0) ? 0 : n - 1;
-      if (gy > 0) edge(ex, gy - 1, X[si - SX]);
-      if (gy < n) edge(ex, gy, X[si + SX]);
-    }
-    if (gy == 0 || gy == n) {
-      const int ey = (gy == 0) ? 0 : n - 1;
-      if (gx > 0) edge(gx - 1, ey, X[si - 1]);
-      if (gx < n) edge(gx, ey, X[si + 1]);
-    }
+  if (gy == 0 || gy == n) {
+    const int ey = (gy == 0) ? 0 : n - 1;
+    if (gx > 0) edge(gx - 1, ey, X[si - 1]);
+    if (gx < n) edge(gx, ey, X[si + 1]);
   }
+  return ax;
 }
 
-// D_p = diag(A_eps) at node (gx, gy): sum over adjacent elements of
-// K^e_pp - lambda_e M^e_pp = 2/3 - lambda_e h^2/9, minus i k_e h/3 per boundary edge.
+// Per-sample constant-coefficient interior stencil  A = c0 xp + c1 (E+W+N+S) + c2 (corners)
+struct Const9 { cplx c0, c1, c2; };
+__device__ __forceinline__ Const9 make_const9(double2 kc, double h, bool eps) {
+  const double h2 = h * h / 36.0;
+  const cplx lam = cmake(kc.x * kc.x, eps ? kc.y : 0.0);
+  Const9 c;
+  c.c0 = cmake(8.0 / 3.0 - 16.0 * h2 * lam.x, -16.0 * h2 * lam.y);
+  c.c1 = cmake(-1.0 / 3.0 - 4.0 * h2 * lam.x, -4.0 * h2 * lam.y);
+  c.c2 = cmake(-1.0 / 3.0 - h2 * lam.x, -h2 * lam.y);
+  return c;
+}
+
+// row of A x at smem slot si (fast interior paths, generic at the boundary)
+template <bool HET, bool EPS>
+__device__ __forceinline__ cplx node_op(const cplx* __restrict__ X, int si, const Tile& t, int gx,
+                                        int gy, int n, double h, const double2* sE, double2 kc,
+                                        const Const9& c9) {
+  if (gx <= 0 || gx >= n || gy <= 0 || gy >= n)
+    return node_op_generic<HET, EPS>(X, si, t, gx, gy, n, h, sE, kc);
+  const int SX = t.SX;
+  const cplx xp = X[si];
+  const cplx W = X[si - 1], E = X[si + 1], S = X[si - SX], N = X[si + SX];
+  const cplx SW = X[si - SX - 1], SE = X[si - SX + 1], NW = X[si + SX - 1], NE = X[si + SX + 1];
+  if (!HET) {
+    const cplx e4 = cmake(W.x + E.x + S.x + N.x, W.y + E.y + S.y + N.y);
+    const cplx c4 = cmake(SW.x + SE.x + NW.x + NE.x, SW.y + SE.y + NW.y + NE.y);
+    cplx ax = cmul(c9.c0, xp);
+    cfma(ax, c9.c1, e4);
+    cfma(ax, c9.c2, c4);
+    return ax;
+  }
+  // K part: (1/3)(8 xp - sum of the 8 neighbours)
+  const double sx8 = W.x + E.x + S.x + N.x + SW.x + SE.x + NW.x + NE.x;
+  const double sy8 = W.y + E.y + S.y + N.y + SW.y + SE.y + NW.y + NE.y;
+  cplx ax = cmake((8.0 * xp.x - sx8) * (1.0 / 3.0), (8.0 * xp.y - sy8) * (1.0 / 3.0));
+  const double h2 = h * h * (1.0 / 36.0);
+  const int e0 = (gx - 1 - (t.X0 - t.R - 1)) + (gy - 1 - (t.Y0 - t.R - 1)) * (t.SX + 1);
+  auto quad = [&](int eidx, cplx xh, cplx xv, cplx xd) {
+    const double2 c = sE[eidx];
+    const cplx lam = cmake(c.x * c.x * h2, EPS ? c.y * h2 : 0.0);
+    const cplx mp = cmake(4.0 * xp.x + 2.0 * (xh.x + xv.x) + xd.x, 4.0 * xp.y + 2.0 * (xh.y + xv.y) + xd.y);
+    cfms(ax, lam, mp);
+  };
+  quad(e0, W, S, SW);
+  quad(e0 + 1, E, S, SE);
+  quad(e0 + t.SX + 1, W, N, NW);
+  quad(e0 + t.SX + 2, E, N, NE);
+  return ax;
+}
+
+// D_p = diag(A_eps): sum over adjacent elements of 2/3 - lambda_e h^2/9, -i k_e h/3 per boundary edge
 template <bool HET>
 __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, double h,
-                                          const double2* sE, double kc, double ec) {
+                                          const double2* sE, double2 kc) {
   const double h2 = h * h * (4.0 / 36.0);
   cplx dg = cmake(0, 0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int ex = gx - 1 + (q & 1), ey = gy - 1 + ((q >> 1) & 1);
     if (ex < 0 || ex >= n || ey < 0 || ey >= n) continue;
-    const double2 c = elem_coef<HET>(sE, t, ex, ey, kc, ec);
+    const double2 c = elem_coef<HET>(sE, t, ex, ey, kc);
     dg.x += 2.0 / 3.0 - c.x * c.x * h2;
     dg.y -= c.y * h2;
   }
@@ -126,91 +155,111 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     const double h3 = h / 3.0;
     if (gx == 0 || gx == n) {
       const int ex = (gx == 0) ? 0 : n - 1;
-      if (gy > 0) dg.y -= elem_coef<HET>(sE, t, ex, gy - 1, kc, ec).x * h3;
-      if (gy < n) dg.y -= elem_coef<HET>(sE, t, ex, gy, kc, ec).x * h3;
+      if (gy > 0) dg.y -= elem_coef<HET>(sE, t, ex, gy - 1, kc).x * h3;
+      if (gy < n) dg.y -= elem_coef<HET>(sE, t, ex, gy, kc).x * h3;
     }
     if (gy == 0 || gy == n) {
       const int ey = (gy == 0) ? 0 : n - 1;
-      if (gx > 0) dg.y -= elem_coef<HET>(sE, t, gx - 1, ey, kc, ec).x * h3;
-      if (gx < n) dg.y -= elem_coef<HET>(sE, t, gx, ey, kc, ec).x * h3;
+      if (gx > 0) dg.y -= elem_coef<HET>(sE, t, gx - 1, ey, kc).x * h3;
+      if (gx < n) dg.y -= elem_coef<HET>(sE, t, gx, ey, kc).x * h3;
     }
   }
   return dg;
 }
 
-template <bool HET>
+// Iterate the region of halo `hal` around the tile without per-element integer
+// division; the body sees sx, sy, gx, gy, si and `in` (node inside the domain).
+#define FOR_REGION(hal, ...)                                                   \
+  {                                                                            \
+    const int _w = TX + 2 * (hal), _h = TY + 2 * (hal);                        \
+    const int _q = NT / _w, _r = NT - _q * _w;                                 \
+    int _x = threadIdx.x % _w, _y = threadIdx.x / _w;                          \
+    for (; _y < _h;) {                                                         \
+      const int sx = t.R - (hal) + _x, sy = t.R - (hal) + _y;                  \
+      const int gx = t.gx(sx), gy = t.gy(sy);                                  \
+      const bool in = (gx >= 0 && gx <= n && gy >= 0 && gy <= n);              \
+      const int si = sy * t.SX + sx;                                           \
+      { __VA_ARGS__ }                                                          \
+      _x += _r; _y += _q;                                                      \
+      if (_x >= _w) { _x -= _w; ++_y; }                                        \
+    }                                                                          \
+  }
+
 __device__ __forceinline__ void load_region(cplx* sX, const cplx* __restrict__ g, const Tile& t,
                                             int n, double scale) {
   const int N1 = n + 1;
-  for (int i = threadIdx.x; i < t.SX * t.SY; i += NT) {
-    const int sx = i % t.SX, sy = i / t.SX;
-    const int gx = t.gx(sx), gy = t.gy(sy);
-    cplx v = cmake(0, 0);
-    if (gx >= 0 && gx <= n && gy >= 0 && gy <= n) {
-      v = g[(int64_t)gy * N1 + gx];
-      v.x *= scale;
-      v.y *= scale;
+  for (int sy = threadIdx.x / 32; sy < t.SY; sy += NT / 32) {
+    const int gy = t.gy(sy);
+    const bool rowin = gy >= 0 && gy <= n;
+    for (int sx = threadIdx.x % 32; sx < t.SX; sx += 32) {
+      const int gx = t.gx(sx);
+      cplx v = cmake(0, 0);
+      if (rowin && gx >= 0 && gx <= n) {
+        v = __ldg(&g[(int64_t)gy * N1 + gx]);
+        v.x *= scale;
+        v.y *= scale;
+      }
+      sX[sy * t.SX + sx] = v;
     }
-    sX[i] = v;
   }
 }
 
 __device__ __forceinline__ void load_coef(double2* sE, const double2* __restrict__ coef,
                                           const Tile& t, int n) {
   const int EX = t.SX + 1, EY = t.SY + 1;
-  for (int i = threadIdx.x; i < EX * EY; i += NT) {
-    const int ex = t.X0 - t.R - 1 + i % EX, ey = t.Y0 - t.R - 1 + i / EX;
-    double2 v = make_double2(0, 0);
-    if (ex >= 0 && ex < n && ey >= 0 && ey < n) v = coef[(int64_t)ey * n + ex];
-    sE[i] = v;
+  for (int ey0 = threadIdx.x / 32; ey0 < EY; ey0 += NT / 32) {
+    const int ey = t.Y0 - t.R - 1 + ey0;
+    for (int ex0 = threadIdx.x % 32; ex0 < EX; ex0 += 32) {
+      const int ex = t.X0 - t.R - 1 + ex0;
+      double2 v = make_double2(0, 0);
+      if (ex >= 0 && ex < n && ey >= 0 && ey < n) v = __ldg(&coef[(int64_t)ey * n + ex]);
+      sE[ey0 * EX + ex0] = v;
+    }
   }
 }
 
-// region of halo `hal` around the tile, clipped to the domain: iterate
-#define FOR_REGION(hal, ...)                                                          \
-  {                                                                                   \
-    const int _w = TX + 2 * (hal), _hgt = TY + 2 * (hal);                             \
-    for (int _i = threadIdx.x; _i < _w * _hgt; _i += NT) {                            \
-      const int sx = t.R - (hal) + _i % _w, sy = t.R - (hal) + _i / _w;               \
-      const int gx = t.gx(sx), gy = t.gy(sy);                                         \
-      if (gx < 0 || gx > n || gy < 0 || gy > n) continue;                             \
-      const int si = sy * t.SX + sx;                                                  \
-      __VA_ARGS__                                                                     \
-    }                                                                                 \
-  }
+struct FineK {   // per-launch constants
+  int n; double h; double omega; int nu;
+  const double2* coef; int64_t coef_bs;   // het
+  const double2* kc;                       // constant k: [B]
+  const int* st;
+};
 
 // --------------------------------------------------------------------- apply
 template <bool HET, bool EPS>
-__global__ void __launch_bounds__(NT) k_apply2d(int n, double h, double kc, double ec,
-                                                const double2* __restrict__ coef,
-                                                const cplx* __restrict__ x, cplx* __restrict__ y,
-                                                const cplx* __restrict__ sub) {
+__global__ void __launch_bounds__(NT) k_apply2d(FineK P, VArg x, VArg y, VArg sub) {
+  const int b = blockIdx.z;
+  if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
+  const int n = P.n;
   Tile t;
   t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = 1; t.SX = TX + 2; t.SY = TY + 2;
   cplx* sX = reinterpret_cast<cplx*>(smem_raw);
   double2* sE = reinterpret_cast<double2*>(sX + t.SX * t.SY);
-  load_region<HET>(sX, x, t, n, 1.0);
-  if (HET) load_coef(sE, coef, t, n);
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const Const9 c9 = make_const9(kc, P.h, EPS);
+  load_region(sX, x.at(b), t, n, 1.0);
+  if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   __syncthreads();
-  FOR_REGION(0, {
-    cplx ax, dg;
-    node_op<HET, EPS, false>(sX, si, t, gx, gy, n, h, sE, kc, ec, ax, dg);
+  cplx* yb = y.at(b);
+  const cplx* sb = sub.p ? sub.at(b) : nullptr;
+  FOR_REGION(0, if (in) {
+    cplx ax = node_op<HET, EPS>(sX, si, t, gx, gy, n, P.h, sE, kc, c9);
     const int64_t gi = (int64_t)gy * (n + 1) + gx;
-    if (sub) ax = csub(sub[gi], ax);
-    y[gi] = ax;
+    if (sb) ax = csub(sb[gi], ax);
+    yb[gi] = ax;
   })
 }
 
 // ------------------------------------------------- pre-smoothing + restriction
 // u = S^nu(0; f), rc = I^T (f - A_eps u).  Halo R = nu + 1.
 template <bool HET>
-__global__ void __launch_bounds__(NT) k_pre2d(int n, double h, double omega, int nu, double kc,
-                                              double ec, const double2* __restrict__ coef,
-                                              const cplx* __restrict__ f,
-                                              const double* __restrict__ fscale,
-                                              cplx* __restrict__ u_out, cplx* __restrict__ rc) {
+__global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
+  const int b = blockIdx.z;
+  if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
+  const int n = P.n, nu = P.nu;
+  const double omega = P.omega, h = P.h;
   Tile t;
   t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = nu + 1;
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
@@ -220,78 +269,86 @@ __global__ void __launch_bounds__(NT) k_pre2d(int n, double h, double omega, int
   cplx* sB = sA + S;
   cplx* sDi = sB + S;
   double2* sE = reinterpret_cast<double2*>(sDi + S);
-  const double sc = fscale ? *fscale : 1.0;
-  load_region<HET>(sF, f, t, n, sc);
-  if (HET) load_coef(sE, coef, t, n);
-  for (int i = threadIdx.x; i < S; i += NT) { sA[i] = cmake(0, 0); sB[i] = cmake(0, 0); }
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const Const9 c9 = make_const9(kc, h, true);
+  load_region(sF, f.at(b), t, n, fs.at(b));
+  if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   __syncthreads();
   // D^{-1} and the first step from u = 0 (pointwise) on the full region
+  const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);   // constant k: interior D = centre coefficient
   FOR_REGION(t.R, {
-    const cplx di = cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc, ec));
+    cplx di = cmake(0, 0), v = cmake(0, 0);
+    if (in) {
+      di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
+                                                          : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
+      v = cscale(cmul(di, sF[si]), omega);
+    }
     sDi[si] = di;
-    sA[si] = cscale(cmul(di, sF[si]), omega);
+    sA[si] = v;
+    sB[si] = cmake(0, 0);
   })
   __syncthreads();
   cplx* cur = sA;
   cplx* nxt = sB;
   for (int step = 2; step <= nu; ++step) {
     const int hal = t.R - step + 1;
-    FOR_REGION(hal, {
-      cplx ax, dg;
-      node_op<HET, true, false>(cur, si, t, gx, gy, n, h, sE, kc, ec, ax, dg);
-      cplx r = csub(sF[si], ax);
+    FOR_REGION(hal, if (in) {
+      const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
       cplx v = cur[si];
-      cfma(v, cscale(sDi[si], omega), r);
+      cfma(v, cscale(sDi[si], omega), csub(sF[si], ax));
       nxt[si] = v;
     })
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
-  // residual on halo 1 -> nxt ; u on tile -> global
-  FOR_REGION(1, {
-    cplx ax, dg;
-    node_op<HET, true, false>(cur, si, t, gx, gy, n, h, sE, kc, ec, ax, dg);
+  // residual on halo 1 -> nxt ; u on the tile -> global
+  cplx* ub = uo.at(b);
+  FOR_REGION(1, if (in) {
+    const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
     nxt[si] = csub(sF[si], ax);
     if (sx >= t.R && sx < t.R + TX && sy >= t.R && sy < t.R + TY)
-      u_out[(int64_t)gy * (n + 1) + gx] = cur[si];
+      ub[(int64_t)gy * (n + 1) + gx] = cur[si];
   })
-  // residual of out-of-domain halo slots must read as 0
   __syncthreads();
   // restriction I^T at coarse nodes (2I, 2J) inside the tile
   const int nc = n / 2;
-  for (int i = threadIdx.x; i < (TX / 2) * (TY / 2); i += NT) {
-    const int cx = t.X0 / 2 + i % (TX / 2), cy = t.Y0 / 2 + i / (TX / 2);
-    if (cx > nc || cy > nc) continue;
-    const int sx = t.R + 2 * cx - t.X0, sy = t.R + 2 * cy - t.Y0;
-    cplx acc = cmake(0, 0);
+  cplx* rcb = rco.at(b);
+  {
+    const int i = threadIdx.x;   // (TX/2) x (TY/2) = 128 coarse nodes per tile
+    if (i < (TX / 2) * (TY / 2)) {
+      const int cx = t.X0 / 2 + (i % (TX / 2)), cy = t.Y0 / 2 + i / (TX / 2);
+      if (cx <= nc && cy <= nc) {
+        const int sx = t.R + 2 * cx - t.X0, sy = t.R + 2 * cy - t.Y0;
+        cplx acc = cmake(0, 0);
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy)
+        for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int gx = 2 * cx + dx, gy = 2 * cy + dy;
-        if (gx < 0 || gx > n || gy < 0 || gy > n) continue;
-        const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0);
-        const cplx r = nxt[(sy + dy) * t.SX + sx + dx];
-        acc.x += w * r.x;
-        acc.y += w * r.y;
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int gx = 2 * cx + dx, gy = 2 * cy + dy;
+            if (gx < 0 || gx > n || gy < 0 || gy > n) continue;
+            const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0);
+            const cplx r = nxt[(sy + dy) * t.SX + sx + dx];
+            acc.x += w * r.x;
+            acc.y += w * r.y;
+          }
+        rcb[(int64_t)cy * (nc + 1) + cx] = acc;
       }
-    rc[(int64_t)cy * (nc + 1) + cx] = acc;
+    }
   }
 }
 
 // ------------------------------------- prolongation + correction + post-smoothing
 // z = S^nu(u + I ec; f); if w: w = A_0 z.  Halo R = nu + (w ? 1 : 0).
-template <bool HET>
-__global__ void __launch_bounds__(NT) k_post2d(int n, double h, double omega, int nu, double kc,
-                                               double ec, const double2* __restrict__ coef,
-                                               const cplx* __restrict__ f,
-                                               const double* __restrict__ fscale,
-                                               const cplx* __restrict__ u,
-                                               const cplx* __restrict__ ecv,
-                                               cplx* __restrict__ z, cplx* __restrict__ w) {
+template <bool HET, bool WITH_W>
+__global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg uin, VArg ecin,
+                                               VArg zo, VArg wo) {
+  const int b = blockIdx.z;
+  if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
+  const int n = P.n, nu = P.nu;
+  const double omega = P.omega, h = P.h;
   Tile t;
-  t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = nu + (w ? 1 : 0);
+  t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = nu + (WITH_W ? 1 : 0);
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
   const int S = t.SX * t.SY;
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
@@ -299,94 +356,96 @@ __global__ void __launch_bounds__(NT) k_post2d(int n, double h, double omega, in
   cplx* sB = sA + S;
   cplx* sDi = sB + S;
   double2* sE = reinterpret_cast<double2*>(sDi + S);
-  const double sc = fscale ? *fscale : 1.0;
-  load_region<HET>(sF, f, t, n, sc);
-  if (HET) load_coef(sE, coef, t, n);
-  const int nc = n / 2, NC1 = nc + 1;
-  // u + I ec on the full region
-  for (int i = threadIdx.x; i < S; i += NT) {
-    const int sx = i % t.SX, sy = i / t.SX;
-    const int gx = t.gx(sx), gy = t.gy(sy);
-    cplx v = cmake(0, 0);
-    if (gx >= 0 && gx <= n && gy >= 0 && gy <= n) {
-      v = u[(int64_t)gy * (n + 1) + gx];
-      const int cx0 = gx >> 1, cy0 = gy >> 1;
-      const int cx1 = (gx & 1) ? cx0 + 1 : cx0, cy1 = (gy & 1) ? cy0 + 1 : cy0;
-      const double wx = (gx & 1) ? 0.5 : 1.0, wy = (gy & 1) ? 0.5 : 1.0;
-      if (gx & 1) {
-        if (gy & 1) {
-          const cplx a = ecv[cy0 * NC1 + cx0], b = ecv[cy0 * NC1 + cx1];
-          const cplx c = ecv[cy1 * NC1 + cx0], d = ecv[cy1 * NC1 + cx1];
-          v.x += 0.25 * (a.x + b.x + c.x + d.x);
-          v.y += 0.25 * (a.y + b.y + c.y + d.y);
-        } else {
-          const cplx a = ecv[cy0 * NC1 + cx0], b = ecv[cy0 * NC1 + cx1];
-          v.x += wx * (a.x + b.x);
-          v.y += wx * (a.y + b.y);
-        }
-      } else {
-        if (gy & 1) {
-          const cplx a = ecv[cy0 * NC1 + cx0], c = ecv[cy1 * NC1 + cx0];
-          v.x += wy * (a.x + c.x);
-          v.y += wy * (a.y + c.y);
-        } else {
-          const cplx a = ecv[cy0 * NC1 + cx0];
-          v.x += a.x;
-          v.y += a.y;
-        }
-      }
-    }
-    sA[i] = v;
-    sB[i] = cmake(0, 0);
-  }
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const Const9 c9e = make_const9(kc, h, true);
+  load_region(sF, f.at(b), t, n, fs.at(b));
+  if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
+  const cplx* u = uin.at(b);
+  const cplx* ecv = ecin.at(b);
+  const int NC1 = n / 2 + 1;
+  // u + I ec on the full region, D^{-1}
+  const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);
   __syncthreads();
-  FOR_REGION(t.R, { sDi[si] = cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc, ec)); })
+  FOR_REGION(t.R, {
+    cplx v = cmake(0, 0), di = cmake(0, 0);
+    if (in) {
+      v = __ldg(&u[(int64_t)gy * (n + 1) + gx]);
+      const int cx0 = gx >> 1, cy0 = gy >> 1;
+      const int cx1 = cx0 + (gx & 1), cy1 = cy0 + (gy & 1);
+      const cplx a = __ldg(&ecv[cy0 * NC1 + cx0]);
+      if (gx & 1) {
+        const cplx bq = __ldg(&ecv[cy0 * NC1 + cx1]);
+        if (gy & 1) {
+          const cplx c = __ldg(&ecv[cy1 * NC1 + cx0]), d = __ldg(&ecv[cy1 * NC1 + cx1]);
+          v.x += 0.25 * (a.x + bq.x + c.x + d.x);
+          v.y += 0.25 * (a.y + bq.y + c.y + d.y);
+        } else {
+          v.x += 0.5 * (a.x + bq.x);
+          v.y += 0.5 * (a.y + bq.y);
+        }
+      } else if (gy & 1) {
+        const cplx c = __ldg(&ecv[cy1 * NC1 + cx0]);
+        v.x += 0.5 * (a.x + c.x);
+        v.y += 0.5 * (a.y + c.y);
+      } else {
+        v.x += a.x;
+        v.y += a.y;
+      }
+      di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
+                                                          : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
+    }
+    sA[si] = v;
+    sB[si] = cmake(0, 0);
+    sDi[si] = di;
+  })
   __syncthreads();
   cplx* cur = sA;
   cplx* nxt = sB;
   for (int step = 1; step <= nu; ++step) {
     const int hal = t.R - step;
-    FOR_REGION(hal, {
-      cplx ax, dg;
-      node_op<HET, true, false>(cur, si, t, gx, gy, n, h, sE, kc, ec, ax, dg);
-      cplx r = csub(sF[si], ax);
+    FOR_REGION(hal, if (in) {
+      const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e);
       cplx v = cur[si];
-      cfma(v, cscale(sDi[si], omega), r);
+      cfma(v, cscale(sDi[si], omega), csub(sF[si], ax));
       nxt[si] = v;
     })
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
-  FOR_REGION(0, {
+  cplx* zb = zo.at(b);
+  cplx* wb = WITH_W ? wo.at(b) : nullptr;
+  const Const9 c90 = make_const9(kc, h, false);
+  FOR_REGION(0, if (in) {
     const int64_t gi = (int64_t)gy * (n + 1) + gx;
-    z[gi] = cur[si];
-    if (w) {
-      cplx ax, dg;
-      node_op<HET, false, false>(cur, si, t, gx, gy, n, h, sE, kc, ec, ax, dg);
-      w[gi] = ax;
-    }
+    zb[gi] = cur[si];
+    if (WITH_W) wb[gi] = node_op<HET, false>(cur, si, t, gx, gy, n, h, sE, kc, c90);
   })
 }
 
 // ------------------------------------------------------------ coarse stencil
-// st[node * 9 + (dx+1) + 3 (dy+1)] = entry of A_eps^{(1)} (rediscretisation on
+// st[b][node * 9 + (dx+1) + 3 (dy+1)] = entry of A_eps^{(1)} (rediscretisation on
 // the 2h mesh; reading C4)
 template <bool HET>
-__global__ void k_stencil2d(int n, double h, double kc, double ec, const double2* __restrict__ coef,
-                            cplx* __restrict__ st) {
+__global__ void k_stencil2d(int n, double h, const double2* __restrict__ coef, int64_t coef_bs,
+                            const double2* __restrict__ kcv, cplx* __restrict__ stv) {
   const int N1 = n + 1;
+  const int b = blockIdx.y;
   const int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (node >= (int64_t)N1 * N1) return;
+  const double2* cf = HET ? coef + b * coef_bs : nullptr;
+  const double2 kc = HET ? make_double2(0, 0) : kcv[b];
+  cplx* st = stv + (int64_t)b * N1 * N1 * 9;
   const int gx = node % N1, gy = node / N1;
   cplx e[9];
 #pragma unroll
   for (int o = 0; o < 9; ++o) e[o] = cmake(0, 0);
   const double h2 = h * h / 36.0;
+#pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int dx = (q & 1) ? 1 : -1, dy = (q & 2) ? 1 : -1;
     const int ex = gx + (dx < 0 ? -1 : 0), ey = gy + (dy < 0 ? -1 : 0);
     if (ex < 0 || ex >= n || ey < 0 || ey >= n) continue;
-    double2 c = HET ? coef[(int64_t)ey * n + ex] : make_double2(kc, ec);
+    const double2 c = HET ? cf[(int64_t)ey * n + ex] : kc;
     const cplx lam = cmake(c.x * c.x, c.y);
     auto add = [&](int o, double kv, double mv) {
       e[o].x += kv - lam.x * mv * h2;
@@ -398,7 +457,7 @@ __global__ void k_stencil2d(int n, double h, double kc, double ec, const double2
     add(4 + dx + 3 * dy, -1.0 / 3.0, 1.0);       // diagonal
   }
   auto bedge = [&](int ex, int ey, int o) {
-    const double k = HET ? coef[(int64_t)ey * n + ex].x : kc;
+    const double k = HET ? cf[(int64_t)ey * n + ex].x : kc.x;
     e[4].y -= k * h / 3.0;
     e[o].y -= k * h / 6.0;
   };
@@ -412,6 +471,7 @@ __global__ void k_stencil2d(int n, double h, double kc, double ec, const double2
     if (gx > 0) bedge(gx - 1, ey, 3);
     if (gx < n) bedge(gx, ey, 5);
   }
+#pragma unroll
   for (int o = 0; o < 9; ++o) st[node * 9 + o] = e[o];
 }
 
@@ -422,85 +482,91 @@ size_t smem_bytes(int R, int nfields, bool het) {
   return b;
 }
 
-}  // namespace
-
-// ----------------------------------------------------------------- host API
-static hh_status set_smem(const void* fn, size_t bytes) {
+hh_status set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
     HH_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   }
   return HH_OK;
 }
 
-hh_status fine_apply2d(const Level& L, int op, const cplx* x, cplx* y, const cplx* sub,
+FineK make_k(const Level& L, int nu, double omega, const int* st) {
+  FineK P;
+  P.n = L.n; P.h = L.h; P.omega = omega; P.nu = nu;
+  P.coef = L.coef; P.coef_bs = L.elems; P.kc = L.kc; P.st = st;
+  return P;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- host API
+hh_status fine_apply2d(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                        cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY);
+  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
   const size_t sm = smem_bytes(1, 1, L.het);
-  const double ec = L.eps_const;
-  if (L.het) {
-    if (op == HH_OP_A0) {
-      HH_TRY(set_smem((const void*)k_apply2d<true, false>, sm));
-      k_apply2d<true, false><<<grid, NT, sm, s>>>(n, L.h, 0, 0, L.coef, x, y, sub);
-    } else {
-      HH_TRY(set_smem((const void*)k_apply2d<true, true>, sm));
-      k_apply2d<true, true><<<grid, NT, sm, s>>>(n, L.h, 0, 0, L.coef, x, y, sub);
-    }
-  } else {
-    if (op == HH_OP_A0) {
-      HH_TRY(set_smem((const void*)k_apply2d<false, false>, sm));
-      k_apply2d<false, false><<<grid, NT, sm, s>>>(n, L.h, L.k_const, ec, nullptr, x, y, sub);
-    } else {
-      HH_TRY(set_smem((const void*)k_apply2d<false, true>, sm));
-      k_apply2d<false, true><<<grid, NT, sm, s>>>(n, L.h, L.k_const, ec, nullptr, x, y, sub);
-    }
+  const FineK P = make_k(L, 0, 0, st);
+#define LAUNCH_APPLY(H, E)                                        \
+  {                                                               \
+    HH_TRY(set_smem((const void*)k_apply2d<H, E>, sm));           \
+    k_apply2d<H, E><<<grid, NT, sm, s>>>(P, x, y, sub);           \
   }
+  if (L.het) {
+    if (op == HH_OP_A0) LAUNCH_APPLY(true, false) else LAUNCH_APPLY(true, true)
+  } else {
+    if (op == HH_OP_A0) LAUNCH_APPLY(false, false) else LAUNCH_APPLY(false, true)
+  }
+#undef LAUNCH_APPLY
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
-hh_status fine_pre2d(const Level& L, int nu, double omega, const cplx* f, const double* fscale,
-                     cplx* u, cplx* rc, cudaStream_t s) {
+hh_status fine_pre2d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
+                     VArg u, VArg rc, cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY);
+  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
   const size_t sm = smem_bytes(nu + 1, 4, L.het);
+  const FineK P = make_k(L, nu, omega, st);
   if (L.het) {
     HH_TRY(set_smem((const void*)k_pre2d<true>, sm));
-    k_pre2d<true><<<grid, NT, sm, s>>>(n, L.h, omega, nu, 0, 0, L.coef, f, fscale, u, rc);
+    k_pre2d<true><<<grid, NT, sm, s>>>(P, f, fs, u, rc);
   } else {
     HH_TRY(set_smem((const void*)k_pre2d<false>, sm));
-    k_pre2d<false><<<grid, NT, sm, s>>>(n, L.h, omega, nu, L.k_const, L.eps_const, nullptr, f,
-                                        fscale, u, rc);
+    k_pre2d<false><<<grid, NT, sm, s>>>(P, f, fs, u, rc);
   }
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
-hh_status fine_post2d(const Level& L, int nu, double omega, const cplx* f, const double* fscale,
-                      const cplx* u, const cplx* ec, cplx* z, cplx* w, cudaStream_t s) {
+hh_status fine_post2d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
+                      VArg u, VArg ec, VArg z, VArg w, cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY);
-  const size_t sm = smem_bytes(nu + (w ? 1 : 0), 4, L.het);
-  if (L.het) {
-    HH_TRY(set_smem((const void*)k_post2d<true>, sm));
-    k_post2d<true><<<grid, NT, sm, s>>>(n, L.h, omega, nu, 0, 0, L.coef, f, fscale, u, ec, z, w);
-  } else {
-    HH_TRY(set_smem((const void*)k_post2d<false>, sm));
-    k_post2d<false><<<grid, NT, sm, s>>>(n, L.h, omega, nu, L.k_const, L.eps_const, nullptr, f,
-                                         fscale, u, ec, z, w);
+  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
+  const bool ww = w.p != nullptr;
+  const size_t sm = smem_bytes(nu + (ww ? 1 : 0), 4, L.het);
+  const FineK P = make_k(L, nu, omega, st);
+#define LAUNCH_POST(H, W)                                              \
+  {                                                                    \
+    HH_TRY(set_smem((const void*)k_post2d<H, W>, sm));                 \
+    k_post2d<H, W><<<grid, NT, sm, s>>>(P, f, fs, u, ec, z, w);        \
   }
+  if (L.het) {
+    if (ww) LAUNCH_POST(true, true) else LAUNCH_POST(true, false)
+  } else {
+    if (ww) LAUNCH_POST(false, true) else LAUNCH_POST(false, false)
+  }
+#undef LAUNCH_POST
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
-hh_status coarse_stencil2d(const Level& C, cplx* st, cudaStream_t s) {
+hh_status coarse_stencil2d(const Level& C, int B, cplx* st, cudaStream_t s) {
   const int64_t N = C.nodes;
   const int bs = 128;
-  const unsigned g = (unsigned)((N + bs - 1) / bs);
+  dim3 g((unsigned)((N + bs - 1) / bs), B);
   if (C.het)
-    k_stencil2d<true><<<g, bs, 0, s>>>(C.n, C.h, 0, 0, C.coef, st);
+    k_stencil2d<true><<<g, bs, 0, s>>>(C.n, C.h, C.coef, C.elems, nullptr, st);
   else
-    k_stencil2d<false><<<g, bs, 0, s>>>(C.n, C.h, C.k_const, C.eps_const, nullptr, st);
+    k_stencil2d<false><<<g, bs, 0, s>>>(C.n, C.h, nullptr, 0, C.kc, st);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

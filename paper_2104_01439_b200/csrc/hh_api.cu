@@ -1,15 +1,29 @@
-// C ABI (include/hh.h): problem setup, operator apply, V-cycle, FGMRES solve
-// and the sample sweep.  Every arithmetic step runs in the CUDA kernels of
-// fine2d.cu / fine3d.cu / coarse_nd.cu / krylov.cu; this file only sequences
-// launches on the handle's stream.
+// C ABI (include/hh.h) and the batched engine behind it.
+//
+// Engine = one CUDA stream + reusable device workspace pools.  Batch = B
+// problems of one grid (dim, n) set up together (coefficients, coarse stencil,
+// ND factorisation) and solved in lockstep: every launch covers all B samples,
+// finished samples are masked by their device status, and one FGMRES
+// iteration (V-cycle + A_0 + CGS + Givens) is captured once as a CUDA graph
+// and replayed with the Arnoldi index j kept in device memory.
+// hh_problem = an engine + a batch of one; hh_sweep = a thread pool of
+// engines draining a queue of equal-n batches.  Every arithmetic step runs in
+// the kernels of fine2d.cu / fine3d.cu / coarse_nd.cu / krylov.cu.
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 #include "hh_internal.cuh"
+#include "krylov.cuh"
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
@@ -20,160 +34,501 @@ void hh_set_error(const char* fmt, ...) {
   va_end(ap);
 }
 extern "C" const char* hh_last_error(void) { return g_err; }
-extern "C" const char* hh_version(void) { return "hh-b200 0.1 (sm_100a, complex fp64)"; }
+extern "C" const char* hh_version(void) { return "hh-b200 0.2 (sm_100a, complex fp64, batched)"; }
 
 // fine-level dispatch (2D / 3D)
-hh_status fine_apply2d(const Level&, int, const cplx*, cplx*, const cplx*, cudaStream_t);
-hh_status fine_pre2d(const Level&, int, double, const cplx*, const double*, cplx*, cplx*, cudaStream_t);
-hh_status fine_post2d(const Level&, int, double, const cplx*, const double*, const cplx*,
-                      const cplx*, cplx*, cplx*, cudaStream_t);
-hh_status coarse_stencil2d(const Level&, cplx*, cudaStream_t);
-hh_status fine_apply3d(const Level&, int, const cplx*, cplx*, const cplx*, cudaStream_t);
-hh_status fine_pre3d(const Level&, int, double, const cplx*, const double*, cplx*, cplx*, cudaStream_t);
-hh_status fine_post3d(const Level&, int, double, const cplx*, const double*, const cplx*,
-                      const cplx*, cplx*, cplx*, cudaStream_t);
-hh_status coarse_stencil3d(const Level&, cplx*, cudaStream_t);
+hh_status fine_apply2d(const Level&, int, const int*, int, VArg, VArg, VArg, cudaStream_t);
+hh_status fine_pre2d(const Level&, int, const int*, int, double, VArg, SArg, VArg, VArg, cudaStream_t);
+hh_status fine_post2d(const Level&, int, const int*, int, double, VArg, SArg, VArg, VArg, VArg,
+                      VArg, cudaStream_t);
+hh_status coarse_stencil2d(const Level&, int, cplx*, cudaStream_t);
+hh_status fine_apply3d(const Level&, int, const int*, int, VArg, VArg, VArg, cudaStream_t);
+hh_status fine_pre3d(const Level&, int, const int*, int, double, VArg, SArg, VArg, VArg, cudaStream_t);
+hh_status fine_post3d(const Level&, int, const int*, int, double, VArg, SArg, VArg, VArg, VArg,
+                      VArg, cudaStream_t);
+hh_status coarse_stencil3d(const Level&, int, cplx*, cudaStream_t);
 
-hh_status fine_apply(const Level& L, int op, const cplx* x, cplx* y, const cplx* sub, cudaStream_t s) {
-  return L.dim == 2 ? fine_apply2d(L, op, x, y, sub, s) : fine_apply3d(L, op, x, y, sub, s);
+hh_status fine_apply(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
+                     cudaStream_t s) {
+  return L.dim == 2 ? fine_apply2d(L, B, st, op, x, y, sub, s) : fine_apply3d(L, B, st, op, x, y, sub, s);
 }
-hh_status fine_pre(const Level& L, int nu, double om, const cplx* f, const double* fs, cplx* u,
-                   cplx* rc, cudaStream_t s) {
-  return L.dim == 2 ? fine_pre2d(L, nu, om, f, fs, u, rc, s) : fine_pre3d(L, nu, om, f, fs, u, rc, s);
+hh_status fine_pre(const Level& L, int B, const int* st, int nu, double om, VArg f, SArg fs, VArg u,
+                   VArg rc, cudaStream_t s) {
+  return L.dim == 2 ? fine_pre2d(L, B, st, nu, om, f, fs, u, rc, s)
+                    : fine_pre3d(L, B, st, nu, om, f, fs, u, rc, s);
 }
-hh_status fine_post(const Level& L, int nu, double om, const cplx* f, const double* fs,
-                    const cplx* u, const cplx* ec, cplx* z, cplx* w, cudaStream_t s) {
-  return L.dim == 2 ? fine_post2d(L, nu, om, f, fs, u, ec, z, w, s)
-                    : fine_post3d(L, nu, om, f, fs, u, ec, z, w, s);
+hh_status fine_post(const Level& L, int B, const int* st, int nu, double om, VArg f, SArg fs,
+                    VArg u, VArg ec, VArg z, VArg w, cudaStream_t s) {
+  return L.dim == 2 ? fine_post2d(L, B, st, nu, om, f, fs, u, ec, z, w, s)
+                    : fine_post3d(L, B, st, nu, om, f, fs, u, ec, z, w, s);
 }
-hh_status coarse_stencil(const Level& C, cplx* st, cudaStream_t s) {
-  return C.dim == 2 ? coarse_stencil2d(C, st, s) : coarse_stencil3d(C, st, s);
+hh_status coarse_stencil(const Level& C, int B, cplx* st, cudaStream_t s) {
+  return C.dim == 2 ? coarse_stencil2d(C, B, st, s) : coarse_stencil3d(C, B, st, s);
 }
-
-// krylov.cu
-hh_status krylov_mdot(const cplx*, int64_t, int, const double*, const cplx*, cplx*, unsigned*,
-                      cplx*, int, const int*, int, cudaStream_t);
-hh_status krylov_update(const cplx*, int64_t, int, const cplx*, cplx*, double*, unsigned*, cplx*,
-                        int, double*, cplx*, cplx*, double*, double*, int*, double*, int, int, int,
-                        int, cudaStream_t);
-hh_status krylov_trisolve(const cplx*, int, const cplx*, int, cplx*, cudaStream_t);
-hh_status krylov_xupdate(const cplx*, int64_t, int, const cplx*, cplx*, int, cudaStream_t);
-hh_status krylov_norm(const cplx*, int64_t, double*, unsigned*, double*, double*, cplx*, double*,
-                      double, int, cudaStream_t);
-
-// ------------------------------------------------------------------ handle
-enum { T_PRE = 0, T_COARSE, T_POST, T_KRYLOV, T_NT };
-
-struct hh_problem {
-  hh_problem_desc d{};
-  Level F, C;
-  cudaStream_t s = nullptr;
-  cplx* stencil = nullptr;
-  NDFactor* nd = nullptr;
-  int m = 0;
-  int64_t N = 0, Nc = 0;
-  cplx *V = nullptr, *Z = nullptr, *w = nullptr, *u = nullptr, *rc = nullptr, *ec = nullptr;
-  cplx *bdev = nullptr, *xdev = nullptr;
-  double* vscale = nullptr;
-  cplx *H = nullptr, *sn = nullptr, *g = nullptr, *y = nullptr, *cpart = nullptr;
-  double *cs = nullptr, *dpart = nullptr, *dscal = nullptr, *hist = nullptr;
-  int* flags = nullptr;
-  unsigned* counter = nullptr;
-  int nblk = 0;
-  int hist_len = 0;
-  double setup_s = 0;
-  // timers
-  bool timing = false;
-  std::vector<cudaEvent_t> ev;
-  std::vector<int> ev_kind;   // per pair (start index 2k) the phase
-  int ev_used = 0;
-  int64_t launches = 0;
-  double acc_ms[T_NT] = {0, 0, 0, 0};
-};
 
 namespace {
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-template <typename T>
-hh_status dalloc(T** p, size_t count) {
-  if (cudaMalloc((void**)p, std::max<size_t>(1, count) * sizeof(T)) != cudaSuccess) {
-    cudaGetLastError();
-    hh_set_error("cudaMalloc of %.3f GB failed", count * sizeof(T) / 1e9);
-    return HH_E_OOM;
-  }
+// ------------------------------------------------------------------ small kernels
+// mode 0: x = 0; mode 1: x = src; mode 2: unit point source at node `idx`
+__global__ void k_vset(VArg x, VArg src, int64_t N, int mode, int64_t idx, const int* st) {
+  const int b = blockIdx.y;
+  if (st && st[b]) return;
+  cplx* xb = x.at(b);
+  const cplx* sb = mode == 1 ? src.at(b) : nullptr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x)
+    xb[i] = mode == 1 ? sb[i] : cmake((mode == 2 && i == idx) ? 1.0 : 0.0, 0.0);
+}
+
+hh_status vset(VArg x, VArg src, int64_t N, int B, int mode, int64_t idx, const int* st, cudaStream_t s) {
+  const unsigned gx = (unsigned)std::min<int64_t>(1024, (N + 255) / 256);
+  k_vset<<<dim3(gx, B), 256, 0, s>>>(x, src, N, mode, idx, st);
+  HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
-void tmark(hh_problem* p, int kind, bool start) {
-  if (!p->timing) return;
-  if (start) {
-    if (p->ev_used + 2 > (int)p->ev.size()) {
-      for (int i = 0; i < 256; ++i) {
-        cudaEvent_t e;
-        cudaEventCreate(&e);
-        p->ev.push_back(e);
+// ------------------------------------------------------------------ pools
+struct Pool {
+  void* p = nullptr;
+  size_t bytes = 0;
+  hh_status ensure(size_t b) {
+    if (b <= bytes && p) return HH_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    const size_t want = std::max<size_t>(b, 256);
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      hh_set_error("cudaMalloc of %.3f GB failed", want / 1e9);
+      return HH_E_OOM;
+    }
+    bytes = want;
+    return HH_OK;
+  }
+  template <typename T> T* as() const { return (T*)p; }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+};
+
+// ND plans are shared by every engine (tree depends on (dim, m) only)
+std::mutex g_plan_mu;
+std::map<std::pair<int, int>, NDPlan*> g_plans;
+hh_status get_plan(int dim, int m, NDPlan** out) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plans.find({dim, m});
+  if (it != g_plans.end()) { *out = it->second; return HH_OK; }
+  NDPlan* p = nullptr;
+  HH_TRY(nd_plan_create(dim, m, &p));
+  g_plans[{dim, m}] = p;
+  *out = p;
+  return HH_OK;
+}
+
+enum { T_PRE = 0, T_COARSE, T_POST, T_KRYLOV, T_NT };
+
+struct BatchSpec {
+  int dim = 2, n = 0, B = 1, nu_pre = 2, nu_post = 2, m = 100;
+  double omega = 0.6;
+  std::vector<double> k, beta, sigma;    // per sample (constant k)
+  const double* kf = nullptr;            // het (B == 1): host per-element k
+  const double* kcoarse = nullptr;
+};
+
+struct SampleOut {
+  int status = 0, iterations = 0, converged = 0, restarts = 0;
+  double rel_res_lsq = 0, rel_res_true = 0, rho = 0;
+};
+
+struct Engine {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
+      cpart, dpart, hist;
+  int* h_status = nullptr;   // pinned
+  // batch
+  BatchSpec spec;
+  Level LF, LC;
+  NDPlan* plan = nullptr;
+  int B = 0, m = 0, nblk = 1, hist_len = 0;
+  int64_t N = 0, Nc = 0;
+  KArgs ka;
+  int* jdev = nullptr;
+  int* nd_flag = nullptr;
+  double setup_s = 0;
+  // graph of one iteration
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_timing = false;
+  // timers
+  bool timing = false;
+  cudaEvent_t ev[2 * T_NT] = {};
+  double acc_ms[T_NT] = {0, 0, 0, 0};
+  double acc_bytes[T_NT] = {0, 0, 0, 0};
+  double acc_launch[T_NT] = {0, 0, 0, 0};
+  int64_t launches = 0;
+  int64_t launches_per_iter = 0;
+
+  ~Engine() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist};
+    for (Pool* p : all) p->release();
+    if (h_status) cudaFreeHost(h_status);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+hh_status engine_init(Engine& E, int device) {
+  E.device = device;
+  HH_CUDA_TRY(cudaSetDevice(device));
+  HH_CUDA_TRY(cudaStreamCreateWithFlags(&E.s, cudaStreamNonBlocking));
+  for (auto& e : E.ev) HH_CUDA_TRY(cudaEventCreate(&e));
+  return HH_OK;
+}
+
+int64_t ipow(int64_t a, int d) { int64_t r = 1; while (d--) r *= a; return r; }
+
+// bytes of device workspace per sample for a (dim, n, m) batch
+int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {
+  const int64_t N = ipow(n + 1, dim), Nc = ipow(n / 2 + 1, dim);
+  const int S = dim == 2 ? 9 : 27;
+  int64_t b = (int64_t)(2 * m + 1 + 4 + (dim == 3 ? 2 : 0)) * N * 16;
+  b += Nc * (2 + S) * 16;
+  b += (nd_front_entries(plan) + nd_cbuf_entries(plan) + nd_work_entries(plan)) * 16;
+  return b;
+}
+
+hh_status batch_setup(Engine& E, const BatchSpec& sp) {
+  const double t0 = now_s();
+  HH_CUDA_TRY(cudaSetDevice(E.device));
+  if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }
+  E.spec = sp;
+  const int B = sp.B, dim = sp.dim, n = sp.n, m = sp.m;
+  E.B = B; E.m = m;
+  E.N = ipow(n + 1, dim);
+  E.Nc = ipow(n / 2 + 1, dim);
+  const int64_t N = E.N, Nc = E.Nc;
+  HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
+  const NDPlan* P = E.plan;
+  const int S = dim == 2 ? 9 : 27;
+  // pools
+  HH_TRY(E.V.ensure((size_t)B * (m + 1) * N * 16));
+  HH_TRY(E.Z.ensure((size_t)B * m * N * 16));
+  HH_TRY(E.w.ensure((size_t)B * N * 16));
+  HH_TRY(E.u.ensure((size_t)B * N * 16));
+  HH_TRY(E.bv.ensure((size_t)B * N * 16));
+  HH_TRY(E.xv.ensure((size_t)B * N * 16));
+  if (dim == 3) HH_TRY(E.tmp3.ensure((size_t)B * 2 * N * 16));
+  HH_TRY(E.rc.ensure((size_t)B * Nc * 16));
+  HH_TRY(E.ec.ensure((size_t)B * Nc * 16));
+  HH_TRY(E.stc.ensure((size_t)B * Nc * S * 16));
+  HH_TRY(E.F.ensure((size_t)B * nd_front_entries(P) * 16));
+  HH_TRY(E.cbuf.ensure((size_t)B * nd_cbuf_entries(P) * 16));
+  HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
+  HH_TRY(E.kcf.ensure((size_t)B * 16));
+  HH_TRY(E.kcc.ensure((size_t)B * 16));
+  // per-level coefficients
+  for (int lev = 0; lev < 2; ++lev) {
+    Level& L = lev == 0 ? E.LF : E.LC;
+    L.dim = dim;
+    L.n = lev == 0 ? n : n / 2;
+    L.h = 1.0 / L.n;
+    L.nodes = ipow(L.n + 1, dim);
+    L.elems = ipow(L.n, dim);
+    L.het = sp.kf != nullptr;
+    L.tmp = lev == 0 && dim == 3 ? E.tmp3.as<cplx>() : nullptr;
+    L.coef = nullptr;
+    L.kc = nullptr;
+    if (L.het) {
+      if (B != 1) { hh_set_error("heterogeneous batches must have B = 1"); return HH_E_CONFIG; }
+      Pool& cp = lev == 0 ? E.coef_f : E.coef_c;
+      HH_TRY(cp.ensure(L.elems * 16));
+      const double* kh = lev == 0 ? sp.kf : sp.kcoarse;
+      std::vector<double2> c(L.elems);
+      for (int64_t e = 0; e < L.elems; ++e) {
+        const double k = kh[e];
+        if (!(k >= 0) || !std::isfinite(k)) {
+          hh_set_error("k_elem[%lld] = %g invalid", (long long)e, k);
+          return HH_E_CONFIG;
+        }
+        c[e] = make_double2(k, sp.beta[0] * std::pow(k, sp.sigma[0]));
       }
-      p->ev_kind.resize(p->ev.size() / 2 + 1);
+      HH_CUDA_TRY(cudaMemcpyAsync(cp.p, c.data(), L.elems * 16, cudaMemcpyHostToDevice, E.s));
+      HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+      L.coef = cp.as<double2>();
+    } else {
+      Pool& kp = lev == 0 ? E.kcf : E.kcc;
+      std::vector<double2> c(B);
+      for (int b = 0; b < B; ++b) c[b] = make_double2(sp.k[b], sp.beta[b] * std::pow(sp.k[b], sp.sigma[b]));
+      HH_CUDA_TRY(cudaMemcpyAsync(kp.p, c.data(), B * 16, cudaMemcpyHostToDevice, E.s));
+      HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+      L.kc = kp.as<double2>();
     }
-    p->ev_kind[p->ev_used / 2] = kind;
-    cudaEventRecord(p->ev[p->ev_used], p->s);
-  } else {
-    cudaEventRecord(p->ev[p->ev_used + 1], p->s);
-    p->ev_used += 2;
   }
+  // Krylov small arrays: vscale, cs (double) ; sn, g, y (cplx) ; H ; state ; jdev ; flags ; counters
+  const int ldv = m + 1, ldh = m + 1;
+  // Krylov CTAs per sample: enough for ONE sample to fill the GPU (the tail of a
+  // batch is a single slow sample); independent of B, so batched == single results
+  E.nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (N + 255) / 256));
+  E.hist_len = 4096;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  const size_t o_vs = carve(B * ldv * 8), o_cs = carve(B * ldv * 8), o_sn = carve(B * ldv * 16),
+               o_g = carve(B * ldv * 16), o_y = carve(B * ldv * 16), o_H = carve((size_t)B * m * ldh * 16),
+               o_bn = carve(B * 8), o_res = carve(B * 8), o_rt = carve(B * 8), o_st = carve(B * 4),
+               o_its = carve(B * 4), o_je = carve(B * 4), o_j = carve(16), o_fl = carve(B * 4),
+               o_cnt = carve(B * 4);
+  HH_TRY(E.ksmall.ensure(off));
+  HH_TRY(E.cpart.ensure((size_t)B * E.nblk * (m + 2) * 16));
+  HH_TRY(E.dpart.ensure((size_t)B * E.nblk * 8));
+  HH_TRY(E.hist.ensure((size_t)B * E.hist_len * 8));
+  char* base = E.ksmall.as<char>();
+  KArgs& A = E.ka;
+  A = KArgs();
+  A.N = N;
+  A.V = E.V.as<cplx>(); A.Vbs = (int64_t)(m + 1) * N;
+  A.Z = E.Z.as<cplx>(); A.Zbs = (int64_t)m * N;
+  A.w = E.w.as<cplx>();
+  A.H = (cplx*)(base + o_H); A.HB = (int64_t)m * ldh; A.ldh = ldh;
+  A.vscale = (double*)(base + o_vs); A.cs = (double*)(base + o_cs);
+  A.sn = (cplx*)(base + o_sn); A.g = (cplx*)(base + o_g); A.y = (cplx*)(base + o_y); A.ldv = ldv;
+  A.cpart = E.cpart.as<cplx>(); A.ldp = m + 2;
+  A.dpart = E.dpart.as<double>();
+  A.counter = (unsigned*)(base + o_cnt);
+  E.jdev = (int*)(base + o_j);
+  A.jdev = E.jdev;
+  A.nblk = E.nblk;
+  A.hist_len = E.hist_len;
+  A.ks.bnorm = (double*)(base + o_bn); A.ks.res = (double*)(base + o_res);
+  A.ks.rtrue = (double*)(base + o_rt); A.ks.status = (int*)(base + o_st);
+  A.ks.its = (int*)(base + o_its); A.ks.jend = (int*)(base + o_je); A.ks.hist = E.hist.as<double>();
+  E.nd_flag = (int*)(base + o_fl);
+  HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
+  if (E.h_status) cudaFreeHost(E.h_status);
+  HH_CUDA_TRY(cudaMallocHost(&E.h_status, std::max(B, 4) * sizeof(int)));
+  // coarse operator + factorisation
+  HH_TRY(coarse_stencil(E.LC, B, E.stc.as<cplx>(), E.s));
+  HH_TRY(nd_factor(P, B, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, B * sizeof(int), cudaMemcpyDeviceToHost, E.s));
+  HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  for (int b = 0; b < B; ++b)
+    if (E.h_status[b]) {
+      hh_set_error("zero pivot in the coarse factorisation (sample %d: k=%g, beta=%g, sigma=%g, h=%g)",
+                   b, sp.k.empty() ? 0.0 : sp.k[b], sp.beta[b], sp.sigma[b], E.LC.h);
+      return HH_E_SINGULAR;
+    }
+  E.setup_s = now_s() - t0;
+  return HH_OK;
 }
 
-void flush_timers(hh_problem* p) {
-  if (!p->ev_used) return;
-  cudaStreamSynchronize(p->s);
-  for (int i = 0; i < p->ev_used; i += 2) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]);
-    p->acc_ms[p->ev_kind[i / 2]] += ms;
-  }
-  p->ev_used = 0;
+// vector views of the engine pools
+VArg vV(Engine& E, int jo) { return varg(E.V.as<cplx>(), (int64_t)(E.m + 1) * E.N, E.N, E.jdev, jo); }
+VArg vZ(Engine& E) { return varg(E.Z.as<cplx>(), (int64_t)E.m * E.N, E.N, E.jdev, 0); }
+VArg vflat(Pool& p, int64_t bs) { return varg(p.as<cplx>(), bs); }
+
+// one FGMRES iteration for the whole batch (graph-capturable)
+hh_status enqueue_iteration(Engine& E, bool timing) {
+  const int* st = E.ka.ks.status;
+  cudaStream_t s = E.s;
+  const SArg fs = sarg(E.ka.vscale, E.ka.ldv, E.jdev, 0);
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[0], s, cudaEventRecordExternal));
+  HH_TRY(fine_pre(E.LF, E.B, st, E.spec.nu_pre, E.spec.omega, vV(E, 0), fs, vflat(E.u, E.N),
+                  vflat(E.rc, E.Nc), s));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[1], s, cudaEventRecordExternal));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[2], s, cudaEventRecordExternal));
+  HH_TRY(nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), vflat(E.rc, E.Nc),
+                  vflat(E.ec, E.Nc), s));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[3], s, cudaEventRecordExternal));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[4], s, cudaEventRecordExternal));
+  HH_TRY(fine_post(E.LF, E.B, st, E.spec.nu_post, E.spec.omega, vV(E, 0), fs, vflat(E.u, E.N),
+                   vflat(E.ec, E.Nc), vZ(E), vflat(E.w, E.N), s));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[5], s, cudaEventRecordExternal));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[6], s, cudaEventRecordExternal));
+  HH_TRY(krylov_mdot(E.ka, E.B, s));
+  HH_TRY(krylov_update(E.ka, E.B, s));
+  if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[7], s, cudaEventRecordExternal));
+  HH_TRY(krylov_advance(E.jdev, -1, s));
+  return HH_OK;
 }
 
-hh_status setup_level(Level& L, int dim, int n, double k_const, const double* k_elem, double beta,
-                      double sigma) {
-  L.dim = dim;
-  L.n = n;
-  L.h = 1.0 / n;
-  L.nodes = 1;
-  L.elems = 1;
-  for (int d = 0; d < dim; ++d) { L.nodes *= (n + 1); L.elems *= n; }
-  L.het = (k_elem != nullptr);
-  L.k_const = k_const;
-  L.eps_const = beta * std::pow(k_const, sigma);
-  if (L.het) {
-    std::vector<double2> c(L.elems);
-    for (int64_t e = 0; e < L.elems; ++e) {
-      const double k = k_elem[e];
-      if (!(k >= 0) || !std::isfinite(k)) { hh_set_error("k_elem[%lld] = %g invalid", (long long)e, k); return HH_E_CONFIG; }
-      c[e] = make_double2(k, beta * std::pow(k, sigma));
+int64_t launches_per_iteration(const Engine& E) {
+  const int fine = E.spec.dim == 2 ? 2 : (E.spec.nu_pre + 2 + 1 + E.spec.nu_post + 1);
+  return fine + nd_solve_launches(E.plan, E.B) + 3;
+}
+
+hh_status run_iteration(Engine& E) {
+  const bool timing = E.timing;
+  if (!E.gexec || E.graph_timing != timing) {
+    if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }
+    cudaGraph_t g;
+    HH_CUDA_TRY(cudaStreamBeginCapture(E.s, cudaStreamCaptureModeThreadLocal));
+    hh_status st = enqueue_iteration(E, timing);
+    cudaError_t ce = cudaStreamEndCapture(E.s, &g);
+    if (st != HH_OK) return st;
+    HH_CUDA_TRY(ce);
+    HH_CUDA_TRY(cudaGraphInstantiate(&E.gexec, g, 0));
+    cudaGraphDestroy(g);
+    E.graph_timing = timing;
+  }
+  HH_CUDA_TRY(cudaGraphLaunch(E.gexec, E.s));
+  E.launches += launches_per_iteration(E);
+  return HH_OK;
+}
+
+void harvest_timers(Engine& E) {
+  float ms = 0;
+  for (int k = 0; k < T_NT; ++k)
+    if (cudaEventElapsedTime(&ms, E.ev[2 * k], E.ev[2 * k + 1]) == cudaSuccess) E.acc_ms[k] += ms;
+    else cudaGetLastError();
+}
+
+// algorithmic HBM bytes of one iteration per running sample:
+// each kernel reads its inputs and writes its outputs exactly once
+void account_bytes(Engine& E, int running, int j) {
+  const double N = (double)E.N, Nc = (double)E.Nc;
+  const double c = E.LF.het ? 16.0 * (double)E.LF.elems : 0.0;
+  const double pre = 32.0 * N + 16.0 * Nc + c;                 // f, u, r_c (+ coef)
+  const double post = 64.0 * N + 16.0 * Nc + c;                // f, u, e_c, z, w (+ coef)
+  const double coarse = (double)nd_stream_bytes(E.plan) + 32.0 * Nc;
+  const double kry = (2.0 * (j + 1) + 3.0) * 16.0 * N;         // mdot + update
+  E.acc_bytes[T_PRE] += running * pre;
+  E.acc_bytes[T_COARSE] += running * coarse;
+  E.acc_bytes[T_POST] += running * post;
+  E.acc_bytes[T_KRYLOV] += running * kry;
+  E.acc_launch[T_PRE] += 1;
+  E.acc_launch[T_COARSE] += 1;
+  E.acc_launch[T_POST] += 1;
+  E.acc_launch[T_KRYLOV] += 1;
+}
+
+int count_running(Engine& E) {
+  int r = 0;
+  for (int b = 0; b < E.B; ++b) r += (E.h_status[b] == HHK_RUN);
+  return r;
+}
+
+hh_status sync_status(Engine& E) {
+  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.ka.ks.status, E.B * sizeof(int), cudaMemcpyDeviceToHost, E.s));
+  HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  return HH_OK;
+}
+
+// FGMRES(m) for every sample of the batch: b, x are [B] device vectors
+hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
+                      std::vector<SampleOut>& out, double* hist_host) {
+  const int B = E.B;
+  const int m = o.restart;
+  if (m < 1 || m > E.m) { hh_set_error("restart %d not in 1..%d", m, E.m); return HH_E_CONFIG; }
+  if (o.max_iters < 1 || o.max_iters >= E.hist_len || o.fixed_iters >= E.hist_len || o.fixed_iters < 0) {
+    hh_set_error("max_iters/fixed_iters out of range");
+    return HH_E_CONFIG;
+  }
+  cudaStream_t s = E.s;
+  KArgs& A = E.ka;
+  A.rtol = o.rtol;
+  A.max_iters = o.max_iters;
+  A.fixed_iters = o.fixed_iters;
+  if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }   // KArgs captured by value
+  const int check = std::max(1, o.check_every);
+  HH_TRY(vset(xvec, VArg(), E.N, B, 0, 0, nullptr, s));
+  HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
+  HH_TRY(vset(varg(A.V, A.Vbs), bvec, E.N, B, 1, 0, nullptr, s));        // V[0] = b
+  HH_TRY(krylov_norm(A, B, bvec, 0, s));                                  // ||b||, status
+  HH_TRY(sync_status(E));
+  std::vector<int> restarts(B, 0);
+  int running = count_running(E);
+  while (running > 0) {
+    HH_TRY(krylov_advance(E.jdev, 0, s));
+    for (int j = 0; j < m; ++j) {
+      HH_TRY(run_iteration(E));
+      if (E.timing) {
+        HH_CUDA_TRY(cudaStreamSynchronize(s));
+        harvest_timers(E);
+        account_bytes(E, running, j);   // samples that ran this iteration
+        HH_TRY(sync_status(E));
+        running = count_running(E);
+        if (!running) break;
+        continue;
+      }
+      if ((j + 1) % check == 0 || j == m - 1) {
+        HH_TRY(sync_status(E));
+        running = count_running(E);
+        if (!running) break;
+      }
     }
-    HH_TRY(dalloc(&L.coef, L.elems));
-    HH_CUDA_TRY(cudaMemcpy(L.coef, c.data(), L.elems * sizeof(double2), cudaMemcpyHostToDevice));
+    HH_TRY(krylov_cycle_end(A, B, xvec, s));
+    E.launches += 3;
+    HH_TRY(sync_status(E));
+    running = count_running(E);
+    if (!running) break;
+    // restart the still-running samples: V[0] = b - A_0 x
+    for (int b = 0; b < B; ++b) if (E.h_status[b] == HHK_RUN) restarts[b]++;
+    HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
+    HH_TRY(fine_apply(E.LF, B, A.ks.status, HH_OP_A0, xvec, varg(A.V, A.Vbs), bvec, s));
+    HH_TRY(krylov_norm(A, B, varg(A.V, A.Vbs), 1, s));
+    E.launches += 2;
+    HH_TRY(sync_status(E));
+    running = count_running(E);
+  }
+  // true residuals ||b - A_0 x||
+  HH_TRY(fine_apply(E.LF, B, nullptr, HH_OP_A0, xvec, vflat(E.w, E.N), bvec, s));
+  HH_TRY(krylov_norm(A, B, vflat(E.w, E.N), 2, s));
+  E.launches += 2;
+  std::vector<double> bn(B), res(B), rt(B);
+  std::vector<int> its(B), stt(B);
+  HH_CUDA_TRY(cudaMemcpyAsync(bn.data(), A.ks.bnorm, B * 8, cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaMemcpyAsync(res.data(), A.ks.res, B * 8, cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaMemcpyAsync(rt.data(), A.ks.rtrue, B * 8, cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaMemcpyAsync(its.data(), A.ks.its, B * 4, cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaMemcpyAsync(stt.data(), A.ks.status, B * 4, cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaStreamSynchronize(s));
+  out.assign(B, SampleOut());
+  for (int b = 0; b < B; ++b) {
+    SampleOut& r = out[b];
+    r.iterations = its[b];
+    r.restarts = restarts[b];
+    r.rel_res_lsq = bn[b] > 0 ? res[b] / bn[b] : 0.0;
+    r.rel_res_true = bn[b] > 0 ? rt[b] / bn[b] : 0.0;
+    r.rho = its[b] > 0 ? std::pow(r.rel_res_true, 1.0 / its[b]) : NAN;
+    r.converged = o.fixed_iters > 0 ? (r.rel_res_true <= o.rtol) : (stt[b] == HHK_CONVERGED);
+    r.status = stt[b] == HHK_NAN ? HH_E_DIVERGED : (stt[b] == HHK_BREAKDOWN ? HH_E_BREAKDOWN : HH_OK);
+  }
+  if (hist_host && B == 1) {
+    std::vector<double> h(its[0] + 1);
+    HH_CUDA_TRY(cudaMemcpy(h.data(), A.ks.hist, (its[0] + 1) * 8, cudaMemcpyDeviceToHost));
+    h[0] = 1.0;
+    memcpy(hist_host, h.data(), (its[0] + 1) * 8);
   }
   return HH_OK;
 }
 
-hh_status vcycle_impl(hh_problem* p, const cplx* f, const double* fscale, cplx* z, cplx* w) {
-  tmark(p, T_PRE, true);
-  HH_TRY(fine_pre(p->F, p->d.nu_pre, p->d.omega, f, fscale, p->u, p->rc, p->s));
-  tmark(p, T_PRE, false);
-  tmark(p, T_COARSE, true);
-  HH_TRY(nd_solve(p->nd, p->rc, p->ec, p->s));
-  tmark(p, T_COARSE, false);
-  tmark(p, T_POST, true);
-  HH_TRY(fine_post(p->F, p->d.nu_post, p->d.omega, f, fscale, p->u, p->ec, z, w, p->s));
-  tmark(p, T_POST, false);
-  p->launches += 2 + 3 * nd_levels(p->nd);
+// wait for the user stream before work on the engine stream, and vice versa
+hh_status enter(Engine& E, cudaStream_t user) {
+  cudaEvent_t e;
+  HH_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  HH_CUDA_TRY(cudaEventRecord(e, user));
+  HH_CUDA_TRY(cudaStreamWaitEvent(E.s, e, 0));
+  cudaEventDestroy(e);
+  return HH_OK;
+}
+hh_status leave(Engine& E, cudaStream_t user) {
+  cudaEvent_t e;
+  HH_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  HH_CUDA_TRY(cudaEventRecord(e, E.s));
+  HH_CUDA_TRY(cudaStreamWaitEvent(user, e, 0));
+  cudaEventDestroy(e);
   return HH_OK;
 }
 }  // namespace
+
+// ================================================================== ABI
+struct hh_problem {
+  hh_problem_desc d{};
+  Engine E;
+  cudaStream_t user = nullptr;
+};
 
 extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out) {
   if (!d || !out) { hh_set_error("NULL argument"); return HH_E_ARG; }
@@ -185,295 +540,277 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   if (d->k_elem && !d->k_elem_coarse) { hh_set_error("k_elem_coarse required with k_elem"); return HH_E_CONFIG; }
   if (!d->k_elem && !(d->k_const >= 0)) { hh_set_error("k_const must be >= 0"); return HH_E_CONFIG; }
   if (d->max_restart < 1 || d->max_restart > 127) { hh_set_error("max_restart must be in 1..127"); return HH_E_CONFIG; }
-  if (d->beta < 0 || !(d->beta == 0 || d->beta > 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
-  const double t0 = now_s();
-  HH_CUDA_TRY(cudaSetDevice(d->device));
+  if (!(d->beta >= 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
   hh_problem* p = new (std::nothrow) hh_problem();
   if (!p) return HH_E_OOM;
   p->d = *d;
-  p->d.k_elem = nullptr;
-  p->d.k_elem_coarse = nullptr;
-  p->s = (cudaStream_t)d->stream;
-  hh_status st;
-#define CHK(x) do { st = (x); if (st != HH_OK) { hh_destroy_problem(p); return st; } } while (0)
-  CHK(setup_level(p->F, d->dim, d->n_cells, d->k_const, d->k_elem, d->beta, d->sigma));
-  CHK(setup_level(p->C, d->dim, d->n_cells / 2, d->k_const, d->k_elem_coarse, d->beta, d->sigma));
-  p->N = p->F.nodes;
-  p->Nc = p->C.nodes;
-  const int S = d->dim == 2 ? 9 : 27;
-  CHK(dalloc(&p->stencil, p->Nc * S));
-  CHK(coarse_stencil(p->C, p->stencil, p->s));
-  CHK(nd_create(p->C, &p->nd, p->s));
-  {
-    hh_status fs = nd_factor(p->nd, p->stencil, p->s);
-    if (fs == HH_E_SINGULAR) {
-      hh_set_error("zero pivot in the coarse factorisation (k=%g, eps=%g, h=%g)", d->k_const,
-                   p->C.eps_const, p->C.h);
-      hh_destroy_problem(p);
-      return fs;
-    }
-    CHK(fs);
+  p->d.k_elem = p->d.k_elem_coarse = nullptr;
+  p->user = (cudaStream_t)d->stream;
+  hh_status st = engine_init(p->E, d->device);
+  if (st == HH_OK) {
+    BatchSpec sp;
+    sp.dim = d->dim; sp.n = d->n_cells; sp.B = 1; sp.nu_pre = d->nu_pre; sp.nu_post = d->nu_post;
+    sp.m = d->max_restart; sp.omega = d->omega;
+    sp.k = {d->k_const}; sp.beta = {d->beta}; sp.sigma = {d->sigma};
+    sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
+    st = enter(p->E, p->user);
+    if (st == HH_OK) st = batch_setup(p->E, sp);
   }
-  // Krylov workspace
-  p->m = d->max_restart;
-  const int m = p->m;
-  CHK(dalloc(&p->V, (size_t)(m + 1) * p->N));
-  CHK(dalloc(&p->Z, (size_t)m * p->N));
-  CHK(dalloc(&p->w, p->N));
-  CHK(dalloc(&p->u, p->N));
-  CHK(dalloc(&p->bdev, p->N));
-  CHK(dalloc(&p->xdev, p->N));
-  CHK(dalloc(&p->rc, p->Nc));
-  CHK(dalloc(&p->ec, p->Nc));
-  CHK(dalloc(&p->vscale, m + 1));
-  CHK(dalloc(&p->H, (size_t)(m + 1) * m));
-  CHK(dalloc(&p->sn, m));
-  CHK(dalloc(&p->cs, m));
-  CHK(dalloc(&p->g, m + 1));
-  CHK(dalloc(&p->y, m));
-  p->nblk = (int)std::min<int64_t>(148 * 4, (p->N + 255) / 256);
-  CHK(dalloc(&p->cpart, (size_t)p->nblk * (m + 1)));
-  CHK(dalloc(&p->dpart, p->nblk));
-  CHK(dalloc(&p->dscal, 8));
-  CHK(dalloc(&p->flags, 4));
-  CHK(dalloc(&p->counter, 1));
-  p->hist_len = 4096;
-  CHK(dalloc(&p->hist, p->hist_len));
-  if (cudaMemsetAsync(p->counter, 0, sizeof(unsigned), p->s) != cudaSuccess) { hh_destroy_problem(p); return HH_E_CUDA; }
-  if (cudaStreamSynchronize(p->s) != cudaSuccess) {
-    hh_set_error("setup: %s", cudaGetErrorString(cudaGetLastError()));
-    hh_destroy_problem(p);
-    return HH_E_CUDA;
-  }
-#undef CHK
-  p->setup_s = now_s() - t0;
+  if (st != HH_OK) { delete p; return st; }
   *out = p;
   return HH_OK;
 }
 
 extern "C" hh_status hh_layout(const hh_problem* p, int64_t* nf, int64_t* nc) {
   if (!p) { hh_set_error("NULL handle"); return HH_E_ARG; }
-  if (nf) *nf = p->N;
-  if (nc) *nc = p->Nc;
+  if (nf) *nf = p->E.N;
+  if (nc) *nc = p->E.Nc;
   return HH_OK;
 }
 
 extern "C" hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void* y) {
   if (!p || !x || !y) { hh_set_error("NULL argument"); return HH_E_ARG; }
   if (x == y) { hh_set_error("apply_op: x and y must be distinct"); return HH_E_ARG; }
-  if (op == HH_OP_A0 || op == HH_OP_AEPS)
-    return fine_apply(p->F, op, (const cplx*)x, (cplx*)y, nullptr, p->s);
-  if (op == HH_OP_AEPS_COARSE)
-    return fine_apply(p->C, HH_OP_AEPS, (const cplx*)x, (cplx*)y, nullptr, p->s);
-  hh_set_error("apply_op: unknown op %d", op);
-  return HH_E_ARG;
+  Engine& E = p->E;
+  HH_TRY(enter(E, p->user));
+  const VArg xv = varg((cplx*)x, 0), yv = varg((cplx*)y, 0);
+  if (op == HH_OP_A0 || op == HH_OP_AEPS) {
+    HH_TRY(fine_apply(E.LF, 1, nullptr, op, xv, yv, VArg(), E.s));
+  } else if (op == HH_OP_AEPS_COARSE) {
+    HH_TRY(fine_apply(E.LC, 1, nullptr, HH_OP_AEPS, xv, yv, VArg(), E.s));
+  } else {
+    hh_set_error("apply_op: unknown op %d", op);
+    return HH_E_ARG;
+  }
+  return leave(E, p->user);
 }
 
 extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   if (!p || !f || !z) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  return vcycle_impl(p, (const cplx*)f, nullptr, (cplx*)z, nullptr);
+  Engine& E = p->E;
+  HH_TRY(enter(E, p->user));
+  HH_TRY(fine_pre(E.LF, 1, nullptr, E.spec.nu_pre, E.spec.omega, varg((cplx*)f, 0), SArg(),
+                  vflat(E.u, E.N), vflat(E.rc, E.Nc), E.s));
+  HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), vflat(E.rc, E.Nc),
+                  vflat(E.ec, E.Nc), E.s));
+  HH_TRY(fine_post(E.LF, 1, nullptr, E.spec.nu_post, E.spec.omega, varg((cplx*)f, 0), SArg(),
+                   vflat(E.u, E.N), vflat(E.ec, E.Nc), varg((cplx*)z, 0), VArg(), E.s));
+  return leave(E, p->user);
 }
 
 extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
   if (!p || !r || !e) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  return nd_solve(p->nd, (const cplx*)r, (cplx*)e, p->s);
+  Engine& E = p->E;
+  HH_TRY(enter(E, p->user));
+  HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
+                  varg((cplx*)e, 0), E.s));
+  return leave(E, p->user);
+}
+
+static void fill_report(const hh_problem* p, const SampleOut& o, double solve_s, hh_fgmres_report* r) {
+  r->iterations = o.iterations;
+  r->restarts = o.restarts;
+  r->converged = o.converged;
+  r->rel_res_lsq = o.rel_res_lsq;
+  r->rel_res_true = o.rel_res_true;
+  r->rho = o.rho;
+  r->setup_s = p->E.setup_s;
+  r->solve_s = solve_s;
 }
 
 extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, const hh_fgmres_opts* o,
                                      hh_fgmres_report* rep, double* res_hist) {
   if (!p || !bv || !xv || !o || !rep) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  if (o->restart < 1 || o->restart > p->m) { hh_set_error("restart %d not in 1..%d", o->restart, p->m); return HH_E_CONFIG; }
-  if (o->max_iters < 1 || o->max_iters >= p->hist_len || o->fixed_iters >= p->hist_len) { hh_set_error("max_iters out of range"); return HH_E_CONFIG; }
-  const cplx* b = (const cplx*)bv;
-  cplx* x = (cplx*)xv;
-  cudaStream_t s = p->s;
-  const int64_t N = p->N;
-  const int m = o->restart;
-  const int ldh = p->m + 1;
+  Engine& E = p->E;
   memset(rep, 0, sizeof(*rep));
+  HH_TRY(enter(E, p->user));
   cudaEvent_t e0, e1;
   HH_CUDA_TRY(cudaEventCreate(&e0));
   HH_CUDA_TRY(cudaEventCreate(&e1));
-  HH_CUDA_TRY(cudaEventRecord(e0, s));
-  HH_CUDA_TRY(cudaMemsetAsync(p->flags, 0, 4 * sizeof(int), s));
-  HH_CUDA_TRY(cudaMemsetAsync(x, 0, N * sizeof(cplx), s));
-  HH_CUDA_TRY(cudaMemsetAsync(p->H, 0, (size_t)ldh * p->m * sizeof(cplx), s));
-  // ||b||, V[0] = b, vscale[0] = 1/||b||, g[0] = ||b||
-  HH_TRY(krylov_norm(b, N, p->dpart, p->counter, p->dscal + 4, p->vscale, p->g, p->dscal, o->rtol,
-                     p->nblk, s));
-  HH_CUDA_TRY(cudaMemcpyAsync(p->V, b, N * sizeof(cplx), cudaMemcpyDeviceToDevice, s));
-  double bnorm = 0;
-  HH_CUDA_TRY(cudaMemcpyAsync(&bnorm, p->dscal, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HH_CUDA_TRY(cudaStreamSynchronize(s));
-  p->launches += 1;
-  if (bnorm == 0.0) {
-    rep->converged = 1;
-    rep->setup_s = p->setup_s;
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
-    return HH_OK;
-  }
-  int total = 0, restarts = 0;
-  bool done = false;
-  double lsq = 1.0;
-  hh_status result = HH_OK;
-  while (!done) {
-    int j_end = 0;
-    for (int j = 0; j < m; ++j) {
-      cplx* Vj = p->V + (int64_t)j * N;
-      cplx* Zj = p->Z + (int64_t)j * N;
-      HH_TRY(vcycle_impl(p, Vj, p->vscale + j, Zj, p->w));
-      tmark(p, T_KRYLOV, true);
-      HH_TRY(krylov_mdot(p->V, N, j + 1, p->vscale, p->w, p->cpart, p->counter,
-                         p->H + (int64_t)j * ldh, 0, nullptr, p->nblk, s));
-      HH_TRY(krylov_update(p->V, N, j + 1, p->w, p->V + (int64_t)(j + 1) * N, p->dpart, p->counter,
-                           p->H, ldh, p->cs, p->sn, p->g, p->vscale, p->dscal, p->flags, p->hist,
-                           j, total + 1, 1, p->nblk, s));
-      tmark(p, T_KRYLOV, false);
-      p->launches += 2;
-      ++total;
-      j_end = j + 1;
-      int fl[4];
-      HH_CUDA_TRY(cudaMemcpyAsync(fl, p->flags, sizeof(fl), cudaMemcpyDeviceToHost, s));
-      HH_CUDA_TRY(cudaStreamSynchronize(s));
-      if (fl[3]) { hh_set_error("FGMRES: NaN/Inf in the Arnoldi recurrence"); result = HH_E_DIVERGED; done = true; break; }
-      if (o->fixed_iters > 0) {
-        if (total >= o->fixed_iters) { done = true; break; }
-      } else if (fl[1] || total >= o->max_iters) {
-        done = true;
-        break;
-      }
-      if (fl[2]) { done = true; break; }   // happy breakdown
-    }
-    // y = H^{-1} g ; x += Z y
-    HH_TRY(krylov_trisolve(p->H, ldh, p->g, j_end, p->y, s));
-    HH_TRY(krylov_xupdate(p->Z, N, j_end, p->y, x, p->nblk, s));
-    p->launches += 2;
-    double res = 0;
-    HH_CUDA_TRY(cudaMemcpyAsync(&res, p->dscal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
-    HH_CUDA_TRY(cudaStreamSynchronize(s));
-    lsq = res / bnorm;
-    if (done) break;
-    // restart: V[0] = b - A_0 x
-    ++restarts;
-    HH_TRY(fine_apply(p->F, HH_OP_A0, x, p->V, b, s));
-    HH_CUDA_TRY(cudaMemsetAsync(p->H, 0, (size_t)ldh * p->m * sizeof(cplx), s));
-    HH_CUDA_TRY(cudaMemsetAsync(p->flags, 0, 4 * sizeof(int), s));
-    HH_TRY(krylov_norm(p->V, N, p->dpart, p->counter, p->dscal + 1, p->vscale, p->g, nullptr, 0,
-                       p->nblk, s));
-    p->launches += 2;
-    double rn = 0;
-    HH_CUDA_TRY(cudaMemcpyAsync(&rn, p->dscal + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
-    HH_CUDA_TRY(cudaStreamSynchronize(s));
-    lsq = rn / bnorm;
-    if (o->fixed_iters == 0 && rn <= o->rtol * bnorm) done = true;
-  }
-  // true residual ||b - A_0 x|| / ||b||
-  HH_TRY(fine_apply(p->F, HH_OP_A0, x, p->w, b, s));
-  HH_TRY(krylov_norm(p->w, N, p->dpart, p->counter, p->dscal + 5, nullptr, nullptr, nullptr, 0,
-                     p->nblk, s));
-  p->launches += 2;
-  double rt = 0;
-  HH_CUDA_TRY(cudaMemcpyAsync(&rt, p->dscal + 5, sizeof(double), cudaMemcpyDeviceToHost, s));
-  HH_CUDA_TRY(cudaEventRecord(e1, s));
-  HH_CUDA_TRY(cudaStreamSynchronize(s));
+  HH_CUDA_TRY(cudaEventRecord(e0, E.s));
+  std::vector<SampleOut> out;
+  hh_status st = batch_solve(E, varg((cplx*)bv, 0), varg((cplx*)xv, 0), *o, out, res_hist);
+  HH_CUDA_TRY(cudaEventRecord(e1, E.s));
+  HH_CUDA_TRY(cudaEventSynchronize(e1));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  flush_timers(p);
-  rep->iterations = total;
-  rep->restarts = restarts;
-  rep->rel_res_lsq = lsq;
-  rep->rel_res_true = rt / bnorm;
-  rep->converged = o->fixed_iters > 0 ? (rep->rel_res_true <= o->rtol) : (lsq <= o->rtol);
-  rep->rho = total > 0 ? std::pow(rep->rel_res_true, 1.0 / total) : NAN;
-  rep->setup_s = p->setup_s;
-  rep->solve_s = ms * 1e-3;
-  if (res_hist) {
-    std::vector<double> h(total + 1);
-    HH_CUDA_TRY(cudaMemcpy(h.data(), p->hist, (total + 1) * sizeof(double), cudaMemcpyDeviceToHost));
-    h[0] = 1.0;
-    memcpy(res_hist, h.data(), (total + 1) * sizeof(double));
+  if (st != HH_OK) return st;
+  fill_report(p, out[0], ms * 1e-3, rep);
+  HH_TRY(leave(E, p->user));
+  if (out[0].status != HH_OK) {
+    hh_set_error(out[0].status == HH_E_DIVERGED ? "FGMRES: NaN/Inf in the Arnoldi recurrence"
+                                                : "FGMRES: breakdown with residual above tolerance");
+    return (hh_status)out[0].status;
   }
-  return result;
+  return HH_OK;
 }
 
 extern "C" hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, void* x_host,
                                           const hh_fgmres_opts* o, hh_fgmres_report* r) {
   if (!p || !b_host || !x_host) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  HH_CUDA_TRY(cudaMemcpyAsync(p->bdev, b_host, p->N * sizeof(cplx), cudaMemcpyHostToDevice, p->s));
-  HH_TRY(hh_fgmres_solve(p, p->bdev, p->xdev, o, r, nullptr));
-  HH_CUDA_TRY(cudaMemcpyAsync(x_host, p->xdev, p->N * sizeof(cplx), cudaMemcpyDeviceToHost, p->s));
-  HH_CUDA_TRY(cudaStreamSynchronize(p->s));
-  return HH_OK;
-}
-
-extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
-                              const hh_sample* smp, int32_t n, hh_sample_result* out) {
-  if (!common || !o || (!smp && n) || (!out && n)) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  for (int i = 0; i < n; ++i) {
-    hh_problem_desc d = *common;
-    d.dim = 2;
-    d.n_cells = smp[i].n_cells;
-    d.k_const = smp[i].k;
-    d.k_elem = d.k_elem_coarse = nullptr;
-    d.beta = smp[i].beta;
-    d.sigma = smp[i].sigma;
-    if (d.max_restart < o->restart) d.max_restart = o->restart;
-    hh_sample_result& r = out[i];
-    memset(&r, 0, sizeof(r));
-    r.id = smp[i].id;
-    hh_problem* p = nullptr;
-    hh_status st = hh_setup_problem(&d, &p);
-    if (st != HH_OK) { r.status = st; continue; }
-    // unit point source at the centre node (BASELINE configs[1], reading C7)
-    const int64_t nn = d.n_cells + 1;
-    const int64_t ctr = (d.n_cells / 2) + nn * (d.n_cells / 2);
-    const cplx one = cmake(1.0, 0.0);
-    st = HH_OK;
-    if (cudaMemsetAsync(p->bdev, 0, p->N * sizeof(cplx), p->s) != cudaSuccess ||
-        cudaMemcpyAsync(p->bdev + ctr, &one, sizeof(cplx), cudaMemcpyHostToDevice, p->s) != cudaSuccess)
-      st = HH_E_CUDA;
-    hh_fgmres_report rep{};
-    if (st == HH_OK) st = hh_fgmres_solve(p, p->bdev, p->xdev, o, &rep, nullptr);
-    r.status = st;
-    r.iterations = rep.iterations;
-    r.converged = rep.converged;
-    r.rel_res_true = rep.rel_res_true;
-    r.rho = rep.rho;
-    r.setup_s = p->setup_s;
-    r.solve_s = rep.solve_s;
-    hh_destroy_problem(p);
-  }
-  return HH_OK;
+  Engine& E = p->E;
+  HH_TRY(enter(E, p->user));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.bv.p, b_host, E.N * 16, cudaMemcpyHostToDevice, E.s));
+  std::vector<SampleOut> out;
+  const double t0 = now_s();
+  HH_TRY(batch_solve(E, vflat(E.bv, E.N), vflat(E.xv, E.N), *o, out, nullptr));
+  HH_CUDA_TRY(cudaMemcpyAsync(x_host, E.xv.p, E.N * 16, cudaMemcpyDeviceToHost, E.s));
+  HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  fill_report(p, out[0], now_s() - t0, r);
+  return (hh_status)out[0].status;
 }
 
 extern "C" hh_status hh_destroy_problem(hh_problem* p) {
   if (!p) return HH_OK;
-  cudaFree(p->F.coef); cudaFree(p->C.coef); cudaFree(p->stencil);
-  nd_destroy(p->nd);
-  cudaFree(p->V); cudaFree(p->Z); cudaFree(p->w); cudaFree(p->u); cudaFree(p->rc); cudaFree(p->ec);
-  cudaFree(p->bdev); cudaFree(p->xdev); cudaFree(p->vscale); cudaFree(p->H); cudaFree(p->sn);
-  cudaFree(p->g); cudaFree(p->y); cudaFree(p->cpart); cudaFree(p->cs); cudaFree(p->dpart);
-  cudaFree(p->dscal); cudaFree(p->hist); cudaFree(p->flags); cudaFree(p->counter);
-  for (auto e : p->ev) cudaEventDestroy(e);
+  cudaSetDevice(p->E.device);
+  cudaStreamSynchronize(p->E.s);
   delete p;
   return HH_OK;
 }
 
 extern "C" hh_status hh_reset_timers(hh_problem* p, int32_t enable) {
   if (!p) return HH_E_ARG;
-  flush_timers(p);
-  p->timing = enable != 0;
-  for (double& a : p->acc_ms) a = 0;
-  p->launches = 0;
+  p->E.timing = enable != 0;
+  for (int i = 0; i < T_NT; ++i) p->E.acc_ms[i] = p->E.acc_bytes[i] = p->E.acc_launch[i] = 0;
+  p->E.launches = 0;
   return HH_OK;
 }
 
-extern "C" hh_status hh_read_timers(hh_problem* p, double* ms4, int64_t* launches) {
+extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launches) {
   if (!p) return HH_E_ARG;
-  flush_timers(p);
-  if (ms4) for (int i = 0; i < T_NT; ++i) ms4[i] = p->acc_ms[i];
-  if (launches) *launches = p->launches;
+  if (st12)
+    for (int i = 0; i < T_NT; ++i) {
+      st12[i] = p->E.acc_ms[i];
+      st12[4 + i] = p->E.acc_bytes[i];
+      st12[8 + i] = p->E.acc_launch[i];
+    }
+  if (launches) *launches = p->E.launches;
+  return HH_OK;
+}
+
+// ================================================================== sweep
+static std::mutex g_sweep_mu;
+static bool g_sweep_timing = false;
+static double g_sweep_st[3 * T_NT] = {0};
+static int64_t g_sweep_launches = 0;
+
+extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_sweep_mu);
+  if (st12)
+    for (int i = 0; i < 3 * T_NT; ++i) st12[i] = g_sweep_st[i];
+  if (launches) *launches = g_sweep_launches;
+  if (reset_enable >= 0) {
+    g_sweep_timing = reset_enable != 0;
+    for (double& a : g_sweep_st) a = 0;
+    g_sweep_launches = 0;
+  }
+  return HH_OK;
+}
+
+extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                              const hh_sample* smp, int32_t n, hh_sample_result* out) {
+  if (!common || !o || (n && (!smp || !out))) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  if (n == 0) return HH_OK;
+  const int m = std::max(o->restart, common->max_restart > 0 ? std::min(common->max_restart, 127) : o->restart);
+  for (int i = 0; i < n; ++i) {
+    memset(&out[i], 0, sizeof(out[i]));
+    out[i].id = smp[i].id;
+    if (smp[i].n_cells < 4 || smp[i].n_cells % 2 || !(smp[i].k >= 0) || !(smp[i].beta >= 0)) {
+      hh_set_error("sweep sample %lld: invalid (n=%d, k=%g, beta=%g)", (long long)smp[i].id,
+                   smp[i].n_cells, smp[i].k, smp[i].beta);
+      return HH_E_CONFIG;
+    }
+  }
+  HH_CUDA_TRY(cudaSetDevice(common->device));
+  // group by grid size; batches bounded by a per-engine memory budget
+  std::map<int, std::vector<int>> groups;
+  for (int i = 0; i < n; ++i) groups[smp[i].n_cells].push_back(i);
+  const char* es = getenv("HH_SWEEP_STREAMS");
+  const int nstreams = std::max(1, es ? atoi(es) : 4);
+  const char* eb = getenv("HH_SWEEP_MAX_BATCH");
+  const int maxB = std::max(1, eb ? atoi(eb) : 256);
+  size_t freeb = 0, totb = 0;
+  HH_CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+  const double budget = 0.75 * (double)freeb / nstreams;
+  std::vector<std::vector<int>> batches;
+  for (auto& kv : groups) {
+    NDPlan* plan = nullptr;
+    HH_TRY(get_plan(2, kv.first / 2 + 1, &plan));
+    const int64_t per = per_sample_bytes(2, kv.first, m, plan);
+    const int bmax = (int)std::max<int64_t>(1, std::min<int64_t>(maxB, (int64_t)(budget / per)));
+    const int cnt = (int)kv.second.size();
+    const int nb = (cnt + bmax - 1) / bmax;
+    for (int k = 0; k < nb; ++k) {
+      std::vector<int> bt;
+      for (int i = k * cnt / nb; i < (k + 1) * cnt / nb; ++i) bt.push_back(kv.second[i]);
+      batches.push_back(bt);
+    }
+  }
+  // largest work first
+  std::sort(batches.begin(), batches.end(), [&](const std::vector<int>& a, const std::vector<int>& b) {
+    return (int64_t)smp[a[0]].n_cells * smp[a[0]].n_cells * a.size() >
+           (int64_t)smp[b[0]].n_cells * smp[b[0]].n_cells * b.size();
+  });
+  std::atomic<int> next(0);
+  std::atomic<int> failed(0);
+  std::string err;
+  std::mutex err_mu;
+  const bool timing = g_sweep_timing;
+  auto worker = [&]() {
+    Engine E;
+    if (engine_init(E, common->device) != HH_OK) { failed = 1; return; }
+    E.timing = timing;
+    for (;;) {
+      const int bi = next.fetch_add(1);
+      if (bi >= (int)batches.size() || failed) break;
+      const std::vector<int>& bt = batches[bi];
+      BatchSpec sp;
+      sp.dim = 2; sp.n = smp[bt[0]].n_cells; sp.B = (int)bt.size();
+      sp.nu_pre = common->nu_pre; sp.nu_post = common->nu_post; sp.omega = common->omega; sp.m = m;
+      for (int i : bt) { sp.k.push_back(smp[i].k); sp.beta.push_back(smp[i].beta); sp.sigma.push_back(smp[i].sigma); }
+      hh_status st = batch_setup(E, sp);
+      std::vector<SampleOut> res;
+      double t_solve = 0;
+      if (st == HH_OK) {
+        const int half = sp.n / 2;
+        const int64_t ctr = half + (int64_t)(sp.n + 1) * half;   // unit point source at the centre (C7)
+        st = vset(vflat(E.bv, E.N), VArg(), E.N, sp.B, 2, ctr, nullptr, E.s);
+        const double t0 = now_s();
+        if (st == HH_OK) st = batch_solve(E, vflat(E.bv, E.N), vflat(E.xv, E.N), *o, res, nullptr);
+        t_solve = now_s() - t0;
+      }
+      if (st != HH_OK) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err = hh_last_error();
+        for (int i : bt) out[i].status = st;
+        if (st != HH_E_SINGULAR) failed = 1;
+        continue;
+      }
+      for (size_t k = 0; k < bt.size(); ++k) {
+        hh_sample_result& r = out[bt[k]];
+        r.status = res[k].status;
+        r.iterations = res[k].iterations;
+        r.converged = res[k].converged;
+        r.rel_res_true = res[k].rel_res_true;
+        r.rho = res[k].rho;
+        r.setup_s = E.setup_s;
+        r.solve_s = t_solve;
+      }
+    }
+    std::lock_guard<std::mutex> lk(g_sweep_mu);
+    for (int t = 0; t < T_NT; ++t) {
+      g_sweep_st[t] += E.acc_ms[t];
+      g_sweep_st[4 + t] += E.acc_bytes[t];
+      g_sweep_st[8 + t] += E.acc_launch[t];
+    }
+    g_sweep_launches += E.launches;
+  };
+  const int nt = std::min<int>(nstreams, (int)batches.size());
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) th.emplace_back(worker);
+  for (auto& t : th) t.join();
+  if (failed) { hh_set_error("%s", err.c_str()); return HH_E_CUDA; }
   return HH_OK;
 }

@@ -1,4 +1,10 @@
 // Internal declarations of the B200 hot path (not part of the ABI).
+//
+// Everything is BATCHED: a batch holds B problems that share the grid (dim, n)
+// and differ in coefficients (k, beta, sigma, or a full k_e field).  A single
+// problem is a batch of one.  Sample b of a batch is blockIdx.z (stencil
+// kernels) / blockIdx.y (Krylov kernels) / a flattened index (ND kernels).
+// Per-sample status (0 = running) masks finished samples out of every launch.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -16,10 +22,6 @@ __host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
-// conj(a) * b
-__host__ __device__ __forceinline__ cplx cconjmul(cplx a, cplx b) {
-  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
-}
 // acc += a * b
 __host__ __device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
@@ -53,8 +55,36 @@ void hh_set_error(const char* fmt, ...);
     if (_s != HH_OK) return _s;        \
   } while (0)
 
-// ---------------------------------------------------------------- level data
-// Per-level (fine or coarse) geometry and element coefficients.
+// ---------------------------------------------------------------- batched refs
+// Vector argument: sample b, Krylov slot (*j + jo) -> p + b*bs + (*j+jo)*vs
+struct VArg {
+  cplx* p = nullptr;
+  int64_t bs = 0, vs = 0;
+  const int* j = nullptr;
+  int jo = 0;
+  __device__ __forceinline__ cplx* at(int b) const {
+    return p + (int64_t)b * bs + (j ? (int64_t)(__ldg(j) + jo) * vs : 0);
+  }
+};
+// Scalar argument (e.g. vscale[j]) -> p[b*bs + *j + jo], or 1 if p == NULL
+struct SArg {
+  const double* p = nullptr;
+  int64_t bs = 0;
+  const int* j = nullptr;
+  int jo = 0;
+  __device__ __forceinline__ double at(int b) const {
+    return p ? p[(int64_t)b * bs + (j ? __ldg(j) + jo : 0)] : 1.0;
+  }
+};
+inline VArg varg(cplx* p, int64_t bs, int64_t vs = 0, const int* j = nullptr, int jo = 0) {
+  VArg a; a.p = p; a.bs = bs; a.vs = vs; a.j = j; a.jo = jo; return a;
+}
+inline SArg sarg(const double* p, int64_t bs, const int* j = nullptr, int jo = 0) {
+  SArg a; a.p = p; a.bs = bs; a.j = j; a.jo = jo; return a;
+}
+
+// ---------------------------------------------------------------- levels
+// Geometry + coefficients of one level for a batch of B samples.
 struct Level {
   int dim = 2;
   int n = 0;            // cells per side
@@ -62,55 +92,32 @@ struct Level {
   int64_t elems = 0;    // n^dim
   double h = 0;
   bool het = false;
-  double k_const = 0, eps_const = 0;
-  double2* coef = nullptr;   // het: per element (k_e, eps_e), device
+  const double2* coef = nullptr;   // het: [B][elems] (k_e, eps_e)
+  const double2* kc = nullptr;     // constant: [B] (k, eps)
+  cplx* tmp = nullptr;             // 3D only: [B][2][nodes] scratch owned by the engine
 };
 
-// ---------------------------------------------------------------- fine-level kernels
-struct FineArgs {
-  int n; double h; double omega;
-  bool het; double k; double eps;      // constant-k case
-  const double2* coef;                 // het: (k_e, eps_e) per element
-};
-
-// y = A x  (op: 0 -> A_0, 1 -> A_eps).  If sub_from != NULL: y = sub_from - A x.
-hh_status fine_apply(const Level& L, int op, const cplx* x, cplx* y, const cplx* sub_from,
+// fine-level kernels (fine2d.cu / fine3d.cu); st: per-sample status (NULL = all run)
+hh_status fine_apply(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                      cudaStream_t s);
-// Pre-smoothing + restriction (fused): u = S^nu (from 0) applied to f*fscale; rc = I^T (f - A_eps u)
-hh_status fine_pre(const Level& L, int nu, double omega, const cplx* f, const double* fscale,
-                   cplx* u, cplx* rc, cudaStream_t s);
-// Prolongation + correction + post-smoothing (+ optional w = A_0 z)
-hh_status fine_post(const Level& L, int nu, double omega, const cplx* f, const double* fscale,
-                    const cplx* u, const cplx* ec, cplx* z, cplx* w, cudaStream_t s);
-// Coarse stencil assembly: st[node*3^d + o] = A_eps^{(1)} entries
-hh_status coarse_stencil(const Level& C, cplx* st, cudaStream_t s);
+hh_status fine_pre(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
+                   VArg u, VArg rc, cudaStream_t s);
+hh_status fine_post(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
+                    VArg u, VArg ec, VArg z, VArg w, cudaStream_t s);
+hh_status coarse_stencil(const Level& C, int B, cplx* st, cudaStream_t s);
 
 // ---------------------------------------------------------------- coarse ND solver
-struct NDFactor;
-hh_status nd_create(const Level& C, NDFactor** out, cudaStream_t s);
-hh_status nd_factor(NDFactor* f, const cplx* stencil, cudaStream_t s);
-hh_status nd_solve(NDFactor* f, const cplx* rhs, cplx* x, cudaStream_t s);
-void nd_destroy(NDFactor* f);
-int64_t nd_factor_bytes(const NDFactor* f);   // bytes streamed per solve (X, H, L blocks)
-int nd_levels(const NDFactor* f);
-
-// ---------------------------------------------------------------- krylov
-struct KrylovWS {
-  int64_t N = 0; int m = 0;
-  cplx* V = nullptr;     // (m+1) x N  (stored unnormalised; vscale[i] scales V[i])
-  cplx* Z = nullptr;     // m x N
-  cplx* w = nullptr;     // N
-  cplx* u = nullptr;     // N (pre-smoothed iterate)
-  cplx* rc = nullptr;    // coarse rhs
-  cplx* ec = nullptr;    // coarse solution
-  // device scalars
-  double* vscale = nullptr;   // m+1
-  cplx* H = nullptr;          // (m+1) x m, column-major H[i + (m+1) j]
-  double* cs = nullptr;       // m
-  cplx* sn = nullptr;         // m
-  cplx* g = nullptr;          // m+1
-  cplx* y = nullptr;          // m
-  cplx* partial = nullptr;    // nblk x (m+2)
-  double* dscal = nullptr;    // misc device scalars [0]=bnorm, [1]=|g_{j+1}|, [2]=flag ...
-  int nblk = 0;
-};
+struct NDPlan;                       // host+device tree data for one (dim, m); shareable
+hh_status nd_plan_create(int dim, int m, NDPlan** out);
+void nd_plan_destroy(NDPlan* p);
+int64_t nd_front_entries(const NDPlan* p);        // complex entries per sample
+int64_t nd_stream_bytes(const NDPlan* p);         // bytes streamed per solve per sample
+int nd_levels(const NDPlan* p);
+int nd_solve_launches(const NDPlan* p, int B);      // kernel launches of one nd_solve
+int64_t nd_work_entries(const NDPlan* p);         // zs + out entries per sample
+int64_t nd_cbuf_entries(const NDPlan* p);         // pivot column buffer per sample
+// F: [B][front_entries]; stencil: [B][Nc*3^d]; work: [B][work]; cbuf: [B][cbuf]
+hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* cbuf, int* flag,
+                    cudaStream_t s);
+hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
+                   VArg x, cudaStream_t s);

@@ -1,15 +1,19 @@
-// FGMRES Arnoldi kernels (flexible right-preconditioned GMRES).
+// FGMRES Arnoldi kernels, batched over samples (flexible
+// right-preconditioned GMRES; Saad 1993).
 //
 // Classical Gram-Schmidt in two batched passes (reading C11: one multi-dot
 // pass h = V_j^H w, one update pass w' = w - V_j h with ||w'||^2 fused),
-// complex Givens rotations and the convergence test |g_{j+1}| <= rtol ||b||
-// (C13) evaluated on the device by the last CTA of each pass (last-block-done
-// pattern: deterministic, no extra launch, no host round trip).
+// complex Givens rotations c = |a|/t, s = (a/|a|) conj(b)/t and the convergence
+// test |g_{j+1}| <= rtol ||b|| (C13), all evaluated on the device by the last
+// CTA of each sample (last-block-done: deterministic, no extra launch, no host
+// round trip).  The Arnoldi index j lives in device memory so one captured
+// iteration replays for every j.
 //
 // V[i] is stored UNNORMALISED; vscale[i] = 1 / ||V[i]|| is applied by every
 // consumer (the V-cycle reads f = vscale[j] V[j]), which saves a full
 // read+write pass per iteration.
 #include "hh_internal.cuh"
+#include "krylov.cuh"
 
 namespace {
 constexpr int KT = 256;     // threads per CTA
@@ -44,226 +48,265 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return amLast;
 }
 
-// h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..nv-1 -> H column (Hcol)
-// If accumulate: Hcol[i] += h_i (re-orthogonalisation pass), else Hcol[i] = h_i.
-__global__ void __launch_bounds__(KT) k_mdot(const cplx* __restrict__ V, int64_t N, int nv,
-                                             const double* __restrict__ vscale,
-                                             const cplx* __restrict__ w, cplx* __restrict__ part,
-                                             unsigned* counter, cplx* __restrict__ Hcol,
-                                             int accumulate, const int* __restrict__ stop) {
-  if (stop && *stop) return;
-  __shared__ cplx sh[KT / 32];
+// h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..j -> H column j
+__global__ void __launch_bounds__(KT) k_mdot(KArgs A) {
+  const int b = blockIdx.y;
+  if (A.ks.status[b]) return;
+  const int j = *A.jdev;
+  const int nv = j + 1;
+  const int64_t N = A.N;
+  const cplx* V = A.V + (int64_t)b * A.Vbs;
+  const cplx* w = A.w + (int64_t)b * N;
+  cplx* part = A.cpart + ((int64_t)b * gridDim.x + blockIdx.x) * A.ldp;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
-  for (int g0 = 0; g0 < nv; g0 += VG) {
-    cplx acc[VG];
-#pragma unroll
-    for (int q = 0; q < VG; ++q) acc[q] = cmake(0, 0);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += KT) {
-      const cplx wi = w[i];
-#pragma unroll
-      for (int q = 0; q < VG; ++q)
-        if (g0 + q < nv) {
-          const cplx v = V[(int64_t)(g0 + q) * N + i];
-          acc[q].x += v.x * wi.x + v.y * wi.y;
-          acc[q].y += v.x * wi.y - v.y * wi.x;
-        }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp-per-vector: warp w streams V[q] for q = w, w+8, ... over this CTA's chunk
+  // (w is re-read from L1); no CTA barrier, 4 independent loads in flight per lane
+  for (int q = warp; q < nv; q += KT / 32) {
+    const cplx* vq = V + (int64_t)q * N;
+    cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
+    int64_t i = lo + lane;
+    for (; i + 96 < hi; i += 128) {
+      const cplx v0 = __ldg(&vq[i]), v1 = __ldg(&vq[i + 32]), v2 = __ldg(&vq[i + 64]),
+                 v3 = __ldg(&vq[i + 96]);
+      const cplx w0 = w[i], w1 = w[i + 32], w2 = w[i + 64], w3 = w[i + 96];
+      a0.x = fma(v0.x, w0.x, fma(v0.y, w0.y, a0.x)); a0.y = fma(v0.x, w0.y, fma(-v0.y, w0.x, a0.y));
+      a1.x = fma(v1.x, w1.x, fma(v1.y, w1.y, a1.x)); a1.y = fma(v1.x, w1.y, fma(-v1.y, w1.x, a1.y));
+      a0.x = fma(v2.x, w2.x, fma(v2.y, w2.y, a0.x)); a0.y = fma(v2.x, w2.y, fma(-v2.y, w2.x, a0.y));
+      a1.x = fma(v3.x, w3.x, fma(v3.y, w3.y, a1.x)); a1.y = fma(v3.x, w3.y, fma(-v3.y, w3.x, a1.y));
     }
-#pragma unroll
-    for (int q = 0; q < VG; ++q) {
-      if (g0 + q >= nv) break;
-      const cplx r = block_sum(acc[q], sh);
-      if (threadIdx.x == 0) part[(int64_t)blockIdx.x * nv + g0 + q] = r;
+    for (; i < hi; i += 32) {
+      const cplx v0 = __ldg(&vq[i]), w0 = w[i];
+      a0.x = fma(v0.x, w0.x, fma(v0.y, w0.y, a0.x)); a0.y = fma(v0.x, w0.y, fma(-v0.y, w0.x, a0.y));
     }
+    cplx acc = cadd(a0, a1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) part[q] = acc;
   }
-  if (last_block(counter)) {
+  if (last_block(A.counter + b)) {
+    cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+    const cplx* P0 = A.cpart + (int64_t)b * gridDim.x * A.ldp;
     for (int q = threadIdx.x; q < nv; q += KT) {
       cplx s = cmake(0, 0);
-      for (int b = 0; b < (int)gridDim.x; ++b) s = cadd(s, part[(int64_t)b * nv + q]);
-      s = cscale(s, vscale[q]);
-      Hcol[q] = accumulate ? cadd(Hcol[q], s) : s;
+      for (int k = 0; k < (int)gridDim.x; ++k) s = cadd(s, P0[(int64_t)k * A.ldp + q]);
+      Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
     }
-    if (threadIdx.x == 0) *counter = 0u;
+    if (threadIdx.x == 0) A.counter[b] = 0u;
   }
 }
 
-struct GivensState {
-  cplx* H; int ldh;          // (m+1) x m column-major
-  double* cs; cplx* sn; cplx* g;
-  double* vscale;
-  double* dscal;             // [0] bnorm, [1] |g_{j+1}|, [2] rtol*bnorm
-  int* flags;                // [0] stop, [1] converged, [2] breakdown, [3] nan
-  double* hist;              // per-iteration |g_{j+1}|/bnorm (device, indexed by total iteration)
-};
-
-// w' = w - sum_i (H_i vscale_i) V_i  -> Vout ; partial ||w'||^2 ; last block:
-// h_{j+1,j} = ||w'||, vscale_{j+1}, Givens on column j, convergence flags.
-__global__ void __launch_bounds__(KT) k_update(const cplx* __restrict__ V, int64_t N, int nv,
-                                               const cplx* __restrict__ w, cplx* __restrict__ Vout,
-                                               double* __restrict__ part, unsigned* counter,
-                                               GivensState gs, int j, int total_it, int finalize) {
-  if (gs.flags[0]) return;
+// w' = w - sum_i (H_i vscale_i) V_i -> V[j+1] ; ||w'||^2 ; last block:
+// h_{j+1,j} = ||w'||, vscale_{j+1}, Givens on column j, status.
+__global__ void __launch_bounds__(KT) k_update(KArgs A) {
+  const int b = blockIdx.y;
+  if (A.ks.status[b]) return;
   __shared__ cplx cf[128];
   __shared__ cplx sh[KT / 32];
-  cplx* Hcol = gs.H + (int64_t)j * gs.ldh;
-  for (int q = threadIdx.x; q < nv; q += KT) cf[q] = cscale(Hcol[q], gs.vscale[q]);
+  const int j = *A.jdev;
+  const int nv = j + 1;
+  const int64_t N = A.N;
+  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+  const double* vs = A.vscale + (int64_t)b * A.ldv;
+  for (int q = threadIdx.x; q < nv; q += KT) cf[q] = cscale(Hcol[q], vs[q]);
   __syncthreads();
+  const cplx* V = A.V + (int64_t)b * A.Vbs;
+  const cplx* w = A.w + (int64_t)b * N;
+  cplx* Vout = A.V + (int64_t)b * A.Vbs + (int64_t)(j + 1) * N;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
   double nrm = 0.0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += KT) {
-    cplx a = w[i];
-    for (int q = 0; q < nv; ++q) cfms(a, cf[q], V[(int64_t)q * N + i]);
+    cplx a = w[i], a2 = cmake(0, 0);
+    int q = 0;
+    for (; q + 8 <= nv; q += 8) {   // 8 independent loads in flight
+      cplx v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = __ldg(&V[(int64_t)(q + t) * N + i]);
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        cfms(a, cf[q + t], v[t]);
+        cfms(a2, cf[q + t + 1], v[t + 1]);
+      }
+    }
+    for (; q < nv; ++q) cfms(a, cf[q], __ldg(&V[(int64_t)q * N + i]));
+    a = cadd(a, a2);
     Vout[i] = a;
     nrm += a.x * a.x + a.y * a.y;
   }
   const cplx r = block_sum(cmake(nrm, 0), sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = r.x;
-  if (!last_block(counter)) return;
+  double* dpart = A.dpart + (int64_t)b * gridDim.x;
+  if (threadIdx.x == 0) dpart[blockIdx.x] = r.x;
+  if (!last_block(A.counter + b)) return;
   if (threadIdx.x != 0) return;
-  double s = 0;
-  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b];
-  *counter = 0u;
-  const double hn = sqrt(s);
-  if (!finalize) {             // first pass of CGS2: only record the norm
-    gs.dscal[3] = hn;
-    return;
-  }
-  // Givens on column j
+  double ssum = 0;
+  for (int k = 0; k < (int)gridDim.x; ++k) ssum += dpart[k];
+  A.counter[b] = 0u;
+  const double hn = sqrt(ssum);
+  double* vsw = A.vscale + (int64_t)b * A.ldv;
+  double* cs = A.cs + (int64_t)b * A.ldv;
+  cplx* sn = A.sn + (int64_t)b * A.ldv;
+  cplx* g = A.g + (int64_t)b * A.ldv;
   Hcol[j + 1] = cmake(hn, 0);
-  gs.vscale[j + 1] = hn > 0 ? 1.0 / hn : 0.0;
-  for (int i = 0; i < j; ++i) {
-    const cplx hi = Hcol[i], hi1 = Hcol[i + 1];
-    const double c = gs.cs[i];
-    const cplx sn = gs.sn[i];
-    cplx a = cscale(hi, c);
-    cfma(a, sn, hi1);
-    cplx b = cscale(hi1, c);
-    cfms(b, cmake(sn.x, -sn.y), hi);
+  vsw[j + 1] = hn > 0 ? 1.0 / hn : 0.0;
+  for (int i = 0; i < j; ++i) {       // previous rotations on column j
+    const cplx hi0 = Hcol[i], hi1 = Hcol[i + 1];
+    const double c = cs[i];
+    const cplx s = sn[i];
+    cplx a = cscale(hi0, c);
+    cfma(a, s, hi1);
+    cplx bb = cscale(hi1, c);
+    cfms(bb, cmake(s.x, -s.y), hi0);
     Hcol[i] = a;
-    Hcol[i + 1] = b;
+    Hcol[i + 1] = bb;
   }
-  const cplx a = Hcol[j], b = Hcol[j + 1];
+  const cplx a = Hcol[j], bq = Hcol[j + 1];
   double c;
-  cplx sn;
-  const double aa = sqrt(cabs2(a)), bb = sqrt(cabs2(b));
-  if (bb == 0.0) { c = 1.0; sn = cmake(0, 0); }
-  else if (aa == 0.0) { c = 0.0; sn = cmake(1, 0); }
+  cplx s;
+  const double aa = sqrt(cabs2(a)), bb = sqrt(cabs2(bq));
+  if (bb == 0.0) { c = 1.0; s = cmake(0, 0); }
+  else if (aa == 0.0) { c = 0.0; s = cmake(1, 0); }
   else {
     const double t = sqrt(aa * aa + bb * bb);
     c = aa / t;
-    sn = cscale(cmul(cscale(a, 1.0 / aa), cmake(b.x, -b.y)), 1.0 / t);
+    s = cscale(cmul(cscale(a, 1.0 / aa), cmake(bq.x, -bq.y)), 1.0 / t);
   }
-  gs.cs[j] = c;
-  gs.sn[j] = sn;
+  cs[j] = c;
+  sn[j] = s;
   cplx r0 = cscale(a, c);
-  cfma(r0, sn, b);
+  cfma(r0, s, bq);
   Hcol[j] = r0;
   Hcol[j + 1] = cmake(0, 0);
-  const cplx gj = gs.g[j];
-  cplx gj1 = cmul(cmake(-sn.x, sn.y), gj);   // -conj(s) g_j
-  gs.g[j + 1] = gj1;
-  gs.g[j] = cscale(gj, c);
+  const cplx gj = g[j];
+  const cplx gj1 = cmul(cmake(-s.x, s.y), gj);   // -conj(s) g_j
+  g[j + 1] = gj1;
+  g[j] = cscale(gj, c);
   const double res = sqrt(cabs2(gj1));
-  gs.dscal[1] = res;
-  gs.hist[total_it] = res / gs.dscal[0];
-  if (!(res == res) || !(hn == hn) || isinf(hn)) { gs.flags[3] = 1; gs.flags[0] = 1; }
-  if (res <= gs.dscal[2]) gs.flags[1] = 1;
-  if (hn == 0.0) gs.flags[2] = 1;
+  const int its = A.ks.its[b] + 1;
+  A.ks.its[b] = its;
+  A.ks.jend[b] = j + 1;
+  A.ks.res[b] = res;
+  const double bn = A.ks.bnorm[b];
+  if (its < A.hist_len) A.ks.hist[(int64_t)b * A.hist_len + its] = res / bn;
+  int stt = 0;
+  if (!(res == res) || !(hn == hn) || isinf(hn)) stt = HHK_NAN;
+  else if (A.fixed_iters > 0) { if (its >= A.fixed_iters) stt = HHK_FIXED; }
+  else if (res <= A.rtol * bn) stt = HHK_CONVERGED;
+  else if (its >= A.max_iters) stt = HHK_MAXIT;
+  if (stt == 0 && hn == 0.0) stt = (res <= A.rtol * bn) ? HHK_CONVERGED : HHK_BREAKDOWN;
+  A.ks.status[b] = stt;
 }
 
-// y = H^{-1} g (upper triangular k x k), one warp, column-oriented back substitution
-__global__ void k_trisolve(const cplx* __restrict__ H, int ldh, const cplx* __restrict__ g, int k,
-                           cplx* __restrict__ y) {
+__global__ void k_advance(int* jdev, int v) { *jdev = (v < 0) ? *jdev + 1 : v; }
+
+// y = H^{-1} g (upper triangular jend x jend), one warp per sample; x += Z y
+__global__ void k_trisolve(KArgs A) {
+  const int b = blockIdx.x;
+  const int k = A.ks.jend[b];
+  if (k <= 0) return;
   __shared__ cplx rhs[128];
+  const cplx* H = A.H + (int64_t)b * A.HB;
+  const cplx* g = A.g + (int64_t)b * A.ldv;
+  cplx* y = A.y + (int64_t)b * A.ldv;
   for (int i = threadIdx.x; i < k; i += 32) rhs[i] = g[i];
   __syncwarp();
   for (int i = k - 1; i >= 0; --i) {
-    const cplx yi = cmul(rhs[i], cinv(H[i + (int64_t)i * ldh]));
+    const cplx yi = cmul(rhs[i], cinv(H[i + (int64_t)i * A.ldh]));
     __syncwarp();
-    for (int r = threadIdx.x; r < i; r += 32) cfms(rhs[r], H[r + (int64_t)i * ldh], yi);
+    for (int r = threadIdx.x; r < i; r += 32) cfms(rhs[r], H[r + (int64_t)i * A.ldh], yi);
     if (threadIdx.x == 0) y[i] = yi;
     __syncwarp();
   }
 }
 
-// x += sum_i y_i Z_i
-__global__ void __launch_bounds__(KT) k_xupdate(const cplx* __restrict__ Z, int64_t N, int k,
-                                                const cplx* __restrict__ y, cplx* __restrict__ x) {
+__global__ void __launch_bounds__(KT) k_xupdate(KArgs A, VArg xv) {
+  const int b = blockIdx.y;
+  const int k = A.ks.jend[b];
+  if (k <= 0) return;
   __shared__ cplx ys[128];
-  for (int q = threadIdx.x; q < k; q += KT) ys[q] = y[q];
+  for (int q = threadIdx.x; q < k; q += KT) ys[q] = A.y[(int64_t)b * A.ldv + q];
   __syncthreads();
+  const int64_t N = A.N;
+  const cplx* Z = A.Z + (int64_t)b * A.Zbs;
+  cplx* x = xv.at(b);
   for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < N; i += (int64_t)gridDim.x * KT) {
     cplx a = x[i];
-    for (int q = 0; q < k; ++q) cfma(a, ys[q], Z[(int64_t)q * N + i]);
+    for (int q = 0; q < k; ++q) cfma(a, ys[q], __ldg(&Z[(int64_t)q * N + i]));
     x[i] = a;
   }
 }
 
-// ||r||^2 -> out_norm (sqrt) ; last block also initialises the Arnoldi state
-// for a new cycle: vscale[0] = 1/||r||, g[0] = ||r||; if set_bnorm: bnorm.
-__global__ void __launch_bounds__(KT) k_norm(const cplx* __restrict__ r, int64_t N,
-                                             double* __restrict__ part, unsigned* counter,
-                                             double* __restrict__ out_norm, double* vscale0,
-                                             cplx* g0, double* bnorm, double rtol) {
+// per-sample ||r||; mode 0: start (bnorm, V0 scale, g0); 1: restart; 2: true residual
+__global__ void __launch_bounds__(KT) k_norm(KArgs A, VArg rv, int mode) {
+  const int b = blockIdx.y;
+  if (mode == 1 && A.ks.status[b]) return;
   __shared__ cplx sh[KT / 32];
+  const cplx* r = rv.at(b);
   double nrm = 0;
-  for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < N; i += (int64_t)gridDim.x * KT) {
+  for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < A.N; i += (int64_t)gridDim.x * KT) {
     const cplx a = r[i];
     nrm += a.x * a.x + a.y * a.y;
   }
   const cplx s = block_sum(cmake(nrm, 0), sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = s.x;
-  if (!last_block(counter)) return;
+  double* dpart = A.dpart + (int64_t)b * gridDim.x;
+  if (threadIdx.x == 0) dpart[blockIdx.x] = s.x;
+  if (!last_block(A.counter + b)) return;
   if (threadIdx.x) return;
   double t = 0;
-  for (int b = 0; b < (int)gridDim.x; ++b) t += part[b];
-  *counter = 0u;
+  for (int k = 0; k < (int)gridDim.x; ++k) t += dpart[k];
+  A.counter[b] = 0u;
   const double nr = sqrt(t);
-  *out_norm = nr;
-  if (vscale0) *vscale0 = nr > 0 ? 1.0 / nr : 0.0;
-  if (g0) *g0 = cmake(nr, 0);
-  if (bnorm) { bnorm[0] = nr; bnorm[2] = rtol * nr; }
+  if (mode == 2) { A.ks.rtrue[b] = nr; return; }
+  A.vscale[(int64_t)b * A.ldv] = nr > 0 ? 1.0 / nr : 0.0;
+  A.g[(int64_t)b * A.ldv] = cmake(nr, 0);
+  A.ks.res[b] = nr;
+  if (mode == 0) {
+    A.ks.bnorm[b] = nr;
+    A.ks.its[b] = 0;
+    A.ks.jend[b] = 0;
+    if (A.hist_len > 0) A.ks.hist[(int64_t)b * A.hist_len] = 1.0;
+    A.ks.status[b] = (nr == 0.0) ? HHK_CONVERGED : 0;
+  } else if (A.fixed_iters == 0 && nr <= A.rtol * A.ks.bnorm[b]) {
+    A.ks.status[b] = HHK_CONVERGED;
+  }
+}
+
+__global__ void k_clear_jend(KArgs A, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) A.ks.jend[b] = 0;
 }
 
 }  // namespace
 
 // ================================================================ host side
-hh_status krylov_mdot(const cplx* V, int64_t N, int nv, const double* vscale, const cplx* w,
-                      cplx* part, unsigned* counter, cplx* Hcol, int accumulate, const int* stop,
-                      int nblk, cudaStream_t s) {
-  k_mdot<<<nblk, KT, 0, s>>>(V, N, nv, vscale, w, part, counter, Hcol, accumulate, stop);
+hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
+  k_mdot<<<dim3(A.nblk, B), KT, 0, s>>>(A);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-
-hh_status krylov_update(const cplx* V, int64_t N, int nv, const cplx* w, cplx* Vout, double* part,
-                        unsigned* counter, cplx* H, int ldh, double* cs, cplx* sn, cplx* g,
-                        double* vscale, double* dscal, int* flags, double* hist, int j,
-                        int total_it, int finalize, int nblk, cudaStream_t s) {
-  GivensState gs{H, ldh, cs, sn, g, vscale, dscal, flags, hist};
-  k_update<<<nblk, KT, 0, s>>>(V, N, nv, w, Vout, part, counter, gs, j, total_it, finalize);
+hh_status krylov_update(const KArgs& A, int B, cudaStream_t s) {
+  k_update<<<dim3(A.nblk, B), KT, 0, s>>>(A);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-
-hh_status krylov_trisolve(const cplx* H, int ldh, const cplx* g, int k, cplx* y, cudaStream_t s) {
-  k_trisolve<<<1, 32, 0, s>>>(H, ldh, g, k, y);
+hh_status krylov_advance(int* jdev, int v, cudaStream_t s) {
+  k_advance<<<1, 1, 0, s>>>(jdev, v);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-
-hh_status krylov_xupdate(const cplx* Z, int64_t N, int k, const cplx* y, cplx* x, int nblk,
-                         cudaStream_t s) {
-  k_xupdate<<<nblk, KT, 0, s>>>(Z, N, k, y, x);
+hh_status krylov_cycle_end(const KArgs& A, int B, VArg x, cudaStream_t s) {
+  k_trisolve<<<B, 32, 0, s>>>(A);
+  k_xupdate<<<dim3(A.nblk, B), KT, 0, s>>>(A, x);
+  k_clear_jend<<<(B + 127) / 128, 128, 0, s>>>(A, B);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-
-hh_status krylov_norm(const cplx* r, int64_t N, double* part, unsigned* counter, double* out,
-                      double* vscale0, cplx* g0, double* bnorm, double rtol, int nblk,
-                      cudaStream_t s) {
-  k_norm<<<nblk, KT, 0, s>>>(r, N, part, counter, out, vscale0, g0, bnorm, rtol);
+hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s) {
+  k_norm<<<dim3(A.nblk, B), KT, 0, s>>>(A, r, mode);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

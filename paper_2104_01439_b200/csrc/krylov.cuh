@@ -1,0 +1,39 @@
+// Batched FGMRES state and kernel launchers (krylov.cu).
+#pragma once
+#include "hh_internal.cuh"
+
+enum { HHK_RUN = 0, HHK_CONVERGED = 1, HHK_MAXIT = 2, HHK_BREAKDOWN = 3, HHK_NAN = 4, HHK_FIXED = 5 };
+
+struct KState {              // per-sample device arrays, [B] each (hist: [B][hist_len])
+  double* bnorm = nullptr;   // ||b||
+  double* res = nullptr;     // |g_{j+1}| (least-squares residual)
+  double* rtrue = nullptr;   // ||b - A_0 x|| at exit
+  int* status = nullptr;     // HHK_*
+  int* its = nullptr;        // preconditioner applications so far
+  int* jend = nullptr;       // Arnoldi steps of the current cycle
+  double* hist = nullptr;    // |g_{j+1}| / ||b|| per iteration
+};
+
+struct KArgs {
+  int64_t N = 0;
+  cplx* V = nullptr; int64_t Vbs = 0;   // [B][m+1][N]
+  cplx* Z = nullptr; int64_t Zbs = 0;   // [B][m][N]
+  cplx* w = nullptr;                    // [B][N]
+  cplx* H = nullptr; int64_t HB = 0; int ldh = 0;   // [B][m][ldh] column-major
+  double* vscale = nullptr; double* cs = nullptr; cplx* sn = nullptr; cplx* g = nullptr;
+  cplx* y = nullptr; int ldv = 0;       // [B][ldv]
+  cplx* cpart = nullptr; int ldp = 0;   // [B][nblk][ldp]
+  double* dpart = nullptr;              // [B][nblk]
+  unsigned* counter = nullptr;          // [B]
+  const int* jdev = nullptr;
+  int nblk = 1;
+  double rtol = 1e-6;
+  int max_iters = 500, fixed_iters = 0, hist_len = 0;
+  KState ks;
+};
+
+hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s);
+hh_status krylov_update(const KArgs& A, int B, cudaStream_t s);
+hh_status krylov_advance(int* jdev, int v, cudaStream_t s);    // v < 0: ++j, else j = v
+hh_status krylov_cycle_end(const KArgs& A, int B, VArg x, cudaStream_t s);
+hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s);

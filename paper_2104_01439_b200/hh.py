@@ -24,7 +24,8 @@ STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_C
 
 EXPORTS = ["hh_setup_problem", "hh_layout", "hh_apply_op", "hh_vcycle", "hh_coarse_solve",
            "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep", "hh_destroy_problem",
-           "hh_reset_timers", "hh_read_timers", "hh_last_error", "hh_version"]
+           "hh_reset_timers", "hh_read_timers", "hh_sweep_timers", "hh_last_error",
+           "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -87,6 +88,7 @@ def _load():
         "hh_destroy_problem": [vp],
         "hh_reset_timers": [vp, i32],
         "hh_read_timers": [vp, dp, C.POINTER(C.c_int64)],
+        "hh_sweep_timers": [i32, dp, C.POINTER(C.c_int64)],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -206,11 +208,10 @@ class Problem:
         _check(lib.hh_reset_timers(self.handle, int(enable)))
 
     def read_timers(self):
-        ms = (C.c_double * 4)()
+        st = (C.c_double * 12)()
         nl = C.c_int64()
-        _check(lib.hh_read_timers(self.handle, ms, C.byref(nl)))
-        return {"pre_ms": ms[0], "coarse_ms": ms[1], "post_ms": ms[2], "krylov_ms": ms[3],
-                "launches": nl.value}
+        _check(lib.hh_read_timers(self.handle, st, C.byref(nl)))
+        return _phase_dict(st, nl.value)
 
     def close(self):
         if self.handle:
@@ -238,6 +239,23 @@ def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_rest
     out = (SampleResult * n)()
     _check(lib.hh_sweep(C.byref(d), C.byref(o), arr, n, out))
     return [r.as_dict() for r in out]
+
+
+PHASES = ("pre", "coarse", "post", "krylov")
+
+
+def _phase_dict(st, launches):
+    d = {"launches": launches}
+    for i, ph in enumerate(PHASES):
+        d[ph] = {"ms": st[i], "bytes": st[4 + i], "launches": st[8 + i]}
+    return d
+
+
+def sweep_timers(reset_enable=-1):
+    st = (C.c_double * 12)()
+    nl = C.c_int64()
+    _check(lib.hh_sweep_timers(reset_enable, st, C.byref(nl)))
+    return _phase_dict(st, nl.value)
 
 
 def version():
