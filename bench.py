@@ -95,8 +95,25 @@ class Clocks:
 
 
 def rank_samples(rank, world):
+    """This rank's fixed share of the sweep: residue class `rank` of the sample id
+    mod 8 (per-GPU work is constant in N; N = 8 covers all 3,520 samples)."""
+    if world > SHARD:
+        raise ValueError(f"the sweep shards over at most {SHARD} ranks")
     all_s = sweep_samples()
     return [s for s in all_s if s["id"] % SHARD == rank % SHARD]
+
+
+def combine_ranks(dev_ms, dofs, its, world, device):
+    """Max over ranks of the device time, sum over ranks of the work (the
+    only collective of the bench; none on the data path)."""
+    t = torch.tensor([dev_ms, float(dofs), float(its)], dtype=torch.float64, device=device)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        return tmax[0].item(), tsum[1].item(), tsum[2].item()
+    return dev_ms, float(dofs), float(its)
 
 
 # ------------------------------------------------------------------ ours
@@ -180,12 +197,7 @@ def run_ours(args, rank, world, dev):
     else:
         timers["on"] = False
         tm = timers["acc"]
-    # max over ranks of time, sum of work
-    t = torch.tensor([dev_ms, float(tot_dofs), float(tot_its)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone(); dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        dev_ms, tot_dofs, tot_its = tmax[0].item(), tsum[1].item(), tsum[2].item()
+    dev_ms, tot_dofs, tot_its = combine_ranks(dev_ms, tot_dofs, tot_its, world, dev)
     value = tot_dofs / (dev_ms * 1e-3)
     out = {"value": value, "ms_per_step": dev_ms / args.steps, "wl": wl, "timers": tm,
            "clocks": clocks, "iterations_total": int(tot_its)}

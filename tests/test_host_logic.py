@@ -1,0 +1,65 @@
+"""Host-side logic of the multi-GPU sweep (no GPU): sample sharding and the
+max-time / sum-work reduction, run as world_size-2 gloo process groups."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bench
+from workloads import sweep_samples
+
+
+def test_residue_shards_partition_the_sweep():
+    allids = {s["id"] for s in sweep_samples()}
+    seen = []
+    for r in range(8):
+        seen += [s["id"] for s in bench.rank_samples(r, 8)]
+    assert sorted(seen) == sorted(allids) and len(seen) == 3520
+    sizes = [len(bench.rank_samples(r, 8)) for r in range(8)]
+    assert sizes == [440] * 8                       # weak scaling: fixed work per rank
+    with pytest.raises(ValueError):
+        bench.rank_samples(0, 9)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = bench.rank_samples(rank, world)
+    ms = 100.0 + 50.0 * rank
+    dofs = sum((s["n"] + 1) ** 2 for s in mine)
+    t, d, i = bench.combine_ranks(ms, dofs, len(mine), world, torch.device("cpu"))
+    ids = [None] * world
+    dist.all_gather_object(ids, [s["id"] for s in mine])
+    q.put((rank, t, d, i, ids))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_reduction():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_dofs = sum((s["n"] + 1) ** 2 for r in range(world) for s in bench.rank_samples(r, world))
+    for rank, t, d, i, ids in out:
+        assert t == 150.0                       # max over ranks
+        assert d == want_dofs and i == 880      # sum over ranks
+        assert not set(ids[0]) & set(ids[1])    # disjoint shards
