@@ -23,11 +23,14 @@
 //    triangular LDL^T solve; every launch is fully parallel.
 // The tree (NDPlan) depends only on (dim, m) and is shared by all samples.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <cooperative_groups.h>
 #include "hh_internal.cuh"
+namespace cg = cooperative_groups;
 
 namespace {
 constexpr int NB = 16;      // pivot block of the partial Gauss-Jordan sweep
@@ -52,6 +55,10 @@ struct LevelInfo {
   int64_t ea_list_off[2];            // offsets into eaList
 };
 }  // namespace
+
+// Solve schedule: levels <= sub_cut run as one-CTA subtree walks, levels
+// (sub_cut, split] as per-level kernels, levels > split inside one cluster kernel.
+struct SolveCfg { int sub_cut, split; };
 
 struct NDPlan {
   int dim = 2, m = 0;            // coarse grid nodes per side
@@ -78,8 +85,13 @@ struct NDPlan {
   std::vector<int> sub_maxf;
   int* d_sub_ptr = nullptr;
   int* d_sub_list = nullptr;
+  // per-level entry ranges + entry -> front maps (cluster solve)
+  std::vector<double> level_bytes;   // factor bytes streamed per level per sample
+  int* d_sep_front = nullptr;
+  int* d_halo_front = nullptr;
+  int64_t* d_lvr = nullptr;          // [nlev][4]: sep begin/end, halo begin/end
   std::mutex cut_mu;
-  std::vector<std::pair<int, int>> cut_cache;   // (B, L)
+  std::vector<std::pair<int, SolveCfg>> cfg_cache;   // (B, schedule) chosen by nd_autotune
 };
 
 // ============================================================ device kernels
@@ -296,14 +308,42 @@ __device__ __forceinline__ void front_gather(const SolveArgs& A, const FrontMeta
   }
 }
 
+// two rows at once (independent load streams: latency hiding for short rows)
+__device__ __forceinline__ void row_dot2(const cplx* __restrict__ ra, const cplx* __restrict__ rb,
+                                         const cplx* v, int len, int lane, cplx& oa, cplx& ob) {
+  cplx a0 = cmake(0, 0), a1 = cmake(0, 0), b0 = cmake(0, 0), b1 = cmake(0, 0);
+  int c = lane;
+  for (; c + 32 < len; c += 64) {
+    const cplx x0 = __ldg(&ra[c]), x1 = __ldg(&ra[c + 32]), y0 = __ldg(&rb[c]), y1 = __ldg(&rb[c + 32]);
+    const cplx v0 = v[c], v1 = v[c + 32];
+    cfma(a0, x0, v0);
+    cfma(a1, x1, v1);
+    cfma(b0, y0, v0);
+    cfma(b1, y1, v1);
+  }
+  if (c < len) {
+    const cplx v0 = v[c];
+    cfma(a0, __ldg(&ra[c]), v0);
+    cfma(b0, __ldg(&rb[c]), v0);
+  }
+  oa = warp_sum(cadd(a0, a1));
+  ob = warp_sum(cadd(b0, b1));
+}
+
 // forward rows b = r0.. (step) : out[b] = F[s+b][0:s] . z
 __device__ __forceinline__ void front_fwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
                                                const cplx* z, int r0, int step, int lane) {
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
   cplx* out = A.work + (int64_t)bs * A.WE + A.zsE + m.outOff;
-  for (int b = r0; b < m.u; b += step) {
-    const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, z, m.s, lane);
-    if (lane == 0) out[b] = acc;
+  for (int b = r0; b < m.u; b += 2 * step) {
+    if (b + step < m.u) {
+      cplx o1, o2;
+      row_dot2(F + (int64_t)(m.s + b) * m.f, F + (int64_t)(m.s + b + step) * m.f, z, m.s, lane, o1, o2);
+      if (lane == 0) { out[b] = o1; out[b + step] = o2; }
+    } else {
+      const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, z, m.s, lane);
+      if (lane == 0) out[b] = acc;
+    }
   }
 }
 
@@ -312,9 +352,15 @@ __device__ __forceinline__ void front_bwd_rows(const SolveArgs& A, const FrontMe
                                                const cplx* v, int r0, int step, int lane) {
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
   cplx* x = A.x.at(bs);
-  for (int a = r0; a < m.s; a += step) {
-    const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
-    if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+  for (int a = r0; a < m.s; a += 2 * step) {
+    if (a + step < m.s) {
+      cplx o1, o2;
+      row_dot2(F + (int64_t)a * m.f, F + (int64_t)(a + step) * m.f, v, m.f, lane, o1, o2);
+      if (lane == 0) { x[A.sep[m.sepOff + a]] = o1; x[A.sep[m.sepOff + a + step]] = o2; }
+    } else {
+      const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
+      if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+    }
   }
 }
 
@@ -383,6 +429,77 @@ __global__ void __launch_bounds__(256) k_nd_bwd(SolveArgs A, int begin) {
       for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
       acc = cadd(acc, warp_sum(acc2));
       if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------ cluster solve
+// One thread-block cluster (CL CTAs on CL SMs) per sample walks the tree levels
+// [L0, nlev): forward (gather, contribution GEMVs) up to the root, then backward
+// down to L0, with a cluster barrier between phases.  Operands go through
+// L2/global memory; the barrier (release/acquire at cluster scope, preceded by a
+// device fence) orders them.  This replaces ~3 launches per level.
+__device__ __forceinline__ void cl_sync(cg::cluster_group& cl) {
+  __threadfence();
+  cl.sync();
+}
+
+__global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* __restrict__ lvr,
+                                                    int L0, int nlev, int fwd, int bwd,
+                                                    const int* __restrict__ sep_front,
+                                                    const int* __restrict__ halo_front) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int b = blockIdx.x / CL;
+  if (A.st && A.st[b]) return;              // uniform over the cluster
+  const int rank = (int)cl.block_rank();
+  const int tid = rank * blockDim.x + threadIdx.x, nth = CL * blockDim.x;
+  const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nth >> 5;
+  cplx* zs = A.work + (int64_t)b * A.WE;
+  cplx* out = zs + A.zsE;
+  const cplx* r = A.rhs.at(b);
+  cplx* x = A.x.at(b);
+  const cplx* Fb = A.F + (int64_t)b * A.FE;
+  if (fwd) {
+    for (int L = L0; L < nlev; ++L) {
+      const int64_t sb = lvr[4 * L], se = lvr[4 * L + 1], hb = lvr[4 * L + 2], he = lvr[4 * L + 3];
+      for (int64_t e = sb + tid; e < se; e += nth) {        // gather z_s
+        cplx v = __ldg(&r[A.sep[e]]);
+        const int64_t p0 = A.gptr[e], p1 = A.gptr[e + 1];
+        for (int64_t p = p0; p < p1; ++p) {
+          const cplx c = out[A.gidx[p]];
+          v.x += c.x;
+          v.y += c.y;
+        }
+        zs[e] = v;
+      }
+      cl_sync(cl);
+      if (he > hb) {
+        for (int64_t hrow = hb + gw; hrow < he; hrow += nw) {   // contribution rows
+          const FrontMeta m = A.fr[halo_front[hrow]];
+          const int brow = (int)(hrow - m.haloOff);
+          const cplx acc = row_dot(Fb + m.Foff + (int64_t)(m.s + brow) * m.f, zs + m.zsOff, m.s, lane);
+          if (lane == 0) out[hrow] = acc;
+        }
+        cl_sync(cl);
+      }
+    }
+  }
+  if (bwd) {
+    for (int L = nlev - 1; L >= L0; --L) {
+      const int64_t sb = lvr[4 * L], se = lvr[4 * L + 1];
+      for (int64_t e = sb + gw; e < se; e += nw) {
+        const FrontMeta m = A.fr[sep_front[e]];
+        const int a = (int)(e - m.sepOff);
+        const cplx* row = Fb + m.Foff + (int64_t)a * m.f;
+        cplx acc = row_dot(row, zs + m.zsOff, m.s, lane);
+        cplx acc2 = cmake(0, 0);
+        const int* hl = A.halo + m.haloOff;
+        for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
+        acc = cadd(acc, warp_sum(acc2));
+        if (lane == 0) x[A.sep[e]] = acc;
+      }
+      if (L > L0) cl_sync(cl);
     }
   }
 }
@@ -692,6 +809,26 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
       nd->sub_maxf.push_back(maxf);
     }
   }
+  // per-level ranges and entry -> front maps for the cluster solve
+  std::vector<int> sep_front(sepAll.size()), halo_front(haloAll.size());
+  std::vector<int64_t> lvr(4 * nlev);
+  for (int i = 0; i < nf; ++i) {
+    const FrontMeta& fm = nd->fronts[i];
+    for (int a = 0; a < fm.s; ++a) sep_front[fm.sepOff + a] = i;
+    for (int b = 0; b < fm.u; ++b) halo_front[fm.haloOff + b] = i;
+  }
+  nd->level_bytes.assign(nlev, 0.0);
+  for (int L = 0; L < nlev; ++L) {
+    const LevelInfo& li = nd->levels[L];
+    const FrontMeta& f0 = nd->fronts[li.begin];
+    const FrontMeta& fl = nd->fronts[li.begin + li.count - 1];
+    lvr[4 * L] = f0.sepOff;
+    lvr[4 * L + 1] = fl.sepOff + fl.s;
+    lvr[4 * L + 2] = f0.haloOff;
+    lvr[4 * L + 3] = fl.haloOff + fl.u;
+    for (int t = li.begin; t < li.begin + li.count; ++t)
+      nd->level_bytes[L] += 16.0 * ((double)nd->fronts[t].s * nd->fronts[t].f + (double)nd->fronts[t].u * nd->fronts[t].s);
+  }
   auto up = [&](auto** dptr, const auto& vec) -> hh_status {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
     const size_t bytes = std::max<size_t>(1, vec.size()) * sizeof(T);
@@ -715,6 +852,9 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   if (st == HH_OK) st = up(&nd->d_Coff, Coff);
   if (st == HH_OK) st = up(&nd->d_sub_ptr, sptr_all);
   if (st == HH_OK) st = up(&nd->d_sub_list, slist_all);
+  if (st == HH_OK) st = up(&nd->d_sep_front, sep_front);
+  if (st == HH_OK) st = up(&nd->d_halo_front, halo_front);
+  if (st == HH_OK) st = up(&nd->d_lvr, lvr);
   if (st != HH_OK) { nd_plan_destroy(nd); return st; }
   *out = nd;
   return HH_OK;
@@ -725,6 +865,7 @@ void nd_plan_destroy(NDPlan* nd) {
   cudaFree(nd->d_fronts); cudaFree(nd->d_sep); cudaFree(nd->d_halo); cudaFree(nd->d_asm);
   cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gptr); cudaFree(nd->d_gidx);
   cudaFree(nd->d_Coff); cudaFree(nd->d_sub_ptr); cudaFree(nd->d_sub_list);
+  cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_lvr);
   delete nd;
 }
 
@@ -769,48 +910,43 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
   return HH_OK;
 }
 
-// cut level for a batch of B samples: levels <= L run as one-CTA subtrees, the rest per level
-static int choose_cut(NDPlan* nd, int B) {
-  if (const char* e = getenv("HH_ND_CUT")) {   // experiment override: -1 = per-level only
-    const int c = atoi(e);
-    return std::min<int>(c, (int)nd->levels.size() - 1);
-  }
-  {
-    std::lock_guard<std::mutex> lk(nd->cut_mu);
-    for (auto& c : nd->cut_cache) if (c.first == B) return c.second;
-  }
-  const int nlev = (int)nd->levels.size();
-  const double launch_us = 10.0;   // measured per-level kernel (fwd or bwd) on small fronts
-  const int slots = 148 * 4;
-  int best = -1;
-  double best_t = 2.0 * nlev * launch_us;
-  for (int L = 0; L < nlev; ++L) {
-    if (nd->sub_maxf[L] > 1024) break;
-    const int64_t ctas = (int64_t)nd->sub_cnt[L] * B;
-    const double waves = std::ceil((double)ctas / slots);
-    const double t = 2.0 * (launch_us + nd->sub_cost_us[L] * waves) + 2.0 * (nlev - 1 - L) * launch_us;
-    if (t < best_t) { best_t = t; best = L; }
-  }
+constexpr int CLUSTER = 8;   // CTAs per sample in the cluster solve (portable cluster size)
+
+static bool cached_cfg(NDPlan* nd, int B, SolveCfg* c) {
   std::lock_guard<std::mutex> lk(nd->cut_mu);
-  nd->cut_cache.push_back({B, best});
-  return best;
+  for (auto& e : nd->cfg_cache)
+    if (e.first == B) { *c = e.second; return true; }
+  return false;
 }
 
-hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s) {
-  NDPlan* nd = const_cast<NDPlan*>(ndc);
+static SolveCfg get_cfg(NDPlan* nd, int B) {
+  SolveCfg c{-1, (int)nd->levels.size() - 1};
+  if (const char* e = getenv("HH_ND_SPLIT")) c.split = std::min<int>(atoi(e), c.split);
+  if (const char* e = getenv("HH_ND_CUT")) c.sub_cut = std::min<int>(atoi(e), c.split);
+  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT")) return c;
+  SolveCfg cc;
+  if (cached_cfg(nd, B, &cc)) return cc;
+  return c;
+}
+
+static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
+                           VArg x, cudaStream_t s, SolveCfg c) {
   const int nlev = (int)nd->levels.size();
   SolveArgs A;
   A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo;
   A.gptr = nd->d_gptr; A.gidx = nd->d_gidx; A.F = F; A.FE = nd->F_entries;
   A.work = work; A.WE = nd_work_entries(nd); A.zsE = nd->zs_entries; A.rhs = rhs; A.x = x;
-  const int cut = choose_cut(nd, B);
+  const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
+    if (sm > 48 * 1024) {
+      HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
     k_nd_fwd_sub<<<dim3(nd->sub_cnt[cut], B), 256, sm, s>>>(A, nd->d_sub_ptr + nd->sub_off[cut],
                                                             nd->d_sub_list + nd->list_off[cut]);
   }
-  for (int L = cut + 1; L < nlev; ++L) {
+  for (int L = cut + 1; L <= Lb; ++L) {
     const LevelInfo& li = nd->levels[L];
     if (li.max_s > VMAX) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_s + 255) / 256)), B);
@@ -818,14 +954,30 @@ hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx*
     }
     const size_t sm = (size_t)std::min(li.max_s, VMAX) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dim3 g(li.count, std::max(1, std::min(1024, (li.max_u + 7) / 8)), B);
+    dim3 g(li.count, std::max(1, std::min(1024, (li.max_u + 31) / 32)), B);
     k_nd_fwd<<<g, 256, sm, s>>>(A, li.begin);
   }
-  for (int L = nlev - 1; L > cut; --L) {
+  if (Lb < nlev - 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CLUSTER * B);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HH_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_nd_cluster, A, (const int64_t*)nd->d_lvr, Lb + 1, nlev, 1,
+                                   1, (const int*)nd->d_sep_front, (const int*)nd->d_halo_front));
+  }
+  for (int L = Lb; L > cut; --L) {
     const LevelInfo& li = nd->levels[L];
     const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dim3 g(li.count, std::max(1, std::min(1024, (li.max_s + 7) / 8)), B);
+    dim3 g(li.count, std::max(1, std::min(1024, (li.max_s + 31) / 32)), B);
     k_nd_bwd<<<g, 256, sm, s>>>(A, li.begin);
   }
   if (cut >= 0) {
@@ -837,10 +989,68 @@ hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx*
   return HH_OK;
 }
 
+hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
+                   VArg x, cudaStream_t s) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B));
+}
+
+// Empirical schedule choice on the real factor (called once per (tree, B) at
+// setup, outside graph capture): time the candidate schedules with CUDA events.
+hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
+                      cudaStream_t s) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  SolveCfg have;
+  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, B, &have)) return HH_OK;
+  const int nlev = (int)nd->levels.size();
+  cudaEvent_t e0, e1;
+  HH_CUDA_TRY(cudaEventCreate(&e0));
+  HH_CUDA_TRY(cudaEventCreate(&e1));
+  auto run = [&](SolveCfg c, float* ms) -> hh_status {
+    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c));   // warm
+    HH_CUDA_TRY(cudaEventRecord(e0, s));
+    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c));
+    HH_CUDA_TRY(cudaEventRecord(e1, s));
+    HH_CUDA_TRY(cudaEventSynchronize(e1));
+    HH_CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    return HH_OK;
+  };
+  SolveCfg best{-1, nlev - 1};
+  float best_ms = 1e30f;
+  for (int cut = -1; cut <= std::min(3, nlev - 1); ++cut) {        // stage 1: bottom subtrees
+    if (cut >= 0 && nd->sub_maxf[cut] > 1024) break;
+    SolveCfg c{cut, nlev - 1};
+    float ms;
+    HH_TRY(run(c, &ms));
+    if (getenv("HH_DEBUG") && atoi(getenv("HH_DEBUG")) > 1)
+      fprintf(stderr, "[hh]   m=%d B=%d cut=%d split=%d: %.1f us\n", nd->m, B, c.sub_cut, c.split, 1e3 * ms / 3);
+    if (ms < best_ms) { best_ms = ms; best = c; }
+  }
+  for (int top = 1; top <= 8; top += (top < 2 ? 1 : 2)) {          // stage 2: cluster top levels
+    const int split = nlev - 1 - top;
+    if (split < best.sub_cut) break;
+    SolveCfg c{best.sub_cut, split};
+    float ms;
+    HH_TRY(run(c, &ms));
+    if (getenv("HH_DEBUG") && atoi(getenv("HH_DEBUG")) > 1)
+      fprintf(stderr, "[hh]   m=%d B=%d cut=%d split=%d: %.1f us\n", nd->m, B, c.sub_cut, c.split, 1e3 * ms / 3);
+    if (ms < best_ms) { best_ms = ms; best = c; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::lock_guard<std::mutex> lk(nd->cut_mu);
+  nd->cfg_cache.push_back({B, best});
+  if (getenv("HH_DEBUG"))
+    fprintf(stderr, "[hh] nd_autotune m=%d dim=%d B=%d levels=%d -> sub_cut=%d split=%d (%.1f us/solve)\n",
+            nd->m, nd->dim, B, nlev, best.sub_cut, best.split, 1e3 * best_ms / 3);
+  return HH_OK;
+}
+
 int nd_solve_launches(const NDPlan* ndc, int B) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
-  const int cut = choose_cut(nd, B);
-  int n = (cut >= 0 ? 2 : 0) + 2 * ((int)nd->levels.size() - 1 - cut);
-  for (int L = cut + 1; L < (int)nd->levels.size(); ++L) n += nd->levels[L].max_s > VMAX;
+  const int nlev = (int)nd->levels.size();
+  const SolveCfg c = get_cfg(nd, B);
+  int n = (c.sub_cut >= 0 ? 2 : 0) + 2 * (c.split - c.sub_cut) + (c.split < nlev - 1 ? 1 : 0);
+  for (int L = c.sub_cut + 1; L <= c.split; ++L) n += nd->levels[L].max_s > VMAX;
   return n;
 }

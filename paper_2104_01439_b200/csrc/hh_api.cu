@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <thread>
@@ -147,6 +148,7 @@ struct Engine {
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
       cpart, dpart, hist;
   int* h_status = nullptr;   // pinned
+  int h_cap = 0;
   // batch
   BatchSpec spec;
   Level LF, LC;
@@ -158,8 +160,15 @@ struct Engine {
   int* nd_flag = nullptr;
   double setup_s = 0;
   // graph of one iteration
-  cudaGraphExec_t gexec = nullptr;
-  bool graph_timing = false;
+  cudaGraphExec_t gexec = nullptr;     // plain iteration
+  cudaGraphExec_t gexec_t = nullptr;   // iteration with phase events
+  int64_t iter_counter = 0;
+  int timing_every = 1;                // sample one iteration in timing_every
+  void drop_graphs() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (gexec_t) cudaGraphExecDestroy(gexec_t);
+    gexec = gexec_t = nullptr;
+  }
   // timers
   bool timing = false;
   cudaEvent_t ev[2 * T_NT] = {};
@@ -170,7 +179,7 @@ struct Engine {
   int64_t launches_per_iter = 0;
 
   ~Engine() {
-    if (gexec) cudaGraphExecDestroy(gexec);
+    drop_graphs();
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
                    &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist};
     for (Pool* p : all) p->release();
@@ -200,20 +209,25 @@ int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {
   return b;
 }
 
-hh_status batch_setup(Engine& E, const BatchSpec& sp) {
-  const double t0 = now_s();
-  HH_CUDA_TRY(cudaSetDevice(E.device));
-  if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }
-  E.spec = sp;
+constexpr int HIST_LEN = 4096;
+
+size_t ksmall_bytes(int B, int m) {
+  const size_t ldv = m + 1, ldh = m + 1;
+  auto r = [](size_t b) { return (b + 255) / 256 * 256; };
+  return r(B * ldv * 8) * 2 + r(B * ldv * 16) * 3 + r((size_t)B * m * ldh * 16) + r(B * 8) * 3 +
+         r(B * 4) * 3 + r(16) + r(B * 4) * 2;
+}
+
+// Grow the engine's pools to hold batch `sp` (no-op when already large enough).
+// cudaMalloc/cudaFree synchronise the device, so the sweep reserves every
+// engine for its largest batch before any worker starts.
+hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   const int B = sp.B, dim = sp.dim, n = sp.n, m = sp.m;
-  E.B = B; E.m = m;
-  E.N = ipow(n + 1, dim);
-  E.Nc = ipow(n / 2 + 1, dim);
-  const int64_t N = E.N, Nc = E.Nc;
-  HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
-  const NDPlan* P = E.plan;
+  const int64_t N = ipow(n + 1, dim), Nc = ipow(n / 2 + 1, dim);
+  NDPlan* P = nullptr;
+  HH_TRY(get_plan(dim, n / 2 + 1, &P));
   const int S = dim == 2 ? 9 : 27;
-  // pools
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (N + 255) / 256));
   HH_TRY(E.V.ensure((size_t)B * (m + 1) * N * 16));
   HH_TRY(E.Z.ensure((size_t)B * m * N * 16));
   HH_TRY(E.w.ensure((size_t)B * N * 16));
@@ -229,6 +243,33 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
   HH_TRY(E.kcf.ensure((size_t)B * 16));
   HH_TRY(E.kcc.ensure((size_t)B * 16));
+  HH_TRY(E.cpart.ensure((size_t)B * nblk * (m + 2) * 16));
+  HH_TRY(E.dpart.ensure((size_t)B * nblk * 8));
+  HH_TRY(E.hist.ensure((size_t)B * HIST_LEN * 8));
+  HH_TRY(E.ksmall.ensure(ksmall_bytes(B, m)));
+  if (E.h_cap < B) {
+    if (E.h_status) cudaFreeHost(E.h_status);
+    E.h_status = nullptr;
+    HH_CUDA_TRY(cudaMallocHost(&E.h_status, std::max(B, 4) * sizeof(int)));
+    E.h_cap = std::max(B, 4);
+  }
+  return HH_OK;
+}
+
+hh_status batch_setup(Engine& E, const BatchSpec& sp) {
+  const double t0 = now_s();
+  HH_CUDA_TRY(cudaSetDevice(E.device));
+  E.drop_graphs();
+  E.spec = sp;
+  const int B = sp.B, dim = sp.dim, n = sp.n, m = sp.m;
+  E.B = B; E.m = m;
+  E.N = ipow(n + 1, dim);
+  E.Nc = ipow(n / 2 + 1, dim);
+  const int64_t N = E.N, Nc = E.Nc;
+  HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
+  const NDPlan* P = E.plan;
+  // pools
+  HH_TRY(reserve_pools(E, sp));
   // per-level coefficients
   for (int lev = 0; lev < 2; ++lev) {
     Level& L = lev == 0 ? E.LF : E.LC;
@@ -272,9 +313,10 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   // Krylov CTAs per sample: enough for ONE sample to fill the GPU (the tail of a
   // batch is a single slow sample); independent of B, so batched == single results
   E.nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (N + 255) / 256));
-  E.hist_len = 4096;
+  E.hist_len = HIST_LEN;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  // (ksmall_bytes() below must mirror this layout)
   const size_t o_vs = carve(B * ldv * 8), o_cs = carve(B * ldv * 8), o_sn = carve(B * ldv * 16),
                o_g = carve(B * ldv * 16), o_y = carve(B * ldv * 16), o_H = carve((size_t)B * m * ldh * 16),
                o_bn = carve(B * 8), o_res = carve(B * 8), o_rt = carve(B * 8), o_st = carve(B * 4),
@@ -306,11 +348,12 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   A.ks.its = (int*)(base + o_its); A.ks.jend = (int*)(base + o_je); A.ks.hist = E.hist.as<double>();
   E.nd_flag = (int*)(base + o_fl);
   HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
-  if (E.h_status) cudaFreeHost(E.h_status);
-  HH_CUDA_TRY(cudaMallocHost(&E.h_status, std::max(B, 4) * sizeof(int)));
   // coarse operator + factorisation
   HH_TRY(coarse_stencil(E.LC, B, E.stc.as<cplx>(), E.s));
   HH_TRY(nd_factor(P, B, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
+  HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
+  HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
+                     varg(E.ec.as<cplx>(), Nc), E.s));
   HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, B * sizeof(int), cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   for (int b = 0; b < B; ++b)
@@ -358,21 +401,20 @@ int64_t launches_per_iteration(const Engine& E) {
   return fine + nd_solve_launches(E.plan, E.B) + 3;
 }
 
-hh_status run_iteration(Engine& E) {
-  const bool timing = E.timing;
-  if (!E.gexec || E.graph_timing != timing) {
-    if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }
+// two captured variants of one iteration: plain, and with phase events (sampled timing)
+hh_status run_iteration(Engine& E, bool timed) {
+  cudaGraphExec_t& ge = timed ? E.gexec_t : E.gexec;
+  if (!ge) {
     cudaGraph_t g;
     HH_CUDA_TRY(cudaStreamBeginCapture(E.s, cudaStreamCaptureModeThreadLocal));
-    hh_status st = enqueue_iteration(E, timing);
+    hh_status st = enqueue_iteration(E, timed);
     cudaError_t ce = cudaStreamEndCapture(E.s, &g);
     if (st != HH_OK) return st;
     HH_CUDA_TRY(ce);
-    HH_CUDA_TRY(cudaGraphInstantiate(&E.gexec, g, 0));
+    HH_CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    E.graph_timing = timing;
   }
-  HH_CUDA_TRY(cudaGraphLaunch(E.gexec, E.s));
+  HH_CUDA_TRY(cudaGraphLaunch(ge, E.s));
   E.launches += launches_per_iteration(E);
   return HH_OK;
 }
@@ -430,7 +472,7 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
   A.rtol = o.rtol;
   A.max_iters = o.max_iters;
   A.fixed_iters = o.fixed_iters;
-  if (E.gexec) { cudaGraphExecDestroy(E.gexec); E.gexec = nullptr; }   // KArgs captured by value
+  E.drop_graphs();   // KArgs (rtol, caps) are captured by value
   const int check = std::max(1, o.check_every);
   HH_TRY(vset(xvec, VArg(), E.N, B, 0, 0, nullptr, s));
   HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
@@ -442,15 +484,19 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
   while (running > 0) {
     HH_TRY(krylov_advance(E.jdev, 0, s));
     for (int j = 0; j < m; ++j) {
-      HH_TRY(run_iteration(E));
-      if (E.timing) {
-        HH_CUDA_TRY(cudaStreamSynchronize(s));
-        harvest_timers(E);
-        account_bytes(E, running, j);   // samples that ran this iteration
+      // sampled instrumentation: every timing_every-th iteration runs the graph
+      // variant with phase events; its bytes use the exact running count
+      const bool timed = E.timing && (E.iter_counter++ % E.timing_every == 0);
+      if (timed) {
         HH_TRY(sync_status(E));
         running = count_running(E);
         if (!running) break;
-        continue;
+      }
+      HH_TRY(run_iteration(E, timed));
+      if (timed) {
+        HH_CUDA_TRY(cudaStreamSynchronize(s));
+        harvest_timers(E);
+        account_bytes(E, running, j);
       }
       if ((j + 1) % check == 0 || j == m - 1) {
         HH_TRY(sync_status(E));
@@ -695,6 +741,7 @@ static std::mutex g_sweep_mu;
 static bool g_sweep_timing = false;
 static double g_sweep_st[3 * T_NT] = {0};
 static int64_t g_sweep_launches = 0;
+static std::vector<std::unique_ptr<Engine>> g_sweep_engines;   // persistent across hh_sweep calls
 
 extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches) {
   std::lock_guard<std::mutex> lk(g_sweep_mu);
@@ -733,7 +780,8 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
   size_t freeb = 0, totb = 0;
   HH_CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
-  const double budget = 0.75 * (double)freeb / nstreams;
+  (void)freeb;
+  const double budget = 0.70 * (double)totb / nstreams;   // engines persist: budget on total HBM
   std::vector<std::vector<int>> batches;
   for (auto& kv : groups) {
     NDPlan* plan = nullptr;
@@ -753,23 +801,64 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
     return (int64_t)smp[a[0]].n_cells * smp[a[0]].n_cells * a.size() >
            (int64_t)smp[b[0]].n_cells * smp[b[0]].n_cells * b.size();
   });
+  // spec of every batch
+  std::vector<BatchSpec> specs(batches.size());
+  for (size_t bi = 0; bi < batches.size(); ++bi) {
+    BatchSpec& sp = specs[bi];
+    const std::vector<int>& bt = batches[bi];
+    sp.dim = 2; sp.n = smp[bt[0]].n_cells; sp.B = (int)bt.size();
+    sp.nu_pre = common->nu_pre; sp.nu_post = common->nu_post; sp.omega = common->omega; sp.m = m;
+    for (int i : bt) { sp.k.push_back(smp[i].k); sp.beta.push_back(smp[i].beta); sp.sigma.push_back(smp[i].sigma); }
+  }
+  const int nt = std::min<int>(nstreams, (int)batches.size());
+  // persistent engines: every allocation happens here, before the workers start
+  // (cudaMalloc/cudaFree synchronise the whole device)
+  std::vector<Engine*> engines;
+  {
+    std::lock_guard<std::mutex> lk(g_sweep_mu);
+    while ((int)g_sweep_engines.size() < nt) {
+      g_sweep_engines.emplace_back(new Engine());
+      HH_TRY(engine_init(*g_sweep_engines.back(), common->device));
+    }
+    for (int t = 0; t < nt; ++t) engines.push_back(g_sweep_engines[t].get());
+  }
+  for (Engine* E : engines)
+    for (const BatchSpec& sp : specs) HH_TRY(reserve_pools(*E, sp));
+  // ND solve schedule per (grid, batch size), timed once on an idle GPU (zero
+  // factor: the schedule depends on sizes only), then cached in the shared tree
+  {
+    Engine& E = *engines[0];
+    for (const BatchSpec& sp : specs) {
+      NDPlan* P = nullptr;
+      HH_TRY(get_plan(2, sp.n / 2 + 1, &P));
+      const int64_t Nc = ipow(sp.n / 2 + 1, 2);
+      HH_CUDA_TRY(cudaMemsetAsync(E.F.p, 0, (size_t)sp.B * nd_front_entries(P) * 16, E.s));
+      HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)sp.B * Nc * 16, E.s));
+      HH_TRY(nd_autotune(P, sp.B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
+                         varg(E.ec.as<cplx>(), Nc), E.s));
+    }
+    HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  }
   std::atomic<int> next(0);
   std::atomic<int> failed(0);
   std::string err;
   std::mutex err_mu;
   const bool timing = g_sweep_timing;
-  auto worker = [&]() {
-    Engine E;
-    if (engine_init(E, common->device) != HH_OK) { failed = 1; return; }
+  auto worker = [&](Engine* Ep) {
+    Engine& E = *Ep;
+    if (cudaSetDevice(common->device) != cudaSuccess) { failed = 1; return; }
     E.timing = timing;
+    for (double& a : E.acc_ms) a = 0;
+    for (double& a : E.acc_bytes) a = 0;
+    for (double& a : E.acc_launch) a = 0;
+    E.launches = 0;
+    if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
+    else E.timing_every = 8;   // sweep: sample 1 iteration in 8 (keeps the pipelines full)
     for (;;) {
       const int bi = next.fetch_add(1);
       if (bi >= (int)batches.size() || failed) break;
       const std::vector<int>& bt = batches[bi];
-      BatchSpec sp;
-      sp.dim = 2; sp.n = smp[bt[0]].n_cells; sp.B = (int)bt.size();
-      sp.nu_pre = common->nu_pre; sp.nu_post = common->nu_post; sp.omega = common->omega; sp.m = m;
-      for (int i : bt) { sp.k.push_back(smp[i].k); sp.beta.push_back(smp[i].beta); sp.sigma.push_back(smp[i].sigma); }
+      const BatchSpec& sp = specs[bi];
       hh_status st = batch_setup(E, sp);
       std::vector<SampleOut> res;
       double t_solve = 0;
@@ -807,9 +896,8 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
     }
     g_sweep_launches += E.launches;
   };
-  const int nt = std::min<int>(nstreams, (int)batches.size());
   std::vector<std::thread> th;
-  for (int t = 0; t < nt; ++t) th.emplace_back(worker);
+  for (int t = 0; t < nt; ++t) th.emplace_back(worker, engines[t]);
   for (auto& t : th) t.join();
   if (failed) { hh_set_error("%s", err.c_str()); return HH_E_CUDA; }
   return HH_OK;

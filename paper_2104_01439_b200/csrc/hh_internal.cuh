@@ -121,3 +121,6 @@ hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* 
                     cudaStream_t s);
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                    VArg x, cudaStream_t s);
+// choose the solve schedule for batch size B by timing candidates on the real factor
+hh_status nd_autotune(const NDPlan* p, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
+                      cudaStream_t s);
