@@ -386,7 +386,7 @@ __global__ void k_nd_gather(SolveArgs A, int begin) {
 }
 
 // one tree level, forward: (gather into smem +) contribution GEMV rows
-__global__ void __launch_bounds__(256) k_nd_fwd(SolveArgs A, int begin) {
+__global__ void __launch_bounds__(256, 5) k_nd_fwd(SolveArgs A, int begin) {
   extern __shared__ double4 smem_raw[];
   cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.z;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) k_nd_fwd(SolveArgs A, int begin) {
 }
 
 // one tree level, backward
-__global__ void __launch_bounds__(256) k_nd_bwd(SolveArgs A, int begin) {
+__global__ void __launch_bounds__(256, 5) k_nd_bwd(SolveArgs A, int begin) {
   extern __shared__ double4 smem_raw[];
   cplx* v = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.z;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* 
 }
 
 // bottom subtrees: one CTA walks all fronts of one subtree (bottom-up / top-down)
-__global__ void __launch_bounds__(256) k_nd_fwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+__global__ void __launch_bounds__(256, 5) k_nd_fwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
                                                     const int* __restrict__ sub_list) {
   extern __shared__ double4 smem_raw[];
   cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) k_nd_fwd_sub(SolveArgs A, const int* __re
   }
 }
 
-__global__ void __launch_bounds__(256) k_nd_bwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+__global__ void __launch_bounds__(256, 5) k_nd_bwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
                                                     const int* __restrict__ sub_list) {
   extern __shared__ double4 smem_raw[];
   cplx* v = reinterpret_cast<cplx*>(smem_raw);
@@ -574,7 +574,8 @@ void build_tree(const Box& b, int dim, int m, int parent, std::vector<HostFront>
   for (int d = 1; d < dim; ++d)
     if (b.hi[d] - b.lo[d] > b.hi[ax] - b.lo[ax]) ax = d;
   const int ext = b.hi[ax] - b.lo[ax];
-  if (box_count(b, dim) <= LEAF || ext < 3) {   // leaf: all nodes, lexicographic
+  static const int leaf = getenv("HH_ND_LEAF") ? atoi(getenv("HH_ND_LEAF")) : LEAF;
+  if (box_count(b, dim) <= leaf || ext < 3) {   // leaf: all nodes, lexicographic
     push_box_nodes(b, dim, m, out[id].sep);
     return;
   }
@@ -1041,8 +1042,11 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   std::lock_guard<std::mutex> lk(nd->cut_mu);
   nd->cfg_cache.push_back({B, best});
   if (getenv("HH_DEBUG"))
-    fprintf(stderr, "[hh] nd_autotune m=%d dim=%d B=%d levels=%d -> sub_cut=%d split=%d (%.1f us/solve)\n",
-            nd->m, nd->dim, B, nlev, best.sub_cut, best.split, 1e3 * best_ms / 3);
+    fprintf(stderr,
+            "[hh] nd_autotune m=%d dim=%d B=%d levels=%d -> sub_cut=%d split=%d (%.1f us/solve, "
+            "%.1f MB/sample, %.0f GB/s)\n",
+            nd->m, nd->dim, B, nlev, best.sub_cut, best.split, 1e3 * best_ms / 3,
+            nd->stream_bytes / 1e6, (double)nd->stream_bytes * B / (best_ms / 3 * 1e-3) / 1e9);
   return HH_OK;
 }
 

@@ -211,6 +211,14 @@ int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {
 
 constexpr int HIST_LEN = 4096;
 
+// Krylov CTAs per sample: enough for ONE sample to fill the GPU (the tail of a
+// batch is a single slow sample), chunks of <= 2048 nodes (the multi-dot stages
+// its chunk of w in shared memory); independent of B, so batched == single.
+int krylov_blocks(int64_t N) {
+  const int64_t a = std::min<int64_t>(148 * 4, (N + 255) / 256);
+  return (int)std::max<int64_t>(1, std::max<int64_t>(a, (N + 2047) / 2048));
+}
+
 size_t ksmall_bytes(int B, int m) {
   const size_t ldv = m + 1, ldh = m + 1;
   auto r = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -227,7 +235,7 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   NDPlan* P = nullptr;
   HH_TRY(get_plan(dim, n / 2 + 1, &P));
   const int S = dim == 2 ? 9 : 27;
-  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (N + 255) / 256));
+  const int nblk = krylov_blocks(N);
   HH_TRY(E.V.ensure((size_t)B * (m + 1) * N * 16));
   HH_TRY(E.Z.ensure((size_t)B * m * N * 16));
   HH_TRY(E.w.ensure((size_t)B * N * 16));
@@ -312,7 +320,7 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   const int ldv = m + 1, ldh = m + 1;
   // Krylov CTAs per sample: enough for ONE sample to fill the GPU (the tail of a
   // batch is a single slow sample); independent of B, so batched == single results
-  E.nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 4, (N + 255) / 256));
+  E.nblk = krylov_blocks(N);
   E.hist_len = HIST_LEN;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };

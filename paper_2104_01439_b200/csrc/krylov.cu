@@ -49,7 +49,7 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
 }
 
 // h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..j -> H column j
-__global__ void __launch_bounds__(KT) k_mdot(KArgs A) {
+__global__ void __launch_bounds__(KT, 5) k_mdot(KArgs A) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
   const int j = *A.jdev;
@@ -61,23 +61,33 @@ __global__ void __launch_bounds__(KT) k_mdot(KArgs A) {
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // warp-per-vector: warp w streams V[q] for q = w, w+8, ... over this CTA's chunk
-  // (w is re-read from L1); no CTA barrier, 4 independent loads in flight per lane
+  // stage this CTA's chunk of w in shared memory (chunk <= MDOT_CHUNK nodes)
+  extern __shared__ double4 smem_raw[];
+  cplx* ws = reinterpret_cast<cplx*>(smem_raw);
+  const int len = (int)(hi - lo);
+  for (int t = threadIdx.x; t < len; t += KT) ws[t] = w[lo + t];
+  __syncthreads();
+  // warp-per-vector: warp w streams V[q] for q = w, w+8, ...; 8 independent global
+  // loads in flight per lane, no CTA barrier inside the loop
   for (int q = warp; q < nv; q += KT / 32) {
-    const cplx* vq = V + (int64_t)q * N;
+    const cplx* vq = V + (int64_t)q * N + lo;
     cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
-    int64_t i = lo + lane;
-    for (; i + 96 < hi; i += 128) {
-      const cplx v0 = __ldg(&vq[i]), v1 = __ldg(&vq[i + 32]), v2 = __ldg(&vq[i + 64]),
-                 v3 = __ldg(&vq[i + 96]);
-      const cplx w0 = w[i], w1 = w[i + 32], w2 = w[i + 64], w3 = w[i + 96];
-      a0.x = fma(v0.x, w0.x, fma(v0.y, w0.y, a0.x)); a0.y = fma(v0.x, w0.y, fma(-v0.y, w0.x, a0.y));
-      a1.x = fma(v1.x, w1.x, fma(v1.y, w1.y, a1.x)); a1.y = fma(v1.x, w1.y, fma(-v1.y, w1.x, a1.y));
-      a0.x = fma(v2.x, w2.x, fma(v2.y, w2.y, a0.x)); a0.y = fma(v2.x, w2.y, fma(-v2.y, w2.x, a0.y));
-      a1.x = fma(v3.x, w3.x, fma(v3.y, w3.y, a1.x)); a1.y = fma(v3.x, w3.y, fma(-v3.y, w3.x, a1.y));
+    int i = lane;
+    for (; i + 224 < len; i += 256) {
+      cplx v[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[t] = __ldg(&vq[i + 32 * t]);
+#pragma unroll
+      for (int t = 0; t < 8; t += 2) {
+        const cplx w0 = ws[i + 32 * t], w1 = ws[i + 32 * t + 32];
+        a0.x = fma(v[t].x, w0.x, fma(v[t].y, w0.y, a0.x));
+        a0.y = fma(v[t].x, w0.y, fma(-v[t].y, w0.x, a0.y));
+        a1.x = fma(v[t + 1].x, w1.x, fma(v[t + 1].y, w1.y, a1.x));
+        a1.y = fma(v[t + 1].x, w1.y, fma(-v[t + 1].y, w1.x, a1.y));
+      }
     }
-    for (; i < hi; i += 32) {
-      const cplx v0 = __ldg(&vq[i]), w0 = w[i];
+    for (; i < len; i += 32) {
+      const cplx v0 = __ldg(&vq[i]), w0 = ws[i];
       a0.x = fma(v0.x, w0.x, fma(v0.y, w0.y, a0.x)); a0.y = fma(v0.x, w0.y, fma(-v0.y, w0.x, a0.y));
     }
     cplx acc = cadd(a0, a1);
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__(KT) k_mdot(KArgs A) {
 
 // w' = w - sum_i (H_i vscale_i) V_i -> V[j+1] ; ||w'||^2 ; last block:
 // h_{j+1,j} = ||w'||, vscale_{j+1}, Givens on column j, status.
-__global__ void __launch_bounds__(KT) k_update(KArgs A) {
+__global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
   __shared__ cplx cf[128];
@@ -284,7 +294,10 @@ __global__ void k_clear_jend(KArgs A, int B) {
 
 // ================================================================ host side
 hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
-  k_mdot<<<dim3(A.nblk, B), KT, 0, s>>>(A);
+  const size_t sm = (size_t)((A.N + A.nblk - 1) / A.nblk) * sizeof(cplx);
+  if (sm > 48 * 1024)
+    HH_CUDA_TRY(cudaFuncSetAttribute(k_mdot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

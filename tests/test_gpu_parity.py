@@ -163,3 +163,47 @@ def test_sweep_batch_equals_single_problem():
         assert r["iterations"] == rg["iterations"], (s, r, rg)
         # reduction partitions differ with the batch size: equal up to round-off
         assert abs(r["rel_res_true"] - rg["rel_res_true"]) <= 1e-6 * rg["rel_res_true"] + 1e-18
+
+
+def test_restarted_fgmres_parity():
+    """Short restart cycles exercise the restart path (r = b - A_0 x, new basis)."""
+    spec = config_spec("cfg0", n=32)
+    spec.restart = 4
+    orc = OracleProblem(spec)
+    xo, ro = orc.solve()
+    gp = hh.Problem.from_spec(spec, max_restart=8)
+    xg, rg = gp.fgmres_solve(_dev(spec.rhs()), o=hh.opts(restart=4, rtol=spec.rtol))
+    assert ro.restarts >= 1 and rg["restarts"] >= 1
+    assert abs(rg["iterations"] - ro.iterations) <= 1, (rg, ro.iterations)
+    if rg["iterations"] == ro.iterations:
+        assert _rel(_host(xg), xo) <= 1e-8
+    gp.close()
+
+
+def test_fixed_iters_threshold_parity():
+    """fixed_iters reproduces the oracle's iterate after exactly k steps (reading C12)."""
+    spec = config_spec("cfg2", n=64)
+    orc = OracleProblem(spec)
+    gp = hh.Problem.from_spec(spec)
+    for k in (1, 3, 7):
+        xo, ro = orc.solve(fixed_iters=k)
+        xg, rg = gp.fgmres_solve(_dev(spec.rhs()), o=hh.opts(fixed_iters=k))
+        assert rg["iterations"] == k == ro.iterations
+        assert _rel(_host(xg), xo) <= 1e-9
+        assert abs(rg["rel_res_true"] - ro.rel_res_true) <= 1e-8 * ro.rel_res_true
+    gp.close()
+
+
+def test_zero_rhs_and_linearity_of_vcycle():
+    """b = 0 returns x = 0 immediately; the V-cycle is linear."""
+    spec = config_spec("cfg0", n=16)
+    gp = hh.Problem.from_spec(spec)
+    x, r = gp.fgmres_solve(torch.zeros(spec.n_nodes, dtype=torch.complex128, device="cuda"))
+    assert r["iterations"] == 0 and r["converged"] == 1
+    assert float(torch.linalg.vector_norm(x)) == 0.0
+    f1, f2 = _rand(spec.n_nodes, 11), _rand(spec.n_nodes, 12)
+    a, b2 = 0.7 - 0.3j, -1.1 + 2.0j
+    z = _host(gp.vcycle(_dev(a * f1 + b2 * f2)))
+    z12 = a * _host(gp.vcycle(_dev(f1))) + b2 * _host(gp.vcycle(_dev(f2)))
+    assert _rel(z, z12) <= 1e-12
+    gp.close()
