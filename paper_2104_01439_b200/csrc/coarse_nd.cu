@@ -40,7 +40,7 @@ struct FrontMeta {          // device-visible per-front data
   int s, u, f, level;
   int64_t Foff;             // offset (complex entries) of the f x f front
   int64_t sepOff, haloOff;  // into sep / halo index arrays
-  int64_t zsOff, outOff;    // into the solve work vector (zs part / out part)
+  int64_t posOff, outOff;   // into the solve work vector: w (f entries) / update vector (u entries)
   int64_t eaOff;            // into extend-add map (u entries)
   int parent;
   int pad;
@@ -72,10 +72,9 @@ struct NDPlan {
   int4* d_asm = nullptr;         // (front, a, b, stencil index)
   int* d_eamap = nullptr;        // child halo pos -> parent front pos
   int* d_eaList = nullptr;       // child front ids grouped by (level, slot)
-  int64_t* d_gptr = nullptr;     // CSR over all separator entries
-  int64_t* d_gidx = nullptr;     // index into the out part of the work vector
+  int2* d_gmap = nullptr;        // per front position: update-vector entries of child 0 / 1 (-1: none)
   int64_t* d_Coff = nullptr;     // per front offset into the pivot column buffer (level-local)
-  int64_t F_entries = 0, zs_entries = 0, out_entries = 0, C_entries = 0;
+  int64_t F_entries = 0, w_entries = 0, out_entries = 0, C_entries = 0;
   int64_t stream_bytes = 0;
   // bottom-subtree decompositions, one per candidate cut level L (fronts of level <= L)
   std::vector<int> sub_cnt;          // number of subtrees for cut L
@@ -89,7 +88,8 @@ struct NDPlan {
   std::vector<double> level_bytes;   // factor bytes streamed per level per sample
   int* d_sep_front = nullptr;
   int* d_halo_front = nullptr;
-  int64_t* d_lvr = nullptr;          // [nlev][4]: sep begin/end, halo begin/end
+  int* d_pos_front = nullptr;
+  int64_t* d_lvr = nullptr;          // [nlev][6]: sep begin/end, halo begin/end, position begin/end
   std::mutex cut_mu;
   std::vector<std::pair<int, SolveCfg>> cfg_cache;   // (B, schedule) chosen by nd_autotune
 };
@@ -254,6 +254,15 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
 }
 
 // ------------------------------------------------------------------ solve
+// Multifrontal solve with the stored blocks.  Front t owns the work vector
+// w_t (f entries: separator part z_s, halo part) and an update vector upd_t
+// (u entries) for its parent:
+//   forward  (leaves -> root):  w_t = [r[sep]; 0] + extend-add of upd_c of its (<= 2)
+//                               children;  upd_t = w_t[halo] - H^T z_s
+//   backward (root -> leaves):  x[sep] = X z_s - H x[halo]
+// The gather of w_t reads at most two child entries per position (gmap), so
+// every stage is one short dependent chain instead of a walk over all
+// descendant contributions.
 constexpr int VMAX = 4096;   // front vectors up to this length are staged in shared memory
 
 __device__ __forceinline__ cplx warp_sum(cplx v) {
@@ -265,17 +274,20 @@ __device__ __forceinline__ cplx warp_sum(cplx v) {
   return v;
 }
 
-// lane-strided dot of a front row with v (2 independent accumulators)
+// lane-strided dot of a front row with v: 4 independent loads in flight per lane
 __device__ __forceinline__ cplx row_dot(const cplx* __restrict__ row, const cplx* v, int len, int lane) {
-  cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
+  cplx a0 = cmake(0, 0), a1 = cmake(0, 0), a2 = cmake(0, 0), a3 = cmake(0, 0);
   int c = lane;
-  for (; c + 32 < len; c += 64) {
-    const cplx r0 = __ldg(&row[c]), r1 = __ldg(&row[c + 32]);
+  for (; c + 96 < len; c += 128) {
+    const cplx r0 = __ldg(&row[c]), r1 = __ldg(&row[c + 32]), r2 = __ldg(&row[c + 64]),
+               r3 = __ldg(&row[c + 96]);
     cfma(a0, r0, v[c]);
     cfma(a1, r1, v[c + 32]);
+    cfma(a2, r2, v[c + 64]);
+    cfma(a3, r3, v[c + 96]);
   }
-  if (c < len) cfma(a0, __ldg(&row[c]), v[c]);
-  return warp_sum(cadd(a0, a1));
+  for (; c < len; c += 32) cfma(a0, __ldg(&row[c]), v[c]);
+  return warp_sum(cadd(cadd(a0, a1), cadd(a2, a3)));
 }
 
 struct SolveArgs {
@@ -283,67 +295,57 @@ struct SolveArgs {
   const int* st;
   const int* sep;
   const int* halo;
-  const int64_t* gptr;
-  const int64_t* gidx;
+  const int2* gmap;
   const cplx* F; int64_t FE;
-  cplx* work; int64_t WE, zsE;
+  cplx* work; int64_t WE, updE;   // work[b] = [w (w_entries) | upd (out_entries)]
   VArg rhs, x;
 };
 
-// z_s[a] = r[sep[a]] + sum of descendant contributions, a = a0 + team_rank (stride team)
+// Programmatic dependent launch: a level kernel may start while its predecessor
+// drains; before griddepcontrol.wait it touches only the (immutable) factor,
+// which it prefetches into L2 with bulk prefetches, so the factor stream of
+// level L+1 overlaps the tail of level L.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// prefetch the rows r0, r0 + step, ... (< nrows, at most 8 per warp) of length len starting at row0
+__device__ __forceinline__ void prefetch_rows(const cplx* row0, int64_t ld, int len, int nrows, int r0,
+                                              int step, int lane) {
+  if (len <= 0) return;
+  const int r = r0 + lane * step;
+  if (lane < 8 && r < nrows) prefetch_l2(row0 + (int64_t)r * ld, len * (int)sizeof(cplx));
+}
+
+__device__ __forceinline__ cplx* w_of(const SolveArgs& A, int b) { return A.work + (int64_t)b * A.WE; }
+__device__ __forceinline__ cplx* upd_of(const SolveArgs& A, int b) { return A.work + (int64_t)b * A.WE + A.updE; }
+
+// w_t[p] for p = p0, p0 + stride, ... -> dst (smem, may be NULL) and wg (global, sep part or all)
 __device__ __forceinline__ void front_gather(const SolveArgs& A, const FrontMeta& m, int b, cplx* dst,
-                                             cplx* dst2, int a0, int stride) {
+                                             cplx* wg, int wg_len, int p0, int stride) {
   const cplx* r = A.rhs.at(b);
-  const cplx* out = A.work + (int64_t)b * A.WE + A.zsE;
-  for (int a = a0; a < m.s; a += stride) {
-    cplx v = __ldg(&r[A.sep[m.sepOff + a]]);
-    const int64_t p0 = A.gptr[m.sepOff + a], p1 = A.gptr[m.sepOff + a + 1];
-    for (int64_t p = p0; p < p1; ++p) {
-      const cplx c = out[A.gidx[p]];
-      v.x += c.x;
-      v.y += c.y;
-    }
-    dst[a] = v;
-    if (dst2) dst2[a] = v;
+  const cplx* upd = upd_of(A, b);
+  const int2* gm = A.gmap + m.posOff;
+  const int* sp = A.sep + m.sepOff;
+  for (int p = p0; p < m.f; p += stride) {
+    const int2 g = __ldg(&gm[p]);
+    cplx v = p < m.s ? __ldg(&r[__ldg(&sp[p])]) : cmake(0, 0);
+    if (g.x >= 0) v = cadd(v, upd[g.x]);
+    if (g.y >= 0) v = cadd(v, upd[g.y]);
+    if (dst) dst[p] = v;
+    if (wg && p < wg_len) wg[p] = v;
   }
 }
 
-// two rows at once (independent load streams: latency hiding for short rows)
-__device__ __forceinline__ void row_dot2(const cplx* __restrict__ ra, const cplx* __restrict__ rb,
-                                         const cplx* v, int len, int lane, cplx& oa, cplx& ob) {
-  cplx a0 = cmake(0, 0), a1 = cmake(0, 0), b0 = cmake(0, 0), b1 = cmake(0, 0);
-  int c = lane;
-  for (; c + 32 < len; c += 64) {
-    const cplx x0 = __ldg(&ra[c]), x1 = __ldg(&ra[c + 32]), y0 = __ldg(&rb[c]), y1 = __ldg(&rb[c + 32]);
-    const cplx v0 = v[c], v1 = v[c + 32];
-    cfma(a0, x0, v0);
-    cfma(a1, x1, v1);
-    cfma(b0, y0, v0);
-    cfma(b1, y1, v1);
-  }
-  if (c < len) {
-    const cplx v0 = v[c];
-    cfma(a0, __ldg(&ra[c]), v0);
-    cfma(b0, __ldg(&rb[c]), v0);
-  }
-  oa = warp_sum(cadd(a0, a1));
-  ob = warp_sum(cadd(b0, b1));
-}
-
-// forward rows b = r0.. (step) : out[b] = F[s+b][0:s] . z
+// forward rows b = r0, r0 + step, ...: upd[b] = w[s + b] + (-H^T row b) . z
 __device__ __forceinline__ void front_fwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
-                                               const cplx* z, int r0, int step, int lane) {
+                                               const cplx* w, int r0, int step, int lane) {
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
-  cplx* out = A.work + (int64_t)bs * A.WE + A.zsE + m.outOff;
-  for (int b = r0; b < m.u; b += 2 * step) {
-    if (b + step < m.u) {
-      cplx o1, o2;
-      row_dot2(F + (int64_t)(m.s + b) * m.f, F + (int64_t)(m.s + b + step) * m.f, z, m.s, lane, o1, o2);
-      if (lane == 0) { out[b] = o1; out[b + step] = o2; }
-    } else {
-      const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, z, m.s, lane);
-      if (lane == 0) out[b] = acc;
-    }
+  cplx* out = upd_of(A, bs) + m.outOff;
+  for (int b = r0; b < m.u; b += step) {
+    const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, w, m.s, lane);
+    if (lane == 0) out[b] = cadd(acc, w[m.s + b]);
   }
 }
 
@@ -352,77 +354,85 @@ __device__ __forceinline__ void front_bwd_rows(const SolveArgs& A, const FrontMe
                                                const cplx* v, int r0, int step, int lane) {
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
   cplx* x = A.x.at(bs);
-  for (int a = r0; a < m.s; a += 2 * step) {
-    if (a + step < m.s) {
-      cplx o1, o2;
-      row_dot2(F + (int64_t)a * m.f, F + (int64_t)(a + step) * m.f, v, m.f, lane, o1, o2);
-      if (lane == 0) { x[A.sep[m.sepOff + a]] = o1; x[A.sep[m.sepOff + a + step]] = o2; }
-    } else {
-      const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
-      if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
-    }
+  for (int a = r0; a < m.s; a += step) {
+    const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
+    if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
   }
 }
 
 __device__ __forceinline__ void stage_bwd(const SolveArgs& A, const FrontMeta& m, int bs, cplx* v) {
-  const cplx* zs = A.work + (int64_t)bs * A.WE + m.zsOff;
+  const cplx* zs = w_of(A, bs) + m.posOff;
   const cplx* x = A.x.at(bs);
   for (int c = threadIdx.x; c < m.f; c += blockDim.x) {
     if (c < m.s) v[c] = zs[c];
     else {
-      const cplx t = x[A.halo[m.haloOff + c - m.s]];
+      const cplx t = x[__ldg(&A.halo[m.haloOff + c - m.s])];
       v[c] = cmake(-t.x, -t.y);
     }
   }
 }
 
-// large fronts only: gather z_s to global (separate pass)
+// large fronts only (f > VMAX): gather w_t to global (separate pass)
 __global__ void k_nd_gather(SolveArgs A, int begin) {
   const int b = blockIdx.z;
+  pdl_trigger();
+  pdl_wait();
   if (A.st && A.st[b]) return;
   const FrontMeta m = A.fr[begin + blockIdx.x];
-  cplx* zs = A.work + (int64_t)b * A.WE + m.zsOff;
-  front_gather(A, m, b, zs, nullptr, threadIdx.x + blockIdx.y * blockDim.x, blockDim.x * gridDim.y);
+  front_gather(A, m, b, nullptr, w_of(A, b) + m.posOff, m.f, threadIdx.x + blockIdx.y * blockDim.x,
+               blockDim.x * gridDim.y);
 }
 
-// one tree level, forward: (gather into smem +) contribution GEMV rows
-__global__ void __launch_bounds__(256, 5) k_nd_fwd(SolveArgs A, int begin) {
+constexpr int LT = 128;   // threads of the per-level solve kernels (4 warps)
+
+// one tree level, forward: gather w_t into smem, write z_s, update-vector rows
+__global__ void __launch_bounds__(LT) k_nd_fwd(SolveArgs A, int begin) {
   extern __shared__ double4 smem_raw[];
-  cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
+  cplx* wsh = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.z;
-  if (A.st && A.st[b]) return;
   const FrontMeta m = A.fr[begin + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const cplx* z;
-  if (m.s <= VMAX) {
-    front_gather(A, m, b, zsh, blockIdx.y == 0 ? A.work + (int64_t)b * A.WE + m.zsOff : nullptr,
-                 threadIdx.x, blockDim.x);
+  pdl_trigger();
+  if (!(A.st && *(volatile const int*)&A.st[b]))   // (possibly stale) status: prefetch hint only
+    prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff + (int64_t)m.s * m.f, m.f, m.s, m.u,
+                  blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32), lane);
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  const cplx* w;
+  if (m.f <= VMAX) {
+    front_gather(A, m, b, wsh, blockIdx.y == 0 ? w_of(A, b) + m.posOff : nullptr, m.s, threadIdx.x,
+                 blockDim.x);
     __syncthreads();
-    z = zsh;
+    w = wsh;
   } else {
-    z = A.work + (int64_t)b * A.WE + m.zsOff;   // gathered by k_nd_gather
+    w = w_of(A, b) + m.posOff;   // gathered by k_nd_gather
   }
-  front_fwd_rows(A, m, b, z, blockIdx.y * 8 + warp, gridDim.y * 8, lane);
+  front_fwd_rows(A, m, b, w, blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32), lane);
 }
 
 // one tree level, backward
-__global__ void __launch_bounds__(256, 5) k_nd_bwd(SolveArgs A, int begin) {
+__global__ void __launch_bounds__(LT) k_nd_bwd(SolveArgs A, int begin) {
   extern __shared__ double4 smem_raw[];
   cplx* v = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.z;
-  if (A.st && A.st[b]) return;
   const FrontMeta m = A.fr[begin + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  if (!(A.st && *(volatile const int*)&A.st[b]))
+    prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff, m.f, m.f, m.s, blockIdx.y * (LT / 32) + warp,
+                  gridDim.y * (LT / 32), lane);
+  pdl_wait();
+  if (A.st && A.st[b]) return;
   if (m.f <= VMAX) {
     stage_bwd(A, m, b, v);
     __syncthreads();
-    front_bwd_rows(A, m, b, v, blockIdx.y * 8 + warp, gridDim.y * 8, lane);
+    front_bwd_rows(A, m, b, v, blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32), lane);
   } else {   // huge fronts: operands straight from global memory
     const cplx* F = A.F + (int64_t)b * A.FE + m.Foff;
-    const cplx* z = A.work + (int64_t)b * A.WE + m.zsOff;
+    const cplx* z = w_of(A, b) + m.posOff;
     const int* hl = A.halo + m.haloOff;
     cplx* x = A.x.at(b);
-    for (int a = blockIdx.y * 8 + warp; a < m.s; a += gridDim.y * 8) {
+    for (int a = blockIdx.y * (LT / 32) + warp; a < m.s; a += gridDim.y * (LT / 32)) {
       const cplx* row = F + (int64_t)a * m.f;
       cplx acc = row_dot(row, z, m.s, lane);
       cplx acc2 = cmake(0, 0);
@@ -435,19 +445,19 @@ __global__ void __launch_bounds__(256, 5) k_nd_bwd(SolveArgs A, int begin) {
 
 // ------------------------------------------------------------ cluster solve
 // One thread-block cluster (CL CTAs on CL SMs) per sample walks the tree levels
-// [L0, nlev): forward (gather, contribution GEMVs) up to the root, then backward
-// down to L0, with a cluster barrier between phases.  Operands go through
-// L2/global memory; the barrier (release/acquire at cluster scope, preceded by a
-// device fence) orders them.  This replaces ~3 launches per level.
+// [L0, nlev): forward (gather, update rows) up to the root, then backward down
+// to L0, with a cluster barrier between phases.  Operands go through L2/global
+// memory; the barrier (release/acquire at cluster scope, preceded by a device
+// fence) orders them.  This replaces ~3 launches per level.
 __device__ __forceinline__ void cl_sync(cg::cluster_group& cl) {
   __threadfence();
   cl.sync();
 }
 
 __global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* __restrict__ lvr,
-                                                    int L0, int nlev, int fwd, int bwd,
-                                                    const int* __restrict__ sep_front,
-                                                    const int* __restrict__ halo_front) {
+                                                    int L0, int nlev, const int* __restrict__ sep_front,
+                                                    const int* __restrict__ halo_front,
+                                                    const int* __restrict__ pos_front) {
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks();
   const int b = blockIdx.x / CL;
@@ -455,73 +465,68 @@ __global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* 
   const int rank = (int)cl.block_rank();
   const int tid = rank * blockDim.x + threadIdx.x, nth = CL * blockDim.x;
   const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nth >> 5;
-  cplx* zs = A.work + (int64_t)b * A.WE;
-  cplx* out = zs + A.zsE;
+  cplx* w = w_of(A, b);
+  cplx* upd = upd_of(A, b);
   const cplx* r = A.rhs.at(b);
   cplx* x = A.x.at(b);
   const cplx* Fb = A.F + (int64_t)b * A.FE;
-  if (fwd) {
-    for (int L = L0; L < nlev; ++L) {
-      const int64_t sb = lvr[4 * L], se = lvr[4 * L + 1], hb = lvr[4 * L + 2], he = lvr[4 * L + 3];
-      for (int64_t e = sb + tid; e < se; e += nth) {        // gather z_s
-        cplx v = __ldg(&r[A.sep[e]]);
-        const int64_t p0 = A.gptr[e], p1 = A.gptr[e + 1];
-        for (int64_t p = p0; p < p1; ++p) {
-          const cplx c = out[A.gidx[p]];
-          v.x += c.x;
-          v.y += c.y;
-        }
-        zs[e] = v;
+  for (int L = L0; L < nlev; ++L) {
+    const int64_t hb = lvr[6 * L + 2], he = lvr[6 * L + 3], pb = lvr[6 * L + 4], pe = lvr[6 * L + 5];
+    for (int64_t e = pb + tid; e < pe; e += nth) {        // gather w of every front of the level
+      const FrontMeta m = A.fr[pos_front[e]];
+      const int p = (int)(e - m.posOff);
+      const int2 g = A.gmap[e];
+      cplx v = p < m.s ? r[A.sep[m.sepOff + p]] : cmake(0, 0);
+      if (g.x >= 0) v = cadd(v, upd[g.x]);
+      if (g.y >= 0) v = cadd(v, upd[g.y]);
+      w[e] = v;
+    }
+    cl_sync(cl);
+    if (he > hb) {
+      for (int64_t hrow = hb + gw; hrow < he; hrow += nw) {   // update rows
+        const FrontMeta m = A.fr[halo_front[hrow]];
+        const int brow = (int)(hrow - m.haloOff);
+        const cplx acc = row_dot(Fb + m.Foff + (int64_t)(m.s + brow) * m.f, w + m.posOff, m.s, lane);
+        if (lane == 0) upd[hrow] = cadd(acc, w[m.posOff + m.s + brow]);
       }
       cl_sync(cl);
-      if (he > hb) {
-        for (int64_t hrow = hb + gw; hrow < he; hrow += nw) {   // contribution rows
-          const FrontMeta m = A.fr[halo_front[hrow]];
-          const int brow = (int)(hrow - m.haloOff);
-          const cplx acc = row_dot(Fb + m.Foff + (int64_t)(m.s + brow) * m.f, zs + m.zsOff, m.s, lane);
-          if (lane == 0) out[hrow] = acc;
-        }
-        cl_sync(cl);
-      }
     }
   }
-  if (bwd) {
-    for (int L = nlev - 1; L >= L0; --L) {
-      const int64_t sb = lvr[4 * L], se = lvr[4 * L + 1];
-      for (int64_t e = sb + gw; e < se; e += nw) {
-        const FrontMeta m = A.fr[sep_front[e]];
-        const int a = (int)(e - m.sepOff);
-        const cplx* row = Fb + m.Foff + (int64_t)a * m.f;
-        cplx acc = row_dot(row, zs + m.zsOff, m.s, lane);
-        cplx acc2 = cmake(0, 0);
-        const int* hl = A.halo + m.haloOff;
-        for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
-        acc = cadd(acc, warp_sum(acc2));
-        if (lane == 0) x[A.sep[e]] = acc;
-      }
-      if (L > L0) cl_sync(cl);
+  for (int L = nlev - 1; L >= L0; --L) {
+    const int64_t sb = lvr[6 * L], se = lvr[6 * L + 1];
+    for (int64_t e = sb + gw; e < se; e += nw) {
+      const FrontMeta m = A.fr[sep_front[e]];
+      const int a = (int)(e - m.sepOff);
+      const cplx* row = Fb + m.Foff + (int64_t)a * m.f;
+      cplx acc = row_dot(row, w + m.posOff, m.s, lane);
+      cplx acc2 = cmake(0, 0);
+      const int* hl = A.halo + m.haloOff;
+      for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
+      acc = cadd(acc, warp_sum(acc2));
+      if (lane == 0) x[A.sep[e]] = acc;
     }
+    if (L > L0) cl_sync(cl);
   }
 }
 
 // bottom subtrees: one CTA walks all fronts of one subtree (bottom-up / top-down)
-__global__ void __launch_bounds__(256, 5) k_nd_fwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+__global__ void __launch_bounds__(256) k_nd_fwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
                                                     const int* __restrict__ sub_list) {
   extern __shared__ double4 smem_raw[];
-  cplx* zsh = reinterpret_cast<cplx*>(smem_raw);
+  cplx* wsh = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.y;
   if (A.st && A.st[b]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = sub_ptr[blockIdx.x]; k < sub_ptr[blockIdx.x + 1]; ++k) {
     const FrontMeta m = A.fr[sub_list[k]];
-    front_gather(A, m, b, zsh, A.work + (int64_t)b * A.WE + m.zsOff, threadIdx.x, blockDim.x);
+    front_gather(A, m, b, wsh, w_of(A, b) + m.posOff, m.s, threadIdx.x, blockDim.x);
     __syncthreads();
-    front_fwd_rows(A, m, b, zsh, warp, 8, lane);
+    front_fwd_rows(A, m, b, wsh, warp, 8, lane);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(256, 5) k_nd_bwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
+__global__ void __launch_bounds__(256) k_nd_bwd_sub(SolveArgs A, const int* __restrict__ sub_ptr,
                                                     const int* __restrict__ sub_list) {
   extern __shared__ double4 smem_raw[];
   cplx* v = reinterpret_cast<cplx*>(smem_raw);
@@ -646,7 +651,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   nd->fronts.resize(nf);
   std::vector<int> sepAll, haloAll, eamap;
   std::vector<int4> asmE;
-  int64_t Foff = 0, zsOff = 0, outOff = 0, eaOff = 0;
+  int64_t Foff = 0, posOff = 0, outOff = 0, eaOff = 0;
   const int S = nd->S;
   std::vector<int> loc(nd->N, -1);
   for (int i = 0; i < nf; ++i) {
@@ -656,7 +661,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     fm.Foff = Foff; Foff += (int64_t)fm.f * fm.f;
     fm.sepOff = (int64_t)sepAll.size(); sepAll.insert(sepAll.end(), h.sep.begin(), h.sep.end());
     fm.haloOff = (int64_t)haloAll.size(); haloAll.insert(haloAll.end(), h.halo.begin(), h.halo.end());
-    fm.zsOff = zsOff; zsOff += fm.s;
+    fm.posOff = posOff; posOff += fm.f;
     fm.outOff = outOff; outOff += fm.u;
     fm.parent = h.parent >= 0 ? newid[h.parent] : -1;
     fm.pad = 0;
@@ -706,21 +711,17 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     for (int a = 0; a < ps; ++a) loc[hp.sep[a]] = -1;
     for (size_t b = 0; b < hp.halo.size(); ++b) loc[hp.halo[b]] = -1;
   }
-  // gather CSR: for every separator entry (front t, a): contributions (front d, halo pos b)
-  std::vector<int> cnt(sepAll.size() + 1, 0);
-  for (int d = 0; d < nf; ++d) {
-    const HostFront& h = tf[order[d]];
-    for (int g : h.halo) cnt[nd->fronts[owner[g]].sepOff + ownpos[g] + 1]++;
-  }
-  std::vector<int64_t> gptr(sepAll.size() + 1, 0);
-  for (size_t e = 0; e < sepAll.size(); ++e) gptr[e + 1] = gptr[e] + cnt[e + 1];
-  std::vector<int64_t> gidx(gptr.back()), fill(gptr.begin(), gptr.end() - 1);
-  for (int d = 0; d < nf; ++d) {
-    const FrontMeta& fm = nd->fronts[d];
-    const HostFront& h = tf[order[d]];
-    for (int b = 0; b < fm.u; ++b) {
-      const int g = h.halo[b];
-      gidx[fill[nd->fronts[owner[g]].sepOff + ownpos[g]]++] = fm.outOff + b;
+  // solve gather map: front position -> update-vector entry of child slot 0 / 1
+  std::vector<int2> gmap(posOff, make_int2(-1, -1));
+  for (int i = 0; i < nf; ++i) {
+    const FrontMeta& fm = nd->fronts[i];
+    if (fm.parent < 0) continue;
+    const HostFront& hp = tf[order[fm.parent]];
+    const int slot = (hp.children.size() > 1 && newid[hp.children[1]] == i) ? 1 : 0;
+    const FrontMeta& pm = nd->fronts[fm.parent];
+    for (int q = 0; q < fm.u; ++q) {
+      int2& g = gmap[pm.posOff + eamap[fm.eaOff + q]];
+      (slot ? g.y : g.x) = (int)(fm.outOff + q);
     }
   }
   // levels
@@ -766,7 +767,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB; }
     Cmax = std::max(Cmax, o);
   }
-  nd->F_entries = Foff; nd->zs_entries = zsOff; nd->out_entries = outOff; nd->C_entries = Cmax;
+  nd->F_entries = Foff; nd->w_entries = posOff; nd->out_entries = outOff; nd->C_entries = Cmax;
   int64_t sb = 0;
   for (auto& fm : nd->fronts) sb += (int64_t)fm.s * fm.f + (int64_t)fm.u * fm.s;
   nd->stream_bytes = sb * (int64_t)sizeof(cplx);
@@ -811,22 +812,25 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     }
   }
   // per-level ranges and entry -> front maps for the cluster solve
-  std::vector<int> sep_front(sepAll.size()), halo_front(haloAll.size());
-  std::vector<int64_t> lvr(4 * nlev);
+  std::vector<int> sep_front(sepAll.size()), halo_front(haloAll.size()), pos_front(posOff);
+  std::vector<int64_t> lvr(6 * nlev);
   for (int i = 0; i < nf; ++i) {
     const FrontMeta& fm = nd->fronts[i];
     for (int a = 0; a < fm.s; ++a) sep_front[fm.sepOff + a] = i;
     for (int b = 0; b < fm.u; ++b) halo_front[fm.haloOff + b] = i;
+    for (int p = 0; p < fm.f; ++p) pos_front[fm.posOff + p] = i;
   }
   nd->level_bytes.assign(nlev, 0.0);
   for (int L = 0; L < nlev; ++L) {
     const LevelInfo& li = nd->levels[L];
     const FrontMeta& f0 = nd->fronts[li.begin];
     const FrontMeta& fl = nd->fronts[li.begin + li.count - 1];
-    lvr[4 * L] = f0.sepOff;
-    lvr[4 * L + 1] = fl.sepOff + fl.s;
-    lvr[4 * L + 2] = f0.haloOff;
-    lvr[4 * L + 3] = fl.haloOff + fl.u;
+    lvr[6 * L] = f0.sepOff;
+    lvr[6 * L + 1] = fl.sepOff + fl.s;
+    lvr[6 * L + 2] = f0.haloOff;
+    lvr[6 * L + 3] = fl.haloOff + fl.u;
+    lvr[6 * L + 4] = f0.posOff;
+    lvr[6 * L + 5] = fl.posOff + fl.f;
     for (int t = li.begin; t < li.begin + li.count; ++t)
       nd->level_bytes[L] += 16.0 * ((double)nd->fronts[t].s * nd->fronts[t].f + (double)nd->fronts[t].u * nd->fronts[t].s);
   }
@@ -848,13 +852,13 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   if (st == HH_OK) st = up(&nd->d_asm, asmE);
   if (st == HH_OK) st = up(&nd->d_eamap, eamap);
   if (st == HH_OK) st = up(&nd->d_eaList, eaList);
-  if (st == HH_OK) st = up(&nd->d_gptr, gptr);
-  if (st == HH_OK) st = up(&nd->d_gidx, gidx);
+  if (st == HH_OK) st = up(&nd->d_gmap, gmap);
   if (st == HH_OK) st = up(&nd->d_Coff, Coff);
   if (st == HH_OK) st = up(&nd->d_sub_ptr, sptr_all);
   if (st == HH_OK) st = up(&nd->d_sub_list, slist_all);
   if (st == HH_OK) st = up(&nd->d_sep_front, sep_front);
   if (st == HH_OK) st = up(&nd->d_halo_front, halo_front);
+  if (st == HH_OK) st = up(&nd->d_pos_front, pos_front);
   if (st == HH_OK) st = up(&nd->d_lvr, lvr);
   if (st != HH_OK) { nd_plan_destroy(nd); return st; }
   *out = nd;
@@ -864,16 +868,17 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
 void nd_plan_destroy(NDPlan* nd) {
   if (!nd) return;
   cudaFree(nd->d_fronts); cudaFree(nd->d_sep); cudaFree(nd->d_halo); cudaFree(nd->d_asm);
-  cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gptr); cudaFree(nd->d_gidx);
+  cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gmap);
   cudaFree(nd->d_Coff); cudaFree(nd->d_sub_ptr); cudaFree(nd->d_sub_list);
-  cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_lvr);
+  cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_pos_front);
+  cudaFree(nd->d_lvr);
   delete nd;
 }
 
 int64_t nd_front_entries(const NDPlan* p) { return p->F_entries; }
 int64_t nd_stream_bytes(const NDPlan* p) { return p->stream_bytes; }
 int nd_levels(const NDPlan* p) { return (int)p->levels.size(); }
-int64_t nd_work_entries(const NDPlan* p) { return p->zs_entries + p->out_entries; }
+int64_t nd_work_entries(const NDPlan* p) { return p->w_entries + p->out_entries; }
 int64_t nd_cbuf_entries(const NDPlan* p) { return std::max<int64_t>(1, p->C_entries); }
 
 hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
@@ -881,8 +886,14 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
   const int64_t FE = nd->F_entries, CE = nd_cbuf_entries(nd);
   const int64_t stS = nd->N * nd->S;
   HH_CUDA_TRY(cudaMemsetAsync(flag, 0, B * sizeof(int), s));
+  static const int prof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
   for (size_t L = 0; L < nd->levels.size(); ++L) {
     const LevelInfo& li = nd->levels[L];
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (prof >= 2) {
+      cudaEventCreate(&pe0); cudaEventCreate(&pe1);
+      cudaEventRecord(pe0, s);
+    }
     {
       const unsigned gx = (unsigned)std::min<int64_t>(4096, (li.Fcount + 255) / 256);
       k_nd_zero<<<dim3(gx, B), 256, 0, s>>>(F, FE, li.Fbegin, li.Fcount);
@@ -907,6 +918,18 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
                                                                  nd->d_Coff + li.begin);
     }
     HH_CUDA_TRY(cudaGetLastError());
+    if (prof >= 2) {
+      cudaEventRecord(pe1, s);
+      cudaEventSynchronize(pe1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe0, pe1);
+      double fl = 0;
+      for (int t = li.begin; t < li.begin + li.count; ++t)
+        fl += 8.0 * (double)nd->fronts[t].s * nd->fronts[t].f * nd->fronts[t].f;
+      fprintf(stderr, "[hh factor] m=%d B=%d level %zu: %d fronts max_s=%d max_f=%d %.3f ms %.2f TFLOP/s\n",
+              nd->m, B, L, li.count, li.max_s, li.max_f, ms, fl * B / (ms * 1e-3) / 1e12);
+      cudaEventDestroy(pe0); cudaEventDestroy(pe1);
+    }
   }
   return HH_OK;
 }
@@ -930,13 +953,41 @@ static SolveCfg get_cfg(NDPlan* nd, int B) {
   return c;
 }
 
+// launch with programmatic stream serialisation (PDL); HH_NO_PDL=1 disables it
+static const bool g_pdl = getenv("HH_NO_PDL") == nullptr;
+template <typename... Args>
+static hh_status launch_pdl(void (*kern)(Args...), dim3 grid, int block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  HH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return HH_OK;
+}
+
+// CTAs per front of a per-level launch: one warp per row at most, and only as
+// many as needed to put ~4 CTAs on every SM
+static int g_fill_ctas = getenv("HH_ND_FILL") ? atoi(getenv("HH_ND_FILL")) : 4 * 148;
+static int level_split(int rows, int count, int B) {
+  const int by_rows = std::max(1, (rows + LT / 32 - 1) / (LT / 32));
+  const int fill = std::max(1, (g_fill_ctas + count * B - 1) / (count * B));
+  return std::max(1, std::min(std::min(by_rows, fill), 65535));
+}
+
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                            VArg x, cudaStream_t s, SolveCfg c) {
   const int nlev = (int)nd->levels.size();
   SolveArgs A;
-  A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo;
-  A.gptr = nd->d_gptr; A.gidx = nd->d_gidx; A.F = F; A.FE = nd->F_entries;
-  A.work = work; A.WE = nd_work_entries(nd); A.zsE = nd->zs_entries; A.rhs = rhs; A.x = x;
+  A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo; A.gmap = nd->d_gmap;
+  A.F = F; A.FE = nd->F_entries;
+  A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
   const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
@@ -949,14 +1000,14 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = cut + 1; L <= Lb; ++L) {
     const LevelInfo& li = nd->levels[L];
-    if (li.max_s > VMAX) {
-      dim3 gg(li.count, std::max(1, std::min(64, (li.max_s + 255) / 256)), B);
-      k_nd_gather<<<gg, 256, 0, s>>>(A, li.begin);
+    if (li.max_f > VMAX) {
+      dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
+      HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
     }
-    const size_t sm = (size_t)std::min(li.max_s, VMAX) * sizeof(cplx);
+    const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dim3 g(li.count, std::max(1, std::min(1024, (li.max_u + 31) / 32)), B);
-    k_nd_fwd<<<g, 256, sm, s>>>(A, li.begin);
+    dim3 g(li.count, level_split(li.max_u, li.count, B), B);
+    HH_TRY(launch_pdl(k_nd_fwd, g, LT, sm, s, A, li.begin));
   }
   if (Lb < nlev - 1) {
     cudaLaunchConfig_t cfg = {};
@@ -971,15 +1022,16 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    HH_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_nd_cluster, A, (const int64_t*)nd->d_lvr, Lb + 1, nlev, 1,
-                                   1, (const int*)nd->d_sep_front, (const int*)nd->d_halo_front));
+    HH_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_nd_cluster, A, (const int64_t*)nd->d_lvr, Lb + 1, nlev,
+                                   (const int*)nd->d_sep_front, (const int*)nd->d_halo_front,
+                                   (const int*)nd->d_pos_front));
   }
   for (int L = Lb; L > cut; --L) {
     const LevelInfo& li = nd->levels[L];
     const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    dim3 g(li.count, std::max(1, std::min(1024, (li.max_s + 31) / 32)), B);
-    k_nd_bwd<<<g, 256, sm, s>>>(A, li.begin);
+    dim3 g(li.count, level_split(li.max_s, li.count, B), B);
+    HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
   }
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
@@ -1055,6 +1107,6 @@ int nd_solve_launches(const NDPlan* ndc, int B) {
   const int nlev = (int)nd->levels.size();
   const SolveCfg c = get_cfg(nd, B);
   int n = (c.sub_cut >= 0 ? 2 : 0) + 2 * (c.split - c.sub_cut) + (c.split < nlev - 1 ? 1 : 0);
-  for (int L = c.sub_cut + 1; L <= c.split; ++L) n += nd->levels[L].max_s > VMAX;
+  for (int L = c.sub_cut + 1; L <= c.split; ++L) n += nd->levels[L].max_f > VMAX;
   return n;
 }

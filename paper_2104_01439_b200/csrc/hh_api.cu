@@ -84,6 +84,16 @@ __global__ void k_vset(VArg x, VArg src, int64_t N, int mode, int64_t idx, const
     xb[i] = mode == 1 ? sb[i] : cmake((mode == 2 && i == idx) ? 1.0 : 0.0, 0.0);
 }
 
+// heterogeneous coefficients: c[e] = (k_e, beta k_e^sigma)
+__global__ void k_coef(const double* __restrict__ k, int64_t n, double beta, double sigma,
+                       double2* __restrict__ c) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double ke = k[e];
+    c[e] = make_double2(ke, beta * pow(ke, sigma));
+  }
+}
+
 hh_status vset(VArg x, VArg src, int64_t N, int B, int mode, int64_t idx, const int* st, cudaStream_t s) {
   const unsigned gx = (unsigned)std::min<int64_t>(1024, (N + 255) / 256);
   k_vset<<<dim3(gx, B), 256, 0, s>>>(x, src, N, mode, idx, st);
@@ -92,25 +102,84 @@ hh_status vset(VArg x, VArg src, int64_t N, int B, int mode, int64_t idx, const 
 }
 
 // ------------------------------------------------------------------ pools
+// Device block cache: buffers released by a destroyed handle / engine are kept
+// (per device, by size) and handed to the next setup of the same shape instead
+// of going back through cudaMalloc/cudaFree, which map/unmap pages and
+// synchronise the device (hundreds of ms for a multi-GB Krylov basis).  The
+// cache holds at most half the device memory; a failed cudaMalloc flushes it.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  size_t cached = 0;
+  void* take(int dev, size_t want, size_t* got) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = free_blocks.lower_bound({dev, want});
+    if (it == free_blocks.end() || it->first.first != dev) return nullptr;
+    if (it->first.second > want + want / 4 + (size_t(8) << 20)) return nullptr;   // too wasteful
+    void* p = it->second;
+    *got = it->first.second;
+    cached -= it->first.second;
+    free_blocks.erase(it);
+    return p;
+  }
+  bool give(int dev, void* p, size_t bytes) {
+    size_t tot = 0, fr = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
+    std::lock_guard<std::mutex> lk(mu);
+    if (cached + bytes > tot / 2) return false;
+    free_blocks.insert({{dev, bytes}, p});
+    cached += bytes;
+    return true;
+  }
+  void flush(int dev) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = free_blocks.begin(); it != free_blocks.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        cached -= it->first.second;
+        it = free_blocks.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+};
+BlockCache& block_cache() { static BlockCache* c = new BlockCache(); return *c; }   // never destroyed
+
 struct Pool {
   void* p = nullptr;
   size_t bytes = 0;
+  int dev = 0;
   hh_status ensure(size_t b) {
     if (b <= bytes && p) return HH_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    const size_t want = std::max<size_t>(b, 256);
+    release();
+    const size_t want = (std::max<size_t>(b, 256) + 511) / 512 * 512;
+    cudaGetDevice(&dev);
+    size_t got = 0;
+    if (void* c = block_cache().take(dev, want, &got)) {   // may be larger than asked
+      p = c;
+      bytes = got;
+      return HH_OK;
+    }
     if (cudaMalloc(&p, want) != cudaSuccess) {
       cudaGetLastError();
-      hh_set_error("cudaMalloc of %.3f GB failed", want / 1e9);
-      return HH_E_OOM;
+      block_cache().flush(dev);
+      if (cudaMalloc(&p, want) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        hh_set_error("cudaMalloc of %.3f GB failed", want / 1e9);
+        return HH_E_OOM;
+      }
     }
     bytes = want;
     return HH_OK;
   }
   template <typename T> T* as() const { return (T*)p; }
-  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  void release() {
+    if (p && !block_cache().give(dev, p, bytes)) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
 };
 
 // ND plans are shared by every engine (tree depends on (dim, m) only)
@@ -146,7 +215,7 @@ struct Engine {
   int device = 0;
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
-      cpart, dpart, hist;
+      cpart, dpart, hist, kstage;
   int* h_status = nullptr;   // pinned
   int h_cap = 0;
   // batch
@@ -181,7 +250,7 @@ struct Engine {
   ~Engine() {
     drop_graphs();
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
-                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist};
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage};
     for (Pool* p : all) p->release();
     if (h_status) cudaFreeHost(h_status);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
@@ -264,8 +333,19 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   return HH_OK;
 }
 
+// HH_PROFILE_SETUP=1: synchronise and print the setup phases (diagnostics only)
+static const bool g_prof_setup = getenv("HH_PROFILE_SETUP") != nullptr;
+static void prof_mark(Engine& E, const char* what, double& t) {
+  if (!g_prof_setup) return;
+  cudaStreamSynchronize(E.s);
+  const double t1 = now_s();
+  fprintf(stderr, "[hh setup] n=%d B=%d %-10s %9.3f ms\n", E.spec.n, E.B, what, 1e3 * (t1 - t));
+  t = t1;
+}
+
 hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   const double t0 = now_s();
+  double tp = t0;
   HH_CUDA_TRY(cudaSetDevice(E.device));
   E.drop_graphs();
   E.spec = sp;
@@ -294,18 +374,24 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
       if (B != 1) { hh_set_error("heterogeneous batches must have B = 1"); return HH_E_CONFIG; }
       Pool& cp = lev == 0 ? E.coef_f : E.coef_c;
       HH_TRY(cp.ensure(L.elems * 16));
+      HH_TRY(E.kstage.ensure(L.elems * 8));
       const double* kh = lev == 0 ? sp.kf : sp.kcoarse;
-      std::vector<double2> c(L.elems);
       for (int64_t e = 0; e < L.elems; ++e) {
         const double k = kh[e];
         if (!(k >= 0) || !std::isfinite(k)) {
           hh_set_error("k_elem[%lld] = %g invalid", (long long)e, k);
           return HH_E_CONFIG;
         }
-        c[e] = make_double2(k, sp.beta[0] * std::pow(k, sp.sigma[0]));
       }
-      HH_CUDA_TRY(cudaMemcpyAsync(cp.p, c.data(), L.elems * 16, cudaMemcpyHostToDevice, E.s));
-      HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+      // upload k_e only; (k_e, eps_e = beta k_e^sigma) is formed on the device (reading C2)
+      HH_CUDA_TRY(cudaMemcpyAsync(E.kstage.p, kh, L.elems * 8, cudaMemcpyHostToDevice, E.s));
+      {
+        const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (L.elems + 255) / 256);
+        k_coef<<<g, 256, 0, E.s>>>(E.kstage.as<double>(), L.elems, sp.beta[0], sp.sigma[0],
+                                   cp.as<double2>());
+        HH_CUDA_TRY(cudaGetLastError());
+      }
+      HH_CUDA_TRY(cudaStreamSynchronize(E.s));   // kh is caller memory (pageable)
       L.coef = cp.as<double2>();
     } else {
       Pool& kp = lev == 0 ? E.kcf : E.kcc;
@@ -356,12 +442,15 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   A.ks.its = (int*)(base + o_its); A.ks.jend = (int*)(base + o_je); A.ks.hist = E.hist.as<double>();
   E.nd_flag = (int*)(base + o_fl);
   HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
+  prof_mark(E, "pools+coef", tp);
   // coarse operator + factorisation
   HH_TRY(coarse_stencil(E.LC, B, E.stc.as<cplx>(), E.s));
   HH_TRY(nd_factor(P, B, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
+  prof_mark(E, "factor", tp);
   HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
   HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
                      varg(E.ec.as<cplx>(), Nc), E.s));
+  prof_mark(E, "autotune", tp);
   HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, B * sizeof(int), cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   for (int b = 0; b < B; ++b)
@@ -779,28 +868,40 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
     }
   }
   HH_CUDA_TRY(cudaSetDevice(common->device));
-  // group by grid size; batches bounded by a per-engine memory budget
+  // group by grid size; within a group, order by shift strength eps = beta k^sigma
+  // (stronger shift -> more FGMRES iterations) so samples of
+  // similar iteration counts share a lockstep batch; batches are bounded by a
+  // per-engine memory budget and by a node budget (B * N <= HH_SWEEP_NODES)
+  // that splits the large grids over several streams.
   std::map<int, std::vector<int>> groups;
   for (int i = 0; i < n; ++i) groups[smp[i].n_cells].push_back(i);
   const char* es = getenv("HH_SWEEP_STREAMS");
-  const int nstreams = std::max(1, es ? atoi(es) : 4);
+  const int nstreams = std::max(1, es ? atoi(es) : 8);
   const char* eb = getenv("HH_SWEEP_MAX_BATCH");
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
+  const char* en = getenv("HH_SWEEP_NODES");
+  const double node_budget = en ? atof(en) : 1.2e6;
   size_t freeb = 0, totb = 0;
   HH_CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
   (void)freeb;
-  const double budget = 0.70 * (double)totb / nstreams;   // engines persist: budget on total HBM
+  const double budget = 0.60 * (double)totb / nstreams;   // engines persist: budget on total HBM
   std::vector<std::vector<int>> batches;
   for (auto& kv : groups) {
+    std::vector<int>& gi = kv.second;
+    std::stable_sort(gi.begin(), gi.end(), [&](int a, int b) {
+      return smp[a].beta * std::pow(smp[a].k, smp[a].sigma) > smp[b].beta * std::pow(smp[b].k, smp[b].sigma);
+    });
     NDPlan* plan = nullptr;
     HH_TRY(get_plan(2, kv.first / 2 + 1, &plan));
     const int64_t per = per_sample_bytes(2, kv.first, m, plan);
-    const int bmax = (int)std::max<int64_t>(1, std::min<int64_t>(maxB, (int64_t)(budget / per)));
-    const int cnt = (int)kv.second.size();
+    const double Nn = (double)(kv.first + 1) * (kv.first + 1);
+    const int bmem = (int)std::max<int64_t>(1, std::min<int64_t>(maxB, (int64_t)(budget / per)));
+    const int bmax = std::max(1, std::min(bmem, (int)(node_budget / Nn)));
+    const int cnt = (int)gi.size();
     const int nb = (cnt + bmax - 1) / bmax;
     for (int k = 0; k < nb; ++k) {
       std::vector<int> bt;
-      for (int i = k * cnt / nb; i < (k + 1) * cnt / nb; ++i) bt.push_back(kv.second[i]);
+      for (int i = k * cnt / nb; i < (k + 1) * cnt / nb; ++i) bt.push_back(gi[i]);
       batches.push_back(bt);
     }
   }

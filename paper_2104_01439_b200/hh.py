@@ -14,7 +14,7 @@ import numpy as np
 import torch   # loads libcudart.so.12 into the process before libhh.so
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhh.so")
+LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")
 
 HH_OP_A0, HH_OP_AEPS, HH_OP_AEPS_COARSE = 0, 1, 2
 HH_COARSE_AUTO, HH_COARSE_ND = 0, 1
