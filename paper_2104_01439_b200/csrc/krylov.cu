@@ -35,6 +35,13 @@ __device__ __forceinline__ cplx block_sum(cplx v, cplx* sh) {
   return r;   // valid in thread 0
 }
 
+// this thread's share of sum_k dpart[k], k < gridDim.x (strided; combined by block_sum)
+__device__ __forceinline__ double grid_partial_sum(const double* dpart) {
+  double t = 0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += KT) t += dpart[k];
+  return t;
+}
+
 __device__ __forceinline__ bool last_block(unsigned* counter) {
   __shared__ bool amLast;
   __threadfence();
@@ -48,8 +55,13 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return amLast;
 }
 
-// h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..j -> H column j
-__global__ void __launch_bounds__(KT, 5) k_mdot(KArgs A) {
+// h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..j -> H column j.
+// Work unit = (vector q, sub-chunk of this CTA's nodes); warps take units
+// round-robin (balanced for any j), each lane keeps 8 predicated loads in
+// flight (no serial tail loop); unit partials are combined in shared memory in
+// a fixed order (deterministic).
+constexpr int MD_UNITS = 1024;   // max units per CTA (nv <= 128, sub-chunks <= 8)
+__global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
   const int j = *A.jdev;
@@ -61,34 +73,33 @@ __global__ void __launch_bounds__(KT, 5) k_mdot(KArgs A) {
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // stage this CTA's chunk of w in shared memory (chunk <= MDOT_CHUNK nodes)
   extern __shared__ double4 smem_raw[];
-  cplx* ws = reinterpret_cast<cplx*>(smem_raw);
-  const int len = (int)(hi - lo);
+  cplx* usum = reinterpret_cast<cplx*>(smem_raw);   // [MD_UNITS]
+  cplx* ws = usum + MD_UNITS;                       // this CTA's chunk of w
+  const int len = hi > lo ? (int)(hi - lo) : 0;
   for (int t = threadIdx.x; t < len; t += KT) ws[t] = w[lo + t];
   __syncthreads();
-  // warp-per-vector: warp w streams V[q] for q = w, w+8, ...; 8 independent global
-  // loads in flight per lane, no CTA barrier inside the loop
-  for (int q = warp; q < nv; q += KT / 32) {
+  const int S = max(1, min(8, (4 * (KT / 32) + nv - 1) / nv));   // sub-chunks per vector
+  const int sl = (len + S - 1) / S;
+  const int units = nv * S;
+  for (int u = warp; u < units; u += KT / 32) {
+    const int q = u / S, sub = u - q * S;
+    const int c0 = sub * sl, c1 = min(len, c0 + sl);
     const cplx* vq = V + (int64_t)q * N + lo;
     cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
-    int i = lane;
-    for (; i + 224 < len; i += 256) {
+    for (int i = c0 + lane; i < c1; i += 256) {
       cplx v[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = __ldg(&vq[i + 32 * t]);
+      for (int t = 0; t < 8; ++t) v[t] = (i + 32 * t < c1) ? __ldg(&vq[i + 32 * t]) : cmake(0, 0);
 #pragma unroll
       for (int t = 0; t < 8; t += 2) {
-        const cplx w0 = ws[i + 32 * t], w1 = ws[i + 32 * t + 32];
+        const cplx w0 = (i + 32 * t < c1) ? ws[i + 32 * t] : cmake(0, 0);
+        const cplx w1 = (i + 32 * t + 32 < c1) ? ws[i + 32 * t + 32] : cmake(0, 0);
         a0.x = fma(v[t].x, w0.x, fma(v[t].y, w0.y, a0.x));
         a0.y = fma(v[t].x, w0.y, fma(-v[t].y, w0.x, a0.y));
         a1.x = fma(v[t + 1].x, w1.x, fma(v[t + 1].y, w1.y, a1.x));
         a1.y = fma(v[t + 1].x, w1.y, fma(-v[t + 1].y, w1.x, a1.y));
       }
-    }
-    for (; i < len; i += 32) {
-      const cplx v0 = __ldg(&vq[i]), w0 = ws[i];
-      a0.x = fma(v0.x, w0.x, fma(v0.y, w0.y, a0.x)); a0.y = fma(v0.x, w0.y, fma(-v0.y, w0.x, a0.y));
     }
     cplx acc = cadd(a0, a1);
 #pragma unroll
@@ -96,15 +107,33 @@ __global__ void __launch_bounds__(KT, 5) k_mdot(KArgs A) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
-    if (lane == 0) part[q] = acc;
+    if (lane == 0) usum[u] = acc;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nv; q += KT) {
+    cplx acc = cmake(0, 0);
+    for (int sub = 0; sub < S; ++sub) acc = cadd(acc, usum[q * S + sub]);
+    part[q] = acc;
   }
   if (last_block(A.counter + b)) {
+    // column sums over the CTAs: one warp per entry, lanes stride the CTAs, fixed-order shuffle
     cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
     const cplx* P0 = A.cpart + (int64_t)b * gridDim.x * A.ldp;
-    for (int q = threadIdx.x; q < nv; q += KT) {
-      cplx s = cmake(0, 0);
-      for (int k = 0; k < (int)gridDim.x; ++k) s = cadd(s, P0[(int64_t)k * A.ldp + q]);
-      Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+    for (int q = warp; q < nv; q += KT / 32) {
+      cplx s0 = cmake(0, 0), s1 = cmake(0, 0);
+      int k = lane;
+      for (; k + 32 < (int)gridDim.x; k += 64) {
+        s0 = cadd(s0, P0[(int64_t)k * A.ldp + q]);
+        s1 = cadd(s1, P0[(int64_t)(k + 32) * A.ldp + q]);
+      }
+      if (k < (int)gridDim.x) s0 = cadd(s0, P0[(int64_t)k * A.ldp + q]);
+      cplx s = cadd(s0, s1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      if (lane == 0) Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
     }
     if (threadIdx.x == 0) A.counter[b] = 0u;
   }
@@ -115,14 +144,14 @@ __global__ void __launch_bounds__(KT, 5) k_mdot(KArgs A) {
 __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
-  __shared__ cplx cf[128];
+  __shared__ cplx cf[136];
   __shared__ cplx sh[KT / 32];
   const int j = *A.jdev;
   const int nv = j + 1;
   const int64_t N = A.N;
   cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
   const double* vs = A.vscale + (int64_t)b * A.ldv;
-  for (int q = threadIdx.x; q < nv; q += KT) cf[q] = cscale(Hcol[q], vs[q]);
+  for (int q = threadIdx.x; q < 136; q += KT) cf[q] = q < nv ? cscale(Hcol[q], vs[q]) : cmake(0, 0);
   __syncthreads();
   const cplx* V = A.V + (int64_t)b * A.Vbs;
   const cplx* w = A.w + (int64_t)b * N;
@@ -132,18 +161,16 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   double nrm = 0.0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += KT) {
     cplx a = w[i], a2 = cmake(0, 0);
-    int q = 0;
-    for (; q + 8 <= nv; q += 8) {   // 8 independent loads in flight
+    for (int q = 0; q < nv; q += 8) {   // 8 independent (predicated) loads in flight
       cplx v[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = __ldg(&V[(int64_t)(q + t) * N + i]);
+      for (int t = 0; t < 8; ++t) v[t] = (q + t < nv) ? __ldg(&V[(int64_t)(q + t) * N + i]) : cmake(0, 0);
 #pragma unroll
       for (int t = 0; t < 8; t += 2) {
         cfms(a, cf[q + t], v[t]);
         cfms(a2, cf[q + t + 1], v[t + 1]);
       }
     }
-    for (; q < nv; ++q) cfms(a, cf[q], __ldg(&V[(int64_t)q * N + i]));
     a = cadd(a, a2);
     Vout[i] = a;
     nrm += a.x * a.x + a.y * a.y;
@@ -152,9 +179,8 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   double* dpart = A.dpart + (int64_t)b * gridDim.x;
   if (threadIdx.x == 0) dpart[blockIdx.x] = r.x;
   if (!last_block(A.counter + b)) return;
+  const double ssum = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;
   if (threadIdx.x != 0) return;
-  double ssum = 0;
-  for (int k = 0; k < (int)gridDim.x; ++k) ssum += dpart[k];
   A.counter[b] = 0u;
   const double hn = sqrt(ssum);
   double* vsw = A.vscale + (int64_t)b * A.ldv;
@@ -265,9 +291,8 @@ __global__ void __launch_bounds__(KT) k_norm(KArgs A, VArg rv, int mode) {
   double* dpart = A.dpart + (int64_t)b * gridDim.x;
   if (threadIdx.x == 0) dpart[blockIdx.x] = s.x;
   if (!last_block(A.counter + b)) return;
+  const double t = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;
   if (threadIdx.x) return;
-  double t = 0;
-  for (int k = 0; k < (int)gridDim.x; ++k) t += dpart[k];
   A.counter[b] = 0u;
   const double nr = sqrt(t);
   if (mode == 2) { A.ks.rtrue[b] = nr; return; }
@@ -294,7 +319,7 @@ __global__ void k_clear_jend(KArgs A, int B) {
 
 // ================================================================ host side
 hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
-  const size_t sm = (size_t)((A.N + A.nblk - 1) / A.nblk) * sizeof(cplx);
+  const size_t sm = (size_t)(MD_UNITS + (A.N + A.nblk - 1) / A.nblk) * sizeof(cplx);
   if (sm > 48 * 1024)
     HH_CUDA_TRY(cudaFuncSetAttribute(k_mdot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A);
