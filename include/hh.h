@@ -71,6 +71,19 @@ typedef struct {
   int32_t device;               /* CUDA device ordinal                                      */
   void*   stream;               /* cudaStream_t for every async call on this handle (NULL = legacy default) */
   int32_t max_restart;          /* Krylov workspace: largest FGMRES restart length (m) this handle will run */
+  /* Slab decomposition of ONE solve (north_star "slab decomposition,
+   * with NCCL halo exchange ... and allreduce for Arnoldi inner products").  The
+   * planes 0..n of the slowest axis (y in 2D, z in 3D) are cut into S slabs with
+   * even boundaries (hh_slab_bounds); the coarse solve is replicated.
+   *  - nslabs_local = S > 1, nccl_id = NULL: all S slabs in this process (the
+   *    exchanges are device copies; same arithmetic as S processes).
+   *  - nccl_id != NULL: slab `rank` of S = nranks processes (one per GPU), NCCL
+   *    communicator created from the id (collective: every rank calls setup).
+   * User vectors of a slab handle hold the handle's OWNED planes only
+   * (hh_local_layout); with S = 1 that is the whole grid.                    */
+  int32_t nslabs_local;         /* 0 or 1: no in-process slabs                              */
+  int32_t rank, nranks;         /* NCCL process group (used iff nccl_id != NULL)            */
+  const void* nccl_id;          /* 128-byte ncclUniqueId from hh_nccl_unique_id(), or NULL  */
 } hh_problem_desc;
 
 typedef struct {
@@ -108,11 +121,27 @@ typedef struct {
  * the 2h mesh) and its factorisation, Krylov workspace.  blocks. */
 hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out);
 
-/* Node counts of the fine and coarse level.                                    */
+/* Node counts: fine = this handle's owned nodes (the user-vector length; the
+ * whole grid (n+1)^dim without slabs), coarse = (n/2+1)^dim (replicated).      */
 hh_status hh_layout(const hh_problem* p, int64_t* n_fine_nodes, int64_t* n_coarse_nodes);
 
+/* Owned part of the fine grid: n_local_nodes = n_planes * (n+1)^(dim-1) nodes of
+ * the global planes [first_plane, first_plane + n_planes), x fastest.          */
+hh_status hh_local_layout(const hh_problem* p, int64_t* n_local_nodes, int64_t* first_plane,
+                          int64_t* n_planes);
+
+/* Slab bounds used by the slab decomposition: z[0..nslabs], slab k owns the
+ * planes [z[k], z[k+1]) (host only, no GPU needed).                            */
+hh_status hh_slab_bounds(int32_t n_cells, int32_t nslabs, int32_t* z);
+
+/* A fresh ncclUniqueId (128 bytes) for hh_problem_desc.nccl_id; call on one rank
+ * and broadcast (e.g. with torch.distributed).  NCCL is loaded at run time;
+ * HH_E_NCCL if it cannot be loaded.                                            */
+hh_status hh_nccl_unique_id(void* id128);
+
 /* y = A x with A = A_0 | A_eps (fine, matrix-free) | A_eps^{(1)} (coarse).
- * x, y: device complex128, distinct.  async. (PAPER.md:387-396 semi matrix-free) */
+ * x, y: device complex128, distinct; fine: owned-node vectors (hh_layout),
+ * coarse: full coarse vectors.  async. (PAPER.md:387-396 semi matrix-free) */
 hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void* y);
 
 /* z = P_eps^{-1} f: one V(nu_pre, nu_post) cycle from a zero initial guess

@@ -982,11 +982,11 @@ static int level_split(int rows, int count, int B) {
 }
 
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                           VArg x, cudaStream_t s, SolveCfg c) {
+                           VArg x, cudaStream_t s, SolveCfg c, bool shareF) {
   const int nlev = (int)nd->levels.size();
   SolveArgs A;
   A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo; A.gmap = nd->d_gmap;
-  A.F = F; A.FE = nd->F_entries;
+  A.F = F; A.FE = shareF ? 0 : nd->F_entries;
   A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
   const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
@@ -1043,15 +1043,15 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
 }
 
 hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s) {
+                   VArg x, cudaStream_t s, bool shareF) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
-  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B));
+  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B), shareF);
 }
 
 // Empirical schedule choice on the real factor (called once per (tree, B) at
 // setup, outside graph capture): time the candidate schedules with CUDA events.
 hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool shareF) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   SolveCfg have;
   if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, B, &have)) return HH_OK;
@@ -1060,9 +1060,9 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   HH_CUDA_TRY(cudaEventCreate(&e0));
   HH_CUDA_TRY(cudaEventCreate(&e1));
   auto run = [&](SolveCfg c, float* ms) -> hh_status {
-    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c));   // warm
+    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF));   // warm
     HH_CUDA_TRY(cudaEventRecord(e0, s));
-    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c));
+    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF));
     HH_CUDA_TRY(cudaEventRecord(e1, s));
     HH_CUDA_TRY(cudaEventSynchronize(e1));
     HH_CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));

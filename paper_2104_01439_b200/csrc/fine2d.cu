@@ -177,7 +177,7 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     for (; _y < _h;) {                                                         \
       const int sx = t.R - (hal) + _x, sy = t.R - (hal) + _y;                  \
       const int gx = t.gx(sx), gy = t.gy(sy);                                  \
-      const bool in = (gx >= 0 && gx <= n && gy >= 0 && gy <= n);              \
+      const bool in = (gx >= 0 && gx <= n && gy >= rlo && gy <= rhi);          \
       const int si = sy * t.SX + sx;                                           \
       { __VA_ARGS__ }                                                          \
       _x += _r; _y += _q;                                                      \
@@ -185,12 +185,13 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     }                                                                          \
   }
 
+// g = virtual global base of the entry's vector; rows outside [rlo, rhi] read as 0
 __device__ __forceinline__ void load_region(cplx* sX, const cplx* __restrict__ g, const Tile& t,
-                                            int n, double scale) {
+                                            int n, double scale, int rlo, int rhi) {
   const int N1 = n + 1;
   for (int sy = threadIdx.x / 32; sy < t.SY; sy += NT / 32) {
     const int gy = t.gy(sy);
-    const bool rowin = gy >= 0 && gy <= n;
+    const bool rowin = gy >= rlo && gy <= rhi;
     for (int sx = threadIdx.x % 32; sx < t.SX; sx += 32) {
       const int gx = t.gx(sx);
       cplx v = cmake(0, 0);
@@ -223,7 +224,15 @@ struct FineK {   // per-launch constants
   const double2* coef; int64_t coef_bs;   // het
   const double2* kc;                       // constant k: [B]
   const int* st;
+  const int2* slab; int G;                 // slab layout (Level)
 };
+
+// tile placement inside entry b's owned rows; false: tile beyond the slab
+#define SLAB_TILE(P, b, n)                                                       \
+  const int2 sl = slab_of(P.slab, b, n);                                         \
+  const int rlo = max(0, sl.x - P.G), rhi = min(n, sl.y - 1 + P.G);              \
+  const int64_t vofs = (int64_t)(sl.x - P.G) * (n + 1);                          \
+  if (sl.x + (int)blockIdx.y * TY >= sl.y) return;
 
 // --------------------------------------------------------------------- apply
 template <bool HET, bool EPS>
@@ -232,18 +241,19 @@ __global__ void __launch_bounds__(NT) k_apply2d(FineK P, VArg x, VArg y, VArg su
   if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
   const int n = P.n;
+  SLAB_TILE(P, b, n)
   Tile t;
-  t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = 1; t.SX = TX + 2; t.SY = TY + 2;
+  t.X0 = blockIdx.x * TX; t.Y0 = sl.x + blockIdx.y * TY; t.R = 1; t.SX = TX + 2; t.SY = TY + 2;
   cplx* sX = reinterpret_cast<cplx*>(smem_raw);
   double2* sE = reinterpret_cast<double2*>(sX + t.SX * t.SY);
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const Const9 c9 = make_const9(kc, P.h, EPS);
-  load_region(sX, x.at(b), t, n, 1.0);
+  load_region(sX, x.at(b) - vofs, t, n, 1.0, rlo, rhi);
   if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   __syncthreads();
-  cplx* yb = y.at(b);
-  const cplx* sb = sub.p ? sub.at(b) : nullptr;
-  FOR_REGION(0, if (in) {
+  cplx* yb = y.at(b) - vofs;
+  const cplx* sb = sub.p ? sub.at(b) - vofs : nullptr;
+  FOR_REGION(0, if (in && gy < sl.y) {
     cplx ax = node_op<HET, EPS>(sX, si, t, gx, gy, n, P.h, sE, kc, c9);
     const int64_t gi = (int64_t)gy * (n + 1) + gx;
     if (sb) ax = csub(sb[gi], ax);
@@ -260,8 +270,9 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   extern __shared__ double4 smem_raw[];
   const int n = P.n, nu = P.nu;
   const double omega = P.omega, h = P.h;
+  SLAB_TILE(P, b, n)
   Tile t;
-  t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = nu + 1;
+  t.X0 = blockIdx.x * TX; t.Y0 = sl.x + blockIdx.y * TY; t.R = nu + 1;
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
   const int S = t.SX * t.SY;
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   double2* sE = reinterpret_cast<double2*>(sDi + S);
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const Const9 c9 = make_const9(kc, h, true);
-  load_region(sF, f.at(b), t, n, fs.at(b));
+  load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
   if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   __syncthreads();
   // D^{-1} and the first step from u = 0 (pointwise) on the full region
@@ -301,12 +312,12 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
-  // residual on halo 1 -> nxt ; u on the tile -> global
-  cplx* ub = uo.at(b);
+  // residual on halo 1 -> nxt ; u on the tile (owned rows) -> global
+  cplx* ub = uo.at(b) - vofs;
   FOR_REGION(1, if (in) {
     const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
     nxt[si] = csub(sF[si], ax);
-    if (sx >= t.R && sx < t.R + TX && sy >= t.R && sy < t.R + TY)
+    if (sx >= t.R && sx < t.R + TX && sy >= t.R && sy < t.R + TY && gy < sl.y)
       ub[(int64_t)gy * (n + 1) + gx] = cur[si];
   })
   __syncthreads();
@@ -317,7 +328,7 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
     const int i = threadIdx.x;   // (TX/2) x (TY/2) = 128 coarse nodes per tile
     if (i < (TX / 2) * (TY / 2)) {
       const int cx = t.X0 / 2 + (i % (TX / 2)), cy = t.Y0 / 2 + i / (TX / 2);
-      if (cx <= nc && cy <= nc) {
+      if (cx <= nc && cy <= nc && 2 * cy < sl.y) {
         const int sx = t.R + 2 * cx - t.X0, sy = t.R + 2 * cy - t.Y0;
         cplx acc = cmake(0, 0);
 #pragma unroll
@@ -347,8 +358,9 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
   extern __shared__ double4 smem_raw[];
   const int n = P.n, nu = P.nu;
   const double omega = P.omega, h = P.h;
+  SLAB_TILE(P, b, n)
   Tile t;
-  t.X0 = blockIdx.x * TX; t.Y0 = blockIdx.y * TY; t.R = nu + (WITH_W ? 1 : 0);
+  t.X0 = blockIdx.x * TX; t.Y0 = sl.x + blockIdx.y * TY; t.R = nu + (WITH_W ? 1 : 0);
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
   const int S = t.SX * t.SY;
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
@@ -358,9 +370,9 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
   double2* sE = reinterpret_cast<double2*>(sDi + S);
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const Const9 c9e = make_const9(kc, h, true);
-  load_region(sF, f.at(b), t, n, fs.at(b));
+  load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
   if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
-  const cplx* u = uin.at(b);
+  const cplx* u = uin.at(b) - vofs;
   const cplx* ecv = ecin.at(b);
   const int NC1 = n / 2 + 1;
   // u + I ec on the full region, D^{-1}
@@ -412,10 +424,10 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
-  cplx* zb = zo.at(b);
-  cplx* wb = WITH_W ? wo.at(b) : nullptr;
+  cplx* zb = zo.at(b) - vofs;
+  cplx* wb = WITH_W ? wo.at(b) - vofs : nullptr;
   const Const9 c90 = make_const9(kc, h, false);
-  FOR_REGION(0, if (in) {
+  FOR_REGION(0, if (in && gy < sl.y) {
     const int64_t gi = (int64_t)gy * (n + 1) + gx;
     zb[gi] = cur[si];
     if (WITH_W) wb[gi] = node_op<HET, false>(cur, si, t, gx, gy, n, h, sE, kc, c90);
@@ -492,7 +504,8 @@ hh_status set_smem(const void* fn, size_t bytes) {
 FineK make_k(const Level& L, int nu, double omega, const int* st) {
   FineK P;
   P.n = L.n; P.h = L.h; P.omega = omega; P.nu = nu;
-  P.coef = L.coef; P.coef_bs = L.elems; P.kc = L.kc; P.st = st;
+  P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc; P.st = st;
+  P.slab = L.slab; P.G = L.G;
   return P;
 }
 
@@ -502,7 +515,7 @@ FineK make_k(const Level& L, int nu, double omega, const int* st) {
 hh_status fine_apply2d(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                        cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
+  dim3 grid((n + 1 + TX - 1) / TX, (L.maxloc + TY - 1) / TY, B);
   const size_t sm = smem_bytes(1, 1, L.het);
   const FineK P = make_k(L, 0, 0, st);
 #define LAUNCH_APPLY(H, E)                                        \
@@ -523,7 +536,7 @@ hh_status fine_apply2d(const Level& L, int B, const int* st, int op, VArg x, VAr
 hh_status fine_pre2d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
                      VArg u, VArg rc, cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
+  dim3 grid((n + 1 + TX - 1) / TX, (L.maxloc + TY - 1) / TY, B);
   const size_t sm = smem_bytes(nu + 1, 4, L.het);
   const FineK P = make_k(L, nu, omega, st);
   if (L.het) {
@@ -540,7 +553,7 @@ hh_status fine_pre2d(const Level& L, int B, const int* st, int nu, double omega,
 hh_status fine_post2d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
                       VArg u, VArg ec, VArg z, VArg w, cudaStream_t s) {
   const int n = L.n;
-  dim3 grid((n + 1 + TX - 1) / TX, (n + 1 + TY - 1) / TY, B);
+  dim3 grid((n + 1 + TX - 1) / TX, (L.maxloc + TY - 1) / TY, B);
   const bool ww = w.p != nullptr;
   const size_t sm = smem_bytes(nu + (ww ? 1 : 0), 4, L.het);
   const FineK P = make_k(L, nu, omega, st);
@@ -564,7 +577,7 @@ hh_status coarse_stencil2d(const Level& C, int B, cplx* st, cudaStream_t s) {
   const int bs = 128;
   dim3 g((unsigned)((N + bs - 1) / bs), B);
   if (C.het)
-    k_stencil2d<true><<<g, bs, 0, s>>>(C.n, C.h, C.coef, C.elems, nullptr, st);
+    k_stencil2d<true><<<g, bs, 0, s>>>(C.n, C.h, C.coef, C.coef_bs, nullptr, st);
   else
     k_stencil2d<false><<<g, bs, 0, s>>>(C.n, C.h, nullptr, 0, C.kc, st);
   HH_CUDA_TRY(cudaGetLastError());

@@ -26,14 +26,22 @@ struct F3 {
   const double2* kc;
   const int* st;
   int N1;
+  const int2* slab; int G; int maxloc;   // slab layout (Level)
+  int ext;                               // planes computed beyond the owned ones (per side)
 };
 
-__device__ __forceinline__ bool node_of(const F3& P, int& b, int& gx, int& gy, int& gz) {
+// node of this thread: planes [max(0, z0 - ext), min(n + 1, z1 + ext)) of entry b;
+// vofs = offset of the virtual global base of entry b's fine vectors
+__device__ __forceinline__ bool node_of(const F3& P, int& b, int& gx, int& gy, int& gz, int64_t& vofs) {
   gx = blockIdx.x * BX + threadIdx.x;
   gy = blockIdx.y * BY + threadIdx.y;
-  gz = blockIdx.z % P.N1;
-  b = blockIdx.z / P.N1;
-  return gx < P.N1 && gy < P.N1;
+  const int span = P.maxloc + 2 * P.ext;
+  b = blockIdx.z / span;
+  const int2 sl = slab_of(P.slab, b, P.n);
+  const int zlo = max(0, sl.x - P.ext), zhi = min(P.N1, sl.y + P.ext);
+  gz = zlo + (int)(blockIdx.z % span);
+  vofs = (int64_t)(sl.x - P.G) * P.N1 * P.N1;
+  return gx < P.N1 && gy < P.N1 && gz < zhi;
 }
 
 template <bool HET>
@@ -169,60 +177,65 @@ __device__ cplx diag3(const F3& P, const double2* cf, double2 kc, int gx, int gy
 template <bool HET, bool EPS>
 __global__ void __launch_bounds__(BX * BY) k_apply3d(F3 P, VArg x, VArg y, VArg sub) {
   int b, gx, gy, gz;
-  if (!node_of(P, b, gx, gy, gz)) return;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
   if (P.st && P.st[b]) return;
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
-  cplx ax = row3<HET, EPS>(P, x.at(b), cf, kc, gx, gy, gz);
+  cplx ax = row3<HET, EPS>(P, x.at(b) - vo, cf, kc, gx, gy, gz);
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
-  if (sub.p) ax = csub(sub.at(b)[gi], ax);
-  y.at(b)[gi] = ax;
+  if (sub.p) ax = csub((sub.at(b) - vo)[gi], ax);
+  (y.at(b) - vo)[gi] = ax;
 }
 
 // u_out = u + omega D^{-1} (f*fs - A_eps u)   (u == NULL: first step from zero)
 template <bool HET>
 __global__ void __launch_bounds__(BX * BY) k_jacobi3d(F3 P, VArg f, SArg fs, VArg u, VArg uo) {
   int b, gx, gy, gz;
-  if (!node_of(P, b, gx, gy, gz)) return;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
   if (P.st && P.st[b]) return;
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
-  const cplx fv = cscale(__ldg(&f.at(b)[gi]), fs.at(b));
+  const cplx fv = cscale(__ldg(&(f.at(b) - vo)[gi]), fs.at(b));
   const cplx di = cinv(diag3<HET>(P, cf, kc, gx, gy, gz));
   cplx v;
   if (u.p) {
-    const cplx* ub = u.at(b);
+    const cplx* ub = u.at(b) - vo;
     const cplx ax = row3<HET, true>(P, ub, cf, kc, gx, gy, gz);
     v = ub[gi];
     cfma(v, cscale(di, P.omega), csub(fv, ax));
   } else {
     v = cscale(cmul(di, fv), P.omega);
   }
-  uo.at(b)[gi] = v;
+  (uo.at(b) - vo)[gi] = v;
 }
 
 // r = f*fs - A_eps u  (fine residual)
 template <bool HET>
 __global__ void __launch_bounds__(BX * BY) k_resid3d(F3 P, VArg f, SArg fs, VArg u, VArg r) {
   int b, gx, gy, gz;
-  if (!node_of(P, b, gx, gy, gz)) return;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
   if (P.st && P.st[b]) return;
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
-  const cplx ax = row3<HET, true>(P, u.at(b), cf, kc, gx, gy, gz);
-  r.at(b)[gi] = csub(cscale(__ldg(&f.at(b)[gi]), fs.at(b)), ax);
+  const cplx ax = row3<HET, true>(P, u.at(b) - vo, cf, kc, gx, gy, gz);
+  (r.at(b) - vo)[gi] = csub(cscale(__ldg(&(f.at(b) - vo)[gi]), fs.at(b)), ax);
 }
 
-// rc = I^T r  (one thread per coarse node)
-__global__ void __launch_bounds__(BX * BY) k_restrict3d(int n, const int* st, VArg r, VArg rc) {
-  const int nc = n / 2, NC1 = nc + 1, N1 = n + 1;
+// rc = I^T r  (one thread per OWNED coarse node: coarse plane cz with 2 cz in [z0, z1))
+__global__ void __launch_bounds__(BX * BY) k_restrict3d(F3 P, int cspan, VArg r, VArg rc) {
+  const int n = P.n, nc = n / 2, NC1 = nc + 1, N1 = n + 1;
   const int cx = blockIdx.x * BX + threadIdx.x, cy = blockIdx.y * BY + threadIdx.y;
-  const int cz = blockIdx.z % NC1, b = blockIdx.z / NC1;
-  if (cx > nc || cy > nc) return;
-  if (st && st[b]) return;
-  const cplx* rb = r.at(b);
+  const int b = blockIdx.z / cspan;
+  const int2 sl = slab_of(P.slab, b, n);
+  const int cz = sl.x / 2 + (int)(blockIdx.z % cspan);
+  if (cx > nc || cy > nc || 2 * cz >= sl.y) return;
+  if (P.st && P.st[b]) return;
+  const cplx* rb = r.at(b) - (int64_t)(sl.x - P.G) * N1 * N1;
   cplx acc = cmake(0, 0);
   for (int dz = -1; dz <= 1; ++dz) {
     const int gz = 2 * cz + dz;
@@ -244,15 +257,15 @@ __global__ void __launch_bounds__(BX * BY) k_restrict3d(int n, const int* st, VA
 }
 
 // uo = u + I ec
-__global__ void __launch_bounds__(BX * BY) k_prolong3d(int n, const int* st, VArg u, VArg ec, VArg uo) {
-  const int N1 = n + 1, NC1 = n / 2 + 1;
-  const int gx = blockIdx.x * BX + threadIdx.x, gy = blockIdx.y * BY + threadIdx.y;
-  const int gz = blockIdx.z % N1, b = blockIdx.z / N1;
-  if (gx >= N1 || gy >= N1) return;
-  if (st && st[b]) return;
+__global__ void __launch_bounds__(BX * BY) k_prolong3d(F3 P, VArg u, VArg ec, VArg uo) {
+  const int n = P.n, N1 = n + 1, NC1 = n / 2 + 1;
+  int b, gx, gy, gz;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
+  if (P.st && P.st[b]) return;
   const cplx* e = ec.at(b);
   const int64_t gi = ((int64_t)gz * N1 + gy) * N1 + gx;
-  cplx v = u.at(b)[gi];
+  cplx v = (u.at(b) - vo)[gi];
   const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
   for (int k = 0; k <= (gz & 1); ++k)
     for (int j = 0; j <= (gy & 1); ++j)
@@ -262,14 +275,15 @@ __global__ void __launch_bounds__(BX * BY) k_prolong3d(int n, const int* st, VAr
         v.x += w * c.x;
         v.y += w * c.y;
       }
-  uo.at(b)[gi] = v;
+  (uo.at(b) - vo)[gi] = v;
 }
 
 // coarse stencil: st[b][node*27 + (dx+1) + 3(dy+1) + 9(dz+1)]
 template <bool HET>
 __global__ void k_stencil3d(F3 P, cplx* __restrict__ stv) {
   int b, gx, gy, gz;
-  if (!node_of(P, b, gx, gy, gz)) return;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
   const int n = P.n, N1 = P.N1;
   const double h = P.h;
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
@@ -323,20 +337,23 @@ __global__ void k_stencil3d(F3 P, cplx* __restrict__ stv) {
   for (int o = 0; o < 27; ++o) st[o] = e[o];
 }
 
-F3 make3(const Level& L, double omega, const int* st) {
+F3 make3(const Level& L, double omega, const int* st, int ext) {
   F3 P;
-  P.n = L.n; P.h = L.h; P.omega = omega; P.coef = L.coef; P.coef_bs = L.elems; P.kc = L.kc;
+  P.n = L.n; P.h = L.h; P.omega = omega; P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc;
   P.st = st; P.N1 = L.n + 1;
+  P.slab = L.slab; P.G = L.G; P.maxloc = L.maxloc; P.ext = ext;
   return P;
 }
-dim3 grid3(int N1, int B) { return dim3((N1 + BX - 1) / BX, (N1 + BY - 1) / BY, N1 * B); }
+dim3 grid3(const F3& P, int B) {
+  return dim3((P.N1 + BX - 1) / BX, (P.N1 + BY - 1) / BY, (P.maxloc + 2 * P.ext) * B);
+}
 
 }  // namespace
 
 hh_status fine_apply3d(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                        cudaStream_t s) {
-  const F3 P = make3(L, 0, st);
-  const dim3 g = grid3(P.N1, B), bl(BX, BY);
+  const F3 P = make3(L, 0, st, 0);
+  const dim3 g = grid3(P, B), bl(BX, BY);
   if (L.het) {
     if (op == HH_OP_A0) k_apply3d<true, false><<<g, bl, 0, s>>>(P, x, y, sub);
     else k_apply3d<true, true><<<g, bl, 0, s>>>(P, x, y, sub);
@@ -350,49 +367,57 @@ hh_status fine_apply3d(const Level& L, int B, const int* st, int op, VArg x, VAr
 
 static hh_status jac3(const Level& L, const F3& P, int B, VArg f, SArg fs, VArg u, VArg uo,
                       cudaStream_t s) {
-  const dim3 g = grid3(P.N1, B), bl(BX, BY);
+  const dim3 g = grid3(P, B), bl(BX, BY);
   if (L.het) k_jacobi3d<true><<<g, bl, 0, s>>>(P, f, fs, u, uo);
   else k_jacobi3d<false><<<g, bl, 0, s>>>(P, f, fs, u, uo);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
+// Pre-smoothing + residual + I^T.  With G ghost planes of f valid, step k of
+// the smoother is computed on ext = G - k + 1 planes beyond the owned ones and
+// the residual on ext = G - nu >= 1, which is what the restriction of the
+// owned coarse planes reads: no exchange inside the V-cycle's pre-smoothing.
 hh_status fine_pre3d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
                      VArg u, VArg rc, cudaStream_t s) {
-  const F3 P = make3(L, omega, st);
-  const int64_t N = L.nodes;
+  const int64_t N = L.stride;
   VArg t0 = varg(L.tmp, 2 * N), t1 = varg(L.tmp + N, 2 * N);
   // nu steps ending in u: ping-pong so that the last write lands in u
   VArg bufs[2] = {t0, u};
   int cur = (nu % 2 == 1) ? 1 : 0;   // first destination
   VArg none;
-  HH_TRY(jac3(L, P, B, f, fs, none, bufs[cur], s));
+  HH_TRY(jac3(L, make3(L, omega, st, L.G), B, f, fs, none, bufs[cur], s));
   for (int k = 2; k <= nu; ++k) {
-    HH_TRY(jac3(L, P, B, f, fs, bufs[cur], bufs[cur ^ 1], s));
+    HH_TRY(jac3(L, make3(L, omega, st, L.G - k + 1), B, f, fs, bufs[cur], bufs[cur ^ 1], s));
     cur ^= 1;
   }
-  const dim3 g = grid3(P.N1, B), bl(BX, BY);
-  if (L.het) k_resid3d<true><<<g, bl, 0, s>>>(P, f, fs, u, t1);
-  else k_resid3d<false><<<g, bl, 0, s>>>(P, f, fs, u, t1);
+  const F3 Pr = make3(L, omega, st, std::max(L.G - nu, 0));
+  const dim3 g = grid3(Pr, B), bl(BX, BY);
+  if (L.het) k_resid3d<true><<<g, bl, 0, s>>>(Pr, f, fs, u, t1);
+  else k_resid3d<false><<<g, bl, 0, s>>>(Pr, f, fs, u, t1);
   const int NC1 = L.n / 2 + 1;
-  const dim3 gc((NC1 + BX - 1) / BX, (NC1 + BY - 1) / BY, NC1 * B);
-  k_restrict3d<<<gc, bl, 0, s>>>(L.n, st, t1, rc);
+  const int cspan = L.maxloc / 2 + 1;
+  const dim3 gc((NC1 + BX - 1) / BX, (NC1 + BY - 1) / BY, cspan * B);
+  k_restrict3d<<<gc, bl, 0, s>>>(make3(L, omega, st, 0), cspan, t1, rc);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 
+// Prolongation + correction + post-smoothing (+ A_0 z): with u valid on G = nu + 1
+// ghost planes the prolongation runs on ext = nu + 1, step k on nu + 1 - k, A_0 on 0.
 hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
                       VArg u, VArg ec, VArg z, VArg w, cudaStream_t s) {
-  const F3 P = make3(L, omega, st);
-  const int64_t N = L.nodes;
+  const int64_t N = L.stride;
   VArg t0 = varg(L.tmp, 2 * N);
-  const dim3 g = grid3(P.N1, B), bl(BX, BY);
+  const int e0 = std::min(L.G, nu + 1);
+  const F3 Pp = make3(L, omega, st, e0);
+  const dim3 bl(BX, BY);
   // the nu post-steps must end in z: pick the prolongation target accordingly
   VArg bufs[2] = {t0, z};
   int cur = (nu % 2 == 0) ? 1 : 0;
-  k_prolong3d<<<g, bl, 0, s>>>(L.n, st, u, ec, bufs[cur]);
+  k_prolong3d<<<grid3(Pp, B), bl, 0, s>>>(Pp, u, ec, bufs[cur]);
   for (int k = 1; k <= nu; ++k) {
-    HH_TRY(jac3(L, P, B, f, fs, bufs[cur], bufs[cur ^ 1], s));
+    HH_TRY(jac3(L, make3(L, omega, st, std::max(e0 - k, 0)), B, f, fs, bufs[cur], bufs[cur ^ 1], s));
     cur ^= 1;
   }
   if (w.p) HH_TRY(fine_apply3d(L, B, st, HH_OP_A0, z, w, VArg(), s));
@@ -401,8 +426,8 @@ hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega
 }
 
 hh_status coarse_stencil3d(const Level& C, int B, cplx* st, cudaStream_t s) {
-  const F3 P = make3(C, 0, nullptr);
-  const dim3 g = grid3(P.N1, B), bl(BX, BY);
+  const F3 P = make3(C, 0, nullptr, 0);
+  const dim3 g = grid3(P, B), bl(BX, BY);
   if (C.het) k_stencil3d<true><<<g, bl, 0, s>>>(P, st);
   else k_stencil3d<false><<<g, bl, 0, s>>>(P, st);
   HH_CUDA_TRY(cudaGetLastError());

@@ -25,6 +25,7 @@
 #include <vector>
 #include "hh_internal.cuh"
 #include "krylov.cuh"
+#include "comm.cuh"
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
@@ -73,15 +74,22 @@ double now_s() {
 }
 
 // ------------------------------------------------------------------ small kernels
-// mode 0: x = 0; mode 1: x = src; mode 2: unit point source at node `idx`
-__global__ void k_vset(VArg x, VArg src, int64_t N, int mode, int64_t idx, const int* st) {
+// Over a whole (ghosted) fine vector of N entries: mode 0: x = 0; mode 1: x = src;
+// mode 2: unit point source at GLOBAL node `idx` (placed if entry b owns it).
+__global__ void k_vset(VArg x, VArg src, int64_t N, int mode, int64_t idx, const int* st,
+                       const int2* slab, int n, int G, int64_t plane) {
   const int b = blockIdx.y;
   if (st && st[b]) return;
   cplx* xb = x.at(b);
   const cplx* sb = mode == 1 ? src.at(b) : nullptr;
+  int64_t loc = -1;
+  if (mode == 2) {
+    const int2 sl = slab_of(slab, b, n);
+    if (idx >= (int64_t)sl.x * plane && idx < (int64_t)sl.y * plane) loc = idx - (int64_t)(sl.x - G) * plane;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x)
-    xb[i] = mode == 1 ? sb[i] : cmake((mode == 2 && i == idx) ? 1.0 : 0.0, 0.0);
+    xb[i] = mode == 1 ? sb[i] : cmake((mode == 2 && i == loc) ? 1.0 : 0.0, 0.0);
 }
 
 // heterogeneous coefficients: c[e] = (k_e, beta k_e^sigma)
@@ -94,9 +102,11 @@ __global__ void k_coef(const double* __restrict__ k, int64_t n, double beta, dou
   }
 }
 
-hh_status vset(VArg x, VArg src, int64_t N, int B, int mode, int64_t idx, const int* st, cudaStream_t s) {
+hh_status vset(const Level& L, VArg x, VArg src, int B, int mode, int64_t idx, const int* st,
+               cudaStream_t s) {
+  const int64_t N = L.stride;
   const unsigned gx = (unsigned)std::min<int64_t>(1024, (N + 255) / 256);
-  k_vset<<<dim3(gx, B), 256, 0, s>>>(x, src, N, mode, idx, st);
+  k_vset<<<dim3(gx, B), 256, 0, s>>>(x, src, N, mode, idx, st, L.slab, L.n, L.G, L.plane);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
@@ -201,10 +211,44 @@ enum { T_PRE = 0, T_COARSE, T_POST, T_KRYLOV, T_NT };
 struct BatchSpec {
   int dim = 2, n = 0, B = 1, nu_pre = 2, nu_post = 2, m = 100;
   double omega = 0.6;
-  std::vector<double> k, beta, sigma;    // per sample (constant k)
-  const double* kf = nullptr;            // het (B == 1): host per-element k
+  std::vector<double> k, beta, sigma;    // per entry (constant k)
+  const double* kf = nullptr;            // het (one problem): host per-element k
   const double* kcoarse = nullptr;
+  // slab decomposition: the B entries are the slabs [slab_first, slab_first + B) of
+  // one problem cut into slabs_total slabs (reductions over the entries + comm)
+  bool slabmode = false;
+  int slabs_total = 1, slab_first = 0;
+  Comm* comm = nullptr;
 };
+
+// fine-vector layout of a batch: G ghost planes, entry stride, slab bounds
+struct FineLayout {
+  int G = 0, maxloc = 0;
+  int64_t plane = 0, stride = 0;
+  int64_t pad = 0;           // leading pad so that every owned view starts 256-B aligned
+  std::vector<int2> slabs;   // per entry
+  std::vector<int> all_z;    // bounds of every process' slab range (slab mode)
+};
+
+int64_t ipow(int64_t a, int d) { int64_t r = 1; while (d--) r *= a; return r; }
+
+FineLayout fine_layout(const BatchSpec& sp) {
+  FineLayout F;
+  F.G = std::max(sp.nu_pre, sp.nu_post) + 1;
+  F.plane = ipow(sp.n + 1, sp.dim - 1);
+  if (sp.slabmode) {
+    const std::vector<int> z = slab_bounds(sp.n, sp.slabs_total);
+    for (int b = 0; b < sp.B; ++b) F.slabs.push_back(make_int2(z[sp.slab_first + b], z[sp.slab_first + b + 1]));
+    const int per = sp.B;   // slabs per process
+    for (int q = 0; q <= sp.slabs_total / per; ++q) F.all_z.push_back(z[std::min(q * per, sp.slabs_total)]);
+  } else {
+    for (int b = 0; b < sp.B; ++b) F.slabs.push_back(make_int2(0, sp.n + 1));
+  }
+  for (const int2& z : F.slabs) F.maxloc = std::max(F.maxloc, z.y - z.x);
+  F.pad = (16 - (F.G * F.plane) % 16) % 16;
+  F.stride = ((F.pad + (int64_t)(F.maxloc + 2 * F.G) * F.plane + 15) / 16) * 16;
+  return F;
+}
 
 struct SampleOut {
   int status = 0, iterations = 0, converged = 0, restarts = 0;
@@ -215,7 +259,7 @@ struct Engine {
   int device = 0;
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
-      cpart, dpart, hist, kstage;
+      cpart, dpart, hist, kstage, slabp, hstage, ustage;
   int* h_status = nullptr;   // pinned
   int h_cap = 0;
   // batch
@@ -223,7 +267,10 @@ struct Engine {
   Level LF, LC;
   NDPlan* plan = nullptr;
   int B = 0, m = 0, nblk = 1, hist_len = 0;
-  int64_t N = 0, Nc = 0;
+  int64_t N = 0, Nc = 0;    // global fine / coarse nodes
+  FineLayout FL;
+  SlabCtx X;                // slab mode transport context
+  int Bf = 0;               // coarse factor copies (1 in slab mode: shared by the slabs)
   KArgs ka;
   int* jdev = nullptr;
   int* nd_flag = nullptr;
@@ -250,7 +297,7 @@ struct Engine {
   ~Engine() {
     drop_graphs();
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
-                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage};
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage};
     for (Pool* p : all) p->release();
     if (h_status) cudaFreeHost(h_status);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
@@ -266,11 +313,9 @@ hh_status engine_init(Engine& E, int device) {
   return HH_OK;
 }
 
-int64_t ipow(int64_t a, int d) { int64_t r = 1; while (d--) r *= a; return r; }
-
 // bytes of device workspace per sample for a (dim, n, m) batch
 int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {
-  const int64_t N = ipow(n + 1, dim), Nc = ipow(n / 2 + 1, dim);
+  const int64_t N = ipow(n + 1, dim + 0) + 6 * ipow(n + 1, dim - 1), Nc = ipow(n / 2 + 1, dim);
   const int S = dim == 2 ? 9 : 27;
   int64_t b = (int64_t)(2 * m + 1 + 4 + (dim == 3 ? 2 : 0)) * N * 16;
   b += Nc * (2 + S) * 16;
@@ -292,7 +337,7 @@ size_t ksmall_bytes(int B, int m) {
   const size_t ldv = m + 1, ldh = m + 1;
   auto r = [](size_t b) { return (b + 255) / 256 * 256; };
   return r(B * ldv * 8) * 2 + r(B * ldv * 16) * 3 + r((size_t)B * m * ldh * 16) + r(B * 8) * 3 +
-         r(B * 4) * 3 + r(16) + r(B * 4) * 2;
+         r(B * 4) * 3 + r(16) + r(B * 4) * 2 + r(B * (ldv + 1) * 16) + r(B * 8);
 }
 
 // Grow the engine's pools to hold batch `sp` (no-op when already large enough).
@@ -300,23 +345,28 @@ size_t ksmall_bytes(int B, int m) {
 // engine for its largest batch before any worker starts.
 hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   const int B = sp.B, dim = sp.dim, n = sp.n, m = sp.m;
-  const int64_t N = ipow(n + 1, dim), Nc = ipow(n / 2 + 1, dim);
+  const FineLayout FL = fine_layout(sp);
+  const int64_t N = FL.stride, Nc = ipow(n / 2 + 1, dim);
+  const int Bf = sp.slabmode ? 1 : B;
   NDPlan* P = nullptr;
   HH_TRY(get_plan(dim, n / 2 + 1, &P));
   const int S = dim == 2 ? 9 : 27;
-  const int nblk = krylov_blocks(N);
-  HH_TRY(E.V.ensure((size_t)B * (m + 1) * N * 16));
-  HH_TRY(E.Z.ensure((size_t)B * m * N * 16));
-  HH_TRY(E.w.ensure((size_t)B * N * 16));
-  HH_TRY(E.u.ensure((size_t)B * N * 16));
-  HH_TRY(E.bv.ensure((size_t)B * N * 16));
-  HH_TRY(E.xv.ensure((size_t)B * N * 16));
-  if (dim == 3) HH_TRY(E.tmp3.ensure((size_t)B * 2 * N * 16));
+  const int nblk = krylov_blocks((int64_t)FL.maxloc * FL.plane);
+  // fine vectors: B entries of N (ghosted, padded) nodes + 16 nodes of slack for the lead pad
+  HH_TRY(E.V.ensure(((size_t)B * (m + 1) * N + 16) * 16));
+  HH_TRY(E.Z.ensure(((size_t)B * m * N + 16) * 16));
+  HH_TRY(E.w.ensure(((size_t)B * N + 16) * 16));
+  HH_TRY(E.u.ensure(((size_t)B * N + 16) * 16));
+  HH_TRY(E.bv.ensure(((size_t)B * N + 16) * 16));
+  HH_TRY(E.xv.ensure(((size_t)B * N + 16) * 16));
+  if (dim == 3) HH_TRY(E.tmp3.ensure(((size_t)B * 2 * N + 16) * 16));
   HH_TRY(E.rc.ensure((size_t)B * Nc * 16));
   HH_TRY(E.ec.ensure((size_t)B * Nc * 16));
-  HH_TRY(E.stc.ensure((size_t)B * Nc * S * 16));
-  HH_TRY(E.F.ensure((size_t)B * nd_front_entries(P) * 16));
-  HH_TRY(E.cbuf.ensure((size_t)B * nd_cbuf_entries(P) * 16));
+  HH_TRY(E.stc.ensure((size_t)Bf * Nc * S * 16));
+  HH_TRY(E.F.ensure((size_t)Bf * nd_front_entries(P) * 16));
+  HH_TRY(E.cbuf.ensure((size_t)Bf * nd_cbuf_entries(P) * 16));
+  HH_TRY(E.slabp.ensure((size_t)B * sizeof(int2)));
+  if (sp.comm) HH_TRY(E.hstage.ensure((size_t)4 * FL.G * FL.plane * 16));
   HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
   HH_TRY(E.kcf.ensure((size_t)B * 16));
   HH_TRY(E.kcc.ensure((size_t)B * 16));
@@ -353,11 +403,38 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   E.B = B; E.m = m;
   E.N = ipow(n + 1, dim);
   E.Nc = ipow(n / 2 + 1, dim);
-  const int64_t N = E.N, Nc = E.Nc;
+  E.FL = fine_layout(sp);
+  E.Bf = sp.slabmode ? 1 : B;
+  const int64_t Nc = E.Nc;
+  const int64_t NS = E.FL.stride;   // entry stride of fine vectors (ghosted)
+  if (sp.slabmode)
+    for (const int2& z : E.FL.slabs)
+      if (z.y - z.x < E.FL.G || z.x % 2) {
+        hh_set_error("slab [%d, %d) has fewer than G = %d planes (n = %d, %d slabs)", z.x, z.y, E.FL.G,
+                     n, sp.slabs_total);
+        return HH_E_CONFIG;
+      }
   HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
   const NDPlan* P = E.plan;
   // pools
   HH_TRY(reserve_pools(E, sp));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.slabp.p, E.FL.slabs.data(), B * sizeof(int2), cudaMemcpyHostToDevice, E.s));
+  // transport context (slab mode)
+  E.X = SlabCtx();
+  E.X.B = B;
+  E.X.slab = E.slabp.as<int2>();
+  E.X.h_slab = E.FL.slabs;
+  E.X.all_z = E.FL.all_z;
+  E.X.G = E.FL.G;
+  E.X.maxloc = E.FL.maxloc;
+  E.X.nc1 = n / 2 + 1;
+  E.X.plane = E.FL.plane;
+  E.X.cplane = ipow(n / 2 + 1, dim - 1);
+  E.X.comm = sp.comm;
+  if (sp.comm) {
+    E.X.hsend = E.hstage.as<cplx>();
+    E.X.hrecv = E.hstage.as<cplx>() + 2 * E.FL.G * E.FL.plane;
+  }
   // per-level coefficients
   for (int lev = 0; lev < 2; ++lev) {
     Level& L = lev == 0 ? E.LF : E.LC;
@@ -366,12 +443,25 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
     L.h = 1.0 / L.n;
     L.nodes = ipow(L.n + 1, dim);
     L.elems = ipow(L.n, dim);
+    L.plane = ipow(L.n + 1, dim - 1);
     L.het = sp.kf != nullptr;
-    L.tmp = lev == 0 && dim == 3 ? E.tmp3.as<cplx>() : nullptr;
+    L.tmp = lev == 0 && dim == 3 ? E.tmp3.as<cplx>() + E.FL.pad : nullptr;
     L.coef = nullptr;
+    L.coef_bs = 0;   // heterogeneous coefficients: one problem, shared by its entries
     L.kc = nullptr;
+    if (lev == 0) {
+      L.slab = E.slabp.as<int2>();
+      L.G = E.FL.G;
+      L.maxloc = E.FL.maxloc;
+      L.stride = NS;
+    } else {
+      L.slab = nullptr;
+      L.G = 0;
+      L.maxloc = L.n + 1;
+      L.stride = L.nodes;
+    }
     if (L.het) {
-      if (B != 1) { hh_set_error("heterogeneous batches must have B = 1"); return HH_E_CONFIG; }
+      if (B != 1 && !sp.slabmode) { hh_set_error("heterogeneous batches must have B = 1"); return HH_E_CONFIG; }
       Pool& cp = lev == 0 ? E.coef_f : E.coef_c;
       HH_TRY(cp.ensure(L.elems * 16));
       HH_TRY(E.kstage.ensure(L.elems * 8));
@@ -406,7 +496,7 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   const int ldv = m + 1, ldh = m + 1;
   // Krylov CTAs per sample: enough for ONE sample to fill the GPU (the tail of a
   // batch is a single slow sample); independent of B, so batched == single results
-  E.nblk = krylov_blocks(N);
+  E.nblk = krylov_blocks((int64_t)E.FL.maxloc * E.FL.plane);
   E.hist_len = HIST_LEN;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
@@ -415,7 +505,7 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
                o_g = carve(B * ldv * 16), o_y = carve(B * ldv * 16), o_H = carve((size_t)B * m * ldh * 16),
                o_bn = carve(B * 8), o_res = carve(B * 8), o_rt = carve(B * 8), o_st = carve(B * 4),
                o_its = carve(B * 4), o_je = carve(B * 4), o_j = carve(16), o_fl = carve(B * 4),
-               o_cnt = carve(B * 4);
+               o_cnt = carve(B * 4), o_red = carve(B * (ldv + 1) * 16), o_red2 = carve(B * 8);
   HH_TRY(E.ksmall.ensure(off));
   HH_TRY(E.cpart.ensure((size_t)B * E.nblk * (m + 2) * 16));
   HH_TRY(E.dpart.ensure((size_t)B * E.nblk * 8));
@@ -423,10 +513,13 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   char* base = E.ksmall.as<char>();
   KArgs& A = E.ka;
   A = KArgs();
-  A.N = N;
-  A.V = E.V.as<cplx>(); A.Vbs = (int64_t)(m + 1) * N;
-  A.Z = E.Z.as<cplx>(); A.Zbs = (int64_t)m * N;
-  A.w = E.w.as<cplx>();
+  A.Nst = NS; A.n = n; A.G = E.FL.G; A.plane = E.FL.plane; A.slab = E.slabp.as<int2>();
+  A.V = E.V.as<cplx>() + E.FL.pad; A.Vbs = (int64_t)(m + 1) * NS;
+  A.Z = E.Z.as<cplx>() + E.FL.pad; A.Zbs = (int64_t)m * NS;
+  A.w = E.w.as<cplx>() + E.FL.pad;
+  A.slabred = sp.slabmode ? 1 : 0;
+  A.red = (cplx*)(base + o_red); A.ldr = ldv + 1;
+  A.red2 = (double*)(base + o_red2);
   A.H = (cplx*)(base + o_H); A.HB = (int64_t)m * ldh; A.ldh = ldh;
   A.vscale = (double*)(base + o_vs); A.cs = (double*)(base + o_cs);
   A.sn = (cplx*)(base + o_sn); A.g = (cplx*)(base + o_g); A.y = (cplx*)(base + o_y); A.ldv = ldv;
@@ -443,17 +536,17 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   E.nd_flag = (int*)(base + o_fl);
   HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
   prof_mark(E, "pools+coef", tp);
-  // coarse operator + factorisation
-  HH_TRY(coarse_stencil(E.LC, B, E.stc.as<cplx>(), E.s));
-  HH_TRY(nd_factor(P, B, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
+  // coarse operator + factorisation (slab mode: one copy, shared by the slabs)
+  HH_TRY(coarse_stencil(E.LC, E.Bf, E.stc.as<cplx>(), E.s));
+  HH_TRY(nd_factor(P, E.Bf, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
   prof_mark(E, "factor", tp);
   HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
   HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
-                     varg(E.ec.as<cplx>(), Nc), E.s));
+                     varg(E.ec.as<cplx>(), Nc), E.s, sp.slabmode));
   prof_mark(E, "autotune", tp);
-  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, B * sizeof(int), cudaMemcpyDeviceToHost, E.s));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, E.Bf * sizeof(int), cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
-  for (int b = 0; b < B; ++b)
+  for (int b = 0; b < E.Bf; ++b)
     if (E.h_status[b]) {
       hh_set_error("zero pivot in the coarse factorisation (sample %d: k=%g, beta=%g, sigma=%g, h=%g)",
                    b, sp.k.empty() ? 0.0 : sp.k[b], sp.beta[b], sp.sigma[b], E.LC.h);
@@ -464,8 +557,36 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
 }
 
 // vector views of the engine pools
-VArg vV(Engine& E, int jo) { return varg(E.V.as<cplx>(), (int64_t)(E.m + 1) * E.N, E.N, E.jdev, jo); }
-VArg vZ(Engine& E) { return varg(E.Z.as<cplx>(), (int64_t)E.m * E.N, E.N, E.jdev, 0); }
+VArg vV(Engine& E, int jo) {
+  return varg(E.V.as<cplx>() + E.FL.pad, (int64_t)(E.m + 1) * E.FL.stride, E.FL.stride, E.jdev, jo);
+}
+VArg vZ(Engine& E) { return varg(E.Z.as<cplx>() + E.FL.pad, (int64_t)E.m * E.FL.stride, E.FL.stride, E.jdev, 0); }
+VArg vfine(Engine& E, Pool& p) { return varg(p.as<cplx>() + E.FL.pad, E.FL.stride); }
+bool slab_mode(const Engine& E) { return E.spec.slabmode; }
+// coarse solve on all entries (shared factor in slab mode)
+hh_status coarse_solve_all(Engine& E, const int* st, VArg rhs, VArg x) {
+  return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E));
+}
+// Arnoldi reductions of the slab mode: partials -> (NCCL allreduce) -> finish on every entry
+hh_status krylov_mdot_all(Engine& E) {
+  HH_TRY(krylov_mdot(E.ka, E.B, E.s));
+  if (!slab_mode(E)) return HH_OK;
+  HH_TRY(slab_allreduce(E.X, (double*)E.ka.red, (size_t)2 * E.ka.ldr * E.B, E.s));
+  return krylov_mdot_fin(E.ka, E.B, E.s);
+}
+hh_status krylov_update_all(Engine& E) {
+  HH_TRY(krylov_update(E.ka, E.B, E.s));
+  if (!slab_mode(E)) return HH_OK;
+  HH_TRY(slab_allreduce(E.X, E.ka.red2, (size_t)E.B, E.s));
+  return krylov_update_fin(E.ka, E.B, E.s);
+}
+hh_status krylov_norm_all(Engine& E, VArg r, int mode) {
+  HH_TRY(krylov_norm(E.ka, E.B, r, mode, E.s));
+  if (!slab_mode(E)) return HH_OK;
+  HH_TRY(slab_allreduce(E.X, E.ka.red2, (size_t)E.B, E.s));
+  return krylov_norm_fin(E.ka, E.B, mode, E.s);
+}
+hh_status halo(Engine& E, VArg v) { return slab_mode(E) ? slab_halo(E.X, v, E.s) : HH_OK; }
 VArg vflat(Pool& p, int64_t bs) { return varg(p.as<cplx>(), bs); }
 
 // one FGMRES iteration for the whole batch (graph-capturable)
@@ -474,20 +595,22 @@ hh_status enqueue_iteration(Engine& E, bool timing) {
   cudaStream_t s = E.s;
   const SArg fs = sarg(E.ka.vscale, E.ka.ldv, E.jdev, 0);
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[0], s, cudaEventRecordExternal));
-  HH_TRY(fine_pre(E.LF, E.B, st, E.spec.nu_pre, E.spec.omega, vV(E, 0), fs, vflat(E.u, E.N),
+  HH_TRY(halo(E, vV(E, 0)));                     // ghost planes of f = v_j (slab mode)
+  HH_TRY(fine_pre(E.LF, E.B, st, E.spec.nu_pre, E.spec.omega, vV(E, 0), fs, vfine(E, E.u),
                   vflat(E.rc, E.Nc), s));
+  if (slab_mode(E)) HH_TRY(slab_coarse_allgather(E.X, vflat(E.rc, E.Nc), s));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[1], s, cudaEventRecordExternal));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[2], s, cudaEventRecordExternal));
-  HH_TRY(nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), vflat(E.rc, E.Nc),
-                  vflat(E.ec, E.Nc), s));
+  HH_TRY(coarse_solve_all(E, st, vflat(E.rc, E.Nc), vflat(E.ec, E.Nc)));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[3], s, cudaEventRecordExternal));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[4], s, cudaEventRecordExternal));
-  HH_TRY(fine_post(E.LF, E.B, st, E.spec.nu_post, E.spec.omega, vV(E, 0), fs, vflat(E.u, E.N),
-                   vflat(E.ec, E.Nc), vZ(E), vflat(E.w, E.N), s));
+  HH_TRY(halo(E, vfine(E, E.u)));                // ghost planes of the pre-smoothed u
+  HH_TRY(fine_post(E.LF, E.B, st, E.spec.nu_post, E.spec.omega, vV(E, 0), fs, vfine(E, E.u),
+                   vflat(E.ec, E.Nc), vZ(E), vfine(E, E.w), s));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[5], s, cudaEventRecordExternal));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[6], s, cudaEventRecordExternal));
-  HH_TRY(krylov_mdot(E.ka, E.B, s));
-  HH_TRY(krylov_update(E.ka, E.B, s));
+  HH_TRY(krylov_mdot_all(E));
+  HH_TRY(krylov_update_all(E));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[7], s, cudaEventRecordExternal));
   HH_TRY(krylov_advance(E.jdev, -1, s));
   return HH_OK;
@@ -495,7 +618,12 @@ hh_status enqueue_iteration(Engine& E, bool timing) {
 
 int64_t launches_per_iteration(const Engine& E) {
   const int fine = E.spec.dim == 2 ? 2 : (E.spec.nu_pre + 2 + 1 + E.spec.nu_post + 1);
-  return fine + nd_solve_launches(E.plan, E.B) + 3;
+  int slab = 0;
+  if (slab_mode(E)) {
+    const bool multi = E.X.comm && E.X.comm->nranks > 1;
+    slab = 2 * ((E.B > 1 ? 1 : 0) + (multi ? 2 : 0)) + (E.B > 1 ? 1 : 0) + 2;
+  }
+  return fine + nd_solve_launches(E.plan, E.B) + 3 + slab;
 }
 
 // two captured variants of one iteration: plain, and with phase events (sampled timing)
@@ -571,10 +699,10 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
   A.fixed_iters = o.fixed_iters;
   E.drop_graphs();   // KArgs (rtol, caps) are captured by value
   const int check = std::max(1, o.check_every);
-  HH_TRY(vset(xvec, VArg(), E.N, B, 0, 0, nullptr, s));
+  HH_TRY(vset(E.LF, xvec, VArg(), B, 0, 0, nullptr, s));
   HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
-  HH_TRY(vset(varg(A.V, A.Vbs), bvec, E.N, B, 1, 0, nullptr, s));        // V[0] = b
-  HH_TRY(krylov_norm(A, B, bvec, 0, s));                                  // ||b||, status
+  HH_TRY(vset(E.LF, varg(A.V, A.Vbs), bvec, B, 1, 0, nullptr, s));       // V[0] = b
+  HH_TRY(krylov_norm_all(E, bvec, 0));                                    // ||b||, status
   HH_TRY(sync_status(E));
   std::vector<int> restarts(B, 0);
   int running = count_running(E);
@@ -609,15 +737,17 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
     // restart the still-running samples: V[0] = b - A_0 x
     for (int b = 0; b < B; ++b) if (E.h_status[b] == HHK_RUN) restarts[b]++;
     HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
+    HH_TRY(halo(E, xvec));
     HH_TRY(fine_apply(E.LF, B, A.ks.status, HH_OP_A0, xvec, varg(A.V, A.Vbs), bvec, s));
-    HH_TRY(krylov_norm(A, B, varg(A.V, A.Vbs), 1, s));
+    HH_TRY(krylov_norm_all(E, varg(A.V, A.Vbs), 1));
     E.launches += 2;
     HH_TRY(sync_status(E));
     running = count_running(E);
   }
   // true residuals ||b - A_0 x||
-  HH_TRY(fine_apply(E.LF, B, nullptr, HH_OP_A0, xvec, vflat(E.w, E.N), bvec, s));
-  HH_TRY(krylov_norm(A, B, vflat(E.w, E.N), 2, s));
+  HH_TRY(halo(E, xvec));
+  HH_TRY(fine_apply(E.LF, B, nullptr, HH_OP_A0, xvec, vfine(E, E.w), bvec, s));
+  HH_TRY(krylov_norm_all(E, vfine(E, E.w), 2));
   E.launches += 2;
   std::vector<double> bn(B), res(B), rt(B);
   std::vector<int> its(B), stt(B);
@@ -638,7 +768,7 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
     r.converged = o.fixed_iters > 0 ? (r.rel_res_true <= o.rtol) : (stt[b] == HHK_CONVERGED);
     r.status = stt[b] == HHK_NAN ? HH_E_DIVERGED : (stt[b] == HHK_BREAKDOWN ? HH_E_BREAKDOWN : HH_OK);
   }
-  if (hist_host && B == 1) {
+  if (hist_host && (B == 1 || slab_mode(E))) {
     std::vector<double> h(its[0] + 1);
     HH_CUDA_TRY(cudaMemcpy(h.data(), A.ks.hist, (its[0] + 1) * 8, cudaMemcpyDeviceToHost));
     h[0] = 1.0;
@@ -671,7 +801,22 @@ struct hh_problem {
   hh_problem_desc d{};
   Engine E;
   cudaStream_t user = nullptr;
+  Comm* comm = nullptr;
+  int64_t n_local = 0;      // user-vector length: owned nodes of this handle's slabs
+  ~hh_problem() { comm_destroy(comm); }
 };
+
+extern "C" hh_status hh_nccl_unique_id(void* id128) {
+  if (!id128) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  return comm_unique_id(id128);
+}
+
+extern "C" hh_status hh_slab_bounds(int32_t n_cells, int32_t nslabs, int32_t* z) {
+  if (!z || nslabs < 1 || n_cells < 4 || n_cells % 2) { hh_set_error("bad argument"); return HH_E_ARG; }
+  const std::vector<int> b = slab_bounds(n_cells, nslabs);
+  for (int i = 0; i <= nslabs; ++i) z[i] = b[i];
+  return HH_OK;
+}
 
 extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out) {
   if (!d || !out) { hh_set_error("NULL argument"); return HH_E_ARG; }
@@ -684,43 +829,77 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   if (!d->k_elem && !(d->k_const >= 0)) { hh_set_error("k_const must be >= 0"); return HH_E_CONFIG; }
   if (d->max_restart < 1 || d->max_restart > 127) { hh_set_error("max_restart must be in 1..127"); return HH_E_CONFIG; }
   if (!(d->beta >= 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
+  const int nloc = std::max(1, d->nslabs_local);
+  const bool use_nccl = d->nccl_id != nullptr;
+  if (use_nccl && (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks || nloc != 1)) {
+    hh_set_error("NCCL slab mode needs 0 <= rank < nranks and nslabs_local <= 1");
+    return HH_E_CONFIG;
+  }
   hh_problem* p = new (std::nothrow) hh_problem();
   if (!p) return HH_E_OOM;
   p->d = *d;
   p->d.k_elem = p->d.k_elem_coarse = nullptr;
+  p->d.nccl_id = nullptr;
   p->user = (cudaStream_t)d->stream;
   hh_status st = engine_init(p->E, d->device);
+  if (st == HH_OK && use_nccl) st = comm_create(d->nccl_id, d->rank, d->nranks, d->device, &p->comm);
   if (st == HH_OK) {
     BatchSpec sp;
-    sp.dim = d->dim; sp.n = d->n_cells; sp.B = 1; sp.nu_pre = d->nu_pre; sp.nu_post = d->nu_post;
+    sp.dim = d->dim; sp.n = d->n_cells; sp.nu_pre = d->nu_pre; sp.nu_post = d->nu_post;
     sp.m = d->max_restart; sp.omega = d->omega;
-    sp.k = {d->k_const}; sp.beta = {d->beta}; sp.sigma = {d->sigma};
+    sp.slabmode = use_nccl || nloc > 1;
+    sp.B = use_nccl ? 1 : nloc;
+    sp.slabs_total = use_nccl ? d->nranks : nloc;
+    sp.slab_first = use_nccl ? d->rank : 0;
+    sp.comm = p->comm;
+    sp.k.assign(sp.B, d->k_const); sp.beta.assign(sp.B, d->beta); sp.sigma.assign(sp.B, d->sigma);
     sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
     st = enter(p->E, p->user);
     if (st == HH_OK) st = batch_setup(p->E, sp);
   }
   if (st != HH_OK) { delete p; return st; }
+  for (const int2& z : p->E.FL.slabs) p->n_local += (int64_t)(z.y - z.x) * p->E.FL.plane;
   *out = p;
   return HH_OK;
 }
 
 extern "C" hh_status hh_layout(const hh_problem* p, int64_t* nf, int64_t* nc) {
   if (!p) { hh_set_error("NULL handle"); return HH_E_ARG; }
-  if (nf) *nf = p->E.N;
+  if (nf) *nf = p->n_local;
   if (nc) *nc = p->E.Nc;
   return HH_OK;
 }
+
+extern "C" hh_status hh_local_layout(const hh_problem* p, int64_t* n_local_nodes, int64_t* first_plane,
+                                     int64_t* n_planes) {
+  if (!p) { hh_set_error("NULL handle"); return HH_E_ARG; }
+  const std::vector<int2>& z = p->E.FL.slabs;
+  if (n_local_nodes) *n_local_nodes = p->n_local;
+  if (first_plane) *first_plane = z.front().x;
+  if (n_planes) *n_planes = z.back().y - z.front().x;
+  return HH_OK;
+}
+
+namespace {
+// user vector (this handle's owned nodes) <-> ghosted engine vector of every entry
+hh_status user_in(Engine& E, const void* u, Pool& dst) {
+  return slab_user_copy(E.X, vfine(E, dst), const_cast<void*>(u), 0, E.s);
+}
+hh_status user_out(Engine& E, Pool& src, void* u) { return slab_user_copy(E.X, vfine(E, src), u, 1, E.s); }
+}  // namespace
 
 extern "C" hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void* y) {
   if (!p || !x || !y) { hh_set_error("NULL argument"); return HH_E_ARG; }
   if (x == y) { hh_set_error("apply_op: x and y must be distinct"); return HH_E_ARG; }
   Engine& E = p->E;
   HH_TRY(enter(E, p->user));
-  const VArg xv = varg((cplx*)x, 0), yv = varg((cplx*)y, 0);
   if (op == HH_OP_A0 || op == HH_OP_AEPS) {
-    HH_TRY(fine_apply(E.LF, 1, nullptr, op, xv, yv, VArg(), E.s));
+    HH_TRY(user_in(E, x, E.xv));
+    HH_TRY(halo(E, vfine(E, E.xv)));
+    HH_TRY(fine_apply(E.LF, E.B, nullptr, op, vfine(E, E.xv), vfine(E, E.w), VArg(), E.s));
+    HH_TRY(user_out(E, E.w, y));
   } else if (op == HH_OP_AEPS_COARSE) {
-    HH_TRY(fine_apply(E.LC, 1, nullptr, HH_OP_AEPS, xv, yv, VArg(), E.s));
+    HH_TRY(fine_apply(E.LC, 1, nullptr, HH_OP_AEPS, varg((cplx*)x, 0), varg((cplx*)y, 0), VArg(), E.s));
   } else {
     hh_set_error("apply_op: unknown op %d", op);
     return HH_E_ARG;
@@ -732,12 +911,16 @@ extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   if (!p || !f || !z) { hh_set_error("NULL argument"); return HH_E_ARG; }
   Engine& E = p->E;
   HH_TRY(enter(E, p->user));
-  HH_TRY(fine_pre(E.LF, 1, nullptr, E.spec.nu_pre, E.spec.omega, varg((cplx*)f, 0), SArg(),
-                  vflat(E.u, E.N), vflat(E.rc, E.Nc), E.s));
-  HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), vflat(E.rc, E.Nc),
-                  vflat(E.ec, E.Nc), E.s));
-  HH_TRY(fine_post(E.LF, 1, nullptr, E.spec.nu_post, E.spec.omega, varg((cplx*)f, 0), SArg(),
-                   vflat(E.u, E.N), vflat(E.ec, E.Nc), varg((cplx*)z, 0), VArg(), E.s));
+  HH_TRY(user_in(E, f, E.bv));
+  HH_TRY(halo(E, vfine(E, E.bv)));
+  HH_TRY(fine_pre(E.LF, E.B, nullptr, E.spec.nu_pre, E.spec.omega, vfine(E, E.bv), SArg(),
+                  vfine(E, E.u), vflat(E.rc, E.Nc), E.s));
+  if (slab_mode(E)) HH_TRY(slab_coarse_allgather(E.X, vflat(E.rc, E.Nc), E.s));
+  HH_TRY(coarse_solve_all(E, nullptr, vflat(E.rc, E.Nc), vflat(E.ec, E.Nc)));
+  HH_TRY(halo(E, vfine(E, E.u)));
+  HH_TRY(fine_post(E.LF, E.B, nullptr, E.spec.nu_post, E.spec.omega, vfine(E, E.bv), SArg(),
+                   vfine(E, E.u), vflat(E.ec, E.Nc), vfine(E, E.xv), VArg(), E.s));
+  HH_TRY(user_out(E, E.xv, z));
   return leave(E, p->user);
 }
 
@@ -746,7 +929,7 @@ extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
   Engine& E = p->E;
   HH_TRY(enter(E, p->user));
   HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
-                  varg((cplx*)e, 0), E.s));
+                  varg((cplx*)e, 0), E.s, true));
   return leave(E, p->user);
 }
 
@@ -772,7 +955,9 @@ extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, co
   HH_CUDA_TRY(cudaEventCreate(&e1));
   HH_CUDA_TRY(cudaEventRecord(e0, E.s));
   std::vector<SampleOut> out;
-  hh_status st = batch_solve(E, varg((cplx*)bv, 0), varg((cplx*)xv, 0), *o, out, res_hist);
+  hh_status st = user_in(E, bv, E.bv);
+  if (st == HH_OK) st = batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, res_hist);
+  if (st == HH_OK) st = user_out(E, E.xv, xv);
   HH_CUDA_TRY(cudaEventRecord(e1, E.s));
   HH_CUDA_TRY(cudaEventSynchronize(e1));
   float ms = 0;
@@ -795,11 +980,14 @@ extern "C" hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, voi
   if (!p || !b_host || !x_host) { hh_set_error("NULL argument"); return HH_E_ARG; }
   Engine& E = p->E;
   HH_TRY(enter(E, p->user));
-  HH_CUDA_TRY(cudaMemcpyAsync(E.bv.p, b_host, E.N * 16, cudaMemcpyHostToDevice, E.s));
+  HH_TRY(E.ustage.ensure((size_t)p->n_local * 16));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.ustage.p, b_host, p->n_local * 16, cudaMemcpyHostToDevice, E.s));
+  HH_TRY(user_in(E, E.ustage.p, E.bv));
   std::vector<SampleOut> out;
   const double t0 = now_s();
-  HH_TRY(batch_solve(E, vflat(E.bv, E.N), vflat(E.xv, E.N), *o, out, nullptr));
-  HH_CUDA_TRY(cudaMemcpyAsync(x_host, E.xv.p, E.N * 16, cudaMemcpyDeviceToHost, E.s));
+  HH_TRY(batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, nullptr));
+  HH_TRY(user_out(E, E.xv, E.ustage.p));
+  HH_CUDA_TRY(cudaMemcpyAsync(x_host, E.ustage.p, p->n_local * 16, cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   fill_report(p, out[0], now_s() - t0, r);
   return (hh_status)out[0].status;
@@ -974,9 +1162,9 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
       if (st == HH_OK) {
         const int half = sp.n / 2;
         const int64_t ctr = half + (int64_t)(sp.n + 1) * half;   // unit point source at the centre (C7)
-        st = vset(vflat(E.bv, E.N), VArg(), E.N, sp.B, 2, ctr, nullptr, E.s);
+        st = vset(E.LF, vfine(E, E.bv), VArg(), sp.B, 2, ctr, nullptr, E.s);
         const double t0 = now_s();
-        if (st == HH_OK) st = batch_solve(E, vflat(E.bv, E.N), vflat(E.xv, E.N), *o, res, nullptr);
+        if (st == HH_OK) st = batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, res, nullptr);
         t_solve = now_s() - t0;
       }
       if (st != HH_OK) {

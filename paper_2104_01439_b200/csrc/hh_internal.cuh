@@ -84,18 +84,35 @@ inline SArg sarg(const double* p, int64_t bs, const int* j = nullptr, int jo = 0
 }
 
 // ---------------------------------------------------------------- levels
-// Geometry + coefficients of one level for a batch of B samples.
+// Geometry + coefficients of one level for a batch of B entries.
+//
+// Slab layout (fine level): entry b owns the global planes [z0, z1) of the
+// slowest axis (y in 2D, z in 3D; slab[b] = (z0, z1)) and stores the planes
+// [z0 - G, z1 + G) (G ghost planes per side, filled by the halo exchange) in a
+// buffer of `stride` nodes.  Kernels index vectors with GLOBAL node numbers
+// through the virtual base  p - (z0 - G) * plane.  An independent sample is an
+// entry with (z0, z1) = (0, n+1); the coarse level has slab == NULL, G = 0.
 struct Level {
   int dim = 2;
   int n = 0;            // cells per side
-  int64_t nodes = 0;    // (n+1)^dim
+  int64_t nodes = 0;    // (n+1)^dim (global)
   int64_t elems = 0;    // n^dim
+  int64_t plane = 0;    // (n+1)^(dim-1)
   double h = 0;
   bool het = false;
-  const double2* coef = nullptr;   // het: [B][elems] (k_e, eps_e)
+  const double2* coef = nullptr;   // het: (k_e, eps_e) per element, global
+  int64_t coef_bs = 0;             // entry stride of coef (0: shared by all entries)
   const double2* kc = nullptr;     // constant: [B] (k, eps)
-  cplx* tmp = nullptr;             // 3D only: [B][2][nodes] scratch owned by the engine
+  cplx* tmp = nullptr;             // 3D only: [B][2][stride] scratch owned by the engine
+  const int2* slab = nullptr;      // device [B] (z0, z1), NULL = whole domain
+  int G = 0;                       // ghost planes per side
+  int maxloc = 0;                  // max owned planes over the entries (n+1 without slabs)
+  int64_t stride = 0;              // entry stride of fine vectors: (maxloc + 2G) * plane
 };
+
+__device__ __forceinline__ int2 slab_of(const int2* sl, int b, int n) {
+  return sl ? sl[b] : make_int2(0, n + 1);
+}
 
 // fine-level kernels (fine2d.cu / fine3d.cu); st: per-sample status (NULL = all run)
 hh_status fine_apply(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
@@ -119,8 +136,9 @@ int64_t nd_cbuf_entries(const NDPlan* p);         // pivot column buffer per sam
 // F: [B][front_entries]; stencil: [B][Nc*3^d]; work: [B][work]; cbuf: [B][cbuf]
 hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* cbuf, int* flag,
                     cudaStream_t s);
+// shareF: every entry uses the one factor at F (slabs of one problem)
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s);
+                   VArg x, cudaStream_t s, bool shareF = false);
 // choose the solve schedule for batch size B by timing candidates on the real factor
 hh_status nd_autotune(const NDPlan* p, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s);
+                      cudaStream_t s, bool shareF = false);

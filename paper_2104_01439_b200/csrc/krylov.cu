@@ -17,7 +17,6 @@
 
 namespace {
 constexpr int KT = 256;     // threads per CTA
-constexpr int VG = 8;       // vectors per dot group
 
 __device__ __forceinline__ cplx block_sum(cplx v, cplx* sh) {
 #pragma unroll
@@ -55,6 +54,12 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return amLast;
 }
 
+__device__ __forceinline__ void owned_view(const KArgs& A, int b, int64_t& off, int64_t& len) {
+  const int2 sl = slab_of(A.slab, b, A.n);
+  off = (int64_t)A.G * A.plane;
+  len = (int64_t)(sl.y - sl.x) * A.plane;
+}
+
 // h_i = <v_i, w> = vscale_i * sum conj(V_i) w, i = 0..j -> H column j.
 // Work unit = (vector q, sub-chunk of this CTA's nodes); warps take units
 // round-robin (balanced for any j), each lane keeps 8 predicated loads in
@@ -66,9 +71,11 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
   if (A.ks.status[b]) return;
   const int j = *A.jdev;
   const int nv = j + 1;
-  const int64_t N = A.N;
-  const cplx* V = A.V + (int64_t)b * A.Vbs;
-  const cplx* w = A.w + (int64_t)b * N;
+  int64_t off, N;
+  owned_view(A, b, off, N);
+  const int64_t NS = A.Nst;
+  const cplx* V = A.V + (int64_t)b * A.Vbs + off;
+  const cplx* w = A.w + (int64_t)b * NS + off;
   cplx* part = A.cpart + ((int64_t)b * gridDim.x + blockIdx.x) * A.ldp;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
@@ -85,7 +92,7 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
   for (int u = warp; u < units; u += KT / 32) {
     const int q = u / S, sub = u - q * S;
     const int c0 = sub * sl, c1 = min(len, c0 + sl);
-    const cplx* vq = V + (int64_t)q * N + lo;
+    const cplx* vq = V + (int64_t)q * NS + lo;
     cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
     for (int i = c0 + lane; i < c1; i += 256) {
       cplx v[8];
@@ -133,11 +140,29 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
         s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
         s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
       }
-      if (lane == 0) Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+      if (lane == 0) {
+        if (A.slabred) A.red[(int64_t)b * A.ldr + q] = s;
+        else Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+      }
     }
     if (threadIdx.x == 0) A.counter[b] = 0u;
   }
 }
+
+// slabred: H column j = vscale * (sum over the entries of the partials)
+__global__ void k_mdot_fin(KArgs A, int B) {
+  const int b = blockIdx.x;
+  if (A.ks.status[b]) return;
+  const int j = *A.jdev;
+  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+  for (int q = threadIdx.x; q <= j; q += blockDim.x) {
+    cplx s = cmake(0, 0);
+    for (int e = 0; e < B; ++e) s = cadd(s, A.red[(int64_t)e * A.ldr + q]);
+    Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+  }
+}
+
+__device__ void givens_tail(const KArgs& A, int b, int j, double ssum);
 
 // w' = w - sum_i (H_i vscale_i) V_i -> V[j+1] ; ||w'||^2 ; last block:
 // h_{j+1,j} = ||w'||, vscale_{j+1}, Givens on column j, status.
@@ -148,14 +173,16 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   __shared__ cplx sh[KT / 32];
   const int j = *A.jdev;
   const int nv = j + 1;
-  const int64_t N = A.N;
+  int64_t off, N;
+  owned_view(A, b, off, N);
+  const int64_t NS = A.Nst;
   cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
   const double* vs = A.vscale + (int64_t)b * A.ldv;
   for (int q = threadIdx.x; q < 136; q += KT) cf[q] = q < nv ? cscale(Hcol[q], vs[q]) : cmake(0, 0);
   __syncthreads();
-  const cplx* V = A.V + (int64_t)b * A.Vbs;
-  const cplx* w = A.w + (int64_t)b * N;
-  cplx* Vout = A.V + (int64_t)b * A.Vbs + (int64_t)(j + 1) * N;
+  const cplx* V = A.V + (int64_t)b * A.Vbs + off;
+  const cplx* w = A.w + (int64_t)b * NS + off;
+  cplx* Vout = A.V + (int64_t)b * A.Vbs + (int64_t)(j + 1) * NS + off;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
   double nrm = 0.0;
@@ -164,7 +191,7 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
     for (int q = 0; q < nv; q += 8) {   // 8 independent (predicated) loads in flight
       cplx v[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[t] = (q + t < nv) ? __ldg(&V[(int64_t)(q + t) * N + i]) : cmake(0, 0);
+      for (int t = 0; t < 8; ++t) v[t] = (q + t < nv) ? __ldg(&V[(int64_t)(q + t) * NS + i]) : cmake(0, 0);
 #pragma unroll
       for (int t = 0; t < 8; t += 2) {
         cfms(a, cf[q + t], v[t]);
@@ -182,6 +209,22 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   const double ssum = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;
   if (threadIdx.x != 0) return;
   A.counter[b] = 0u;
+  if (A.slabred) { A.red2[b] = ssum; return; }
+  givens_tail(A, b, j, ssum);
+}
+
+// slabred: ||w'||^2 = sum over the entries, then the Givens tail
+__global__ void k_update_fin(KArgs A, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || A.ks.status[b]) return;
+  double ssum = 0;
+  for (int e = 0; e < B; ++e) ssum += A.red2[e];
+  givens_tail(A, b, *A.jdev, ssum);
+}
+
+// h_{j+1,j} = sqrt(ssum), vscale_{j+1}, Givens rotations on column j, status
+__device__ void givens_tail(const KArgs& A, int b, int j, double ssum) {
+  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
   const double hn = sqrt(ssum);
   double* vsw = A.vscale + (int64_t)b * A.ldv;
   double* cs = A.cs + (int64_t)b * A.ldv;
@@ -266,24 +309,29 @@ __global__ void __launch_bounds__(KT) k_xupdate(KArgs A, VArg xv) {
   __shared__ cplx ys[128];
   for (int q = threadIdx.x; q < k; q += KT) ys[q] = A.y[(int64_t)b * A.ldv + q];
   __syncthreads();
-  const int64_t N = A.N;
-  const cplx* Z = A.Z + (int64_t)b * A.Zbs;
-  cplx* x = xv.at(b);
+  int64_t off, N;
+  owned_view(A, b, off, N);
+  const cplx* Z = A.Z + (int64_t)b * A.Zbs + off;
+  cplx* x = xv.at(b) + off;
   for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < N; i += (int64_t)gridDim.x * KT) {
     cplx a = x[i];
-    for (int q = 0; q < k; ++q) cfma(a, ys[q], __ldg(&Z[(int64_t)q * N + i]));
+    for (int q = 0; q < k; ++q) cfma(a, ys[q], __ldg(&Z[(int64_t)q * A.Nst + i]));
     x[i] = a;
   }
 }
+
+__device__ void norm_tail(const KArgs& A, int b, int mode, double t);
 
 // per-sample ||r||; mode 0: start (bnorm, V0 scale, g0); 1: restart; 2: true residual
 __global__ void __launch_bounds__(KT) k_norm(KArgs A, VArg rv, int mode) {
   const int b = blockIdx.y;
   if (mode == 1 && A.ks.status[b]) return;
   __shared__ cplx sh[KT / 32];
-  const cplx* r = rv.at(b);
+  int64_t off, N;
+  owned_view(A, b, off, N);
+  const cplx* r = rv.at(b) + off;
   double nrm = 0;
-  for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < A.N; i += (int64_t)gridDim.x * KT) {
+  for (int64_t i = (int64_t)blockIdx.x * KT + threadIdx.x; i < N; i += (int64_t)gridDim.x * KT) {
     const cplx a = r[i];
     nrm += a.x * a.x + a.y * a.y;
   }
@@ -294,6 +342,19 @@ __global__ void __launch_bounds__(KT) k_norm(KArgs A, VArg rv, int mode) {
   const double t = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;
   if (threadIdx.x) return;
   A.counter[b] = 0u;
+  if (A.slabred) { A.red2[b] = t; return; }
+  norm_tail(A, b, mode, t);
+}
+
+__global__ void k_norm_fin(KArgs A, int B, int mode) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || (mode == 1 && A.ks.status[b])) return;
+  double t = 0;
+  for (int e = 0; e < B; ++e) t += A.red2[e];
+  norm_tail(A, b, mode, t);
+}
+
+__device__ void norm_tail(const KArgs& A, int b, int mode, double t) {
   const double nr = sqrt(t);
   if (mode == 2) { A.ks.rtrue[b] = nr; return; }
   A.vscale[(int64_t)b * A.ldv] = nr > 0 ? 1.0 / nr : 0.0;
@@ -319,7 +380,7 @@ __global__ void k_clear_jend(KArgs A, int B) {
 
 // ================================================================ host side
 hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
-  const size_t sm = (size_t)(MD_UNITS + (A.N + A.nblk - 1) / A.nblk) * sizeof(cplx);
+  const size_t sm = (size_t)(MD_UNITS + (A.Nst + A.nblk - 1) / A.nblk) * sizeof(cplx);
   if (sm > 48 * 1024)
     HH_CUDA_TRY(cudaFuncSetAttribute(k_mdot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A);
@@ -345,6 +406,21 @@ hh_status krylov_cycle_end(const KArgs& A, int B, VArg x, cudaStream_t s) {
 }
 hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s) {
   k_norm<<<dim3(A.nblk, B), KT, 0, s>>>(A, r, mode);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s) {
+  k_mdot_fin<<<B, 128, 0, s>>>(A, B);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s) {
+  k_update_fin<<<(B + 31) / 32, 32, 0, s>>>(A, B);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+hh_status krylov_norm_fin(const KArgs& A, int B, int mode, cudaStream_t s) {
+  k_norm_fin<<<(B + 31) / 32, 32, 0, s>>>(A, B, mode);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

@@ -14,11 +14,21 @@ struct KState {              // per-sample device arrays, [B] each (hist: [B][hi
   double* hist = nullptr;    // |g_{j+1}| / ||b|| per iteration
 };
 
+// Fine vectors of entry b are ghosted slabs of Nst nodes (Level.stride); the
+// Krylov kernels work on the OWNED view: offset G * plane, length
+// (z1 - z0) * plane with (z0, z1) = slab[b] (the whole grid without slabs).
+// slabred = 1: the entries are slabs of ONE problem (and possibly one slab of a
+// multi-process problem): every reduction is left as a per-entry partial in
+// red*, summed over the entries (and across processes by the transport) and
+// finished by the *_fin kernels, so every entry holds identical Krylov state.
 struct KArgs {
-  int64_t N = 0;
-  cplx* V = nullptr; int64_t Vbs = 0;   // [B][m+1][N]
-  cplx* Z = nullptr; int64_t Zbs = 0;   // [B][m][N]
-  cplx* w = nullptr;                    // [B][N]
+  int64_t Nst = 0;                      // entry stride of a fine vector
+  int n = 0, G = 0;
+  int64_t plane = 0;
+  const int2* slab = nullptr;
+  cplx* V = nullptr; int64_t Vbs = 0;   // [B][m+1][Nst]
+  cplx* Z = nullptr; int64_t Zbs = 0;   // [B][m][Nst]
+  cplx* w = nullptr;                    // [B][Nst]
   cplx* H = nullptr; int64_t HB = 0; int ldh = 0;   // [B][m][ldh] column-major
   double* vscale = nullptr; double* cs = nullptr; cplx* sn = nullptr; cplx* g = nullptr;
   cplx* y = nullptr; int ldv = 0;       // [B][ldv]
@@ -30,6 +40,9 @@ struct KArgs {
   double rtol = 1e-6;
   int max_iters = 500, fixed_iters = 0, hist_len = 0;
   KState ks;
+  int slabred = 0;
+  cplx* red = nullptr; int ldr = 0;     // [B][ldr] multi-dot partials (slabred)
+  double* red2 = nullptr;               // [B] norm partials (slabred)
 };
 
 hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s);
@@ -37,3 +50,7 @@ hh_status krylov_update(const KArgs& A, int B, cudaStream_t s);
 hh_status krylov_advance(int* jdev, int v, cudaStream_t s);    // v < 0: ++j, else j = v
 hh_status krylov_cycle_end(const KArgs& A, int B, VArg x, cudaStream_t s);
 hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s);
+// slabred: finish a reduction after the partials were combined across processes
+hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s);
+hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s);
+hh_status krylov_norm_fin(const KArgs& A, int B, int mode, cudaStream_t s);

@@ -22,10 +22,10 @@ STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_C
           5: "HH_E_NCCL", 6: "HH_E_OOM", 7: "HH_E_SINGULAR", 8: "HH_E_BREAKDOWN",
           9: "HH_E_DIVERGED", 10: "HH_E_STATE"}
 
-EXPORTS = ["hh_setup_problem", "hh_layout", "hh_apply_op", "hh_vcycle", "hh_coarse_solve",
-           "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep", "hh_destroy_problem",
-           "hh_reset_timers", "hh_read_timers", "hh_sweep_timers", "hh_last_error",
-           "hh_version"]
+EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "hh_vcycle",
+           "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
+           "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
+           "hh_slab_bounds", "hh_nccl_unique_id", "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -33,7 +33,9 @@ class ProblemDesc(C.Structure):
                 ("k_elem", C.POINTER(C.c_double)), ("k_elem_coarse", C.POINTER(C.c_double)),
                 ("beta", C.c_double), ("sigma", C.c_double), ("nu_pre", C.c_int32),
                 ("nu_post", C.c_int32), ("omega", C.c_double), ("coarse_solver", C.c_int32),
-                ("device", C.c_int32), ("stream", C.c_void_p), ("max_restart", C.c_int32)]
+                ("device", C.c_int32), ("stream", C.c_void_p), ("max_restart", C.c_int32),
+                ("nslabs_local", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("nccl_id", C.c_void_p)]
 
 
 class FgmresOpts(C.Structure):
@@ -78,6 +80,9 @@ def _load():
     sigs = {
         "hh_setup_problem": [C.POINTER(ProblemDesc), C.POINTER(vp)],
         "hh_layout": [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+        "hh_local_layout": [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+        "hh_slab_bounds": [i32, i32, C.POINTER(C.c_int32)],
+        "hh_nccl_unique_id": [vp],
         "hh_apply_op": [vp, i32, vp, vp],
         "hh_vcycle": [vp, vp, vp],
         "hh_coarse_solve": [vp, vp, vp],
@@ -127,7 +132,12 @@ class Problem:
     """Owns one hh_problem handle (setup_problem ... destroy_problem)."""
 
     def __init__(self, dim, n_cells, k_const=0.0, k_elem=None, k_elem_coarse=None, beta=1.0,
-                 sigma=1.5, nu_pre=2, nu_post=2, omega=0.6, max_restart=100, device=None):
+                 sigma=1.5, nu_pre=2, nu_post=2, omega=0.6, max_restart=100, device=None,
+                 nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None):
+        """nslabs_local > 1: the solve is cut into that many slabs held by this
+        process; nccl_id (from nccl_unique_id(), shared by all ranks): this
+        process holds slab `rank` of `nranks` (one GPU per process).  Vectors
+        then hold this handle's owned planes (local_layout())."""
         self.handle = C.c_void_p()
         dev = torch.cuda.current_device() if device is None else device
         d = ProblemDesc()
@@ -146,13 +156,26 @@ class Problem:
         d.device = dev
         d.stream = _stream()
         d.max_restart = max_restart
+        d.nslabs_local, d.rank, d.nranks = nslabs_local, rank, nranks
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            d.nccl_id = C.cast(idbuf, C.c_void_p)
         with torch.cuda.device(dev):
             _check(lib.hh_setup_problem(C.byref(d), C.byref(self.handle)))
-        del keep
+        del keep, idbuf
         nf, nc = C.c_int64(), C.c_int64()
         _check(lib.hh_layout(self.handle, C.byref(nf), C.byref(nc)))
         self.n_fine, self.n_coarse = nf.value, nc.value
         self.dim, self.n_cells, self.device = dim, n_cells, dev
+
+    def local_layout(self):
+        """(n_local_nodes, first_plane, n_planes) of the owned slab range."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.hh_local_layout(self.handle, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     @classmethod
     def from_spec(cls, spec, max_restart=None, **kw):
@@ -260,3 +283,17 @@ def sweep_timers(reset_enable=-1):
 
 def version():
     return lib.hh_version().decode()
+
+
+def slab_bounds(n_cells, nslabs):
+    """Plane bounds z[0..nslabs] of the slab decomposition (slab k owns [z[k], z[k+1]))."""
+    z = (C.c_int32 * (nslabs + 1))()
+    _check(lib.hh_slab_bounds(n_cells, nslabs, z))
+    return list(z)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (call on one rank, broadcast to the others)."""
+    buf = C.create_string_buffer(128)
+    _check(lib.hh_nccl_unique_id(buf))
+    return buf.raw
