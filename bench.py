@@ -116,6 +116,22 @@ def combine_ranks(dev_ms, dofs, its, world, device):
     return dev_ms, float(dofs), float(its)
 
 
+def share_nccl_id(make_id, rank, device):
+    """Rank 0's 128-byte NCCL id, broadcast over the default process group."""
+    t = torch.zeros(128, dtype=torch.uint8, device=device)
+    if rank == 0:
+        t.copy_(torch.tensor(list(make_id()), dtype=torch.uint8))
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.broadcast(t, 0)
+    return bytes(t.cpu().tolist())
+
+
+def slab_part(vec, n, dim, z, rank):
+    """This rank's owned planes [z[rank], z[rank+1]) of a global fine vector."""
+    plane = (n + 1) ** (dim - 1)
+    return vec[z[rank] * plane: z[rank + 1] * plane]
+
+
 # ------------------------------------------------------------------ ours
 def run_ours(args, rank, world, dev):
     import paper_2104_01439_b200.hh as hh
@@ -138,12 +154,20 @@ def run_ours(args, rank, world, dev):
               "l2": "per-sample working sets are L2-resident; L2 flushed (512 MB write) between steps"}
     else:
         spec = config_spec(args.workload)
+        slabkw = {}
+        rhs = spec.rhs()
+        if world > 1:
+            # one solve, slab-decomposed over the ranks (NCCL halos + allreduces)
+            nid = share_nccl_id(hh.nccl_unique_id, rank, dev)
+            z = hh.slab_bounds(spec.n, world)
+            rhs = slab_part(rhs, spec.n, spec.dim, z, rank)
+            slabkw = {"nccl_id": nid, "rank": rank, "nranks": world}
 
-        b_dev = torch.from_numpy(spec.rhs()).to(dev)
+        b_dev = torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
         timers = {"on": False, "acc": None}
 
         def step():
-            gp = hh.Problem.from_spec(spec)       # setup + coarse factorisation (inside the step)
+            gp = hh.Problem.from_spec(spec, **slabkw)   # setup + coarse factorisation (inside the step)
             if timers["on"]:
                 gp.reset_timers(True)
             x, r = gp.fgmres_solve(b_dev, o=hh.opts(restart=spec.restart, rtol=spec.rtol,
@@ -158,11 +182,13 @@ def run_ours(args, rank, world, dev):
                             timers["acc"][ph][key] += t[ph][key]
                     timers["acc"]["launches"] += t["launches"]
             gp.close()
-            return r["iterations"], r["iterations"] * spec.n_nodes, [r]
+            # one solve over all ranks: each rank counts its share of the work
+            return r["iterations"] / world, r["iterations"] * spec.n_nodes / world, [r]
 
         wl = {"workload": f"{args.workload} (BASELINE configs[{args.workload[-1]}])",
               "n_cells": spec.n, "dim": spec.dim, "restart": spec.restart, "rtol": spec.rtol,
-              "l2": "Krylov basis > L2 (126 MB); L2 flushed between steps"}
+              "l2": "Krylov basis > L2 (126 MB); L2 flushed between steps",
+              "parallelism": f"slab{world}" if world > 1 else "single"}
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
         step()
@@ -210,18 +236,21 @@ def run_ours(args, rank, world, dev):
                       "h2d_bytes_per_step": len(samples) * (40 + 16),
                       "d2h_bytes_per_step": len(samples) * 56}
     else:
-        import paper_2104_01439_b200.hh as hh2
-        bh = torch.from_numpy(spec.rhs()).pin_memory().numpy()
-        xh = torch.zeros(spec.n_nodes, dtype=torch.complex128).pin_memory().numpy()
+        bh = torch.from_numpy(np.ascontiguousarray(rhs)).pin_memory().numpy()
+        xh = torch.zeros(bh.size, dtype=torch.complex128).pin_memory().numpy()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        gp = hh2.Problem.from_spec(spec)
-        r = gp.fgmres_solve_host(bh, xh, hh2.opts(restart=spec.restart, rtol=spec.rtol))
+        gp = hh.Problem.from_spec(spec, **slabkw)
+        r = gp.fgmres_solve_host(bh, xh, hh.opts(restart=spec.restart, rtol=spec.rtol))
         gp.close()
         e2e_s = time.perf_counter() - t0
+        if world > 1:
+            e2e_s = combine_ranks(e2e_s, 0.0, 0.0, world, dev)[0]
         kb = 0 if spec.k_fine is None else 8 * (spec.k_fine.size + spec.k_coarse.size)
         out["e2e"] = {"value": r["iterations"] * spec.n_nodes / e2e_s, "unit": UNIT,
-                      "h2d_bytes_per_step": 16 * spec.n_nodes + kb,
-                      "d2h_bytes_per_step": 16 * spec.n_nodes}
+                      "h2d_bytes_per_step": 16 * bh.size + kb,
+                      "d2h_bytes_per_step": 16 * bh.size}
     return out
 
 
@@ -332,7 +361,9 @@ def main():
                     "phases": phases}
     line = {"metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": out["ms_per_step"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "higher_is_better": True,
+            "scaling": "weak" if args.workload == "sweep" or world == 1 else "strong",
+            "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": out["wl"], "e2e": out["e2e"], "roofline": roof,
             "clocks": out["clocks"], "gpu_launches": int(tm["launches"]) if tm else None,
             "iterations_total": out["iterations_total"]}

@@ -63,3 +63,56 @@ def test_two_rank_gloo_reduction():
         assert t == 150.0                       # max over ranks
         assert d == want_dofs and i == 880      # sum over ranks
         assert not set(ids[0]) & set(ids[1])    # disjoint shards
+
+
+# ------------------------------------------------------------------ slab decomposition host logic
+def test_slab_bounds_partition_planes():
+    import paper_2104_01439_b200.hh as hh   # host-only entry point: no GPU needed
+    for n, S in [(8, 1), (64, 2), (64, 5), (256, 8), (1024, 8), (128, 3)]:
+        z = hh.slab_bounds(n, S)
+        assert len(z) == S + 1 and z[0] == 0 and z[-1] == n + 1
+        assert all(a < b for a, b in zip(z, z[1:]))
+        assert all(v % 2 == 0 for v in z[:-1])          # coarse planes 2Z split the same way
+        sizes = [b - a for a, b in zip(z, z[1:])]
+        assert max(sizes) - min(sizes) <= 3             # balanced up to the even rounding
+
+
+def _slab_worker(rank, world, port, q):
+    import numpy as np
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2104_01439_b200.hh as hh
+    rng = np.random.default_rng(123)
+    nid = bench.share_nccl_id(lambda: rng.integers(0, 256, 128, dtype=np.uint8).tobytes(), rank,
+                              torch.device("cpu"))
+    n, dim = 16, 3
+    glob = np.arange((n + 1) ** dim, dtype=np.complex128)
+    part = bench.slab_part(glob, n, dim, hh.slab_bounds(n, world), rank)
+    parts = [None] * world
+    dist.all_gather_object(parts, part.tolist())
+    ids = [None] * world
+    dist.all_gather_object(ids, nid)
+    q.put((rank, ids, parts))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_slab_setup():
+    """The bench's multi-GPU slab path: rank 0's NCCL id reaches every rank, and
+    the ranks' owned parts of a global vector tile it in order."""
+    import numpy as np
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ids, parts in out:
+        assert ids[0] == ids[1] and len(ids[0]) == 128
+        glue = np.concatenate([np.array(p) for p in parts])
+        assert np.array_equal(glue, np.arange(17 ** 3))
