@@ -39,6 +39,7 @@ from workloads import config_spec, sweep_samples  # noqa: E402
 from workloads.configs import sweep_sample_spec  # noqa: E402
 
 METRIC = "preconditioned FGMRES iterations*DOF/s (complex fp64)"
+SEARCH_COUNT, SEARCH_LEVELS = 48, (4, 5, 6, 7, 8, 9)
 UNIT = "it*DOF/s"
 SHARD = 8   # sweep residue classes
 
@@ -152,6 +153,22 @@ def run_ours(args, rank, world, dev):
         wl = {"workload": "cfg1 shift sweep (BASELINE configs[1])", "samples_per_rank": len(samples),
               "samples_total": len(samples) * world, "restart": 100, "rtol": 1e-6,
               "l2": "per-sample working sets are L2-resident; L2 flushed (512 MB write) between steps"}
+    elif args.workload == "search":
+        from workloads.configs import search_rhs, search_samples
+        samples = [x for x in search_samples(SEARCH_COUNT, seed=0, levels=SEARCH_LEVELS)
+                   if x["id"] % world == rank]
+        rhs = [search_rhs(x, seed=0) for x in samples]
+
+        def step():
+            res = hh.shift_search(samples, rhs)
+            its = sum(r["iterations_total"] for r in res)
+            dofs = sum(r["iterations_total"] * (x["n"] + 1) ** 2 for r, x in zip(res, samples))
+            return its, dofs, res
+
+        wl = {"workload": "shift search (PAPER.md Sec. 5 steps 1-6, SURVEY 8(f) 1)",
+              "samples_per_rank": len(samples), "levels": list(SEARCH_LEVELS), "tol": 1e-2,
+              "budget": "rtol 1e-8 / 50 iterations", "rhs": "U[-1,1] per sample, seeded",
+              "l2": "L2 flushed (512 MB write) between steps"}
     else:
         spec = config_spec(args.workload)
         slabkw = {}
@@ -196,7 +213,7 @@ def run_ours(args, rank, world, dev):
     if world > 1:
         dist.barrier()
     clk = Clocks(dev) if rank == 0 else None
-    if args.workload == "sweep":
+    if args.workload in ("sweep", "search"):
         hh.sweep_timers(1)
     else:
         timers["on"] = True
@@ -218,7 +235,7 @@ def run_ours(args, rank, world, dev):
         dist.barrier()
     clocks = clk.stop() if clk else None
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
-    if args.workload == "sweep":
+    if args.workload in ("sweep", "search"):
         tm = hh.sweep_timers(0)
     else:
         timers["on"] = False
@@ -228,13 +245,15 @@ def run_ours(args, rank, world, dev):
     out = {"value": value, "ms_per_step": dev_ms / args.steps, "wl": wl, "timers": tm,
            "clocks": clocks, "iterations_total": int(tot_its)}
     # e2e: same metric through the public API with host-side inputs/outputs each step
-    if args.workload == "sweep":
+    if args.workload in ("sweep", "search"):
         t0 = time.perf_counter()
-        its, dofs, _ = step()          # hh_sweep: host sample list in, host records out
+        its, dofs, _ = step()          # hh_sweep / hh_shift_search: host inputs in, host records out
         e2e_s = time.perf_counter() - t0
+        h2d = len(samples) * (40 + 16)
+        if args.workload == "search":
+            h2d = sum(16 * (x["n"] + 1) ** 2 for x in samples) * 12   # rhs per evaluation
         out["e2e"] = {"value": dofs / e2e_s, "unit": UNIT,
-                      "h2d_bytes_per_step": len(samples) * (40 + 16),
-                      "d2h_bytes_per_step": len(samples) * 56}
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": len(samples) * 56}
     else:
         bh = torch.from_numpy(np.ascontiguousarray(rhs)).pin_memory().numpy()
         xh = torch.zeros(bh.size, dtype=torch.complex128).pin_memory().numpy()
@@ -275,6 +294,22 @@ def oracle_rate(args, budget_s):
         dt = time.perf_counter() - t0
         return dofs / dt, (f"{done} samples of rank 0's sweep share (size-stratified), "
                            f"setup+factor+solve each, {its} iterations in {dt:.1f} s"), cores, dt
+    if args.workload == "search":
+        from oracle.shift_search import search_sample
+        from workloads.configs import search_rhs, search_sample_spec, search_samples
+        smp = sorted(search_samples(SEARCH_COUNT, seed=0, levels=SEARCH_LEVELS), key=lambda x: x["n"])
+        t0 = time.perf_counter()
+        dofs = done = 0
+        for x in smp[::max(1, len(smp) // 12)]:
+            its = []
+            search_sample(search_sample_spec(x), search_rhs(x, seed=0), iters=its)
+            dofs += sum(its) * (x["n"] + 1) ** 2
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return dofs / dt, (f"{done} search samples (size-stratified; golden-section, 12 oracle "
+                           f"solves each) in {dt:.1f} s"), cores, dt
     spec = config_spec(args.workload)
     t0 = time.perf_counter()
     op = OracleProblem(spec)
@@ -292,7 +327,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "cfg0", "cfg2", "cfg3"])
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "search", "cfg0", "cfg2", "cfg3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -84,6 +84,11 @@ typedef struct {
   int32_t nslabs_local;         /* 0 or 1: no in-process slabs                              */
   int32_t rank, nranks;         /* NCCL process group (used iff nccl_id != NULL)            */
   const void* nccl_id;          /* 128-byte ncclUniqueId from hh_nccl_unique_id(), or NULL  */
+  /* Shift exponent: 0 = fixed sigma; p = 1..3 = the fitted map sigma_p(k_e, l)
+   * of PAPER.md:437-443 with Table 1 row p, l = log2(n_cells)
+   * of the FINE mesh, evaluated per element on both levels (eps = beta k^sigma_p,
+   * PAPER.md:532-533).                                                       */
+  int32_t shift_map;
 } hh_problem_desc;
 
 typedef struct {
@@ -163,11 +168,36 @@ hh_status hh_fgmres_solve(hh_problem* p, const void* b, void* x, const hh_fgmres
 hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, void* x_host,
                                const hh_fgmres_opts* o, hh_fgmres_report* r);
 
+typedef struct {
+  int64_t id;
+  int32_t n_cells;              /* 2D, constant k                                          */
+  double  k, beta;              /* eps = beta k^sigma, sigma searched                       */
+} hh_search_sample;
+
+typedef struct {
+  int64_t id;
+  int32_t status, evaluations, iterations_total;
+  double  sigma_hat;            /* midpoint of the final bracket (width <= tol)             */
+  double  sigma_best, rho_best; /* best evaluated point and its rho                         */
+} hh_search_result;
+
 /* Sweep: for each 2D constant-k sample, set up, factor and solve with a unit
  * point source at the centre node (BASELINE configs[1]); common carries dim,
  * nu, omega, device, stream.  s, out: HOST arrays of n entries.  blocks. */
 hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
                    const hh_sample* s, int32_t n, hh_sample_result* out);
+
+/* Near-optimal shift search (Sec. 5 steps 1-6, step 5):
+ * for each sample, golden-section search of sigma in [sigma_lo, sigma_hi] (paper:
+ * [1, 2], tol 1e-2) minimising rho(sigma) = (r_end/r_0)^(1/end) of the FGMRES
+ * solve of A_0 u = f (x0 = 0, budget o: paper rtol 1e-8, max_iters 50)
+ * preconditioned by the V-cycle on A(k, beta k^sigma).  rhs[i]: HOST complex128
+ * right-hand side of sample i ((n+1)^2 nodes; paper: components U[-1,1]), reused
+ * for every sigma.  Tie f(c) == f(d) keeps [c, b]; a failed solve scores rho = 1.
+ * Every round of evaluations is one batched sweep.  s, rhs, out: HOST.  blocks. */
+hh_status hh_shift_search(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                          const hh_search_sample* s, int32_t n, const void* const* rhs,
+                          double sigma_lo, double sigma_hi, double tol, hh_search_result* out);
 
 hh_status hh_destroy_problem(hh_problem* p);
 

@@ -13,10 +13,12 @@ import numpy as np
 from . import fem
 from .fgmres import fgmres
 from .twogrid import TwoGrid
+from .shiftmap import map_shifts
 
 
 def coefficients(spec):
-    """Per-element k and eps on the fine and coarse meshes (readings C1, C2, C4)."""
+    """Per-element k and eps on the fine and coarse meshes (readings C1, C2, C4;
+    with spec.shift_map = p the fitted map sigma_p of PAPER.md:437-443, C20)."""
     ne_f = spec.n ** spec.dim
     ne_c = (spec.n // 2) ** spec.dim
     if spec.k_const is not None:
@@ -24,6 +26,10 @@ def coefficients(spec):
         kc = np.full(ne_c, spec.k_const)
     else:
         kf, kc = spec.k_fine, spec.k_coarse
+    p = getattr(spec, "shift_map", 0)
+    if p:
+        l = np.log2(spec.n)
+        return kf, map_shifts(kf, spec.beta, p, l), kc, map_shifts(kc, spec.beta, p, l)
     return kf, fem.shifts(kf, spec.beta, spec.sigma), kc, fem.shifts(kc, spec.beta, spec.sigma)
 
 

@@ -92,13 +92,32 @@ __global__ void k_vset(VArg x, VArg src, int64_t N, int mode, int64_t idx, const
     xb[i] = mode == 1 ? sb[i] : cmake((mode == 2 && i == loc) ? 1.0 : 0.0, 0.0);
 }
 
-// heterogeneous coefficients: c[e] = (k_e, beta k_e^sigma)
-__global__ void k_coef(const double* __restrict__ k, int64_t n, double beta, double sigma,
-                       double2* __restrict__ c) {
+// Shift-exponent map sigma_p(k, l) (Eq. shiftexp) with the
+// fitted weights of Table 1, rows p = 1, 2, 3:
+// (k_c0, k_c1, alpha_0, alpha_1)
+__host__ __device__ inline double sigma_map(double k, double l, int p) {
+  const double W[3][4] = {{0.4592788619853418, 2.5790032999702346, -0.6261637288068426, 1.7580549857142198},
+                          {0.5736926870738827, 2.5729974893966001, -0.6615199737374460, 1.5966386518185063},
+                          {0.6305770719029798, 2.4284320222555804, -0.4465407372367102, 0.1287828338493968}};
+  const double* w = W[p - 1];
+  const double kc = w[1] * exp(w[0] * l);
+  const double al = w[3] * exp(w[2] * l);
+  const double b = 2.0 - exp(-al * (k - kc));
+  return fmin(fmax(b, 1.0), 2.0);
+}
+
+// eps_e = beta k_e^sigma, sigma = the fixed exponent or sigma_p(k_e, l) (map_p > 0)
+__host__ __device__ inline double shift_of(double k, double beta, double sigma, int map_p, double l) {
+  return beta * pow(k, map_p > 0 ? sigma_map(k, l, map_p) : sigma);
+}
+
+// heterogeneous coefficients: c[e] = (k_e, eps_e)
+__global__ void k_coef(const double* __restrict__ k, int64_t n, double beta, double sigma, int map_p,
+                       double l, double2* __restrict__ c) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const double ke = k[e];
-    c[e] = make_double2(ke, beta * pow(ke, sigma));
+    c[e] = make_double2(ke, shift_of(ke, beta, sigma, map_p, l));
   }
 }
 
@@ -219,6 +238,7 @@ struct BatchSpec {
   bool slabmode = false;
   int slabs_total = 1, slab_first = 0;
   Comm* comm = nullptr;
+  int shift_map = 0;                     // > 0: sigma = sigma_p(k_e, log2 n) of Table 1 row p
 };
 
 // fine-vector layout of a batch: G ghost planes, entry stride, slab bounds
@@ -477,8 +497,8 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
       HH_CUDA_TRY(cudaMemcpyAsync(E.kstage.p, kh, L.elems * 8, cudaMemcpyHostToDevice, E.s));
       {
         const unsigned g = (unsigned)std::min<int64_t>(148 * 8, (L.elems + 255) / 256);
-        k_coef<<<g, 256, 0, E.s>>>(E.kstage.as<double>(), L.elems, sp.beta[0], sp.sigma[0],
-                                   cp.as<double2>());
+        k_coef<<<g, 256, 0, E.s>>>(E.kstage.as<double>(), L.elems, sp.beta[0], sp.sigma[0], sp.shift_map,
+                                   std::log2((double)n), cp.as<double2>());
         HH_CUDA_TRY(cudaGetLastError());
       }
       HH_CUDA_TRY(cudaStreamSynchronize(E.s));   // kh is caller memory (pageable)
@@ -486,7 +506,8 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
     } else {
       Pool& kp = lev == 0 ? E.kcf : E.kcc;
       std::vector<double2> c(B);
-      for (int b = 0; b < B; ++b) c[b] = make_double2(sp.k[b], sp.beta[b] * std::pow(sp.k[b], sp.sigma[b]));
+      for (int b = 0; b < B; ++b)
+        c[b] = make_double2(sp.k[b], shift_of(sp.k[b], sp.beta[b], sp.sigma[b], sp.shift_map, std::log2((double)n)));
       HH_CUDA_TRY(cudaMemcpyAsync(kp.p, c.data(), B * 16, cudaMemcpyHostToDevice, E.s));
       HH_CUDA_TRY(cudaStreamSynchronize(E.s));
       L.kc = kp.as<double2>();
@@ -829,6 +850,7 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   if (!d->k_elem && !(d->k_const >= 0)) { hh_set_error("k_const must be >= 0"); return HH_E_CONFIG; }
   if (d->max_restart < 1 || d->max_restart > 127) { hh_set_error("max_restart must be in 1..127"); return HH_E_CONFIG; }
   if (!(d->beta >= 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
+  if (d->shift_map < 0 || d->shift_map > 3) { hh_set_error("shift_map must be 0..3"); return HH_E_CONFIG; }
   const int nloc = std::max(1, d->nslabs_local);
   const bool use_nccl = d->nccl_id != nullptr;
   if (use_nccl && (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks || nloc != 1)) {
@@ -854,6 +876,7 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
     sp.comm = p->comm;
     sp.k.assign(sp.B, d->k_const); sp.beta.assign(sp.B, d->beta); sp.sigma.assign(sp.B, d->sigma);
     sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
+    sp.shift_map = d->shift_map;
     st = enter(p->E, p->user);
     if (st == HH_OK) st = batch_setup(p->E, sp);
   }
@@ -1041,8 +1064,12 @@ extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t
   return HH_OK;
 }
 
-extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
-                              const hh_sample* smp, int32_t n, hh_sample_result* out) {
+// Batched solves of independent 2D constant-k samples (shared by hh_sweep and
+// hh_shift_search): rhs == NULL -> unit point source at the centre node (C7),
+// else rhs[i] = HOST complex128 right-hand side of sample i ((n+1)^2 nodes).
+static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                           const hh_sample* smp, int32_t n, const void* const* rhs,
+                           hh_sample_result* out) {
   if (!common || !o || (n && (!smp || !out))) { hh_set_error("NULL argument"); return HH_E_ARG; }
   if (n == 0) return HH_OK;
   const int m = std::max(o->restart, common->max_restart > 0 ? std::min(common->max_restart, 127) : o->restart);
@@ -1162,7 +1189,18 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
       if (st == HH_OK) {
         const int half = sp.n / 2;
         const int64_t ctr = half + (int64_t)(sp.n + 1) * half;   // unit point source at the centre (C7)
-        st = vset(E.LF, vfine(E, E.bv), VArg(), sp.B, 2, ctr, nullptr, E.s);
+        if (!rhs) {
+          st = vset(E.LF, vfine(E, E.bv), VArg(), sp.B, 2, ctr, nullptr, E.s);
+        } else {
+          cplx* base = E.bv.as<cplx>() + E.FL.pad + (int64_t)E.FL.G * E.FL.plane;   // owned view, entry 0
+          for (size_t k = 0; k < bt.size() && st == HH_OK; ++k)
+            if (cudaMemcpyAsync(base + (int64_t)k * E.FL.stride, rhs[bt[k]], E.N * 16, cudaMemcpyHostToDevice,
+                                E.s) != cudaSuccess) {
+              cudaGetLastError();
+              hh_set_error("sweep: rhs upload failed");
+              st = HH_E_CUDA;
+            }
+        }
         const double t0 = now_s();
         if (st == HH_OK) st = batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, res, nullptr);
         t_solve = now_s() - t0;
@@ -1197,5 +1235,106 @@ extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opt
   for (int t = 0; t < nt; ++t) th.emplace_back(worker, engines[t]);
   for (auto& t : th) t.join();
   if (failed) { hh_set_error("%s", err.c_str()); return HH_E_CUDA; }
+  return HH_OK;
+}
+
+extern "C" hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                              const hh_sample* smp, int32_t n, hh_sample_result* out) {
+  return sweep_run(common, o, smp, n, nullptr, out);
+}
+
+// ================================================================== shift search
+// Golden-section search of the near-optimal shift exponent (PAPER.md:404-421,
+// Sec. 5 step 5): for each sample minimise rho(sigma) = (r_end / r_0)^(1/end)
+// of an FGMRES solve of A_0 u = f preconditioned by the V-cycle on
+// A(k, beta k^sigma), over sigma in [lo, hi] to a bracket width <= tol.
+// Classic two-interior-point reduction with ratio 1/phi; tie f(c) == f(d) keeps
+// the right bracket [c, b].  All samples advance in lockstep rounds; every
+// round's evaluations are one batched sweep.  A failed solve scores rho = 1.
+extern "C" hh_status hh_shift_search(const hh_problem_desc* common, const hh_fgmres_opts* o,
+                                     const hh_search_sample* smp, int32_t n, const void* const* rhs,
+                                     double sigma_lo, double sigma_hi, double tol,
+                                     hh_search_result* out) {
+  if (!common || !o || (n && (!smp || !out || !rhs))) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  if (!(sigma_lo < sigma_hi) || !(tol > 0)) { hh_set_error("need sigma_lo < sigma_hi and tol > 0"); return HH_E_CONFIG; }
+  if (n == 0) return HH_OK;
+  const double invphi = (std::sqrt(5.0) - 1.0) / 2.0;
+  struct St { double a, b, c, d, fc, fd, best_s, best_f; int evals, its; bool active; };
+  std::vector<St> S(n);
+  for (int i = 0; i < n; ++i) {
+    St& t = S[i];
+    t.a = sigma_lo; t.b = sigma_hi;
+    t.c = t.b - invphi * (t.b - t.a);
+    t.d = t.a + invphi * (t.b - t.a);
+    t.fc = t.fd = 0; t.best_s = t.c; t.best_f = 2; t.evals = 0; t.its = 0;
+    t.active = (t.b - t.a) > tol;
+    memset(&out[i], 0, sizeof(out[i]));
+    out[i].id = smp[i].id;
+  }
+  auto evaluate = [&](const std::vector<std::pair<int, double>>& pts, std::vector<double>& f) -> hh_status {
+    const int m = (int)pts.size();
+    std::vector<hh_sample> q(m);
+    std::vector<const void*> r(m);
+    for (int k = 0; k < m; ++k) {
+      const hh_search_sample& z = smp[pts[k].first];
+      q[k].id = k; q[k].n_cells = z.n_cells; q[k].k = z.k; q[k].beta = z.beta; q[k].sigma = pts[k].second;
+      r[k] = rhs[pts[k].first];
+    }
+    std::vector<hh_sample_result> res(m);
+    HH_TRY(sweep_run(common, o, q.data(), m, r.data(), res.data()));
+    f.resize(m);
+    for (int k = 0; k < m; ++k) {
+      const bool ok = res[k].status == HH_OK && std::isfinite(res[k].rho);
+      f[k] = ok ? res[k].rho : 1.0;
+      St& t = S[pts[k].first];
+      t.evals++;
+      t.its += res[k].iterations;
+      if (f[k] < t.best_f) { t.best_f = f[k]; t.best_s = pts[k].second; }
+    }
+    return HH_OK;
+  };
+  // round 0: both interior points
+  {
+    std::vector<std::pair<int, double>> pts;
+    for (int i = 0; i < n; ++i) { pts.push_back({i, S[i].c}); pts.push_back({i, S[i].d}); }
+    std::vector<double> f;
+    HH_TRY(evaluate(pts, f));
+    for (int i = 0; i < n; ++i) { S[i].fc = f[2 * i]; S[i].fd = f[2 * i + 1]; }
+  }
+  for (;;) {
+    std::vector<std::pair<int, double>> pts;
+    std::vector<int> side;
+    for (int i = 0; i < n; ++i) {
+      St& t = S[i];
+      if (!t.active) continue;
+      if (t.fc < t.fd) {   // minimum in [a, d]
+        t.b = t.d; t.d = t.c; t.fd = t.fc;
+        t.c = t.b - invphi * (t.b - t.a);
+        side.push_back(0);
+        pts.push_back({i, t.c});
+      } else {             // minimum in [c, b]
+        t.a = t.c; t.c = t.d; t.fc = t.fd;
+        t.d = t.a + invphi * (t.b - t.a);
+        side.push_back(1);
+        pts.push_back({i, t.d});
+      }
+    }
+    if (pts.empty()) break;
+    std::vector<double> f;
+    HH_TRY(evaluate(pts, f));
+    for (size_t k = 0; k < pts.size(); ++k) {
+      St& t = S[pts[k].first];
+      (side[k] == 0 ? t.fc : t.fd) = f[k];
+      t.active = (t.b - t.a) > tol;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    out[i].sigma_hat = 0.5 * (S[i].a + S[i].b);
+    out[i].sigma_best = S[i].best_s;
+    out[i].rho_best = S[i].best_f;
+    out[i].evaluations = S[i].evals;
+    out[i].iterations_total = S[i].its;
+    out[i].status = HH_OK;
+  }
   return HH_OK;
 }

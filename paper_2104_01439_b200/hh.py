@@ -25,7 +25,7 @@ STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_C
 EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "hh_vcycle",
            "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
            "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
-           "hh_slab_bounds", "hh_nccl_unique_id", "hh_last_error", "hh_version"]
+           "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -35,7 +35,7 @@ class ProblemDesc(C.Structure):
                 ("nu_post", C.c_int32), ("omega", C.c_double), ("coarse_solver", C.c_int32),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("max_restart", C.c_int32),
                 ("nslabs_local", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("shift_map", C.c_int32)]
 
 
 class FgmresOpts(C.Structure):
@@ -55,6 +55,19 @@ class FgmresReport(C.Structure):
 class Sample(C.Structure):
     _fields_ = [("id", C.c_int64), ("n_cells", C.c_int32), ("k", C.c_double),
                 ("beta", C.c_double), ("sigma", C.c_double)]
+
+
+class SearchSample(C.Structure):
+    _fields_ = [("id", C.c_int64), ("n_cells", C.c_int32), ("k", C.c_double), ("beta", C.c_double)]
+
+
+class SearchResult(C.Structure):
+    _fields_ = [("id", C.c_int64), ("status", C.c_int32), ("evaluations", C.c_int32),
+                ("iterations_total", C.c_int32), ("sigma_hat", C.c_double),
+                ("sigma_best", C.c_double), ("rho_best", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class SampleResult(C.Structure):
@@ -83,6 +96,9 @@ def _load():
         "hh_local_layout": [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
         "hh_slab_bounds": [i32, i32, C.POINTER(C.c_int32)],
         "hh_nccl_unique_id": [vp],
+        "hh_shift_search": [C.POINTER(ProblemDesc), C.POINTER(FgmresOpts), C.POINTER(SearchSample), i32,
+                            C.POINTER(C.c_void_p), C.c_double, C.c_double, C.c_double,
+                            C.POINTER(SearchResult)],
         "hh_apply_op": [vp, i32, vp, vp],
         "hh_vcycle": [vp, vp, vp],
         "hh_coarse_solve": [vp, vp, vp],
@@ -133,7 +149,7 @@ class Problem:
 
     def __init__(self, dim, n_cells, k_const=0.0, k_elem=None, k_elem_coarse=None, beta=1.0,
                  sigma=1.5, nu_pre=2, nu_post=2, omega=0.6, max_restart=100, device=None,
-                 nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None):
+                 nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None, shift_map=0):
         """nslabs_local > 1: the solve is cut into that many slabs held by this
         process; nccl_id (from nccl_unique_id(), shared by all ranks): this
         process holds slab `rank` of `nranks` (one GPU per process).  Vectors
@@ -157,6 +173,7 @@ class Problem:
         d.stream = _stream()
         d.max_restart = max_restart
         d.nslabs_local, d.rank, d.nranks = nslabs_local, rank, nranks
+        d.shift_map = shift_map
         idbuf = None
         if nccl_id is not None:
             if len(nccl_id) != 128:
@@ -180,6 +197,7 @@ class Problem:
     @classmethod
     def from_spec(cls, spec, max_restart=None, **kw):
         """Build from a workloads.ProblemSpec (inputs only)."""
+        kw.setdefault("shift_map", getattr(spec, "shift_map", 0))
         return cls(spec.dim, spec.n, k_const=spec.k_const or 0.0, k_elem=spec.k_fine,
                    k_elem_coarse=spec.k_coarse, beta=spec.beta, sigma=spec.sigma,
                    nu_pre=spec.nu_pre, nu_post=spec.nu_post, omega=spec.omega,
@@ -261,6 +279,31 @@ def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_rest
     arr = (Sample * n)(*[Sample(s["id"], s["n"], s["k"], s["beta"], s["sigma"]) for s in samples])
     out = (SampleResult * n)()
     _check(lib.hh_sweep(C.byref(d), C.byref(o), arr, n, out))
+    return [r.as_dict() for r in out]
+
+
+def shift_search(samples, rhs, lo=1.0, hi=2.0, tol=1e-2, o=None, nu_pre=2, nu_post=2, omega=0.6,
+                 device=None, max_restart=100):
+    """hh_shift_search: golden-section sigma search per sample (dicts with id, n, k,
+    beta); rhs[i] = host complex128 right-hand side of sample i (reused for all sigma).
+    Default budget = the paper's: rtol 1e-8, 50 iterations, no restart."""
+    o = o or opts(restart=50, max_iters=50, rtol=1e-8)
+    d = ProblemDesc()
+    d.dim, d.nu_pre, d.nu_post, d.omega = 2, nu_pre, nu_post, omega
+    d.device = torch.cuda.current_device() if device is None else device
+    d.stream = _stream()
+    d.max_restart = max_restart
+    d.coarse_solver = HH_COARSE_ND
+    n = len(samples)
+    arr = (SearchSample * n)(*[SearchSample(s["id"], s["n"], s["k"], s.get("beta", 1.0)) for s in samples])
+    keep = [np.ascontiguousarray(r, dtype=np.complex128) for r in rhs]
+    for s_, r in zip(samples, keep):
+        if r.size != (s_["n"] + 1) ** 2:
+            raise ValueError("rhs size mismatch")
+    ptrs = (C.c_void_p * n)(*[r.ctypes.data for r in keep])
+    out = (SearchResult * n)()
+    _check(lib.hh_shift_search(C.byref(d), C.byref(o), arr, n, ptrs, lo, hi, tol, out))
+    del keep
     return [r.as_dict() for r in out]
 
 

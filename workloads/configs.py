@@ -42,6 +42,7 @@ class ProblemSpec:
     max_iters: int = 500
     source: tuple = (0.5, 0.5)
     meta: dict = field(default_factory=dict)
+    shift_map: int = 0           # > 0: sigma = sigma_p(k_e, log2 n) of Table 1 row p
 
     @property
     def h(self) -> float:
@@ -156,3 +157,34 @@ def sweep_sample_spec(sample: dict) -> ProblemSpec:
     return ProblemSpec(f"cfg1#{sample['id']}", 2, sample["n"], sample["k"],
                        beta=sample["beta"], sigma=sample["sigma"], restart=100,
                        source=(0.5, 0.5), meta=dict(sample))
+
+
+# ------------------------------------------------------------------ shift-search recipe
+def search_samples(count: int, seed: int = 0, levels=(4, 5, 6, 7, 8, 9, 10), p: int = 1):
+    """Sec. 5 steps 1-3 for Q1 (p = 1): l uniform in `levels`,
+    h = 2^-l (n = 2^l), k uniform in [3p/(16h), 3p/(4h)]; shift eps = k^sigma
+    (beta = 1).  Seeded; returns dicts with id, n, k, l."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(count):
+        l = int(rng.choice(levels))
+        n = 2 ** l
+        k = float(rng.uniform(3 * p * n / 16, 3 * p * n / 4))
+        out.append({"id": i, "dim": 2, "n": n, "l": l, "k": k, "beta": 1.0})
+    return out
+
+
+def search_rhs(sample: dict, seed: int = 0) -> np.ndarray:
+    """Step 4: right-hand side with components uniform in [-1, 1]
+    (real), drawn once per sample (seed, id) and reused for every sigma."""
+    rng = np.random.default_rng([seed, int(sample["id"])])
+    n1 = (sample["n"] + 1) ** 2
+    return rng.uniform(-1.0, 1.0, n1).astype(np.complex128)
+
+
+def search_sample_spec(sample: dict) -> ProblemSpec:
+    """ProblemSpec of one search sample at sigma = 1.5 (sigma is the search variable);
+    BASELINE's V-cycle settings (2 + 2, omega 0.6), no restart within the 50-iteration
+    budget (the paper uses none)."""
+    return ProblemSpec(f"search#{sample['id']}", 2, sample["n"], sample["k"], beta=1.0, sigma=1.5,
+                       restart=50, rtol=1e-8, max_iters=50, meta=dict(sample))
