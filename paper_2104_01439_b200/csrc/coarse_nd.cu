@@ -274,19 +274,22 @@ __device__ __forceinline__ cplx warp_sum(cplx v) {
   return v;
 }
 
-// lane-strided dot of a front row with v: 4 independent loads in flight per lane
+// lane-strided dot of a front row with v: 4 independent (predicated) loads in
+// flight per lane for every 128 entries -- no serial tail loop, so short rows
+// (the 36..100-entry rows of the leaves) cost one load round trip
 __device__ __forceinline__ cplx row_dot(const cplx* __restrict__ row, const cplx* v, int len, int lane) {
   cplx a0 = cmake(0, 0), a1 = cmake(0, 0), a2 = cmake(0, 0), a3 = cmake(0, 0);
-  int c = lane;
-  for (; c + 96 < len; c += 128) {
-    const cplx r0 = __ldg(&row[c]), r1 = __ldg(&row[c + 32]), r2 = __ldg(&row[c + 64]),
-               r3 = __ldg(&row[c + 96]);
+  for (int c = lane; c < len; c += 128) {
+    const bool p1 = c + 32 < len, p2 = c + 64 < len, p3 = c + 96 < len;
+    const cplx r0 = __ldg(&row[c]);
+    const cplx r1 = p1 ? __ldg(&row[c + 32]) : cmake(0, 0);
+    const cplx r2 = p2 ? __ldg(&row[c + 64]) : cmake(0, 0);
+    const cplx r3 = p3 ? __ldg(&row[c + 96]) : cmake(0, 0);
     cfma(a0, r0, v[c]);
-    cfma(a1, r1, v[c + 32]);
-    cfma(a2, r2, v[c + 64]);
-    cfma(a3, r3, v[c + 96]);
+    if (p1) cfma(a1, r1, v[c + 32]);
+    if (p2) cfma(a2, r2, v[c + 64]);
+    if (p3) cfma(a3, r3, v[c + 96]);
   }
-  for (; c < len; c += 32) cfma(a0, __ldg(&row[c]), v[c]);
   return warp_sum(cadd(cadd(a0, a1), cadd(a2, a3)));
 }
 
