@@ -34,6 +34,7 @@ namespace cg = cooperative_groups;
 
 namespace {
 constexpr int NB = 16;      // pivot block of the partial Gauss-Jordan sweep
+constexpr int PIV_CHUNK = 256;   // rows / columns per k_nd_piv CTA
 constexpr int LEAF = 64;    // max nodes of a leaf box
 
 struct FrontMeta {          // device-visible per-front data
@@ -148,13 +149,17 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
   if (kb >= m.s) return;
   const int nb = min(NB, m.s - kb);
   const int f = m.f;
+  // chunk blockIdx.z of PIV_CHUNK rows (column-block save) / columns (row scaling)
+  const int c0 = blockIdx.z * PIV_CHUNK, c1 = min(f, c0 + PIV_CHUNK);
+  if (c0 >= f) return;
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.x];
+  cplx* Pg = C + (int64_t)f * NB;   // P for k_nd_upd (the pivot block itself is rewritten there)
   __shared__ cplx P[NB][NB + 1];
   const int ti = threadIdx.x / NB, tj = threadIdx.x % NB;   // 16 x 16
   if (ti < nb && tj < nb) P[ti][tj] = A[(int64_t)(kb + ti) * f + kb + tj];
-  // save column block (rows outside K only are used later)
-  for (int i = threadIdx.x / NB; i < f; i += 256 / NB) {
+  // save this chunk's rows of the column block (rows outside K only are used later)
+  for (int i = c0 + threadIdx.x / NB; i < c1; i += 256 / NB) {
     const int k = threadIdx.x % NB;
     if (k < nb) C[(int64_t)i * NB + k] = A[(int64_t)i * f + kb + k];
   }
@@ -188,12 +193,11 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
     if (threadIdx.x == 0) P[p][p] = pinv;
     __syncthreads();
   }
-  // rows K: R[k][j] = sum_l P[k][l] A[kb+l][j] for j not in K; P for j in K
-  for (int j = threadIdx.x; j < f; j += blockDim.x) {
-    if (j >= kb && j < kb + nb) {
-      for (int k = 0; k < nb; ++k) A[(int64_t)(kb + k) * f + j] = P[k][j - kb];
-      continue;
-    }
+  if (blockIdx.z == 0 && ti < NB && tj < NB) Pg[ti * NB + tj] = (ti < nb && tj < nb) ? P[ti][tj] : cmake(0, 0);
+  // rows K of this chunk's columns: R[k][j] = sum_l P[k][l] A[kb+l][j] for j not in K
+  // (F[K,K] = P is written by k_nd_upd: the pivot block is read by every chunk here)
+  for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+    if (j >= kb && j < kb + nb) continue;
     cplx col[NB];
 #pragma unroll
     for (int l = 0; l < NB; ++l) col[l] = (l < nb) ? A[(int64_t)(kb + l) * f + j] : cmake(0, 0);
@@ -226,6 +230,7 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   const int nb = min(NB, m.s - kb);
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
+  const cplx* Pg = C + (int64_t)f * NB;
   __shared__ cplx Cs[UT][NB + 1];
   __shared__ cplx Rs[NB][UT + 1];
   for (int idx = threadIdx.x; idx < UT * NB; idx += 256) {
@@ -234,7 +239,10 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   }
   for (int idx = threadIdx.x; idx < NB * UT; idx += 256) {
     const int k = idx / UT, j = idx % UT;
-    Rs[k][j] = (k < nb && j0 + j < f) ? A[(int64_t)(kb + k) * f + j0 + j] : cmake(0, 0);
+    const int jj = j0 + j;
+    cplx r = cmake(0, 0);
+    if (k < nb && jj < f) r = (jj >= kb && jj < kb + nb) ? Pg[k * NB + (jj - kb)] : A[(int64_t)(kb + k) * f + jj];
+    Rs[k][j] = r;
   }
   __syncthreads();
   const int tx = threadIdx.x % UT, ty = threadIdx.x / UT;   // 32 x 8
@@ -245,7 +253,11 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   for (int r = 0; r < UT / 8; ++r) {
     const int il = ty + 8 * r;
     const int i = i0 + il;
-    if (i >= f || (i >= kb && i < kb + nb)) continue;
+    if (i >= f) continue;
+    if (i >= kb && i < kb + nb) {             // rows K: F[K,K] = P (F[K, not K] scaled by k_nd_piv)
+      if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NB + (j - kb)];
+      continue;
+    }
     cplx acc = jK ? cmake(0, 0) : A[(int64_t)i * f + j];
 #pragma unroll
     for (int k = 0; k < NB; ++k) cfms(acc, Cs[il][k], Rs[k][tx]);
@@ -767,7 +779,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   std::vector<int64_t> Coff(nf);
   for (auto& li : nd->levels) {
     int64_t o = 0;
-    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB; }
+    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB + NB * NB; }
     Cmax = std::max(Cmax, o);
   }
   nd->F_entries = Foff; nd->w_entries = posOff; nd->out_entries = outOff; nd->C_entries = Cmax;
@@ -914,8 +926,8 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
     }
     const int tiles = (li.max_f + UT - 1) / UT;
     for (int kb = 0; kb < li.max_s; kb += NB) {
-      k_nd_piv<<<dim3(li.count, B), 256, 0, s>>>(nd->d_fronts, li.begin, kb, F, FE, cbuf, CE,
-                                                  nd->d_Coff + li.begin, flag);
+      k_nd_piv<<<dim3(li.count, B, (li.max_f + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
+          nd->d_fronts, li.begin, kb, F, FE, cbuf, CE, nd->d_Coff + li.begin, flag);
       k_nd_upd<<<dim3(tiles * tiles, li.count, B), 256, 0, s>>>(nd->d_fronts, li.begin, kb, tiles,
                                                                  F, FE, cbuf, CE,
                                                                  nd->d_Coff + li.begin);
