@@ -1178,11 +1178,16 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     E.launches = 0;
     if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
     else E.timing_every = 8;   // sweep: sample 1 iteration in 8 (keeps the pipelines full)
+    const double w0 = now_s();
+    int nbat = 0;
+    double busy = 0;
     for (;;) {
       const int bi = next.fetch_add(1);
       if (bi >= (int)batches.size() || failed) break;
       const std::vector<int>& bt = batches[bi];
       const BatchSpec& sp = specs[bi];
+      const double b0 = now_s();
+      ++nbat;
       hh_status st = batch_setup(E, sp);
       std::vector<SampleOut> res;
       double t_solve = 0;
@@ -1222,7 +1227,11 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
         r.setup_s = E.setup_s;
         r.solve_s = t_solve;
       }
+      busy += now_s() - b0;
     }
+    if (getenv("HH_DEBUG") && atoi(getenv("HH_DEBUG")) >= 3)
+      fprintf(stderr, "[hh sweep] worker %p: %d batches, busy %.3f s, finished at %.3f s\n", (void*)Ep, nbat,
+              busy, now_s() - w0);
     std::lock_guard<std::mutex> lk(g_sweep_mu);
     for (int t = 0; t < T_NT; ++t) {
       g_sweep_st[t] += E.acc_ms[t];
