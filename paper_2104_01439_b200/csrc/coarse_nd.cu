@@ -276,6 +276,10 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
 // every stage is one short dependent chain instead of a walk over all
 // descendant contributions.
 constexpr int VMAX = 4096;   // front vectors up to this length are staged in shared memory
+int nd_vmax() {              // HH_ND_VMAX lowers it (tests of the global-memory path on small grids)
+  static const int v = getenv("HH_ND_VMAX") ? std::min(VMAX, atoi(getenv("HH_ND_VMAX"))) : VMAX;
+  return v;
+}
 
 __device__ __forceinline__ cplx warp_sum(cplx v) {
 #pragma unroll
@@ -314,6 +318,7 @@ struct SolveArgs {
   const cplx* F; int64_t FE;
   cplx* work; int64_t WE, updE;   // work[b] = [w (w_entries) | upd (out_entries)]
   VArg rhs, x;
+  int vmax;                        // fronts with f <= vmax stage their vectors in shared memory
 };
 
 // Programmatic dependent launch: a level kernel may start while its predecessor
@@ -325,12 +330,17 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
-// prefetch the rows r0, r0 + step, ... (< nrows, at most 8 per warp) of length len starting at row0
+// prefetch the rows r0, r0 + step, ... (< nrows, at most 8 per warp) of length len starting at
+// row0; one bulk prefetch per <= 32 KB piece
 __device__ __forceinline__ void prefetch_rows(const cplx* row0, int64_t ld, int len, int nrows, int r0,
                                               int step, int lane) {
   if (len <= 0) return;
   const int r = r0 + lane * step;
-  if (lane < 8 && r < nrows) prefetch_l2(row0 + (int64_t)r * ld, len * (int)sizeof(cplx));
+  if (lane < 8 && r < nrows) {
+    const char* p = reinterpret_cast<const char*>(row0 + (int64_t)r * ld);
+    for (int64_t left = (int64_t)len * (int64_t)sizeof(cplx); left > 0; left -= 32768, p += 32768)
+      prefetch_l2(p, (int)(left < 32768 ? left : 32768));
+  }
 }
 
 __device__ __forceinline__ cplx* w_of(const SolveArgs& A, int b) { return A.work + (int64_t)b * A.WE; }
@@ -414,7 +424,7 @@ __global__ void __launch_bounds__(LT) k_nd_fwd(SolveArgs A, int begin) {
   pdl_wait();
   if (A.st && A.st[b]) return;
   const cplx* w;
-  if (m.f <= VMAX) {
+  if (m.f <= A.vmax) {
     front_gather(A, m, b, wsh, blockIdx.y == 0 ? w_of(A, b) + m.posOff : nullptr, m.s, threadIdx.x,
                  blockDim.x);
     __syncthreads();
@@ -438,23 +448,114 @@ __global__ void __launch_bounds__(LT) k_nd_bwd(SolveArgs A, int begin) {
                   gridDim.y * (LT / 32), lane);
   pdl_wait();
   if (A.st && A.st[b]) return;
-  if (m.f <= VMAX) {
+  if (m.f <= A.vmax) {
     stage_bwd(A, m, b, v);
     __syncthreads();
     front_bwd_rows(A, m, b, v, blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32), lane);
-  } else {   // huge fronts: operands straight from global memory
-    const cplx* F = A.F + (int64_t)b * A.FE + m.Foff;
-    const cplx* z = w_of(A, b) + m.posOff;
-    const int* hl = A.halo + m.haloOff;
-    cplx* x = A.x.at(b);
-    for (int a = blockIdx.y * (LT / 32) + warp; a < m.s; a += gridDim.y * (LT / 32)) {
-      const cplx* row = F + (int64_t)a * m.f;
-      cplx acc = row_dot(row, z, m.s, lane);
-      cplx acc2 = cmake(0, 0);
-      for (int c = lane; c < m.u; c += 32) cfms(acc2, __ldg(&row[m.s + c]), x[hl[c]]);
-      acc = cadd(acc, warp_sum(acc2));
-      if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+  } else {   // huge fronts: v = [z_s ; -x[halo]] was staged in w (k_nd_bwd_stage)
+    front_bwd_rows(A, m, b, w_of(A, b) + m.posOff, blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32),
+                   lane);
+  }
+}
+
+// huge fronts (f > VMAX): stage -x[halo] into the halo part of w (the forward
+// halo values are dead by now), so the backward rows are plain contiguous dots
+__global__ void k_nd_bwd_stage(SolveArgs A, int begin) {
+  const int b = blockIdx.z;
+  pdl_trigger();
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  const FrontMeta m = A.fr[begin + blockIdx.x];
+  cplx* wv = w_of(A, b) + m.posOff + m.s;
+  const cplx* x = A.x.at(b);
+  for (int c = threadIdx.x + blockIdx.y * blockDim.x; c < m.u; c += blockDim.x * gridDim.y) {
+    const cplx t = x[__ldg(&A.halo[m.haloOff + c])];
+    wv[c] = cmake(-t.x, -t.y);
+  }
+}
+
+// Wide levels (many rows per front): the front vector is gathered / staged once
+// into global w (k_nd_gather / k_nd_bwd_stage), and the rows are spread over
+// many CTAs (WIDE_RPC rows each) that copy only what they need (z_s forward,
+// [z_s ; -x[halo]] backward) from L2 into shared memory -- instead of every CTA
+// re-gathering the whole front, which capped the CTAs per front.
+constexpr int WIDE_RPC = 8;   // rows per CTA for rows longer than 64 entries
+
+// dot of one row with v by a group of G lanes (G = 32, 16, 8, 4), 4 predicated
+// loads in flight per lane; the group sum is left in every lane of the group
+template <int G>
+__device__ __forceinline__ cplx row_dot_g(const cplx* __restrict__ row, const cplx* v, int len, int sub) {
+  cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
+  for (int c = sub; c < len; c += 4 * G) {
+    cplx r[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) r[t] = (c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (c + G * t < len) cfma(t & 1 ? a1 : a0, r[t], v[c + G * t]);
+  }
+  cplx a = cadd(a0, a1);
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+    a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+  }
+  return a;
+}
+
+template <int DIR, int G>
+__device__ __forceinline__ void wide_rows(const SolveArgs& A, const FrontMeta& m, int b, const cplx* row0,
+                                          const cplx* v, const cplx* wg, int len, int r0, int r1, int warp,
+                                          int lane) {
+  constexpr int RPW = 32 / G;                 // rows per warp pass
+  const int grp = lane / G, sub = lane % G;
+  for (int rb = r0 + warp * RPW; rb < r1; rb += (LT / 32) * RPW) {
+    const int r = rb + grp;
+    const bool ok = r < r1;
+    const cplx acc = row_dot_g<G>(row0 + (int64_t)(ok ? r : r0) * m.f, v, ok ? len : 0, sub);
+    if (ok && sub == 0) {
+      if (DIR == 0) upd_of(A, b)[m.outOff + r] = cadd(acc, wg[m.s + r]);
+      else A.x.at(b)[A.sep[m.sepOff + r]] = acc;
     }
+  }
+}
+
+// rows per CTA of the wide kernels: 8 warp passes of 32 / G rows
+__host__ __device__ inline int wide_group(int len) { return len > 64 ? 32 : (len > 32 ? 16 : (len > 16 ? 8 : 4)); }
+__host__ __device__ inline int wide_rpc(int len) { return WIDE_RPC * (32 / wide_group(len)); }
+
+template <int DIR>
+__global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin) {
+  extern __shared__ double4 smem_raw[];
+  cplx* vs = reinterpret_cast<cplx*>(smem_raw);
+  const int b = blockIdx.z;
+  const FrontMeta m = A.fr[begin + blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows = DIR == 0 ? m.u : m.s;
+  const int len = DIR == 0 ? m.s : m.f;
+  const int rpc = wide_rpc(len);
+  const int r0 = blockIdx.y * rpc;
+  if (r0 >= rows) return;
+  const int r1 = min(rows, r0 + rpc);
+  const cplx* F = A.F + (int64_t)b * A.FE + m.Foff;
+  const cplx* row0 = DIR == 0 ? F + (int64_t)m.s * m.f : F;
+  pdl_trigger();
+  if (!(A.st && *(volatile const int*)&A.st[b]))
+    prefetch_rows(row0, m.f, len, r1, r0 + warp, LT / 32, lane);
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  const cplx* wg = w_of(A, b) + m.posOff;
+  const cplx* v = wg;
+  if (len <= A.vmax) {
+    for (int c = threadIdx.x; c < len; c += blockDim.x) vs[c] = wg[c];
+    __syncthreads();
+    v = vs;
+  }
+  switch (wide_group(len)) {
+    case 32: wide_rows<DIR, 32>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
+    case 16: wide_rows<DIR, 16>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
+    case 8: wide_rows<DIR, 8>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
+    default: wide_rows<DIR, 4>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
   }
 }
 
@@ -968,6 +1069,19 @@ static SolveCfg get_cfg(NDPlan* nd, int B) {
   return c;
 }
 
+// levels with at least this many rows per front run the wide path (HH_ND_WIDE)
+static int wide_rows() {
+  static const int v = getenv("HH_ND_WIDE") ? atoi(getenv("HH_ND_WIDE")) : 128;
+  return v;
+}
+
+// ... and fronts of at least this order (HH_ND_WIDE_F): the 2D fronts (f <= ~770)
+// are faster with the per-front gather in shared memory
+static int wide_f() {
+  static const int v = getenv("HH_ND_WIDE_F") ? atoi(getenv("HH_ND_WIDE_F")) : 1024;
+  return v;
+}
+
 // launch with programmatic stream serialisation (PDL); HH_NO_PDL=1 disables it
 static const bool g_pdl = getenv("HH_NO_PDL") == nullptr;
 template <typename... Args>
@@ -1003,6 +1117,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo; A.gmap = nd->d_gmap;
   A.F = F; A.FE = shareF ? 0 : nd->F_entries;
   A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
+  A.vmax = nd_vmax();
   const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
@@ -1015,11 +1130,18 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = cut + 1; L <= Lb; ++L) {
     const LevelInfo& li = nd->levels[L];
-    if (li.max_f > VMAX) {
+    if (li.max_f > A.vmax || (li.max_u >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
+      if (li.max_u == 0) continue;
+      const size_t sm = (size_t)std::min(li.max_s, A.vmax) * sizeof(cplx);
+      if (sm > 48 * 1024)
+        HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      dim3 g(li.count, (li.max_u + WIDE_RPC - 1) / WIDE_RPC, B);   // covers the smallest rows-per-CTA
+      HH_TRY(launch_pdl(k_nd_rows_wide<0>, g, LT, sm, s, A, li.begin));
+      continue;
     }
-    const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
+    const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 g(li.count, level_split(li.max_u, li.count, B), B);
     HH_TRY(launch_pdl(k_nd_fwd, g, LT, sm, s, A, li.begin));
@@ -1043,7 +1165,17 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = Lb; L > cut; --L) {
     const LevelInfo& li = nd->levels[L];
-    const size_t sm = (size_t)std::min(li.max_f, VMAX) * sizeof(cplx);
+    if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
+      dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
+      HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
+      const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
+      if (sm > 48 * 1024)
+        HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      dim3 g(li.count, (li.max_s + WIDE_RPC - 1) / WIDE_RPC, B);
+      HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin));
+      continue;
+    }
+    const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     dim3 g(li.count, level_split(li.max_s, li.count, B), B);
     HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
@@ -1122,6 +1254,11 @@ int nd_solve_launches(const NDPlan* ndc, int B) {
   const int nlev = (int)nd->levels.size();
   const SolveCfg c = get_cfg(nd, B);
   int n = (c.sub_cut >= 0 ? 2 : 0) + 2 * (c.split - c.sub_cut) + (c.split < nlev - 1 ? 1 : 0);
-  for (int L = c.sub_cut + 1; L <= c.split; ++L) n += nd->levels[L].max_f > VMAX;
+  for (int L = c.sub_cut + 1; L <= c.split; ++L) {
+    const LevelInfo& li = nd->levels[L];
+    const bool big = li.max_f > nd_vmax() || li.max_f >= wide_f() || nd->dim == 3;
+    n += (big && (li.max_f > nd_vmax() || li.max_u >= wide_rows())) +
+         (big && (li.max_f > nd_vmax() || li.max_s >= wide_rows()));
+  }
   return n;
 }
