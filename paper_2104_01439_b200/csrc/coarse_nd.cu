@@ -319,6 +319,7 @@ struct SolveArgs {
   cplx* work; int64_t WE, updE;   // work[b] = [w (w_entries) | upd (out_entries)]
   VArg rhs, x;
   int vmax;                        // fronts with f <= vmax stage their vectors in shared memory
+  int prefetch;                    // L2 bulk prefetch of the factor rows before the PDL wait
 };
 
 // Programmatic dependent launch: a level kernel may start while its predecessor
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(LT) k_nd_fwd(SolveArgs A, int begin) {
   const FrontMeta m = A.fr[begin + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
-  if (!(A.st && *(volatile const int*)&A.st[b]))   // (possibly stale) status: prefetch hint only
+  if (A.prefetch && !(A.st && *(volatile const int*)&A.st[b]))   // (possibly stale) status: prefetch hint only
     prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff + (int64_t)m.s * m.f, m.f, m.s, m.u,
                   blockIdx.y * (LT / 32) + warp, gridDim.y * (LT / 32), lane);
   pdl_wait();
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(LT) k_nd_bwd(SolveArgs A, int begin) {
   const FrontMeta m = A.fr[begin + blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
-  if (!(A.st && *(volatile const int*)&A.st[b]))
+  if (A.prefetch && !(A.st && *(volatile const int*)&A.st[b]))
     prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff, m.f, m.f, m.s, blockIdx.y * (LT / 32) + warp,
                   gridDim.y * (LT / 32), lane);
   pdl_wait();
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin) {
   const cplx* F = A.F + (int64_t)b * A.FE + m.Foff;
   const cplx* row0 = DIR == 0 ? F + (int64_t)m.s * m.f : F;
   pdl_trigger();
-  if (!(A.st && *(volatile const int*)&A.st[b]))
+  if (A.prefetch && !(A.st && *(volatile const int*)&A.st[b]))
     prefetch_rows(row0, m.f, len, r1, r0 + warp, LT / 32, lane);
   pdl_wait();
   if (A.st && A.st[b]) return;
@@ -1118,6 +1119,8 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   A.F = F; A.FE = shareF ? 0 : nd->F_entries;
   A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
   A.vmax = nd_vmax();
+  static const int pf = getenv("HH_NO_PREFETCH") ? 0 : 1;
+  A.prefetch = pf;
   const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
