@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <cooperative_groups.h>
@@ -45,6 +46,19 @@ struct FrontMeta {          // device-visible per-front data
   int64_t eaOff;            // into extend-add map (u entries)
   int parent;
   int pad;
+};
+
+// lean storage (large 3D trees): a level is factored in chunks of fronts that
+// fit a reusable workspace W; afterwards only the rows [X | H] (s x f) of every
+// front are kept (the forward solve reads H transposed), the Schur complement S
+// goes packed (lower triangle) into a per-level-parity buffer for the parent's
+// extend-add, and W is reused by the next chunk.
+struct Chunk {
+  int level, t0, t1;
+  int64_t Wcount;                    // workspace entries of the chunk
+  int64_t asmBegin, asmCount;
+  int ea_count[2];
+  int64_t ea_list_off[2];            // children (by slot) of the chunk's fronts, in eaListC
 };
 
 struct LevelInfo {
@@ -93,6 +107,15 @@ struct NDPlan {
   int64_t* d_lvr = nullptr;          // [nlev][6]: sep begin/end, halo begin/end, position begin/end
   std::mutex cut_mu;
   std::vector<std::pair<int, SolveCfg>> cfg_cache;   // (B, schedule) chosen by nd_autotune
+  // lean storage
+  bool lean = false;
+  std::vector<Chunk> chunks;
+  FrontMeta* d_fronts_w = nullptr;   // Foff = chunk-relative workspace offset
+  int64_t* d_Coff_w = nullptr;       // chunk-local pivot column buffer offsets
+  int64_t* d_Soff = nullptr;         // packed S offset (in the level-parity buffer)
+  int64_t* d_Poff = nullptr;         // forward partial-sum offset (level-local)
+  int* d_eaListC = nullptr;
+  int64_t Wmax = 0, Cw = 0, Smax[2] = {0, 0}, Pmax = 0;
 };
 
 // ============================================================ device kernels
@@ -262,6 +285,53 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
 #pragma unroll
     for (int k = 0; k < NB; ++k) cfms(acc, Cs[il][k], Rs[k][tx]);
     A[(int64_t)i * f + j] = acc;
+  }
+}
+
+// ------------------------------------------------------------ lean storage kernels
+// extend-add of packed child Schur complements into the parents' workspace
+__global__ void k_nd_ea_packed(const int* __restrict__ list, const FrontMeta* __restrict__ frw,
+                               const int64_t* __restrict__ Soff, const cplx* __restrict__ Sprev,
+                               const int* __restrict__ eamap, cplx* __restrict__ W) {
+  const int c = list[blockIdx.x];
+  const FrontMeta mc = frw[c];
+  const FrontMeta mp = frw[mc.parent];
+  const int* map = eamap + mc.eaOff;
+  const cplx* S = Sprev + Soff[c];
+  for (int a = blockIdx.y; a < mc.u; a += gridDim.y) {
+    cplx* dst = W + mp.Foff + (int64_t)map[a] * mp.f;
+    for (int b = threadIdx.x; b < mc.u; b += blockDim.x) {
+      const int hi = max(a, b), lo = min(a, b);
+      const cplx v = S[(int64_t)hi * (hi + 1) / 2 + lo];
+      cplx& d = dst[map[b]];
+      d.x += v.x;
+      d.y += v.y;
+    }
+  }
+}
+
+// copy out of a factored chunk: rows [X | H] -> the solve factor, S -> packed store
+__global__ void k_nd_copyout(const FrontMeta* __restrict__ frw, const FrontMeta* __restrict__ frx,
+                             const int64_t* __restrict__ Soff, int t0, const cplx* __restrict__ W,
+                             cplx* __restrict__ XH, cplx* __restrict__ Scur) {
+  const int t = t0 + blockIdx.x;
+  const FrontMeta mw = frw[t];
+  const int s = mw.s, u = mw.u, f = mw.f;
+  const cplx* src = W + mw.Foff;
+  cplx* dst = XH + frx[t].Foff;
+  const int64_t n1 = (int64_t)s * f;
+  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < n1; i += (int64_t)gridDim.y * blockDim.x)
+    dst[i] = src[i];
+  if (u == 0) return;
+  cplx* S = Scur + Soff[t];
+  const int64_t n2 = (int64_t)u * (u + 1) / 2;
+  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.y * blockDim.x) {
+    // i = a (a + 1) / 2 + b, b <= a
+    int a = (int)((sqrt(8.0 * (double)i + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(a + 1) * (a + 2) / 2 <= i) ++a;
+    while ((int64_t)a * (a + 1) / 2 > i) --a;
+    const int b = (int)(i - (int64_t)a * (a + 1) / 2);
+    S[i] = src[(int64_t)(s + a) * f + s + b];
   }
 }
 
@@ -558,6 +628,64 @@ __global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin) {
     case 8: wide_rows<DIR, 8>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
     default: wide_rows<DIR, 4>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
   }
+}
+
+// Lean forward (no stored -H^T rows): upd[b] = w[s+b] - sum_a H[a][b] z[a] with
+// H = rows [0, s) x columns [s, f) of [X | H]; CTAs take (128-column block, 256-row
+// chunk) tiles, threads own one column (coalesced row reads, 8 rows in flight),
+// and the row-chunk partials are summed in a fixed order by k_nd_fwdT_red.
+constexpr int FT_COLS = 128, FT_ROWS = 256;
+__global__ void __launch_bounds__(FT_COLS) k_nd_fwdT(SolveArgs A, int begin, const int64_t* __restrict__ Poff,
+                                                     int ncb, int64_t PE) {
+  __shared__ cplx zs[FT_ROWS];
+  const int b = blockIdx.z;
+  const int t = begin + blockIdx.y;
+  const FrontMeta m = A.fr[t];
+  const int cb = blockIdx.x % ncb, rc = blockIdx.x / ncb;
+  const int a0 = rc * FT_ROWS;
+  pdl_trigger();
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  if (cb * FT_COLS >= m.u || a0 >= m.s) return;
+  const int a1 = min(m.s, a0 + FT_ROWS);
+  const cplx* w = w_of(A, b) + m.posOff;
+  for (int i = threadIdx.x; i < a1 - a0; i += blockDim.x) zs[i] = w[a0 + i];
+  __syncthreads();
+  const int col = cb * FT_COLS + threadIdx.x;
+  if (col >= m.u) return;
+  const cplx* H = A.F + (int64_t)b * A.FE + m.Foff + m.s + col;   // H[a][col] at H + a * f
+  cplx acc0 = cmake(0, 0), acc1 = cmake(0, 0);
+  int a = a0;
+  for (; a + 8 <= a1; a += 8) {
+    cplx h[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) h[k] = __ldg(&H[(int64_t)(a + k) * m.f]);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      cfma(acc0, h[k], zs[a + k - a0]);
+      cfma(acc1, h[k + 1], zs[a + k + 1 - a0]);
+    }
+  }
+  for (; a < a1; ++a) cfma(acc0, __ldg(&H[(int64_t)a * m.f]), zs[a - a0]);
+  cplx* part = A.work + (int64_t)b * A.WE + PE + Poff[t];
+  part[(int64_t)rc * m.u + col] = cadd(acc0, acc1);
+}
+
+__global__ void k_nd_fwdT_red(SolveArgs A, int begin, const int64_t* __restrict__ Poff, int64_t PE) {
+  const int b = blockIdx.z;
+  pdl_trigger();
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  const int t = begin + blockIdx.y;
+  const FrontMeta m = A.fr[t];
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m.u) return;
+  const int nrc = (m.s + FT_ROWS - 1) / FT_ROWS;
+  const cplx* part = A.work + (int64_t)b * A.WE + PE + Poff[t];
+  cplx sum = cmake(0, 0);
+  for (int rc = 0; rc < nrc; ++rc) sum = cadd(sum, part[(int64_t)rc * m.u + col]);
+  const cplx* w = w_of(A, b) + m.posOff;
+  upd_of(A, b)[m.outOff + col] = csub(w[m.s + col], sum);
 }
 
 // ------------------------------------------------------------ cluster solve
@@ -885,6 +1013,110 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     Cmax = std::max(Cmax, o);
   }
   nd->F_entries = Foff; nd->w_entries = posOff; nd->out_entries = outOff; nd->C_entries = Cmax;
+  // lean storage for trees whose full fronts would not fit (3D coarse grids of
+  // cfg4 size); HH_ND_LEAN=0/1 overrides, HH_ND_WMAX sets the workspace (entries)
+  std::vector<FrontMeta> fronts_w;
+  std::vector<int64_t> Coff_w(nf, 0), Soff(nf, 0), Poff(nf, 0);
+  std::vector<int> eaListC;
+  {
+    const char* el = getenv("HH_ND_LEAN");
+    nd->lean = el ? atoi(el) != 0 : 16.0 * (double)Foff > 24e9;
+  }
+  if (nd->lean) {
+    const int64_t Wlim = getenv("HH_ND_WMAX") ? atoll(getenv("HH_ND_WMAX")) : (int64_t)750000000;
+    fronts_w = nd->fronts;
+    int64_t xh = 0;
+    std::vector<int64_t> asmFirst(nf + 1, (int64_t)asmE.size());
+    for (int64_t q = (int64_t)asmE.size() - 1; q >= 0; --q) asmFirst[asmE[q].x] = q;
+    for (int t = nf - 1; t >= 0; --t) asmFirst[t] = std::min(asmFirst[t], asmFirst[t + 1]);
+    for (int L = 0; L < nlev; ++L) {
+      const LevelInfo& li = nd->levels[L];
+      int64_t so = 0, po = 0;
+      int t = li.begin;
+      const int tend = li.begin + li.count;
+      while (t < tend) {
+        Chunk ch;
+        ch.level = L; ch.t0 = t;
+        int64_t w = 0, co = 0;
+        while (t < tend) {
+          const int64_t ff = (int64_t)nd->fronts[t].f * nd->fronts[t].f;
+          if (t > ch.t0 && w + ff > Wlim) break;
+          fronts_w[t].Foff = w;
+          w += ff;
+          Coff_w[t] = co;
+          co += (int64_t)nd->fronts[t].f * NB + NB * NB;
+          ++t;
+        }
+        ch.t1 = t;
+        ch.Wcount = w;
+        nd->Wmax = std::max(nd->Wmax, w);
+        nd->Cw = std::max(nd->Cw, co);
+        ch.asmBegin = asmFirst[ch.t0];
+        ch.asmCount = asmFirst[ch.t1] - asmFirst[ch.t0];
+        for (int slot = 0; slot < 2; ++slot) {
+          ch.ea_list_off[slot] = (int64_t)eaListC.size();
+          ch.ea_count[slot] = 0;
+          for (int pp = ch.t0; pp < ch.t1; ++pp) {
+            const HostFront& hp = tf[order[pp]];
+            if ((int)hp.children.size() > slot) {
+              eaListC.push_back(newid[hp.children[slot]]);
+              ++ch.ea_count[slot];
+            }
+          }
+        }
+        nd->chunks.push_back(ch);
+      }
+      for (int q = li.begin; q < tend; ++q) {
+        FrontMeta& fm = nd->fronts[q];
+        Poff[q] = po;
+        po += (int64_t)((fm.s + 255) / 256) * fm.u;
+        fm.Foff = xh;                      // the solve reads [X | H] here
+        xh += (int64_t)fm.s * fm.f;
+      }
+      nd->Pmax = std::max(nd->Pmax, po);
+      (void)so;
+    }
+    nd->F_entries = xh;
+    // packed-S store: a front's S lives from its own level to its parent's level;
+    // offsets by first-fit over the levels (S read by level L is freed after level L)
+    std::map<int64_t, int64_t> freel;   // offset -> length
+    int64_t top = 0;
+    auto alloc = [&](int64_t n) -> int64_t {
+      for (auto it = freel.begin(); it != freel.end(); ++it)
+        if (it->second >= n) {
+          const int64_t o = it->first, len = it->second;
+          freel.erase(it);
+          if (len > n) freel[o + n] = len - n;
+          return o;
+        }
+      const int64_t o = top;
+      top += n;
+      return o;
+    };
+    auto release = [&](int64_t o, int64_t n) {
+      auto it = freel.emplace(o, n).first;
+      auto nx = std::next(it);
+      if (nx != freel.end() && it->first + it->second == nx->first) { it->second += nx->second; freel.erase(nx); }
+      if (it != freel.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) { pv->second += it->second; freel.erase(it); }
+      }
+    };
+    for (int L = 0; L < nlev; ++L) {
+      const LevelInfo& li = nd->levels[L];
+      for (int q = li.begin; q < li.begin + li.count; ++q) {
+        const FrontMeta& fm = nd->fronts[q];
+        Soff[q] = fm.parent >= 0 ? alloc((int64_t)fm.u * (fm.u + 1) / 2) : 0;
+      }
+      for (int q = li.begin; q < li.begin + li.count; ++q)
+        for (int c : tf[order[q]].children) {
+          const FrontMeta& fc = nd->fronts[newid[c]];
+          release(Soff[newid[c]], (int64_t)fc.u * (fc.u + 1) / 2);
+        }
+    }
+    nd->Smax[0] = std::max<int64_t>(1, top);
+    nd->Smax[1] = 0;
+  }
   int64_t sb = 0;
   for (auto& fm : nd->fronts) sb += (int64_t)fm.s * fm.f + (int64_t)fm.u * fm.s;
   nd->stream_bytes = sb * (int64_t)sizeof(cplx);
@@ -976,6 +1208,11 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   if (st == HH_OK) st = up(&nd->d_sep_front, sep_front);
   if (st == HH_OK) st = up(&nd->d_halo_front, halo_front);
   if (st == HH_OK) st = up(&nd->d_pos_front, pos_front);
+  if (st == HH_OK && nd->lean) st = up(&nd->d_fronts_w, fronts_w);
+  if (st == HH_OK && nd->lean) st = up(&nd->d_Coff_w, Coff_w);
+  if (st == HH_OK && nd->lean) st = up(&nd->d_Soff, Soff);
+  if (st == HH_OK && nd->lean) st = up(&nd->d_Poff, Poff);
+  if (st == HH_OK && nd->lean) st = up(&nd->d_eaListC, eaListC);
   if (st == HH_OK) st = up(&nd->d_lvr, lvr);
   if (st != HH_OK) { nd_plan_destroy(nd); return st; }
   *out = nd;
@@ -989,20 +1226,60 @@ void nd_plan_destroy(NDPlan* nd) {
   cudaFree(nd->d_Coff); cudaFree(nd->d_sub_ptr); cudaFree(nd->d_sub_list);
   cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_pos_front);
   cudaFree(nd->d_lvr);
+  cudaFree(nd->d_fronts_w); cudaFree(nd->d_Coff_w); cudaFree(nd->d_Soff); cudaFree(nd->d_Poff);
+  cudaFree(nd->d_eaListC);
   delete nd;
 }
 
 int64_t nd_front_entries(const NDPlan* p) { return p->F_entries; }
 int64_t nd_stream_bytes(const NDPlan* p) { return p->stream_bytes; }
 int nd_levels(const NDPlan* p) { return (int)p->levels.size(); }
-int64_t nd_work_entries(const NDPlan* p) { return p->w_entries + p->out_entries; }
-int64_t nd_cbuf_entries(const NDPlan* p) { return std::max<int64_t>(1, p->C_entries); }
+int64_t nd_work_entries(const NDPlan* p) { return p->w_entries + p->out_entries + (p->lean ? p->Pmax : 0); }
+int64_t nd_cbuf_entries(const NDPlan* p) {
+  if (p->lean) return p->Cw + p->Wmax + p->Smax[0] + p->Smax[1];
+  return std::max<int64_t>(1, p->C_entries);
+}
 
 hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
                     cudaStream_t s) {
   const int64_t FE = nd->F_entries, CE = nd_cbuf_entries(nd);
   const int64_t stS = nd->N * nd->S;
   HH_CUDA_TRY(cudaMemsetAsync(flag, 0, B * sizeof(int), s));
+  if (nd->lean) {
+    if (B != 1) { hh_set_error("lean ND storage needs one problem per factorisation"); return HH_E_CONFIG; }
+    cplx* C = cbuf;
+    cplx* W = C + nd->Cw;
+    cplx* Sst = W + nd->Wmax;   // packed Schur complements (first-fit offsets, see the plan)
+    for (const Chunk& ch : nd->chunks) {
+      const int cnt = ch.t1 - ch.t0;
+      int ms = 0, mf = 0;
+      for (int t = ch.t0; t < ch.t1; ++t) { ms = std::max(ms, nd->fronts[t].s); mf = std::max(mf, nd->fronts[t].f); }
+      {
+        const unsigned gx = (unsigned)std::min<int64_t>(8192, (ch.Wcount + 255) / 256);
+        k_nd_zero<<<dim3(gx, 1), 256, 0, s>>>(W, 0, 0, ch.Wcount);
+      }
+      if (ch.asmCount) {
+        k_nd_assemble<<<dim3((unsigned)((ch.asmCount + 255) / 256), 1), 256, 0, s>>>(
+            nd->d_asm + ch.asmBegin, ch.asmCount, nd->d_fronts_w, st, stS, W, 0);
+      }
+      for (int slot = 0; slot < 2; ++slot) {
+        if (!ch.ea_count[slot]) continue;
+        k_nd_ea_packed<<<dim3(ch.ea_count[slot], 64), 128, 0, s>>>(nd->d_eaListC + ch.ea_list_off[slot],
+                                                                   nd->d_fronts_w, nd->d_Soff, Sst,
+                                                                   nd->d_eamap, W);
+      }
+      const int tiles = (mf + UT - 1) / UT;
+      for (int kb = 0; kb < ms; kb += NB) {
+        k_nd_piv<<<dim3(cnt, 1, (mf + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
+            nd->d_fronts_w, ch.t0, kb, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag);
+        k_nd_upd<<<dim3(tiles * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0, C, 0,
+                                                             nd->d_Coff_w + ch.t0);
+      }
+      k_nd_copyout<<<dim3(cnt, 64), 256, 0, s>>>(nd->d_fronts_w, nd->d_fronts, nd->d_Soff, ch.t0, W, F, Sst);
+      HH_CUDA_TRY(cudaGetLastError());
+    }
+    return HH_OK;
+  }
   static const int prof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
   for (size_t L = 0; L < nd->levels.size(); ++L) {
     const LevelInfo& li = nd->levels[L];
@@ -1121,6 +1398,10 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   A.vmax = nd_vmax();
   static const int pf = getenv("HH_NO_PREFETCH") ? 0 : 1;
   A.prefetch = pf;
+  if (nd->lean) {   // no stored -H^T rows: transposed forward, then the per-level backward
+    c.sub_cut = -1;
+    c.split = nlev - 1;
+  }
   const int cut = c.sub_cut, Lb = c.split;
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
@@ -1133,6 +1414,18 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = cut + 1; L <= Lb; ++L) {
     const LevelInfo& li = nd->levels[L];
+    if (nd->lean) {
+      dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
+      HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
+      if (li.max_u == 0) continue;
+      const int ncb = (li.max_u + FT_COLS - 1) / FT_COLS, nrc = (li.max_s + FT_ROWS - 1) / FT_ROWS;
+      const int64_t PE = nd->w_entries + nd->out_entries;
+      HH_TRY(launch_pdl(k_nd_fwdT, dim3(ncb * nrc, li.count, B), FT_COLS, 0, s, A, li.begin,
+                        (const int64_t*)nd->d_Poff, ncb, PE));
+      HH_TRY(launch_pdl(k_nd_fwdT_red, dim3((li.max_u + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
+                        (const int64_t*)nd->d_Poff, PE));
+      continue;
+    }
     if (li.max_f > A.vmax || (li.max_u >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
@@ -1204,7 +1497,7 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
                       cudaStream_t s, bool shareF) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   SolveCfg have;
-  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, B, &have)) return HH_OK;
+  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, B, &have) || nd->lean) return HH_OK;
   const int nlev = (int)nd->levels.size();
   cudaEvent_t e0, e1;
   HH_CUDA_TRY(cudaEventCreate(&e0));
@@ -1255,7 +1548,8 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
 int nd_solve_launches(const NDPlan* ndc, int B) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   const int nlev = (int)nd->levels.size();
-  const SolveCfg c = get_cfg(nd, B);
+  SolveCfg c = get_cfg(nd, B);
+  if (nd->lean) { c.sub_cut = -1; c.split = nlev - 1; }
   int n = (c.sub_cut >= 0 ? 2 : 0) + 2 * (c.split - c.sub_cut) + (c.split < nlev - 1 ? 1 : 0);
   for (int L = c.sub_cut + 1; L <= c.split; ++L) {
     const LevelInfo& li = nd->levels[L];
