@@ -163,3 +163,42 @@ def shifts(k_elem, beta: float, sigma: float):
     """eps_e = beta * k_e^sigma (reading C2; the paper's eps = k^sigma has beta=1,
     PAPER.md:27, 532)."""
     return beta * np.asarray(k_elem, dtype=np.float64) ** sigma
+
+
+def apply_rows(dim: int, n: int, k_elem, eps_elem, x, rows):
+    """Rows `rows` of A(k, eps) x by a direct element loop around each node
+    (the same element and face matrices as `assemble`), for
+    sampled checks at sizes where assembling A is impractical."""
+    h = 1.0 / n
+    N1 = n + 1
+    Ke, Me, Bf = element_matrices(dim, h)
+    k_elem = np.asarray(k_elem, dtype=np.float64)
+    eps_elem = np.asarray(eps_elem, dtype=np.float64)
+    scalar = k_elem.ndim == 0
+    out = np.zeros(len(rows), dtype=np.complex128)
+    for r, node in enumerate(rows):
+        c = [(int(node) // N1 ** d) % N1 for d in range(dim)]
+        acc = 0.0 + 0.0j
+        for a in range(2 ** dim):                       # node = local node a of element e
+            e = [c[d] - ((a >> d) & 1) for d in range(dim)]
+            if any(v < 0 or v >= n for v in e):
+                continue
+            eidx = sum(e[d] * n ** d for d in range(dim))
+            ke = float(k_elem) if scalar else float(k_elem[eidx])
+            ee = float(eps_elem) if eps_elem.ndim == 0 else float(eps_elem[eidx])
+            lam = ke * ke + 1j * ee
+            first = sum(e[d] * N1 ** d for d in range(dim))
+            for b in range(2 ** dim):
+                gb = first + sum(((b >> d) & 1) * N1 ** d for d in range(dim))
+                acc += (Ke[a, b] - lam * Me[a, b]) * x[gb]
+            for d in range(dim):                        # boundary faces of this element
+                side = (a >> d) & 1
+                if not ((side == 0 and e[d] == 0) or (side == 1 and e[d] == n - 1)):
+                    continue
+                face = [q for q in range(2 ** dim) if ((q >> d) & 1) == side]
+                fa = face.index(a)
+                for fb, b in enumerate(face):
+                    gb = first + sum(((b >> dd) & 1) * N1 ** dd for dd in range(dim))
+                    acc += -1j * ke * Bf[fa, fb] * x[gb]
+        out[r] = acc
+    return out
