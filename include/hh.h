@@ -203,16 +203,18 @@ hh_status hh_destroy_problem(hh_problem* p);
 
 /* Phase instrumentation for the bench roofline (device events around each
  * phase of every FGMRES iteration; enabling it adds one host sync per
- * iteration).  st12 = [ms x4, algorithmic HBM bytes x4, phase launches x4]
+ * iteration).  st16 = [ms x4, algorithmic HBM bytes x4, phase launches x4,
+ * algorithmic HBM bytes of EVERY iteration x4] (the first three over the timed,
+ * i.e. sampled, iterations)
  * for the phases [pre-smooth+restrict, coarse solve, prolong+post-smooth+A_0,
  * Krylov (multi-dot + update)], accumulated since the last reset. */
 hh_status hh_reset_timers(hh_problem* p, int32_t enable);
-hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launches);
+hh_status hh_read_timers(hh_problem* p, double* st16, int64_t* launches);
 
-/* Sweep-wide phase instrumentation (same st12 layout as hh_read_timers) and
+/* Sweep-wide phase instrumentation (same st16 layout as hh_read_timers) and
  * kernel-launch count since the last reset; reset_enable >= 0 resets and sets
  * timing on (1) / off (0); -1 only reads. */
-hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches);
+hh_status hh_sweep_timers(int32_t reset_enable, double* st16, int64_t* launches);
 
 const char* hh_last_error(void);
 const char* hh_version(void);

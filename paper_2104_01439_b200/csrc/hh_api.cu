@@ -309,7 +309,8 @@ struct Engine {
   bool timing = false;
   cudaEvent_t ev[2 * T_NT] = {};
   double acc_ms[T_NT] = {0, 0, 0, 0};
-  double acc_bytes[T_NT] = {0, 0, 0, 0};
+  double acc_bytes[T_NT] = {0, 0, 0, 0};      // timed (sampled) iterations
+  double acc_bytes_all[T_NT] = {0, 0, 0, 0};  // every iteration (aggregate throughput)
   double acc_launch[T_NT] = {0, 0, 0, 0};
   int64_t launches = 0;
   int64_t launches_per_iter = 0;
@@ -674,21 +675,26 @@ void harvest_timers(Engine& E) {
 
 // algorithmic HBM bytes of one iteration per running sample:
 // each kernel reads its inputs and writes its outputs exactly once
-void account_bytes(Engine& E, int running, int j) {
+void phase_bytes(const Engine& E, int j, double* out) {
   const double N = (double)E.N, Nc = (double)E.Nc;
   const double c = E.LF.het ? 16.0 * (double)E.LF.elems : 0.0;
-  const double pre = 32.0 * N + 16.0 * Nc + c;                 // f, u, r_c (+ coef)
-  const double post = 64.0 * N + 16.0 * Nc + c;                // f, u, e_c, z, w (+ coef)
-  const double coarse = (double)nd_stream_bytes(E.plan) + 32.0 * Nc;
-  const double kry = (2.0 * (j + 1) + 3.0) * 16.0 * N;         // mdot + update
-  E.acc_bytes[T_PRE] += running * pre;
-  E.acc_bytes[T_COARSE] += running * coarse;
-  E.acc_bytes[T_POST] += running * post;
-  E.acc_bytes[T_KRYLOV] += running * kry;
-  E.acc_launch[T_PRE] += 1;
-  E.acc_launch[T_COARSE] += 1;
-  E.acc_launch[T_POST] += 1;
-  E.acc_launch[T_KRYLOV] += 1;
+  out[T_PRE] = 32.0 * N + 16.0 * Nc + c;                   // f, u, r_c (+ coef)
+  out[T_POST] = 64.0 * N + 16.0 * Nc + c;                  // f, u, e_c, z, w (+ coef)
+  out[T_COARSE] = (double)nd_stream_bytes(E.plan) + 32.0 * Nc;
+  out[T_KRYLOV] = (2.0 * (j + 1) + 3.0) * 16.0 * N;        // mdot + update
+}
+void account_bytes(Engine& E, int running, int j) {
+  double pb[T_NT];
+  phase_bytes(E, j, pb);
+  for (int t = 0; t < T_NT; ++t) {
+    E.acc_bytes[t] += running * pb[t];
+    E.acc_launch[t] += 1;
+  }
+}
+void account_bytes_all(Engine& E, int running, int j) {
+  double pb[T_NT];
+  phase_bytes(E, j, pb);
+  for (int t = 0; t < T_NT; ++t) E.acc_bytes_all[t] += running * pb[t];
 }
 
 int count_running(Engine& E) {
@@ -739,6 +745,7 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
         if (!running) break;
       }
       HH_TRY(run_iteration(E, timed));
+      if (E.timing) account_bytes_all(E, running, j);
       if (timed) {
         HH_CUDA_TRY(cudaStreamSynchronize(s));
         harvest_timers(E);
@@ -1027,7 +1034,7 @@ extern "C" hh_status hh_destroy_problem(hh_problem* p) {
 extern "C" hh_status hh_reset_timers(hh_problem* p, int32_t enable) {
   if (!p) return HH_E_ARG;
   p->E.timing = enable != 0;
-  for (int i = 0; i < T_NT; ++i) p->E.acc_ms[i] = p->E.acc_bytes[i] = p->E.acc_launch[i] = 0;
+  for (int i = 0; i < T_NT; ++i) p->E.acc_ms[i] = p->E.acc_bytes[i] = p->E.acc_launch[i] = p->E.acc_bytes_all[i] = 0;
   p->E.launches = 0;
   return HH_OK;
 }
@@ -1039,6 +1046,7 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
       st12[i] = p->E.acc_ms[i];
       st12[4 + i] = p->E.acc_bytes[i];
       st12[8 + i] = p->E.acc_launch[i];
+      st12[12 + i] = p->E.acc_bytes_all[i];
     }
   if (launches) *launches = p->E.launches;
   return HH_OK;
@@ -1047,14 +1055,14 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
 // ================================================================== sweep
 static std::mutex g_sweep_mu;
 static bool g_sweep_timing = false;
-static double g_sweep_st[3 * T_NT] = {0};
+static double g_sweep_st[4 * T_NT] = {0};
 static int64_t g_sweep_launches = 0;
 static std::vector<std::unique_ptr<Engine>> g_sweep_engines;   // persistent across hh_sweep calls
 
 extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches) {
   std::lock_guard<std::mutex> lk(g_sweep_mu);
   if (st12)
-    for (int i = 0; i < 3 * T_NT; ++i) st12[i] = g_sweep_st[i];
+    for (int i = 0; i < 4 * T_NT; ++i) st12[i] = g_sweep_st[i];
   if (launches) *launches = g_sweep_launches;
   if (reset_enable >= 0) {
     g_sweep_timing = reset_enable != 0;
@@ -1174,6 +1182,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     E.timing = timing;
     for (double& a : E.acc_ms) a = 0;
     for (double& a : E.acc_bytes) a = 0;
+    for (double& a : E.acc_bytes_all) a = 0;
     for (double& a : E.acc_launch) a = 0;
     E.launches = 0;
     if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
@@ -1236,6 +1245,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     for (int t = 0; t < T_NT; ++t) {
       g_sweep_st[t] += E.acc_ms[t];
       g_sweep_st[4 + t] += E.acc_bytes[t];
+      g_sweep_st[12 + t] += E.acc_bytes_all[t];
       g_sweep_st[8 + t] += E.acc_launch[t];
     }
     g_sweep_launches += E.launches;

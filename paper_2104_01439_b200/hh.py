@@ -249,7 +249,7 @@ class Problem:
         _check(lib.hh_reset_timers(self.handle, int(enable)))
 
     def read_timers(self):
-        st = (C.c_double * 12)()
+        st = (C.c_double * 16)()
         nl = C.c_int64()
         _check(lib.hh_read_timers(self.handle, st, C.byref(nl)))
         return _phase_dict(st, nl.value)
@@ -313,12 +313,12 @@ PHASES = ("pre", "coarse", "post", "krylov")
 def _phase_dict(st, launches):
     d = {"launches": launches}
     for i, ph in enumerate(PHASES):
-        d[ph] = {"ms": st[i], "bytes": st[4 + i], "launches": st[8 + i]}
+        d[ph] = {"ms": st[i], "bytes": st[4 + i], "launches": st[8 + i], "bytes_all": st[12 + i]}
     return d
 
 
 def sweep_timers(reset_enable=-1):
-    st = (C.c_double * 12)()
+    st = (C.c_double * 16)()
     nl = C.c_int64()
     _check(lib.hh_sweep_timers(reset_enable, st, C.byref(nl)))
     return _phase_dict(st, nl.value)
