@@ -185,22 +185,26 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     }                                                                          \
   }
 
-// g = virtual global base of the entry's vector; rows outside [rlo, rhi] read as 0
+// g = virtual global base of the entry's vector; rows outside [rlo, rhi] read as 0.
+// Flat index over the region, 4 loads issued per thread before any is used.
 __device__ __forceinline__ void load_region(cplx* sX, const cplx* __restrict__ g, const Tile& t,
                                             int n, double scale, int rlo, int rhi) {
   const int N1 = n + 1;
-  for (int sy = threadIdx.x / 32; sy < t.SY; sy += NT / 32) {
-    const int gy = t.gy(sy);
-    const bool rowin = gy >= rlo && gy <= rhi;
-    for (int sx = threadIdx.x % 32; sx < t.SX; sx += 32) {
-      const int gx = t.gx(sx);
-      cplx v = cmake(0, 0);
-      if (rowin && gx >= 0 && gx <= n) {
-        v = __ldg(&g[(int64_t)gy * N1 + gx]);
-        v.x *= scale;
-        v.y *= scale;
-      }
-      sX[sy * t.SX + sx] = v;
+  const int total = t.SX * t.SY;
+  for (int base = threadIdx.x; base < total; base += 4 * NT) {
+    cplx v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = base + k * NT;
+      const int sy = idx / t.SX, sx = idx - sy * t.SX;
+      const int gy = t.gy(sy), gx = t.gx(sx);
+      v[k] = (idx < total && gy >= rlo && gy <= rhi && gx >= 0 && gx <= n)
+                 ? __ldg(&g[(int64_t)gy * N1 + gx]) : cmake(0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = base + k * NT;
+      if (idx < total) sX[idx] = cscale(v[k], scale);
     }
   }
 }
@@ -208,13 +212,21 @@ __device__ __forceinline__ void load_region(cplx* sX, const cplx* __restrict__ g
 __device__ __forceinline__ void load_coef(double2* sE, const double2* __restrict__ coef,
                                           const Tile& t, int n) {
   const int EX = t.SX + 1, EY = t.SY + 1;
-  for (int ey0 = threadIdx.x / 32; ey0 < EY; ey0 += NT / 32) {
-    const int ey = t.Y0 - t.R - 1 + ey0;
-    for (int ex0 = threadIdx.x % 32; ex0 < EX; ex0 += 32) {
-      const int ex = t.X0 - t.R - 1 + ex0;
-      double2 v = make_double2(0, 0);
-      if (ex >= 0 && ex < n && ey >= 0 && ey < n) v = __ldg(&coef[(int64_t)ey * n + ex]);
-      sE[ey0 * EX + ex0] = v;
+  const int total = EX * EY;
+  for (int base = threadIdx.x; base < total; base += 4 * NT) {
+    double2 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = base + k * NT;
+      const int ey0 = idx / EX, ex0 = idx - ey0 * EX;
+      const int ey = t.Y0 - t.R - 1 + ey0, ex = t.X0 - t.R - 1 + ex0;
+      v[k] = (idx < total && ex >= 0 && ex < n && ey >= 0 && ey < n) ? __ldg(&coef[(int64_t)ey * n + ex])
+                                                                     : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int idx = base + k * NT;
+      if (idx < total) sE[idx] = v[k];
     }
   }
 }
