@@ -232,6 +232,7 @@ __device__ __forceinline__ void load_coef(double2* sE, const double2* __restrict
 }
 
 struct FineK {   // per-launch constants
+  const cplx* dinv; int64_t stride;        // precomputed D^{-1} (het), entry stride
   int n; double h; double omega; int nu;
   const double2* coef; int64_t coef_bs;   // het
   const double2* kc;                       // constant k: [B]
@@ -295,6 +296,8 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const Const9 c9 = make_const9(kc, h, true);
   load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
+  const bool pre_di = HET && P.dinv;
+  if (pre_di) load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
   if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   __syncthreads();
   // D^{-1} and the first step from u = 0 (pointwise) on the full region
@@ -302,11 +305,12 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   FOR_REGION(t.R, {
     cplx di = cmake(0, 0), v = cmake(0, 0);
     if (in) {
-      di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
-                                                          : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
+      di = pre_di ? sDi[si]
+                  : ((!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
+                                                                   : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc)));
       v = cscale(cmul(di, sF[si]), omega);
     }
-    sDi[si] = di;
+    if (!pre_di) sDi[si] = di;
     sA[si] = v;
     sB[si] = cmake(0, 0);
   })
@@ -383,6 +387,8 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const Const9 c9e = make_const9(kc, h, true);
   load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
+  const bool pre_di = HET && P.dinv;
+  if (pre_di) load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
   if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
   const cplx* u = uin.at(b) - vofs;
   const cplx* ecv = ecin.at(b);
@@ -415,12 +421,13 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
         v.x += a.x;
         v.y += a.y;
       }
-      di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
-                                                          : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
+      if (!pre_di)
+        di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
+                                                            : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
     }
     sA[si] = v;
     sB[si] = cmake(0, 0);
-    sDi[si] = di;
+    if (!pre_di) sDi[si] = di;
   })
   __syncthreads();
   cplx* cur = sA;
@@ -444,6 +451,41 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
     zb[gi] = cur[si];
     if (WITH_W) wb[gi] = node_op<HET, false>(cur, si, t, gx, gy, n, h, sE, kc, c90);
   })
+}
+
+// ------------------------------------------------------------ precomputed D^{-1}
+// D_p = sum over adjacent elements of 2/3 - lambda_e h^2/9, -i k_e h/3 per boundary
+// edge (reading C6), at every stored node of entry b (owned + ghost rows)
+__global__ void k_dinv2d(int n, double h, const double2* __restrict__ coef, int64_t coef_bs,
+                         const int2* __restrict__ slab, int G, int64_t stride, int rows, cplx* __restrict__ dinv) {
+  const int b = blockIdx.z;
+  const int N1 = n + 1;
+  const int2 sl = slab_of(slab, b, n);
+  const int gx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gy = sl.x - G + (int)blockIdx.y;
+  if (gx > n || gy < 0 || gy > n || (int)blockIdx.y >= rows) return;
+  const double2* cf = coef + b * coef_bs;
+  const double h2 = h * h * (4.0 / 36.0), h3 = h / 3.0;
+  auto K = [&](int ex, int ey) { return __ldg(&cf[(int64_t)ey * n + ex]); };
+  cplx dg = cmake(0, 0);
+  for (int q = 0; q < 4; ++q) {
+    const int ex = gx - 1 + (q & 1), ey = gy - 1 + ((q >> 1) & 1);
+    if (ex < 0 || ex >= n || ey < 0 || ey >= n) continue;
+    const double2 c = K(ex, ey);
+    dg.x += 2.0 / 3.0 - c.x * c.x * h2;
+    dg.y -= c.y * h2;
+  }
+  if (gx == 0 || gx == n) {
+    const int ex = gx == 0 ? 0 : n - 1;
+    if (gy > 0) dg.y -= K(ex, gy - 1).x * h3;
+    if (gy < n) dg.y -= K(ex, gy).x * h3;
+  }
+  if (gy == 0 || gy == n) {
+    const int ey = gy == 0 ? 0 : n - 1;
+    if (gx > 0) dg.y -= K(gx - 1, ey).x * h3;
+    if (gx < n) dg.y -= K(gx, ey).x * h3;
+  }
+  dinv[(int64_t)b * stride + (int64_t)blockIdx.y * N1 + gx] = cinv(dg);
 }
 
 // ------------------------------------------------------------ coarse stencil
@@ -517,6 +559,7 @@ FineK make_k(const Level& L, int nu, double omega, const int* st) {
   FineK P;
   P.n = L.n; P.h = L.h; P.omega = omega; P.nu = nu;
   P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc; P.st = st;
+  P.dinv = L.dinv; P.stride = L.stride;
   P.slab = L.slab; P.G = L.G;
   return P;
 }
@@ -592,6 +635,14 @@ hh_status coarse_stencil2d(const Level& C, int B, cplx* st, cudaStream_t s) {
     k_stencil2d<true><<<g, bs, 0, s>>>(C.n, C.h, C.coef, C.coef_bs, nullptr, st);
   else
     k_stencil2d<false><<<g, bs, 0, s>>>(C.n, C.h, nullptr, 0, C.kc, st);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
+hh_status fine_dinv2d(const Level& L, int B, cudaStream_t s) {
+  const int rows = L.maxloc + 2 * L.G;
+  dim3 g((L.n + 1 + 127) / 128, rows, B);
+  k_dinv2d<<<g, 128, 0, s>>>(L.n, L.h, L.coef, L.coef_bs, L.slab, L.G, L.stride, rows, L.dinv);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

@@ -21,6 +21,7 @@ namespace {
 constexpr int BX = 32, BY = 8;
 
 struct F3 {
+  const cplx* dinv; int64_t stride;      // precomputed D^{-1} (het), entry stride
   int n; double h; double omega;
   const double2* coef; int64_t coef_bs;
   const double2* kc;
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(BX * BY) k_jacobi3d(F3 P, VArg f, SArg fs, VAr
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
   const cplx fv = cscale(__ldg(&(f.at(b) - vo)[gi]), fs.at(b));
-  const cplx di = cinv(diag3<HET>(P, cf, kc, gx, gy, gz));
+  const cplx di = (HET && P.dinv) ? __ldg(&(P.dinv + (int64_t)b * P.stride - vo)[gi])
+                                  : cinv(diag3<HET>(P, cf, kc, gx, gy, gz));
   cplx v;
   if (u.p) {
     const cplx* ub = u.at(b) - vo;
@@ -278,6 +280,18 @@ __global__ void __launch_bounds__(BX * BY) k_prolong3d(F3 P, VArg u, VArg ec, VA
   (uo.at(b) - vo)[gi] = v;
 }
 
+// D^{-1} at every stored node of every entry (het setup)
+template <bool HET>
+__global__ void __launch_bounds__(BX * BY) k_dinv3d(F3 P, cplx* __restrict__ dinv) {
+  int b, gx, gy, gz;
+  int64_t vo;
+  if (!node_of(P, b, gx, gy, gz, vo)) return;
+  const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
+  (dinv + (int64_t)b * P.stride - vo)[gi] = cinv(diag3<HET>(P, cf, kc, gx, gy, gz));
+}
+
 // coarse stencil: st[b][node*27 + (dx+1) + 3(dy+1) + 9(dz+1)]
 template <bool HET>
 __global__ void k_stencil3d(F3 P, cplx* __restrict__ stv) {
@@ -342,6 +356,7 @@ F3 make3(const Level& L, double omega, const int* st, int ext) {
   P.n = L.n; P.h = L.h; P.omega = omega; P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc;
   P.st = st; P.N1 = L.n + 1;
   P.slab = L.slab; P.G = L.G; P.maxloc = L.maxloc; P.ext = ext;
+  P.dinv = L.dinv; P.stride = L.stride;
   return P;
 }
 dim3 grid3(const F3& P, int B) {
@@ -421,6 +436,16 @@ hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega
     cur ^= 1;
   }
   if (w.p) HH_TRY(fine_apply3d(L, B, st, HH_OP_A0, z, w, VArg(), s));
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
+hh_status fine_dinv3d(const Level& L, int B, cudaStream_t s) {
+  F3 P = make3(L, 0, nullptr, L.G);
+  P.dinv = nullptr;
+  const dim3 g = grid3(P, B), bl(BX, BY);
+  if (L.het) k_dinv3d<true><<<g, bl, 0, s>>>(P, L.dinv);
+  else k_dinv3d<false><<<g, bl, 0, s>>>(P, L.dinv);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }

@@ -49,6 +49,11 @@ hh_status fine_pre3d(const Level&, int, const int*, int, double, VArg, SArg, VAr
 hh_status fine_post3d(const Level&, int, const int*, int, double, VArg, SArg, VArg, VArg, VArg,
                       VArg, cudaStream_t);
 hh_status coarse_stencil3d(const Level&, int, cplx*, cudaStream_t);
+hh_status fine_dinv2d(const Level&, int, cudaStream_t);
+hh_status fine_dinv3d(const Level&, int, cudaStream_t);
+hh_status fine_dinv(const Level& L, int B, cudaStream_t s) {
+  return L.dim == 2 ? fine_dinv2d(L, B, s) : fine_dinv3d(L, B, s);
+}
 
 hh_status fine_apply(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                      cudaStream_t s) {
@@ -279,7 +284,7 @@ struct Engine {
   int device = 0;
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
-      cpart, dpart, hist, kstage, slabp, hstage, ustage;
+      cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp;
   int* h_status = nullptr;   // pinned
   int h_cap = 0;
   // batch
@@ -318,7 +323,7 @@ struct Engine {
   ~Engine() {
     drop_graphs();
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
-                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage};
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp};
     for (Pool* p : all) p->release();
     if (h_status) cudaFreeHost(h_status);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
@@ -558,6 +563,13 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   E.nd_flag = (int*)(base + o_fl);
   HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
   prof_mark(E, "pools+coef", tp);
+  // precomputed D^{-1} of the heterogeneous fine operator (read by the smoothers)
+  E.LF.dinv = nullptr;
+  if (E.LF.het) {
+    HH_TRY(E.dinvp.ensure(((size_t)B * NS + 16) * 16));
+    E.LF.dinv = E.dinvp.as<cplx>() + E.FL.pad;
+    HH_TRY(fine_dinv(E.LF, B, E.s));
+  }
   // coarse operator + factorisation (slab mode: one copy, shared by the slabs)
   HH_TRY(coarse_stencil(E.LC, E.Bf, E.stc.as<cplx>(), E.s));
   HH_TRY(nd_factor(P, E.Bf, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));

@@ -108,6 +108,7 @@ struct Level {
   int G = 0;                       // ghost planes per side
   int maxloc = 0;                  // max owned planes over the entries (n+1 without slabs)
   int64_t stride = 0;              // entry stride of fine vectors: (maxloc + 2G) * plane
+  cplx* dinv = nullptr;            // het fine level: D^{-1} = diag(A_eps)^{-1} per node (vector layout)
 };
 
 __device__ __forceinline__ int2 slab_of(const int2* sl, int b, int n) {
@@ -122,6 +123,8 @@ hh_status fine_pre(const Level& L, int B, const int* st, int nu, double omega, V
 hh_status fine_post(const Level& L, int B, const int* st, int nu, double omega, VArg f, SArg fs,
                     VArg u, VArg ec, VArg z, VArg w, cudaStream_t s);
 hh_status coarse_stencil(const Level& C, int B, cplx* st, cudaStream_t s);
+// L.dinv = diag(A_eps)^{-1} at every stored node of every entry (setup; het levels)
+hh_status fine_dinv(const Level& L, int B, cudaStream_t s);
 
 // ---------------------------------------------------------------- coarse ND solver
 struct NDPlan;                       // host+device tree data for one (dim, m); shareable
