@@ -53,11 +53,14 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler.  Started BEFORE the warm-up (its start-up takes driver
+    locks that stall CUDA calls for tens of ms); only the samples taken inside
+    the timed region [mark(), stop()] are reported."""
 
     def __init__(self, dev):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        self.t0 = None
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -67,9 +70,22 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def mark(self):
+        """Start of the timed region."""
+        self.t0 = time.time()
+
+    @staticmethod
+    def _ts(text):
+        import datetime
+        try:
+            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def stop(self):
         if self.p is None:
             return None
+        t1 = time.time()
         self.p.terminate()
         try:
             self.p.wait(timeout=5)
@@ -80,6 +96,9 @@ class Clocks:
         for line in open(self.f.name):
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
+                continue
+            ts = self._ts(parts[0])
+            if ts is not None and self.t0 is not None and not (self.t0 - 0.05 <= ts <= t1 + 0.05):
                 continue
             try:
                 rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
@@ -207,12 +226,14 @@ def run_ours(args, rank, world, dev):
               "l2": "Krylov basis > L2 (126 MB); L2 flushed between steps",
               "parallelism": f"slab{world}" if world > 1 else "single"}
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+    clk = Clocks(dev) if rank == 0 and not os.environ.get("HH_BENCH_NO_CLOCKS") else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = Clocks(dev) if rank == 0 else None
+    if clk:
+        clk.mark()
     if args.workload in ("sweep", "search"):
         hh.sweep_timers(1)
     else:
@@ -234,7 +255,9 @@ def run_ours(args, rank, world, dev):
     if world > 1:
         dist.barrier()
     clocks = clk.stop() if clk else None
-    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    print("step ms: " + " ".join(f"{x:.1f}" for x in step_ms), file=sys.stderr)
+    dev_ms = sum(step_ms)
     if args.workload in ("sweep", "search"):
         tm = hh.sweep_timers(0)
     else:
