@@ -554,15 +554,15 @@ constexpr int WIDE_RPC = 8;   // rows per CTA for rows longer than 64 entries
 
 // dot of one row with v by a group of G lanes (G = 32, 16, 8, 4), 4 predicated
 // loads in flight per lane; the group sum is left in every lane of the group
-template <int G>
+template <int G, int DEPTH = 4>
 __device__ __forceinline__ cplx row_dot_g(const cplx* __restrict__ row, const cplx* v, int len, int sub) {
   cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
-  for (int c = sub; c < len; c += 4 * G) {
-    cplx r[4];
+  for (int c = sub; c < len; c += DEPTH * G) {
+    cplx r[DEPTH];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) r[t] = (c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
+    for (int t = 0; t < DEPTH; ++t) r[t] = (c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+    for (int t = 0; t < DEPTH; ++t)
       if (c + G * t < len) cfma(t & 1 ? a1 : a0, r[t], v[c + G * t]);
   }
   cplx a = cadd(a0, a1);
@@ -574,7 +574,7 @@ __device__ __forceinline__ cplx row_dot_g(const cplx* __restrict__ row, const cp
   return a;
 }
 
-template <int DIR, int G>
+template <int DIR, int G, int DEPTH = 4>
 __device__ __forceinline__ void wide_rows(const SolveArgs& A, const FrontMeta& m, int b, const cplx* row0,
                                           const cplx* v, const cplx* wg, int len, int r0, int r1, int warp,
                                           int lane) {
@@ -583,7 +583,7 @@ __device__ __forceinline__ void wide_rows(const SolveArgs& A, const FrontMeta& m
   for (int rb = r0 + warp * RPW; rb < r1; rb += (LT / 32) * RPW) {
     const int r = rb + grp;
     const bool ok = r < r1;
-    const cplx acc = row_dot_g<G>(row0 + (int64_t)(ok ? r : r0) * m.f, v, ok ? len : 0, sub);
+    const cplx acc = row_dot_g<G, DEPTH>(row0 + (int64_t)(ok ? r : r0) * m.f, v, ok ? len : 0, sub);
     if (ok && sub == 0) {
       if (DIR == 0) upd_of(A, b)[m.outOff + r] = cadd(acc, wg[m.s + r]);
       else A.x.at(b)[A.sep[m.sepOff + r]] = acc;
@@ -596,7 +596,7 @@ __host__ __device__ inline int wide_group(int len) { return len > 64 ? 32 : (len
 __host__ __device__ inline int wide_rpc(int len) { return WIDE_RPC * (32 / wide_group(len)); }
 
 template <int DIR>
-__global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin) {
+__global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin, int cap) {
   extern __shared__ double4 smem_raw[];
   cplx* vs = reinterpret_cast<cplx*>(smem_raw);
   const int b = blockIdx.z;
@@ -617,10 +617,14 @@ __global__ void __launch_bounds__(LT) k_nd_rows_wide(SolveArgs A, int begin) {
   if (A.st && A.st[b]) return;
   const cplx* wg = w_of(A, b) + m.posOff;
   const cplx* v = wg;
-  if (len <= A.vmax) {
+  if (len <= cap) {                            // cap = shared-memory entries of this launch
     for (int c = threadIdx.x; c < len; c += blockDim.x) vs[c] = wg[c];
     __syncthreads();
     v = vs;
+  }
+  if (len > 1024) {   // long rows (3D top levels): 8 loads in flight per lane
+    wide_rows<DIR, 32, 8>(A, m, b, row0, v, wg, len, r0, r1, warp, lane);
+    return;
   }
   switch (wide_group(len)) {
     case 32: wide_rows<DIR, 32>(A, m, b, row0, v, wg, len, r0, r1, warp, lane); break;
@@ -1391,6 +1395,29 @@ static int level_split(int rows, int count, int B) {
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                            VArg x, cudaStream_t s, SolveCfg c, bool shareF) {
   const int nlev = (int)nd->levels.size();
+  // HH_ND_LEVEL_TIMING=1: per-level event timing (diagnostics; synchronises, never in graphs)
+  static const bool lt = getenv("HH_ND_LEVEL_TIMING") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const bool timing = lt && cap == cudaStreamCaptureStatusNone;
+  cudaEvent_t tev[2];
+  if (timing) { cudaEventCreate(&tev[0]); cudaEventCreate(&tev[1]); }
+  auto tick = [&]() { if (timing) cudaEventRecord(tev[0], s); };
+  auto tock = [&](const char* what, int L) {
+    if (!timing) return;
+    cudaEventRecord(tev[1], s);
+    cudaEventSynchronize(tev[1]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tev[0], tev[1]);
+    const LevelInfo& li = nd->levels[L];
+    double by = 0;
+    for (int t = li.begin; t < li.begin + li.count; ++t) {
+      const FrontMeta& fm = nd->fronts[t];
+      by += 16.0 * (what[0] == 'f' ? (double)fm.u * fm.s : (double)fm.s * fm.f);
+    }
+    fprintf(stderr, "[hh nd] %s L%-2d fronts %5d max_s %5d max_u %5d: %8.1f us %8.1f MB %6.0f GB/s\n", what, L,
+            li.count, li.max_s, li.max_u, 1e3 * ms, by * B / 1e6, by * B / (ms * 1e-3) / 1e9);
+  };
   SolveArgs A;
   A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo; A.gmap = nd->d_gmap;
   A.F = F; A.FE = shareF ? 0 : nd->F_entries;
@@ -1414,6 +1441,8 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = cut + 1; L <= Lb; ++L) {
     const LevelInfo& li = nd->levels[L];
+    tick();
+    struct Tk { decltype(tock)& f; int L; ~Tk() { f("fwd", L); } } tk_{tock, L};
     if (nd->lean) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
@@ -1430,11 +1459,11 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
       if (li.max_u == 0) continue;
-      const size_t sm = (size_t)std::min(li.max_s, A.vmax) * sizeof(cplx);
+      const size_t sm = li.max_s > A.vmax ? 0 : (size_t)li.max_s * sizeof(cplx);
       if (sm > 48 * 1024)
         HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       dim3 g(li.count, (li.max_u + WIDE_RPC - 1) / WIDE_RPC, B);   // covers the smallest rows-per-CTA
-      HH_TRY(launch_pdl(k_nd_rows_wide<0>, g, LT, sm, s, A, li.begin));
+      HH_TRY(launch_pdl(k_nd_rows_wide<0>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
       continue;
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
@@ -1461,14 +1490,17 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   for (int L = Lb; L > cut; --L) {
     const LevelInfo& li = nd->levels[L];
+    tick();
+    struct Tk { decltype(tock)& f; int L; ~Tk() { f("bwd", L); } } tk_{tock, L};
     if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
-      const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
+      // fronts whose vector does not fit read it from L2: no shared memory then (occupancy)
+      const size_t sm = li.max_f > A.vmax ? 0 : (size_t)li.max_f * sizeof(cplx);
       if (sm > 48 * 1024)
         HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       dim3 g(li.count, (li.max_s + WIDE_RPC - 1) / WIDE_RPC, B);
-      HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin));
+      HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
       continue;
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
