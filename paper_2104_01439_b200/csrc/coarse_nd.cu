@@ -116,6 +116,9 @@ struct NDPlan {
   int64_t* d_Poff = nullptr;         // forward partial-sum offset (level-local)
   int* d_eaListC = nullptr;
   int64_t Wmax = 0, Cw = 0, Smax[2] = {0, 0}, Pmax = 0;
+  // K-split backward of long rows (3D): per front ceil(f / KC) x s partial sums
+  int64_t Kmax = 0;
+  int64_t* d_Koff = nullptr;
 };
 
 // ============================================================ device kernels
@@ -692,6 +695,50 @@ __global__ void k_nd_fwdT_red(SolveArgs A, int begin, const int64_t* __restrict_
   upd_of(A, b)[m.outOff + col] = csub(w[m.s + col], sum);
 }
 
+// K-split backward for long rows (3D levels with f > 1024): CTA = (32 rows,
+// KC-column chunk); the chunk of v = [z_s ; -x[halo]] (staged in w) goes to shared
+// memory, each warp dots 8 rows over it (8 loads in flight per lane); the chunk
+// partials are summed in a fixed order by k_nd_bwdK_red.
+constexpr int KC = 2048, KR = 32;
+__global__ void __launch_bounds__(LT) k_nd_bwdK(SolveArgs A, int begin, int ncb, const int64_t* __restrict__ Koff,
+                                                int64_t KE) {
+  __shared__ cplx vs[KC];
+  const int b = blockIdx.z;
+  const FrontMeta m = A.fr[begin + blockIdx.y];
+  const int rb = blockIdx.x / ncb, cb = blockIdx.x % ncb;
+  const int r0 = rb * KR, c0 = cb * KC;
+  pdl_trigger();
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  if (r0 >= m.s || c0 >= m.f) return;
+  const int r1 = min(m.s, r0 + KR), len = min(m.f - c0, KC);
+  const cplx* wg = w_of(A, b) + m.posOff + c0;
+  for (int c = threadIdx.x; c < len; c += blockDim.x) vs[c] = wg[c];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const cplx* F = A.F + (int64_t)b * A.FE + m.Foff + c0;
+  cplx* part = A.work + (int64_t)b * A.WE + KE + Koff[begin + blockIdx.y] + (int64_t)cb * m.s;
+  for (int r = r0 + warp; r < r1; r += LT / 32) {
+    const cplx acc = row_dot_g<32, 8>(F + (int64_t)r * m.f, vs, len, lane);
+    if (lane == 0) part[r] = acc;
+  }
+}
+
+__global__ void k_nd_bwdK_red(SolveArgs A, int begin, const int64_t* __restrict__ Koff, int64_t KE) {
+  const int b = blockIdx.z;
+  pdl_trigger();
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  const FrontMeta m = A.fr[begin + blockIdx.y];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m.s) return;
+  const int ncb = (m.f + KC - 1) / KC;
+  const cplx* part = A.work + (int64_t)b * A.WE + KE + Koff[begin + blockIdx.y];
+  cplx sum = cmake(0, 0);
+  for (int cb = 0; cb < ncb; ++cb) sum = cadd(sum, part[(int64_t)cb * m.s + r]);
+  A.x.at(b)[A.sep[m.sepOff + r]] = sum;
+}
+
 // ------------------------------------------------------------ cluster solve
 // One thread-block cluster (CL CTAs on CL SMs) per sample walks the tree levels
 // [L0, nlev): forward (gather, update rows) up to the root, then backward down
@@ -1017,6 +1064,15 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     Cmax = std::max(Cmax, o);
   }
   nd->F_entries = Foff; nd->w_entries = posOff; nd->out_entries = outOff; nd->C_entries = Cmax;
+  std::vector<int64_t> Koff(nf, 0);
+  for (const LevelInfo& li : nd->levels) {
+    int64_t ko = 0;
+    for (int t = li.begin; t < li.begin + li.count; ++t) {
+      Koff[t] = ko;
+      ko += (int64_t)((nd->fronts[t].f + 2047) / 2048) * nd->fronts[t].s;
+    }
+    if (li.max_f > 1024) nd->Kmax = std::max(nd->Kmax, ko);
+  }
   // lean storage for trees whose full fronts would not fit (3D coarse grids of
   // cfg4 size); HH_ND_LEAN=0/1 overrides, HH_ND_WMAX sets the workspace (entries)
   std::vector<FrontMeta> fronts_w;
@@ -1212,6 +1268,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   if (st == HH_OK) st = up(&nd->d_sep_front, sep_front);
   if (st == HH_OK) st = up(&nd->d_halo_front, halo_front);
   if (st == HH_OK) st = up(&nd->d_pos_front, pos_front);
+  if (st == HH_OK) st = up(&nd->d_Koff, Koff);
   if (st == HH_OK && nd->lean) st = up(&nd->d_fronts_w, fronts_w);
   if (st == HH_OK && nd->lean) st = up(&nd->d_Coff_w, Coff_w);
   if (st == HH_OK && nd->lean) st = up(&nd->d_Soff, Soff);
@@ -1231,14 +1288,17 @@ void nd_plan_destroy(NDPlan* nd) {
   cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_pos_front);
   cudaFree(nd->d_lvr);
   cudaFree(nd->d_fronts_w); cudaFree(nd->d_Coff_w); cudaFree(nd->d_Soff); cudaFree(nd->d_Poff);
-  cudaFree(nd->d_eaListC);
+  cudaFree(nd->d_eaListC); cudaFree(nd->d_Koff);
   delete nd;
 }
 
 int64_t nd_front_entries(const NDPlan* p) { return p->F_entries; }
 int64_t nd_stream_bytes(const NDPlan* p) { return p->stream_bytes; }
 int nd_levels(const NDPlan* p) { return (int)p->levels.size(); }
-int64_t nd_work_entries(const NDPlan* p) { return p->w_entries + p->out_entries + (p->lean ? p->Pmax : 0); }
+// per sample: w | update vectors | lean forward partials | K-split backward partials
+int64_t nd_work_entries(const NDPlan* p) {
+  return p->w_entries + p->out_entries + (p->lean ? p->Pmax : 0) + p->Kmax;
+}
 int64_t nd_cbuf_entries(const NDPlan* p) {
   if (p->lean) return p->Cw + p->Wmax + p->Smax[0] + p->Smax[1];
   return std::max<int64_t>(1, p->C_entries);
@@ -1495,6 +1555,15 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
+      if (li.max_f > 1024 && !getenv("HH_NO_BWDK")) {   // long rows: K-split over column chunks
+        const int ncb = (li.max_f + KC - 1) / KC, nrb = (li.max_s + KR - 1) / KR;
+        const int64_t KE = nd->w_entries + nd->out_entries + (nd->lean ? nd->Pmax : 0);
+        HH_TRY(launch_pdl(k_nd_bwdK, dim3(nrb * ncb, li.count, B), LT, 0, s, A, li.begin, ncb,
+                          (const int64_t*)nd->d_Koff, KE));
+        HH_TRY(launch_pdl(k_nd_bwdK_red, dim3((li.max_s + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
+                          (const int64_t*)nd->d_Koff, KE));
+        continue;
+      }
       // fronts whose vector does not fit read it from L2: no shared memory then (occupancy)
       const size_t sm = li.max_f > A.vmax ? 0 : (size_t)li.max_f * sizeof(cplx);
       if (sm > 48 * 1024)
