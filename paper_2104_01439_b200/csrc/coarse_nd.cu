@@ -1392,7 +1392,11 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
   return HH_OK;
 }
 
-constexpr int CLUSTER = 8;   // CTAs per sample in the cluster solve (portable cluster size)
+// CTAs per sample in the cluster solve (16: non-portable cluster size, opted in below)
+static int cluster_size() {
+  static const int v = getenv("HH_ND_CLUSTER") ? atoi(getenv("HH_ND_CLUSTER")) : 16;
+  return v;
+}
 
 static bool cached_cfg(NDPlan* nd, int B, SolveCfg* c) {
   std::lock_guard<std::mutex> lk(nd->cut_mu);
@@ -1533,6 +1537,9 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   }
   if (Lb < nlev - 1) {
     cudaLaunchConfig_t cfg = {};
+    const int CLUSTER = cluster_size();
+    if (CLUSTER > 8)
+      HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cfg.gridDim = dim3(CLUSTER * B);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = 0;
