@@ -53,65 +53,69 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler.  Started BEFORE the warm-up (its start-up takes driver
-    locks that stall CUDA calls for tens of ms); only the samples taken inside
-    the timed region [mark(), stop()] are reported."""
+    """SM clock and throttle-reason sampler (NVML, every 100 ms, in a thread of
+    this process: only the SM clock and the clocks-event-reason bits are read,
+    which do not stall concurrent CUDA calls the way an nvidia-smi process polling
+    the full query set did).  Started before the warm-up; only the samples inside
+    the timed region [mark(), stop()] are reported.  Falls back to nvidia-smi if
+    NVML cannot be loaded."""
+
+    NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+             ("sw_power_cap", 0x4))
 
     def __init__(self, dev):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
         self.t0 = None
-        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.ok = False
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={dev}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            idx = dev
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[dev])
+                except ValueError:
+                    idx = dev
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
         except Exception:
-            self.p = None
+            self.ok = False
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.wait(0.1):
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((time.time(), float(sm), rs))
+            except Exception:
+                pass
 
     def mark(self):
         """Start of the timed region."""
         self.t0 = time.time()
 
-    @staticmethod
-    def _ts(text):
-        import datetime
-        try:
-            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
-        except ValueError:
-            return None
-
     def stop(self):
-        if self.p is None:
+        if not self.ok:
             return None
         t1 = time.time()
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            ts = self._ts(parts[0])
-            if ts is not None and self.t0 is not None and not (self.t0 - 0.05 <= ts <= t1 + 0.05):
-                continue
-            try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
-            except ValueError:
-                continue
-        os.unlink(self.f.name)
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        rows = [r for r in self.rows if self.t0 is None or self.t0 - 0.05 <= r[0] <= t1 + 0.05]
         if not rows:
             return None
-        sm = sorted(r[0] for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
-                "samples": len(rows), "reasons": reasons}
+        sm = sorted(r[1] for r in rows)
+        reasons = sorted({n for r in rows for n, bit in self.NAMES if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.max), "samples": len(rows),
+                "reasons": reasons, "source": "nvml"}
 
 
 def rank_samples(rank, world):

@@ -156,9 +156,20 @@ struct BlockCache {
     free_blocks.erase(it);
     return p;
   }
+  std::map<int, size_t> total;   // device memory size, queried once per device
   bool give(int dev, void* p, size_t bytes) {
-    size_t tot = 0, fr = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
+    size_t tot = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = total.find(dev);
+      if (it != total.end()) tot = it->second;
+    }
+    if (!tot) {
+      size_t fr = 0;
+      if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return false; }
+      std::lock_guard<std::mutex> lk(mu);
+      total[dev] = tot;
+    }
     std::lock_guard<std::mutex> lk(mu);
     if (cached + bytes > tot / 2) return false;
     free_blocks.insert({{dev, bytes}, p});
@@ -320,6 +331,12 @@ struct Engine {
   int64_t launches = 0;
   int64_t launches_per_iter = 0;
 
+  // return every pool to the device block cache (the engine itself is reused)
+  void release_pools() {
+    Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp};
+    for (Pool* p : all) p->release();
+  }
   ~Engine() {
     drop_graphs();
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
@@ -837,13 +854,52 @@ hh_status leave(Engine& E, cudaStream_t user) {
 }  // namespace
 
 // ================================================================== ABI
+// Engines of destroyed handles are kept (per device, at most 4) and handed to
+// the next setup: destroying an engine (graph execs, events, stream, pinned
+// buffers, pools) costs 2-170 ms of driver work, re-creating it as much.
+static std::mutex g_engine_mu;
+static std::vector<Engine*> g_engine_cache;
+
+static Engine* engine_take(int device) {
+  std::lock_guard<std::mutex> lk(g_engine_mu);
+  for (size_t i = 0; i < g_engine_cache.size(); ++i)
+    if (g_engine_cache[i]->device == device) {
+      Engine* e = g_engine_cache[i];
+      g_engine_cache.erase(g_engine_cache.begin() + i);
+      return e;
+    }
+  return nullptr;
+}
+
+static void engine_give(Engine* e) {
+  const double t0 = now_s();
+  e->drop_graphs();
+  const double t1 = now_s();
+  e->release_pools();   // memory goes back to the block cache (flushed on OOM)
+  if (g_prof_setup)
+    fprintf(stderr, "[hh destroy] drop_graphs %.3f ms release_pools %.3f ms\n", 1e3 * (t1 - t0),
+            1e3 * (now_s() - t1));
+  {
+    std::lock_guard<std::mutex> lk(g_engine_mu);
+    if (g_engine_cache.size() < 4) {
+      e->timing = false;
+      g_engine_cache.push_back(e);
+      return;
+    }
+  }
+  delete e;
+}
+
 struct hh_problem {
   hh_problem_desc d{};
-  Engine E;
+  Engine* ep = nullptr;
   cudaStream_t user = nullptr;
   Comm* comm = nullptr;
   int64_t n_local = 0;      // user-vector length: owned nodes of this handle's slabs
-  ~hh_problem() { comm_destroy(comm); }
+  ~hh_problem() {
+    comm_destroy(comm);
+    if (ep) engine_give(ep);
+  }
 };
 
 extern "C" hh_status hh_nccl_unique_id(void* id128) {
@@ -882,7 +938,14 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   p->d.k_elem = p->d.k_elem_coarse = nullptr;
   p->d.nccl_id = nullptr;
   p->user = (cudaStream_t)d->stream;
-  hh_status st = engine_init(p->E, d->device);
+  hh_status st = HH_OK;
+  p->ep = engine_take(d->device);
+  if (!p->ep) {
+    p->ep = new (std::nothrow) Engine();
+    if (!p->ep) { delete p; return HH_E_OOM; }
+    st = engine_init(*p->ep, d->device);
+    if (st != HH_OK) { delete p->ep; p->ep = nullptr; }
+  }
   if (st == HH_OK && use_nccl) st = comm_create(d->nccl_id, d->rank, d->nranks, d->device, &p->comm);
   if (st == HH_OK) {
     BatchSpec sp;
@@ -896,11 +959,11 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
     sp.k.assign(sp.B, d->k_const); sp.beta.assign(sp.B, d->beta); sp.sigma.assign(sp.B, d->sigma);
     sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
     sp.shift_map = d->shift_map;
-    st = enter(p->E, p->user);
-    if (st == HH_OK) st = batch_setup(p->E, sp);
+    st = enter(*p->ep, p->user);
+    if (st == HH_OK) st = batch_setup(*p->ep, sp);
   }
   if (st != HH_OK) { delete p; return st; }
-  for (const int2& z : p->E.FL.slabs) p->n_local += (int64_t)(z.y - z.x) * p->E.FL.plane;
+  for (const int2& z : p->ep->FL.slabs) p->n_local += (int64_t)(z.y - z.x) * p->ep->FL.plane;
   *out = p;
   return HH_OK;
 }
@@ -908,14 +971,14 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
 extern "C" hh_status hh_layout(const hh_problem* p, int64_t* nf, int64_t* nc) {
   if (!p) { hh_set_error("NULL handle"); return HH_E_ARG; }
   if (nf) *nf = p->n_local;
-  if (nc) *nc = p->E.Nc;
+  if (nc) *nc = p->ep->Nc;
   return HH_OK;
 }
 
 extern "C" hh_status hh_local_layout(const hh_problem* p, int64_t* n_local_nodes, int64_t* first_plane,
                                      int64_t* n_planes) {
   if (!p) { hh_set_error("NULL handle"); return HH_E_ARG; }
-  const std::vector<int2>& z = p->E.FL.slabs;
+  const std::vector<int2>& z = p->ep->FL.slabs;
   if (n_local_nodes) *n_local_nodes = p->n_local;
   if (first_plane) *first_plane = z.front().x;
   if (n_planes) *n_planes = z.back().y - z.front().x;
@@ -933,7 +996,7 @@ hh_status user_out(Engine& E, Pool& src, void* u) { return slab_user_copy(E.X, v
 extern "C" hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void* y) {
   if (!p || !x || !y) { hh_set_error("NULL argument"); return HH_E_ARG; }
   if (x == y) { hh_set_error("apply_op: x and y must be distinct"); return HH_E_ARG; }
-  Engine& E = p->E;
+  Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
   if (op == HH_OP_A0 || op == HH_OP_AEPS) {
     HH_TRY(user_in(E, x, E.xv));
@@ -951,7 +1014,7 @@ extern "C" hh_status hh_apply_op(hh_problem* p, int32_t op, const void* x, void*
 
 extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   if (!p || !f || !z) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  Engine& E = p->E;
+  Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
   HH_TRY(user_in(E, f, E.bv));
   HH_TRY(halo(E, vfine(E, E.bv)));
@@ -968,7 +1031,7 @@ extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
 
 extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
   if (!p || !r || !e) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  Engine& E = p->E;
+  Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
   HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
                   varg((cplx*)e, 0), E.s, true));
@@ -982,14 +1045,14 @@ static void fill_report(const hh_problem* p, const SampleOut& o, double solve_s,
   r->rel_res_lsq = o.rel_res_lsq;
   r->rel_res_true = o.rel_res_true;
   r->rho = o.rho;
-  r->setup_s = p->E.setup_s;
+  r->setup_s = p->ep->setup_s;
   r->solve_s = solve_s;
 }
 
 extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, const hh_fgmres_opts* o,
                                      hh_fgmres_report* rep, double* res_hist) {
   if (!p || !bv || !xv || !o || !rep) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  Engine& E = p->E;
+  Engine& E = *p->ep;
   memset(rep, 0, sizeof(*rep));
   HH_TRY(enter(E, p->user));
   cudaEvent_t e0, e1;
@@ -1020,7 +1083,7 @@ extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, co
 extern "C" hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, void* x_host,
                                           const hh_fgmres_opts* o, hh_fgmres_report* r) {
   if (!p || !b_host || !x_host) { hh_set_error("NULL argument"); return HH_E_ARG; }
-  Engine& E = p->E;
+  Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
   HH_TRY(E.ustage.ensure((size_t)p->n_local * 16));
   HH_CUDA_TRY(cudaMemcpyAsync(E.ustage.p, b_host, p->n_local * 16, cudaMemcpyHostToDevice, E.s));
@@ -1037,17 +1100,17 @@ extern "C" hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, voi
 
 extern "C" hh_status hh_destroy_problem(hh_problem* p) {
   if (!p) return HH_OK;
-  cudaSetDevice(p->E.device);
-  cudaStreamSynchronize(p->E.s);
+  cudaSetDevice(p->ep->device);
+  cudaStreamSynchronize(p->ep->s);
   delete p;
   return HH_OK;
 }
 
 extern "C" hh_status hh_reset_timers(hh_problem* p, int32_t enable) {
   if (!p) return HH_E_ARG;
-  p->E.timing = enable != 0;
-  for (int i = 0; i < T_NT; ++i) p->E.acc_ms[i] = p->E.acc_bytes[i] = p->E.acc_launch[i] = p->E.acc_bytes_all[i] = 0;
-  p->E.launches = 0;
+  p->ep->timing = enable != 0;
+  for (int i = 0; i < T_NT; ++i) p->ep->acc_ms[i] = p->ep->acc_bytes[i] = p->ep->acc_launch[i] = p->ep->acc_bytes_all[i] = 0;
+  p->ep->launches = 0;
   return HH_OK;
 }
 
@@ -1055,12 +1118,12 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
   if (!p) return HH_E_ARG;
   if (st12)
     for (int i = 0; i < T_NT; ++i) {
-      st12[i] = p->E.acc_ms[i];
-      st12[4 + i] = p->E.acc_bytes[i];
-      st12[8 + i] = p->E.acc_launch[i];
-      st12[12 + i] = p->E.acc_bytes_all[i];
+      st12[i] = p->ep->acc_ms[i];
+      st12[4 + i] = p->ep->acc_bytes[i];
+      st12[8 + i] = p->ep->acc_launch[i];
+      st12[12 + i] = p->ep->acc_bytes_all[i];
     }
-  if (launches) *launches = p->E.launches;
+  if (launches) *launches = p->ep->launches;
   return HH_OK;
 }
 
@@ -1116,9 +1179,22 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
   const char* en = getenv("HH_SWEEP_NODES");
   const double node_budget = en ? atof(en) : 1.2e6;
-  size_t freeb = 0, totb = 0;
-  HH_CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
-  (void)freeb;
+  // device memory size, queried once per device (cudaMemGetInfo takes driver locks
+  // that can stall for tens of ms)
+  static std::mutex tot_mu;
+  static std::map<int, size_t> tot_cache;
+  size_t totb = 0;
+  {
+    std::lock_guard<std::mutex> lk(tot_mu);
+    auto it = tot_cache.find(common->device);
+    if (it != tot_cache.end()) totb = it->second;
+  }
+  if (!totb) {
+    size_t freeb = 0;
+    HH_CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+    std::lock_guard<std::mutex> lk(tot_mu);
+    tot_cache[common->device] = totb;
+  }
   const double budget = 0.60 * (double)totb / nstreams;   // engines persist: budget on total HBM
   std::vector<std::vector<int>> batches;
   for (auto& kv : groups) {
