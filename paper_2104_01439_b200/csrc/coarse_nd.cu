@@ -1497,8 +1497,8 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
     if (sm > 48 * 1024) {
-      HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      HH_CUDA_TRY(smem_attr((const void*)k_nd_fwd_sub, sm));
+      HH_CUDA_TRY(smem_attr((const void*)k_nd_bwd_sub, sm));
     }
     k_nd_fwd_sub<<<dim3(nd->sub_cnt[cut], B), 256, sm, s>>>(A, nd->d_sub_ptr + nd->sub_off[cut],
                                                             nd->d_sub_list + nd->list_off[cut]);
@@ -1525,13 +1525,13 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
       if (li.max_u == 0) continue;
       const size_t sm = li.max_s > A.vmax ? 0 : (size_t)li.max_s * sizeof(cplx);
       if (sm > 48 * 1024)
-        HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        HH_CUDA_TRY(smem_attr((const void*)k_nd_rows_wide<0>, sm));
       dim3 g(li.count, (li.max_u + WIDE_RPC - 1) / WIDE_RPC, B);   // covers the smallest rows-per-CTA
       HH_TRY(launch_pdl(k_nd_rows_wide<0>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
       continue;
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
-    if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_fwd, sm));
     dim3 g(li.count, level_split(li.max_u, li.count, B), B);
     HH_TRY(launch_pdl(k_nd_fwd, g, LT, sm, s, A, li.begin));
   }
@@ -1574,13 +1574,13 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
       // fronts whose vector does not fit read it from L2: no shared memory then (occupancy)
       const size_t sm = li.max_f > A.vmax ? 0 : (size_t)li.max_f * sizeof(cplx);
       if (sm > 48 * 1024)
-        HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_rows_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        HH_CUDA_TRY(smem_attr((const void*)k_nd_rows_wide<1>, sm));
       dim3 g(li.count, (li.max_s + WIDE_RPC - 1) / WIDE_RPC, B);
       HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
       continue;
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
-    if (sm > 48 * 1024) HH_CUDA_TRY(cudaFuncSetAttribute(k_nd_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_bwd, sm));
     dim3 g(li.count, level_split(li.max_s, li.count, B), B);
     HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
   }

@@ -550,7 +550,7 @@ size_t smem_bytes(int R, int nfields, bool het) {
 
 hh_status set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
-    HH_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    HH_CUDA_TRY(smem_attr((const void*)fn, bytes));
   }
   return HH_OK;
 }

@@ -27,6 +27,21 @@
 #include "krylov.cuh"
 #include "comm.cuh"
 
+// ------------------------------------------------------------------ smem limits
+cudaError_t smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{dev, fn}];
+  if (bytes <= cur) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
 void hh_set_error(const char* fmt, ...) {

@@ -111,6 +111,11 @@ struct Level {
   cplx* dinv = nullptr;            // het fine level: D^{-1} = diag(A_eps)^{-1} per node (vector layout)
 };
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes`, never lower
+// it: engines on several host threads launch the same kernel with different
+// sizes, and a concurrent lower setting would make a larger launch fail.
+cudaError_t smem_attr(const void* fn, size_t bytes);
+
 __device__ __forceinline__ int2 slab_of(const int2* sl, int b, int n) {
   return sl ? sl[b] : make_int2(0, n + 1);
 }

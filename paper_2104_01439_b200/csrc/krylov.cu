@@ -382,7 +382,7 @@ __global__ void k_clear_jend(KArgs A, int B) {
 hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
   const size_t sm = (size_t)(MD_UNITS + (A.Nst + A.nblk - 1) / A.nblk) * sizeof(cplx);
   if (sm > 48 * 1024)
-    HH_CUDA_TRY(cudaFuncSetAttribute(k_mdot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    HH_CUDA_TRY(smem_attr((const void*)k_mdot, sm));
   k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
