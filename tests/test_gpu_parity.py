@@ -207,3 +207,43 @@ def test_zero_rhs_and_linearity_of_vcycle():
     z12 = a * _host(gp.vcycle(_dev(f1))) + b2 * _host(gp.vcycle(_dev(f2)))
     assert _rel(z, z12) <= 1e-12
     gp.close()
+
+
+def test_sweep_empty_and_smallest_grid():
+    """An empty sweep is a no-op; the smallest grid (n = 4, one coarse cell per
+    side... 3x3 coarse nodes) solves at the parity bar."""
+    assert hh.sweep([]) == []
+    s = {"id": 7, "dim": 2, "n": 4, "k": 1.5, "kh_target": 0.6, "sigma": 1.5, "beta": 0.5}
+    r = hh.sweep([s])[0]
+    _, ro = OracleProblem(sweep_sample_spec(s)).solve()
+    assert r["status"] == 0 and abs(r["iterations"] - ro.iterations) <= 1
+
+
+def test_nonconvergence_is_a_result():
+    """Hitting max_iters is a result (converged = 0, status OK), not an error."""
+    spec = config_spec("cfg0")
+    gp = hh.Problem.from_spec(spec)
+    x, r = gp.fgmres_solve(_dev(spec.rhs()), o=hh.opts(max_iters=3, rtol=1e-12))
+    assert r["iterations"] == 3 and r["converged"] == 0 and r["rel_res_true"] > 1e-12
+    xo, ro = OracleProblem(spec).solve(fixed_iters=3)
+    assert _rel(_host(x), xo) <= 1e-9
+    gp.close()
+
+
+def test_lean_storage_with_slabs(monkeypatch):
+    """Lean ND storage (cfg4's mode: chunked factorisation, packed Schur store,
+    transposed forward) combined with in-process slabs, on a 3D heterogeneous
+    grid whose coarse tree is created here for the first time."""
+    monkeypatch.setenv("HH_ND_LEAN", "1")
+    monkeypatch.setenv("HH_ND_WMAX", "30000")
+    spec = config_spec("cfg4", n=18)
+    gp = hh.Problem.from_spec(spec, nslabs_local=3)
+    orc = OracleProblem(spec)
+    x, r = gp.fgmres_solve(_dev(spec.rhs()), o=hh.opts(restart=spec.restart, rtol=spec.rtol))
+    xo, ro = orc.solve()
+    assert abs(r["iterations"] - ro.iterations) <= 1
+    xf, _ = gp.fgmres_solve(_dev(spec.rhs()), o=hh.opts(restart=spec.restart, fixed_iters=ro.iterations))
+    assert _rel(_host(xf), xo) <= 1e-8
+    f = _rand(spec.n_nodes, 31)
+    assert _rel(_host(gp.vcycle(_dev(f))), orc.vcycle(f)) <= 1e-10
+    gp.close()
