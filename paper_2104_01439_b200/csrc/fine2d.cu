@@ -274,16 +274,41 @@ __global__ void __launch_bounds__(NT) k_apply2d(FineK P, VArg x, VArg y, VArg su
   })
 }
 
+// D^{-1} at a region node: heterogeneous -> the precomputed copy staged in smem;
+// constant k -> the interior centre coefficient, the element loop at the boundary
+template <bool HET>
+__device__ __forceinline__ cplx dinv_at(const cplx* sDi, int si, const Tile& t, int gx, int gy,
+                                        int n, double h, const double2* sE, double2 kc, cplx di_int) {
+  if (HET) return sDi[si];
+  if (gx > 0 && gx < n && gy > 0 && gy < n) return di_int;
+  return cinv(node_diag<false>(t, gx, gy, n, h, sE, kc));
+}
+
+// Per-sample scalars of a fine launch, loaded together before any is used
+// (status, slab bounds, the Krylov slot behind f, its scale, constant k) so the
+// prologue pays one memory latency instead of a chain of them.
+#define FINE_PROLOGUE(P, b, n, f, fs)                                            \
+  const int stb = P.st ? __ldg(P.st + b) : 0;                                    \
+  const int2 sl = slab_of(P.slab, b, n);                                         \
+  const cplx* fg = f.at(b);                                                      \
+  const double fsc = fs.at(b);                                                   \
+  const double2 kc = HET ? make_double2(0, 0) : __ldg(P.kc + b);                 \
+  if (stb) return;                                                               \
+  const int rlo = max(0, sl.x - P.G), rhi = min(n, sl.y - 1 + P.G);              \
+  const int64_t vofs = (int64_t)(sl.x - P.G) * (n + 1);                          \
+  if (sl.x + (int)blockIdx.y * TY >= sl.y) return;
+
 // ------------------------------------------------- pre-smoothing + restriction
 // u = S^nu(0; f), rc = I^T (f - A_eps u).  Halo R = nu + 1.
-template <bool HET>
-__global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
+// NUC > 0: nu fixed at compile time (region sizes, smem strides and the step
+// loop fold to constants); NUC = 0: nu from P.
+template <bool HET, int NUC>
+__global__ void __launch_bounds__(NT, HET ? 3 : 4) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
   const int b = blockIdx.z;
-  if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
-  const int n = P.n, nu = P.nu;
+  const int n = P.n, nu = NUC > 0 ? NUC : P.nu;
   const double omega = P.omega, h = P.h;
-  SLAB_TILE(P, b, n)
+  FINE_PROLOGUE(P, b, n, f, fs)
   Tile t;
   t.X0 = blockIdx.x * TX; t.Y0 = sl.x + blockIdx.y * TY; t.R = nu + 1;
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
@@ -291,26 +316,20 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
   cplx* sA = sF + S;
   cplx* sB = sA + S;
-  cplx* sDi = sB + S;
-  double2* sE = reinterpret_cast<double2*>(sDi + S);
-  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  cplx* sDi = sB + S;                                   // HET only
+  double2* sE = reinterpret_cast<double2*>(sDi + S);    // HET only
   const Const9 c9 = make_const9(kc, h, true);
-  load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
-  const bool pre_di = HET && P.dinv;
-  if (pre_di) load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
-  if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
+  load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
+  if (HET) {
+    load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
+    load_coef(sE, P.coef + b * P.coef_bs, t, n);
+  }
   __syncthreads();
-  // D^{-1} and the first step from u = 0 (pointwise) on the full region
+  // the first step from u = 0 (pointwise) on the full region
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);   // constant k: interior D = centre coefficient
   FOR_REGION(t.R, {
-    cplx di = cmake(0, 0), v = cmake(0, 0);
-    if (in) {
-      di = pre_di ? sDi[si]
-                  : ((!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
-                                                                   : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc)));
-      v = cscale(cmul(di, sF[si]), omega);
-    }
-    if (!pre_di) sDi[si] = di;
+    cplx v = cmake(0, 0);
+    if (in) v = cscale(cmul(dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega);
     sA[si] = v;
     sB[si] = cmake(0, 0);
   })
@@ -321,8 +340,9 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
     const int hal = t.R - step + 1;
     FOR_REGION(hal, if (in) {
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
+      const cplx di = dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
-      cfma(v, cscale(sDi[si], omega), csub(sF[si], ax));
+      cfma(v, cscale(di, omega), csub(sF[si], ax));
       nxt[si] = v;
     })
     __syncthreads();
@@ -364,70 +384,90 @@ __global__ void __launch_bounds__(NT) k_pre2d(FineK P, VArg f, SArg fs, VArg uo,
   }
 }
 
+// coarse block staged by the post-smoother: coarse nodes (cx0 + i, cy0 + j)
+constexpr int CW_EXTRA = 2;
+__host__ __device__ constexpr int post_cw(int R) { return TX / 2 + R + CW_EXTRA; }
+__host__ __device__ constexpr int post_ch(int R) { return TY / 2 + R + CW_EXTRA; }
+
 // ------------------------------------- prolongation + correction + post-smoothing
 // z = S^nu(u + I ec; f); if w: w = A_0 z.  Halo R = nu + (w ? 1 : 0).
-template <bool HET, bool WITH_W>
-__global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg uin, VArg ecin,
-                                               VArg zo, VArg wo) {
+template <bool HET, bool WITH_W, int NUC>
+__global__ void __launch_bounds__(NT, HET ? 3 : 4) k_post2d(FineK P, VArg f, SArg fs, VArg uin, VArg ecin,
+                                                            VArg zo, VArg wo) {
   const int b = blockIdx.z;
-  if (P.st && P.st[b]) return;
   extern __shared__ double4 smem_raw[];
-  const int n = P.n, nu = P.nu;
+  const int n = P.n, nu = NUC > 0 ? NUC : P.nu;
   const double omega = P.omega, h = P.h;
-  SLAB_TILE(P, b, n)
+  FINE_PROLOGUE(P, b, n, f, fs)
   Tile t;
   t.X0 = blockIdx.x * TX; t.Y0 = sl.x + blockIdx.y * TY; t.R = nu + (WITH_W ? 1 : 0);
   t.SX = TX + 2 * t.R; t.SY = TY + 2 * t.R;
   const int S = t.SX * t.SY;
+  const int CW = post_cw(t.R), CH = post_ch(t.R);
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
   cplx* sA = sF + S;
   cplx* sB = sA + S;
-  cplx* sDi = sB + S;
-  double2* sE = reinterpret_cast<double2*>(sDi + S);
-  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  cplx* sC = sB + S;                                    // coarse block, CW x CH
+  cplx* sDi = sC + CW * CH;                             // HET only
+  double2* sE = reinterpret_cast<double2*>(sDi + S);    // HET only
   const Const9 c9e = make_const9(kc, h, true);
-  load_region(sF, f.at(b) - vofs, t, n, fs.at(b), rlo, rhi);
-  const bool pre_di = HET && P.dinv;
-  if (pre_di) load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
-  if (HET) load_coef(sE, P.coef + b * P.coef_bs, t, n);
-  const cplx* u = uin.at(b) - vofs;
-  const cplx* ecv = ecin.at(b);
-  const int NC1 = n / 2 + 1;
-  // u + I ec on the full region, D^{-1}
+  load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
+  load_region(sA, uin.at(b) - vofs, t, n, 1.0, rlo, rhi);
+  // coarse nodes under the region: cx in [cx0, cx0 + CW), cy in [cy0, cy0 + CH)
+  const int nc = n / 2, NC1 = nc + 1;
+  const int cx0 = (t.X0 - t.R) >> 1, cy0 = (t.Y0 - t.R) >> 1;
+  {
+    const cplx* ecv = ecin.at(b);
+    const int total = CW * CH;
+    for (int base = threadIdx.x; base < total; base += 2 * NT) {
+      cplx v[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int idx = base + k * NT;
+        const int j = idx / CW, i = idx - j * CW;
+        const int cx = cx0 + i, cy = cy0 + j;
+        v[k] = (idx < total && cx >= 0 && cx <= nc && cy >= 0 && cy <= nc) ? __ldg(&ecv[cy * NC1 + cx])
+                                                                           : cmake(0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (base + k * NT < total) sC[base + k * NT] = v[k];
+    }
+  }
+  if (HET) {
+    load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
+    load_coef(sE, P.coef + b * P.coef_bs, t, n);
+  }
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);
   __syncthreads();
+  // u + I ec on the full region (bilinear interpolation from the staged block)
   FOR_REGION(t.R, {
-    cplx v = cmake(0, 0), di = cmake(0, 0);
     if (in) {
-      v = __ldg(&u[(int64_t)gy * (n + 1) + gx]);
-      const int cx0 = gx >> 1, cy0 = gy >> 1;
-      const int cx1 = cx0 + (gx & 1), cy1 = cy0 + (gy & 1);
-      const cplx a = __ldg(&ecv[cy0 * NC1 + cx0]);
+      cplx v = sA[si];
+      const int ci = (gx >> 1) - cx0, cj = (gy >> 1) - cy0;
+      const cplx* c = sC + cj * CW + ci;
+      const cplx a = c[0];
       if (gx & 1) {
-        const cplx bq = __ldg(&ecv[cy0 * NC1 + cx1]);
+        const cplx bq = c[1];
         if (gy & 1) {
-          const cplx c = __ldg(&ecv[cy1 * NC1 + cx0]), d = __ldg(&ecv[cy1 * NC1 + cx1]);
-          v.x += 0.25 * (a.x + bq.x + c.x + d.x);
-          v.y += 0.25 * (a.y + bq.y + c.y + d.y);
+          const cplx cc = c[CW], d = c[CW + 1];
+          v.x += 0.25 * (a.x + bq.x + cc.x + d.x);
+          v.y += 0.25 * (a.y + bq.y + cc.y + d.y);
         } else {
           v.x += 0.5 * (a.x + bq.x);
           v.y += 0.5 * (a.y + bq.y);
         }
       } else if (gy & 1) {
-        const cplx c = __ldg(&ecv[cy1 * NC1 + cx0]);
-        v.x += 0.5 * (a.x + c.x);
-        v.y += 0.5 * (a.y + c.y);
+        const cplx cc = c[CW];
+        v.x += 0.5 * (a.x + cc.x);
+        v.y += 0.5 * (a.y + cc.y);
       } else {
         v.x += a.x;
         v.y += a.y;
       }
-      if (!pre_di)
-        di = (!HET && gx > 0 && gx < n && gy > 0 && gy < n) ? di_int
-                                                            : cinv(node_diag<HET>(t, gx, gy, n, h, sE, kc));
+      sA[si] = v;
     }
-    sA[si] = v;
     sB[si] = cmake(0, 0);
-    if (!pre_di) sDi[si] = di;
   })
   __syncthreads();
   cplx* cur = sA;
@@ -436,8 +476,9 @@ __global__ void __launch_bounds__(NT) k_post2d(FineK P, VArg f, SArg fs, VArg ui
     const int hal = t.R - step;
     FOR_REGION(hal, if (in) {
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e);
+      const cplx di = dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
-      cfma(v, cscale(sDi[si], omega), csub(sF[si], ax));
+      cfma(v, cscale(di, omega), csub(sF[si], ax));
       nxt[si] = v;
     })
     __syncthreads();
@@ -547,6 +588,12 @@ size_t smem_bytes(int R, int nfields, bool het) {
   if (het) b += (size_t)(SX + 1) * (SY + 1) * sizeof(double2);
   return b;
 }
+// pre: f, two iterates (+ D^{-1}, element coefficients if heterogeneous)
+size_t pre_smem(int R, bool het) { return smem_bytes(R, het ? 4 : 3, het); }
+// post: as pre plus the staged coarse block
+size_t post_smem(int R, bool het) {
+  return pre_smem(R, het) + (size_t)post_cw(R) * post_ch(R) * sizeof(cplx);
+}
 
 hh_status set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) {
@@ -592,15 +639,20 @@ hh_status fine_pre2d(const Level& L, int B, const int* st, int nu, double omega,
                      VArg u, VArg rc, cudaStream_t s) {
   const int n = L.n;
   dim3 grid((n + 1 + TX - 1) / TX, (L.maxloc + TY - 1) / TY, B);
-  const size_t sm = smem_bytes(nu + 1, 4, L.het);
+  if (L.het && !L.dinv) { hh_set_error("fine_pre2d: heterogeneous level without D^-1"); return HH_E_STATE; }
+  const size_t sm = pre_smem(nu + 1, L.het);
   const FineK P = make_k(L, nu, omega, st);
-  if (L.het) {
-    HH_TRY(set_smem((const void*)k_pre2d<true>, sm));
-    k_pre2d<true><<<grid, NT, sm, s>>>(P, f, fs, u, rc);
-  } else {
-    HH_TRY(set_smem((const void*)k_pre2d<false>, sm));
-    k_pre2d<false><<<grid, NT, sm, s>>>(P, f, fs, u, rc);
+#define LAUNCH_PRE(H, NU)                                         \
+  {                                                               \
+    HH_TRY(set_smem((const void*)k_pre2d<H, NU>, sm));            \
+    k_pre2d<H, NU><<<grid, NT, sm, s>>>(P, f, fs, u, rc);         \
   }
+  if (L.het) {
+    if (nu == 2) LAUNCH_PRE(true, 2) else LAUNCH_PRE(true, 0)
+  } else {
+    if (nu == 2) LAUNCH_PRE(false, 2) else LAUNCH_PRE(false, 0)
+  }
+#undef LAUNCH_PRE
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
@@ -610,18 +662,22 @@ hh_status fine_post2d(const Level& L, int B, const int* st, int nu, double omega
   const int n = L.n;
   dim3 grid((n + 1 + TX - 1) / TX, (L.maxloc + TY - 1) / TY, B);
   const bool ww = w.p != nullptr;
-  const size_t sm = smem_bytes(nu + (ww ? 1 : 0), 4, L.het);
+  if (L.het && !L.dinv) { hh_set_error("fine_post2d: heterogeneous level without D^-1"); return HH_E_STATE; }
+  const size_t sm = post_smem(nu + (ww ? 1 : 0), L.het);
   const FineK P = make_k(L, nu, omega, st);
-#define LAUNCH_POST(H, W)                                              \
-  {                                                                    \
-    HH_TRY(set_smem((const void*)k_post2d<H, W>, sm));                 \
-    k_post2d<H, W><<<grid, NT, sm, s>>>(P, f, fs, u, ec, z, w);        \
+#define LAUNCH_POST1(H, W, NU)                                             \
+  {                                                                        \
+    HH_TRY(set_smem((const void*)k_post2d<H, W, NU>, sm));                 \
+    k_post2d<H, W, NU><<<grid, NT, sm, s>>>(P, f, fs, u, ec, z, w);        \
   }
+#define LAUNCH_POST(H, W) \
+  if (nu == 2) LAUNCH_POST1(H, W, 2) else LAUNCH_POST1(H, W, 0)
   if (L.het) {
-    if (ww) LAUNCH_POST(true, true) else LAUNCH_POST(true, false)
+    if (ww) { LAUNCH_POST(true, true) } else { LAUNCH_POST(true, false) }
   } else {
-    if (ww) LAUNCH_POST(false, true) else LAUNCH_POST(false, false)
+    if (ww) { LAUNCH_POST(false, true) } else { LAUNCH_POST(false, false) }
   }
+#undef LAUNCH_POST1
 #undef LAUNCH_POST
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
