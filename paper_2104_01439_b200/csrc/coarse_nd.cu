@@ -73,7 +73,7 @@ struct LevelInfo {
 
 // Solve schedule: levels <= sub_cut run as one-CTA subtree walks, levels
 // (sub_cut, split] as per-level kernels, levels > split inside one cluster kernel.
-struct SolveCfg { int sub_cut, split; };
+struct SolveCfg { int sub_cut, split, flow = 0; };
 
 struct NDPlan {
   int dim = 2, m = 0;            // coarse grid nodes per side
@@ -105,6 +105,9 @@ struct NDPlan {
   int* d_halo_front = nullptr;
   int* d_pos_front = nullptr;
   int64_t* d_lvr = nullptr;          // [nlev][6]: sep begin/end, halo begin/end, position begin/end
+  // dataflow solve
+  int2* d_child = nullptr;           // per front: children (-1: none)
+  int* d_lvbeg = nullptr;            // per level: first front
   std::mutex cut_mu;
   std::vector<std::pair<int, SolveCfg>> cfg_cache;   // (B, schedule) chosen by nd_autotune
   // lean storage
@@ -382,6 +385,31 @@ __device__ __forceinline__ cplx row_dot(const cplx* __restrict__ row, const cplx
   return warp_sum(cadd(cadd(a0, a1), cadd(a2, a3)));
 }
 
+// dot of one row with v by a group of G lanes (G = 32, 16, 8, 4), 4 predicated
+// loads in flight per lane; the group sum is left in every lane of the group
+template <int G, int DEPTH = 4>
+__device__ __forceinline__ cplx row_dot_g(const cplx* __restrict__ row, const cplx* v, int len, int sub) {
+  cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
+  for (int c = sub; c < len; c += DEPTH * G) {
+    cplx r[DEPTH];
+#pragma unroll
+    for (int t = 0; t < DEPTH; ++t) r[t] = (c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
+#pragma unroll
+    for (int t = 0; t < DEPTH; ++t)
+      if (c + G * t < len) cfma(t & 1 ? a1 : a0, r[t], v[c + G * t]);
+  }
+  cplx a = cadd(a0, a1);
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+    a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+  }
+  return a;
+}
+
+// lanes per row for rows of length len (4 loads per lane at most, 16 B each)
+__host__ __device__ inline int wide_group(int len) { return len > 64 ? 32 : (len > 32 ? 16 : (len > 16 ? 8 : 4)); }
+
 struct SolveArgs {
   const FrontMeta* fr;
   const int* st;
@@ -437,26 +465,46 @@ __device__ __forceinline__ void front_gather(const SolveArgs& A, const FrontMeta
   }
 }
 
-// forward rows b = r0, r0 + step, ...: upd[b] = w[s + b] + (-H^T row b) . z
-__device__ __forceinline__ void front_fwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
-                                               const cplx* w, int r0, int step, int lane) {
+// Rows of one front, DIR 0 (forward): upd[r] = w[s + r] + (-H^T row r) . z_s
+// (rows s + r of F, length s); DIR 1 (backward): x[sep[r]] = F[r][0:f] . v.
+// Warp slots gw, gw + nw, ... each take 32 / G consecutive rows at once (G
+// lanes per row, G from the row length), so the short rows of the low levels
+// keep every lane loading instead of walking one row per warp round trip.
+template <int DIR, int G>
+__device__ __forceinline__ void front_rows_g(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* v,
+                                             int gw, int nw, int lane) {
+  constexpr int RPW = 32 / G;
+  const int rows = DIR == 0 ? m.u : m.s, len = DIR == 0 ? m.s : m.f;
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
-  cplx* out = upd_of(A, bs) + m.outOff;
-  for (int b = r0; b < m.u; b += step) {
-    const cplx acc = row_dot(F + (int64_t)(m.s + b) * m.f, w, m.s, lane);
-    if (lane == 0) out[b] = cadd(acc, w[m.s + b]);
+  const cplx* row0 = DIR == 0 ? F + (int64_t)m.s * m.f : F;
+  const int grp = lane / G, sub = lane % G;
+  for (int base = gw * RPW; base < rows; base += nw * RPW) {
+    const int r = base + grp;
+    const bool ok = r < rows;
+    const cplx acc = row_dot_g<G>(row0 + (int64_t)(ok ? r : 0) * m.f, v, ok ? len : 0, sub);
+    if (ok && sub == 0) {
+      if (DIR == 0) upd_of(A, bs)[m.outOff + r] = cadd(acc, v[m.s + r]);
+      else A.x.at(bs)[A.sep[m.sepOff + r]] = acc;
+    }
   }
 }
-
-// backward rows a: x[sep[a]] = F[a][0:f] . v,  v = [z_s ; -x[halo]] (staged)
-__device__ __forceinline__ void front_bwd_rows(const SolveArgs& A, const FrontMeta& m, int bs,
-                                               const cplx* v, int r0, int step, int lane) {
-  const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
-  cplx* x = A.x.at(bs);
-  for (int a = r0; a < m.s; a += step) {
-    const cplx acc = row_dot(F + (int64_t)a * m.f, v, m.f, lane);
-    if (lane == 0) x[A.sep[m.sepOff + a]] = acc;
+template <int DIR>
+__device__ __forceinline__ void front_rows(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* v,
+                                           int gw, int nw, int lane) {
+  switch (wide_group(DIR == 0 ? m.s : m.f)) {
+    case 32: front_rows_g<DIR, 32>(A, m, bs, v, gw, nw, lane); break;
+    case 16: front_rows_g<DIR, 16>(A, m, bs, v, gw, nw, lane); break;
+    case 8: front_rows_g<DIR, 8>(A, m, bs, v, gw, nw, lane); break;
+    default: front_rows_g<DIR, 4>(A, m, bs, v, gw, nw, lane); break;
   }
+}
+__device__ __forceinline__ void front_fwd_rows(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* w,
+                                               int gw, int nw, int lane) {
+  front_rows<0>(A, m, bs, w, gw, nw, lane);
+}
+__device__ __forceinline__ void front_bwd_rows(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* v,
+                                               int gw, int nw, int lane) {
+  front_rows<1>(A, m, bs, v, gw, nw, lane);
 }
 
 __device__ __forceinline__ void stage_bwd(const SolveArgs& A, const FrontMeta& m, int bs, cplx* v) {
@@ -555,28 +603,6 @@ __global__ void k_nd_bwd_stage(SolveArgs A, int begin) {
 // re-gathering the whole front, which capped the CTAs per front.
 constexpr int WIDE_RPC = 8;   // rows per CTA for rows longer than 64 entries
 
-// dot of one row with v by a group of G lanes (G = 32, 16, 8, 4), 4 predicated
-// loads in flight per lane; the group sum is left in every lane of the group
-template <int G, int DEPTH = 4>
-__device__ __forceinline__ cplx row_dot_g(const cplx* __restrict__ row, const cplx* v, int len, int sub) {
-  cplx a0 = cmake(0, 0), a1 = cmake(0, 0);
-  for (int c = sub; c < len; c += DEPTH * G) {
-    cplx r[DEPTH];
-#pragma unroll
-    for (int t = 0; t < DEPTH; ++t) r[t] = (c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
-#pragma unroll
-    for (int t = 0; t < DEPTH; ++t)
-      if (c + G * t < len) cfma(t & 1 ? a1 : a0, r[t], v[c + G * t]);
-  }
-  cplx a = cadd(a0, a1);
-#pragma unroll
-  for (int o = G / 2; o; o >>= 1) {
-    a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
-    a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
-  }
-  return a;
-}
-
 template <int DIR, int G, int DEPTH = 4>
 __device__ __forceinline__ void wide_rows(const SolveArgs& A, const FrontMeta& m, int b, const cplx* row0,
                                           const cplx* v, const cplx* wg, int len, int r0, int r1, int warp,
@@ -595,7 +621,6 @@ __device__ __forceinline__ void wide_rows(const SolveArgs& A, const FrontMeta& m
 }
 
 // rows per CTA of the wide kernels: 8 warp passes of 32 / G rows
-__host__ __device__ inline int wide_group(int len) { return len > 64 ? 32 : (len > 32 ? 16 : (len > 16 ? 8 : 4)); }
 __host__ __device__ inline int wide_rpc(int len) { return WIDE_RPC * (32 / wide_group(len)); }
 
 template <int DIR>
@@ -802,6 +827,161 @@ __global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* 
       if (lane == 0) x[A.sep[e]] = acc;
     }
     if (L > L0) cl_sync(cl);
+  }
+}
+
+// ------------------------------------------------------------ dataflow solve
+// The per-level kernels of levels (sub_cut, split] replaced by ONE forward and
+// ONE backward kernel: a CTA (front t, sample b, row chunk c) starts as soon as
+// the fronts it depends on are complete -- its children (forward) or its
+// parent (backward) -- instead of waiting for a whole level and a launch.
+// CTAs are numbered in dependency order (forward: levels bottom-up, backward:
+// top-down), so every CTA a CTA waits for has a smaller index and was
+// dispatched before it (the ordering decoupled look-back scans rely on).
+// Completion: per (sample, front) counters in the work buffer, one atomic
+// increment per finished CTA after a device fence; consumers poll with
+// ld.acquire and read the producers' values through L2 (__ldcg).  The forward
+// counters are cleared by the backward kernel and vice versa, so they are zero
+// again at the start of every solve.  A wait that exceeds ~1 s gives up and
+// raises g_flow_timeout (no hang; the autotuner then rejects the schedule).
+constexpr int FLOW_MAXL = 40;
+struct FlowArgs {
+  int L0, nl;                    // flow levels [L0, L0 + nl)
+  int base[FLOW_MAXL + 1];       // CTA index ranges in launch order
+  int lev[FLOW_MAXL];            // level offset of launch slot k
+  int nch[FLOW_MAXL];            // CTAs per front of level offset j (this direction)
+  int64_t cnt_off;               // counters: (int*)(work[b] + cnt_off) (complex entries), [2][nfronts]
+  int nfr;
+};
+__device__ int g_flow_timeout = 0;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void flow_wait(const int* c, int target) {
+  if (target <= 0) return;
+  unsigned polls = 0;
+  while (ld_acquire(c) < target) {
+    __nanosleep(64);
+    if (++polls > (1u << 24)) { atomicExch(&g_flow_timeout, 1); break; }
+    if ((polls & 1023u) == 0 && *(volatile int*)&g_flow_timeout) break;   // another wait gave up
+  }
+}
+__device__ __forceinline__ int* flow_cnt(const SolveArgs& A, const FlowArgs& W, int b) {
+  return reinterpret_cast<int*>(A.work + (int64_t)b * A.WE + W.cnt_off);
+}
+// CTA index -> (level offset j, front t, sample b, chunk c)
+__device__ __forceinline__ void flow_item(const FlowArgs& W, int B, int i, int& j, int& t, int& b, int& c) {
+  int k = 0;
+  while (k + 1 < W.nl && i >= W.base[k + 1]) ++k;
+  j = W.lev[k];
+  int rem = i - W.base[k];
+  c = rem % W.nch[j];
+  rem /= W.nch[j];
+  b = rem % B;
+  t = rem / B;
+}
+
+template <bool CG>
+__device__ __forceinline__ cplx ld_v(const cplx* p) { return CG ? __ldcg(p) : *p; }
+
+__global__ void __launch_bounds__(LT) k_nd_flow_fwd(SolveArgs A, FlowArgs W, const int* __restrict__ lvbeg,
+                                                   const int2* __restrict__ child, int B) {
+  extern __shared__ double4 smem_raw[];
+  cplx* wsh = reinterpret_cast<cplx*>(smem_raw);
+  int j, t, b, c;
+  flow_item(W, B, blockIdx.x, j, t, b, c);
+  t += lvbeg[W.L0 + j];
+  const FrontMeta m = A.fr[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = W.nch[j];
+  pdl_trigger();
+  if (A.prefetch && !(A.st && *(volatile const int*)&A.st[b]))
+    prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff + (int64_t)m.s * m.f, m.f, m.s, m.u,
+                  c * (LT / 32) + warp, nch * (LT / 32), lane);
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  int* cnt = flow_cnt(A, W, b);
+  if (threadIdx.x == 0) {
+    if (c == 0) cnt[W.nfr + t] = 0;          // backward counter of t, for this solve's backward
+    const int2 ch = child[t];
+    for (int q = 0; q < 2; ++q) {
+      const int cc = q ? ch.y : ch.x;
+      if (cc < 0) continue;
+      const int jc = A.fr[cc].level - W.L0;
+      if (jc >= 0) flow_wait(cnt + cc, W.nch[jc]);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  {   // gather w_t (children's update vectors through L2)
+    const cplx* r = A.rhs.at(b);
+    const cplx* upd = upd_of(A, b);
+    const int2* gm = A.gmap + m.posOff;
+    const int* sp = A.sep + m.sepOff;
+    cplx* wg = c == 0 ? w_of(A, b) + m.posOff : nullptr;
+    for (int p = threadIdx.x; p < m.f; p += blockDim.x) {
+      const int2 g = __ldg(&gm[p]);
+      cplx v = p < m.s ? __ldg(&r[__ldg(&sp[p])]) : cmake(0, 0);
+      if (g.x >= 0) v = cadd(v, __ldcg(&upd[g.x]));
+      if (g.y >= 0) v = cadd(v, __ldcg(&upd[g.y]));
+      wsh[p] = v;
+      if (wg && p < m.s) wg[p] = v;
+    }
+  }
+  __syncthreads();
+  front_fwd_rows(A, m, b, wsh, c * (LT / 32) + warp, nch * (LT / 32), lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt + t, 1);
+  }
+}
+
+__global__ void __launch_bounds__(LT) k_nd_flow_bwd(SolveArgs A, FlowArgs W, const int* __restrict__ lvbeg,
+                                                   int B) {
+  extern __shared__ double4 smem_raw[];
+  cplx* v = reinterpret_cast<cplx*>(smem_raw);
+  int j, t, b, c;
+  flow_item(W, B, blockIdx.x, j, t, b, c);
+  t += lvbeg[W.L0 + j];
+  const FrontMeta m = A.fr[t];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = W.nch[j];
+  pdl_trigger();
+  if (A.prefetch && !(A.st && *(volatile const int*)&A.st[b]))
+    prefetch_rows(A.F + (int64_t)b * A.FE + m.Foff, m.f, m.f, m.s, c * (LT / 32) + warp, nch * (LT / 32), lane);
+  pdl_wait();
+  if (A.st && A.st[b]) return;
+  int* cnt = flow_cnt(A, W, b);
+  if (threadIdx.x == 0) {
+    if (c == 0) cnt[t] = 0;                  // forward counter of t, for the next solve's forward
+    if (m.parent >= 0) {
+      const int jp = A.fr[m.parent].level - W.L0;
+      if (jp < W.nl) flow_wait(cnt + W.nfr + m.parent, W.nch[jp]);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  {   // v = [z_s ; -x[halo]]  (halo values written by ancestors: through L2)
+    const cplx* zs = w_of(A, b) + m.posOff;
+    const cplx* x = A.x.at(b);
+    for (int q = threadIdx.x; q < m.f; q += blockDim.x) {
+      if (q < m.s) v[q] = zs[q];
+      else {
+        const cplx tv = __ldcg(&x[__ldg(&A.halo[m.haloOff + q - m.s])]);
+        v[q] = cmake(-tv.x, -tv.y);
+      }
+    }
+  }
+  __syncthreads();
+  front_bwd_rows(A, m, b, v, c * (LT / 32) + warp, nch * (LT / 32), lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt + W.nfr + t, 1);
   }
 }
 
@@ -1275,6 +1455,18 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   if (st == HH_OK && nd->lean) st = up(&nd->d_Poff, Poff);
   if (st == HH_OK && nd->lean) st = up(&nd->d_eaListC, eaListC);
   if (st == HH_OK) st = up(&nd->d_lvr, lvr);
+  {
+    std::vector<int2> child(nd->fronts.size(), make_int2(-1, -1));
+    for (size_t t = 0; t < nd->fronts.size(); ++t) {
+      const int p = nd->fronts[t].parent;
+      if (p < 0) continue;
+      if (child[p].x < 0) child[p].x = (int)t; else child[p].y = (int)t;
+    }
+    std::vector<int> lvbeg(nd->levels.size());
+    for (size_t L = 0; L < nd->levels.size(); ++L) lvbeg[L] = nd->levels[L].begin;
+    if (st == HH_OK) st = up(&nd->d_child, child);
+    if (st == HH_OK) st = up(&nd->d_lvbeg, lvbeg);
+  }
   if (st != HH_OK) { nd_plan_destroy(nd); return st; }
   *out = nd;
   return HH_OK;
@@ -1286,7 +1478,7 @@ void nd_plan_destroy(NDPlan* nd) {
   cudaFree(nd->d_eamap); cudaFree(nd->d_eaList); cudaFree(nd->d_gmap);
   cudaFree(nd->d_Coff); cudaFree(nd->d_sub_ptr); cudaFree(nd->d_sub_list);
   cudaFree(nd->d_sep_front); cudaFree(nd->d_halo_front); cudaFree(nd->d_pos_front);
-  cudaFree(nd->d_lvr);
+  cudaFree(nd->d_lvr); cudaFree(nd->d_child); cudaFree(nd->d_lvbeg);
   cudaFree(nd->d_fronts_w); cudaFree(nd->d_Coff_w); cudaFree(nd->d_Soff); cudaFree(nd->d_Poff);
   cudaFree(nd->d_eaListC); cudaFree(nd->d_Koff);
   delete nd;
@@ -1296,9 +1488,14 @@ int64_t nd_front_entries(const NDPlan* p) { return p->F_entries; }
 int64_t nd_stream_bytes(const NDPlan* p) { return p->stream_bytes; }
 int nd_levels(const NDPlan* p) { return (int)p->levels.size(); }
 // per sample: w | update vectors | lean forward partials | K-split backward partials
-int64_t nd_work_entries(const NDPlan* p) {
+// flow-solve completion counters (2 ints per front) at the end of each sample's work
+static int64_t flow_cnt_off(const NDPlan* p) {
   return p->w_entries + p->out_entries + (p->lean ? p->Pmax : 0) + p->Kmax;
 }
+static int64_t flow_cnt_entries(const NDPlan* p) {
+  return p->lean ? 0 : ((int64_t)p->fronts.size() * 2 * (int64_t)sizeof(int) + 15) / 16;
+}
+int64_t nd_work_entries(const NDPlan* p) { return flow_cnt_off(p) + flow_cnt_entries(p); }
 int64_t nd_cbuf_entries(const NDPlan* p) {
   if (p->lean) return p->Cw + p->Wmax + p->Smax[0] + p->Smax[1];
   return std::max<int64_t>(1, p->C_entries);
@@ -1398,20 +1595,22 @@ static int cluster_size() {
   return v;
 }
 
-static bool cached_cfg(NDPlan* nd, int B, SolveCfg* c) {
+static bool cached_cfg(NDPlan* nd, int key, SolveCfg* c) {
   std::lock_guard<std::mutex> lk(nd->cut_mu);
   for (auto& e : nd->cfg_cache)
-    if (e.first == B) { *c = e.second; return true; }
+    if (e.first == key) { *c = e.second; return true; }
   return false;
 }
 
-static SolveCfg get_cfg(NDPlan* nd, int B) {
+static int cfg_key(int B, bool conc) { return 2 * B + (conc ? 1 : 0); }
+static SolveCfg get_cfg(NDPlan* nd, int B, bool conc) {
   SolveCfg c{-1, (int)nd->levels.size() - 1};
   if (const char* e = getenv("HH_ND_SPLIT")) c.split = std::min<int>(atoi(e), c.split);
   if (const char* e = getenv("HH_ND_CUT")) c.sub_cut = std::min<int>(atoi(e), c.split);
+  if (const char* e = getenv("HH_ND_FLOW")) c.flow = atoi(e);
   if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT")) return c;
   SolveCfg cc;
-  if (cached_cfg(nd, B, &cc)) return cc;
+  if (cached_cfg(nd, cfg_key(B, conc), &cc)) return cc;
   return c;
 }
 
@@ -1450,10 +1649,54 @@ static hh_status launch_pdl(void (*kern)(Args...), dim3 grid, int block, size_t 
 // CTAs per front of a per-level launch: one warp per row at most, and only as
 // many as needed to put ~4 CTAs on every SM
 static int g_fill_ctas = getenv("HH_ND_FILL") ? atoi(getenv("HH_ND_FILL")) : 4 * 148;
-static int level_split(int rows, int count, int B) {
-  const int by_rows = std::max(1, (rows + LT / 32 - 1) / (LT / 32));
+static int level_split(int rows, int count, int B, int len) {
+  const int rpc = (LT / 32) * (32 / wide_group(std::max(1, len)));   // rows per CTA pass
+  const int by_rows = std::max(1, (rows + rpc - 1) / rpc);
   const int fill = std::max(1, (g_fill_ctas + count * B - 1) / (count * B));
   return std::max(1, std::min(std::min(by_rows, fill), 65535));
+}
+
+// the dataflow kernels cover levels (cut, Lb] when every one of them takes the
+// narrow per-level path (front vectors staged in shared memory, no wide rows)
+static bool flow_ok(const NDPlan* nd, int cut, int Lb) {
+  if (nd->lean || nd->dim != 2 || Lb - cut < 1 || Lb - cut > FLOW_MAXL || getenv("HH_NO_FLOW")) return false;
+  for (int L = cut + 1; L <= Lb; ++L) {
+    const LevelInfo& li = nd->levels[L];
+    if (li.max_f > nd_vmax()) return false;
+    if ((li.max_u >= wide_rows() || li.max_s >= wide_rows()) && li.max_f >= wide_f()) return false;
+  }
+  return true;
+}
+
+static hh_status flow_launch(const NDPlan* nd, const SolveArgs& A, int B, int L0, int L1, bool fwd,
+                             cudaStream_t s) {
+  FlowArgs W;
+  W.L0 = L0; W.nl = L1 - L0 + 1;
+  W.cnt_off = flow_cnt_off(nd);
+  W.nfr = (int)nd->fronts.size();
+  int maxf = 1;
+  for (int j = 0; j < W.nl; ++j) {
+    const LevelInfo& li = nd->levels[L0 + j];
+    W.nch[j] = level_split(fwd ? li.max_u : li.max_s, li.count, B, fwd ? li.max_s : li.max_f);
+    maxf = std::max(maxf, li.max_f);
+  }
+  int64_t tot = 0;
+  for (int k = 0; k < W.nl; ++k) {
+    const int j = fwd ? k : W.nl - 1 - k;
+    W.lev[k] = j;
+    W.base[k] = (int)tot;
+    tot += (int64_t)nd->levels[L0 + j].count * B * W.nch[j];
+  }
+  W.base[W.nl] = (int)tot;
+  if (tot > INT32_MAX) { hh_set_error("nd flow: too many CTAs"); return HH_E_CONFIG; }
+  const size_t sm = (size_t)maxf * sizeof(cplx);
+  if (fwd) {
+    if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_flow_fwd, sm));
+    return launch_pdl(k_nd_flow_fwd, dim3((unsigned)tot), LT, sm, s, A, W, (const int*)nd->d_lvbeg,
+                      (const int2*)nd->d_child, B);
+  }
+  if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_flow_bwd, sm));
+  return launch_pdl(k_nd_flow_bwd, dim3((unsigned)tot), LT, sm, s, A, W, (const int*)nd->d_lvbeg, B);
 }
 
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
@@ -1494,6 +1737,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     c.split = nlev - 1;
   }
   const int cut = c.sub_cut, Lb = c.split;
+  const bool flow = c.flow && flow_ok(nd, cut, Lb);
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
     if (sm > 48 * 1024) {
@@ -1503,7 +1747,8 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     k_nd_fwd_sub<<<dim3(nd->sub_cnt[cut], B), 256, sm, s>>>(A, nd->d_sub_ptr + nd->sub_off[cut],
                                                             nd->d_sub_list + nd->list_off[cut]);
   }
-  for (int L = cut + 1; L <= Lb; ++L) {
+  if (flow) HH_TRY(flow_launch(nd, A, B, cut + 1, Lb, true, s));
+  for (int L = cut + 1; L <= Lb && !flow; ++L) {
     const LevelInfo& li = nd->levels[L];
     tick();
     struct Tk { decltype(tock)& f; int L; ~Tk() { f("fwd", L); } } tk_{tock, L};
@@ -1532,7 +1777,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_fwd, sm));
-    dim3 g(li.count, level_split(li.max_u, li.count, B), B);
+    dim3 g(li.count, level_split(li.max_u, li.count, B, li.max_s), B);
     HH_TRY(launch_pdl(k_nd_fwd, g, LT, sm, s, A, li.begin));
   }
   if (Lb < nlev - 1) {
@@ -1555,7 +1800,8 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
                                    (const int*)nd->d_sep_front, (const int*)nd->d_halo_front,
                                    (const int*)nd->d_pos_front));
   }
-  for (int L = Lb; L > cut; --L) {
+  if (flow) HH_TRY(flow_launch(nd, A, B, cut + 1, Lb, false, s));
+  for (int L = Lb; L > cut && !flow; --L) {
     const LevelInfo& li = nd->levels[L];
     tick();
     struct Tk { decltype(tock)& f; int L; ~Tk() { f("bwd", L); } } tk_{tock, L};
@@ -1581,7 +1827,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     }
     const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
     if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_bwd, sm));
-    dim3 g(li.count, level_split(li.max_s, li.count, B), B);
+    dim3 g(li.count, level_split(li.max_s, li.count, B, li.max_f), B);
     HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
   }
   if (cut >= 0) {
@@ -1593,19 +1839,29 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   return HH_OK;
 }
 
+// zero the dataflow counters of B samples (after the work buffer is (re)allocated)
+hh_status nd_flow_reset(const NDPlan* nd, int B, cplx* work, cudaStream_t s) {
+  const int64_t ce = flow_cnt_entries(nd);
+  if (ce == 0 || B <= 0) return HH_OK;
+  const size_t pitch = (size_t)nd_work_entries(nd) * sizeof(cplx);
+  HH_CUDA_TRY(cudaMemset2DAsync(work + flow_cnt_off(nd), pitch, 0, (size_t)ce * sizeof(cplx), B, s));
+  return HH_OK;
+}
+
 hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s, bool shareF) {
+                   VArg x, cudaStream_t s, bool shareF, bool conc) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
-  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B), shareF);
+  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B, conc), shareF);
 }
 
 // Empirical schedule choice on the real factor (called once per (tree, B) at
 // setup, outside graph capture): time the candidate schedules with CUDA events.
 hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s, bool shareF) {
+                      cudaStream_t s, bool shareF, bool conc) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   SolveCfg have;
-  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, B, &have) || nd->lean) return HH_OK;
+  if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, cfg_key(B, conc), &have) || nd->lean)
+    return HH_OK;
   const int nlev = (int)nd->levels.size();
   cudaEvent_t e0, e1;
   HH_CUDA_TRY(cudaEventCreate(&e0));
@@ -1640,24 +1896,55 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
       fprintf(stderr, "[hh]   m=%d B=%d cut=%d split=%d: %.1f us\n", nd->m, B, c.sub_cut, c.split, 1e3 * ms / 3);
     if (ms < best_ms) { best_ms = ms; best = c; }
   }
+  // stage 3: dataflow kernels for the per-level range (with and without the cluster top)
+  if (!conc) {
+    SolveCfg cands[2] = {best, best};
+    cands[0].flow = 1;
+    cands[1].flow = 1;
+    cands[1].split = nlev - 1;
+    HH_TRY(nd_flow_reset(nd, B, work, s));
+    for (int k = 0; k < 2; ++k) {
+      const SolveCfg c = cands[k];
+      if (k == 1 && c.split == best.split) break;
+      if (!flow_ok(nd, c.sub_cut, c.split)) continue;
+      float ms;
+      HH_TRY(run(c, &ms));
+      HH_CUDA_TRY(cudaStreamSynchronize(s));
+      int to = 0;
+      HH_CUDA_TRY(cudaMemcpyFromSymbol(&to, g_flow_timeout, sizeof(int)));
+      if (to) {   // a wait gave up: never use the dataflow schedule for this plan
+        const int z = 0;
+        HH_CUDA_TRY(cudaMemcpyToSymbol(g_flow_timeout, &z, sizeof(int)));
+        HH_TRY(nd_flow_reset(nd, B, work, s));
+        if (getenv("HH_DEBUG")) fprintf(stderr, "[hh] nd flow: wait timeout (m=%d B=%d), disabled\n", nd->m, B);
+        break;
+      }
+      if (getenv("HH_DEBUG") && atoi(getenv("HH_DEBUG")) > 1)
+        fprintf(stderr, "[hh]   m=%d B=%d cut=%d split=%d flow: %.1f us\n", nd->m, B, c.sub_cut, c.split,
+                1e3 * ms / 3);
+      if (ms < best_ms) { best_ms = ms; best = c; }
+    }
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   std::lock_guard<std::mutex> lk(nd->cut_mu);
-  nd->cfg_cache.push_back({B, best});
+  nd->cfg_cache.push_back({cfg_key(B, conc), best});
   if (getenv("HH_DEBUG"))
     fprintf(stderr,
-            "[hh] nd_autotune m=%d dim=%d B=%d levels=%d -> sub_cut=%d split=%d (%.1f us/solve, "
+            "[hh] nd_autotune m=%d dim=%d B=%d levels=%d -> sub_cut=%d split=%d flow=%d (%.1f us/solve, "
             "%.1f MB/sample, %.0f GB/s)\n",
-            nd->m, nd->dim, B, nlev, best.sub_cut, best.split, 1e3 * best_ms / 3,
+            nd->m, nd->dim, B, nlev, best.sub_cut, best.split, best.flow, 1e3 * best_ms / 3,
             nd->stream_bytes / 1e6, (double)nd->stream_bytes * B / (best_ms / 3 * 1e-3) / 1e9);
   return HH_OK;
 }
 
-int nd_solve_launches(const NDPlan* ndc, int B) {
+int nd_solve_launches(const NDPlan* ndc, int B, bool conc) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   const int nlev = (int)nd->levels.size();
-  SolveCfg c = get_cfg(nd, B);
+  SolveCfg c = get_cfg(nd, B, conc);
   if (nd->lean) { c.sub_cut = -1; c.split = nlev - 1; }
+  if (c.flow && flow_ok(nd, c.sub_cut, c.split))
+    return (c.sub_cut >= 0 ? 2 : 0) + 2 + (c.split < nlev - 1 ? 1 : 0);
   int n = (c.sub_cut >= 0 ? 2 : 0) + 2 * (c.split - c.sub_cut) + (c.split < nlev - 1 ? 1 : 0);
   for (int L = c.sub_cut + 1; L <= c.split; ++L) {
     const LevelInfo& li = nd->levels[L];

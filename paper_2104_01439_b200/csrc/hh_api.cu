@@ -308,6 +308,7 @@ struct SampleOut {
 
 struct Engine {
   int device = 0;
+  bool conc = false;         // runs beside other sweep workers (ND schedule choice)
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
       cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp;
@@ -426,6 +427,7 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   HH_TRY(E.slabp.ensure((size_t)B * sizeof(int2)));
   if (sp.comm) HH_TRY(E.hstage.ensure((size_t)4 * FL.G * FL.plane * 16));
   HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
+  HH_TRY(nd_flow_reset(P, B, E.work.as<cplx>(), E.s));
   HH_TRY(E.kcf.ensure((size_t)B * 16));
   HH_TRY(E.kcc.ensure((size_t)B * 16));
   HH_TRY(E.cpart.ensure((size_t)B * nblk * (m + 2) * 16));
@@ -608,7 +610,7 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   prof_mark(E, "factor", tp);
   HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
   HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
-                     varg(E.ec.as<cplx>(), Nc), E.s, sp.slabmode));
+                     varg(E.ec.as<cplx>(), Nc), E.s, sp.slabmode, E.conc));
   prof_mark(E, "autotune", tp);
   HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, E.Bf * sizeof(int), cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
@@ -631,7 +633,7 @@ VArg vfine(Engine& E, Pool& p) { return varg(p.as<cplx>() + E.FL.pad, E.FL.strid
 bool slab_mode(const Engine& E) { return E.spec.slabmode; }
 // coarse solve on all entries (shared factor in slab mode)
 hh_status coarse_solve_all(Engine& E, const int* st, VArg rhs, VArg x) {
-  return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E));
+  return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E), E.conc);
 }
 // Arnoldi reductions of the slab mode: partials -> (NCCL allreduce) -> finish on every entry
 hh_status krylov_mdot_all(Engine& E) {
@@ -689,7 +691,7 @@ int64_t launches_per_iteration(const Engine& E) {
     const bool multi = E.X.comm && E.X.comm->nranks > 1;
     slab = 2 * ((E.B > 1 ? 1 : 0) + (multi ? 2 : 0)) + (E.B > 1 ? 1 : 0) + 2;
   }
-  return fine + nd_solve_launches(E.plan, E.B) + 3 + slab;
+  return fine + nd_solve_launches(E.plan, E.B, E.conc) + 3 + slab;
 }
 
 // two captured variants of one iteration: plain, and with phase events (sampled timing)
@@ -1257,6 +1259,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     }
     for (int t = 0; t < nt; ++t) engines.push_back(g_sweep_engines[t].get());
   }
+  for (Engine* E : engines) E->conc = nt > 1;
   for (Engine* E : engines)
     for (const BatchSpec& sp : specs) HH_TRY(reserve_pools(*E, sp));
   // ND solve schedule per (grid, batch size), timed once on an idle GPU (zero
@@ -1270,7 +1273,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
       HH_CUDA_TRY(cudaMemsetAsync(E.F.p, 0, (size_t)sp.B * nd_front_entries(P) * 16, E.s));
       HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)sp.B * Nc * 16, E.s));
       HH_TRY(nd_autotune(P, sp.B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
-                         varg(E.ec.as<cplx>(), Nc), E.s));
+                         varg(E.ec.as<cplx>(), Nc), E.s, false, E.conc));
     }
     HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   }

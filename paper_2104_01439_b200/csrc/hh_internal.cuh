@@ -138,15 +138,20 @@ void nd_plan_destroy(NDPlan* p);
 int64_t nd_front_entries(const NDPlan* p);        // complex entries per sample
 int64_t nd_stream_bytes(const NDPlan* p);         // bytes streamed per solve per sample
 int nd_levels(const NDPlan* p);
-int nd_solve_launches(const NDPlan* p, int B);      // kernel launches of one nd_solve
+int nd_solve_launches(const NDPlan* p, int B, bool conc = false);      // kernel launches of one nd_solve
 int64_t nd_work_entries(const NDPlan* p);         // zs + out entries per sample
+// zero the dataflow-solve counters in the work of B samples (after allocation)
+hh_status nd_flow_reset(const NDPlan* p, int B, cplx* work, cudaStream_t s);
 int64_t nd_cbuf_entries(const NDPlan* p);         // pivot column buffer per sample
 // F: [B][front_entries]; stencil: [B][Nc*3^d]; work: [B][work]; cbuf: [B][cbuf]
 hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* cbuf, int* flag,
                     cudaStream_t s);
 // shareF: every entry uses the one factor at F (slabs of one problem)
+// conc: the solve shares the GPU with other streams (concurrent sweep workers):
+// schedules are tuned and cached separately, and the dataflow kernels (whose
+// waiting CTAs hold SM slots) are not used
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s, bool shareF = false);
+                   VArg x, cudaStream_t s, bool shareF = false, bool conc = false);
 // choose the solve schedule for batch size B by timing candidates on the real factor
 hh_status nd_autotune(const NDPlan* p, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s, bool shareF = false);
+                      cudaStream_t s, bool shareF = false, bool conc = false);
