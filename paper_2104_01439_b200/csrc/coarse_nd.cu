@@ -473,18 +473,48 @@ __device__ __forceinline__ void front_gather(const SolveArgs& A, const FrontMeta
 template <int DIR, int G>
 __device__ __forceinline__ void front_rows_g(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* v,
                                              int gw, int nw, int lane) {
-  constexpr int RPW = 32 / G;
+  constexpr int RPW = 32 / G;   // row groups per warp
+  constexpr int RB = 2;         // rows per group and pass: their loads are in flight together
+  constexpr int DEPTH = 4;
   const int rows = DIR == 0 ? m.u : m.s, len = DIR == 0 ? m.s : m.f;
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
   const cplx* row0 = DIR == 0 ? F + (int64_t)m.s * m.f : F;
   const int grp = lane / G, sub = lane % G;
-  for (int base = gw * RPW; base < rows; base += nw * RPW) {
-    const int r = base + grp;
-    const bool ok = r < rows;
-    const cplx acc = row_dot_g<G>(row0 + (int64_t)(ok ? r : 0) * m.f, v, ok ? len : 0, sub);
-    if (ok && sub == 0) {
-      if (DIR == 0) upd_of(A, bs)[m.outOff + r] = cadd(acc, v[m.s + r]);
-      else A.x.at(bs)[A.sep[m.sepOff + r]] = acc;
+  for (int base = gw * RPW * RB; base < rows; base += nw * RPW * RB) {
+    cplx a0[RB], a1[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) a0[k] = a1[k] = cmake(0, 0);
+    for (int c = sub; c < len; c += DEPTH * G) {
+      cplx x[RB][DEPTH];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = base + grp + k * RPW;
+        const cplx* row = row0 + (int64_t)(r < rows ? r : 0) * m.f;
+#pragma unroll
+        for (int t = 0; t < DEPTH; ++t)
+          x[k][t] = (r < rows && c + G * t < len) ? __ldg(&row[c + G * t]) : cmake(0, 0);
+      }
+#pragma unroll
+      for (int t = 0; t < DEPTH; ++t) {
+        if (c + G * t >= len) break;
+        const cplx vt = v[c + G * t];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) cfma(t & 1 ? a1[k] : a0[k], x[k][t], vt);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      cplx a = cadd(a0[k], a1[k]);
+#pragma unroll
+      for (int o = G / 2; o; o >>= 1) {
+        a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+        a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+      }
+      const int r = base + grp + k * RPW;
+      if (r < rows && sub == 0) {
+        if (DIR == 0) upd_of(A, bs)[m.outOff + r] = cadd(a, v[m.s + r]);
+        else A.x.at(bs)[A.sep[m.sepOff + r]] = a;
+      }
     }
   }
 }
@@ -1650,7 +1680,7 @@ static hh_status launch_pdl(void (*kern)(Args...), dim3 grid, int block, size_t 
 // many as needed to put ~4 CTAs on every SM
 static int g_fill_ctas = getenv("HH_ND_FILL") ? atoi(getenv("HH_ND_FILL")) : 4 * 148;
 static int level_split(int rows, int count, int B, int len) {
-  const int rpc = (LT / 32) * (32 / wide_group(std::max(1, len)));   // rows per CTA pass
+  const int rpc = (LT / 32) * (32 / wide_group(std::max(1, len))) * 2;   // rows per CTA pass (RB = 2)
   const int by_rows = std::max(1, (rows + rpc - 1) / rpc);
   const int fill = std::max(1, (g_fill_ctas + count * B - 1) / (count * B));
   return std::max(1, std::min(std::min(by_rows, fill), 65535));
