@@ -37,6 +37,9 @@ namespace {
 constexpr int NB = 16;      // pivot block of the partial Gauss-Jordan sweep
 constexpr int PIV_CHUNK = 256;   // rows / columns per k_nd_piv CTA
 constexpr int LEAF = 64;    // max nodes of a leaf box
+#ifndef ND_RB
+#define ND_RB 2
+#endif
 
 struct FrontMeta {          // device-visible per-front data
   int s, u, f, level;
@@ -474,7 +477,7 @@ template <int DIR, int G>
 __device__ __forceinline__ void front_rows_g(const SolveArgs& A, const FrontMeta& m, int bs, const cplx* v,
                                              int gw, int nw, int lane) {
   constexpr int RPW = 32 / G;   // row groups per warp
-  constexpr int RB = 2;         // rows per group and pass: their loads are in flight together
+  constexpr int RB = ND_RB;     // rows per group and pass: their loads are in flight together
   constexpr int DEPTH = 4;
   const int rows = DIR == 0 ? m.u : m.s, len = DIR == 0 ? m.s : m.f;
   const cplx* F = A.F + (int64_t)bs * A.FE + m.Foff;
@@ -1680,7 +1683,7 @@ static hh_status launch_pdl(void (*kern)(Args...), dim3 grid, int block, size_t 
 // many as needed to put ~4 CTAs on every SM
 static int g_fill_ctas = getenv("HH_ND_FILL") ? atoi(getenv("HH_ND_FILL")) : 4 * 148;
 static int level_split(int rows, int count, int B, int len) {
-  const int rpc = (LT / 32) * (32 / wide_group(std::max(1, len))) * 2;   // rows per CTA pass (RB = 2)
+  const int rpc = (LT / 32) * (32 / wide_group(std::max(1, len))) * ND_RB;   // rows per CTA pass
   const int by_rows = std::max(1, (rows + rpc - 1) / rpc);
   const int fill = std::max(1, (g_fill_ctas + count * B - 1) / (count * B));
   return std::max(1, std::min(std::min(by_rows, fill), 65535));
