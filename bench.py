@@ -420,12 +420,25 @@ def main():
             gbs = ball / (out["ms_per_step"] * args.steps * 1e-3) / 1e9
             agg = {"bytes_per_step": ball / args.steps, "achieved_gbs": gbs, "frac": gbs / peak,
                    "note": "all algorithmic bytes of every iteration / whole step time (setup included)"}
+        tot_ms = sum(v["ms"] for v in phases.values())
+        step_s = out["ms_per_step"] * 1e-3
+        for ph, v in phases.items():
+            # concurrent streams overlap launches, so per-launch durations overstate
+            # each kernel's cost: split the step's wall time over the phases in
+            # proportion to their summed sampled device time (setup time is split
+            # over them too, so this is a lower bound on the rate)
+            ba = tm[ph].get("bytes_all", 0.0) / args.steps
+            if ba > 0 and tot_ms > 0:
+                g = ba / (step_s * v["ms"] / tot_ms) / 1e9
+                v["wall_share_gbs"] = g
+                v["wall_share_frac"] = g / peak
         if dom:
             p = phases[dom]
             roof = {"bound": "hbm", "kernel": names[dom], "achieved": p["achieved_gbs"],
                     "peak": peak, "unit": "GB/s", "frac": p["frac"], "traffic": None,
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                     "bytes_model": "algorithmic bytes per launch (DESIGN.md 'Roofline')",
+                    "frac_wall_share": p.get("wall_share_frac"),
                     "phases": phases, "aggregate": agg}
     line = {"metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": out["ms_per_step"],
