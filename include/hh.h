@@ -199,6 +199,41 @@ hh_status hh_shift_search(const hh_problem_desc* common, const hh_fgmres_opts* o
                           const hh_search_sample* s, int32_t n, const void* const* rhs,
                           double sigma_lo, double sigma_hi, double tol, hh_search_result* out);
 
+/* Local Fourier analysis of the two-grid method (Sec. 3,
+ * symbols PAPER.md:273-334; NEXT f4 alternative in SURVEY.md 8(f)): for the 2D Q1
+ * operator with lambda = k^2 + i beta k^sigma (readings C1, C2), the 4 x 4 symbol
+ *   T(theta) = S^nu2 (I - P L_2h^{-1} R L_h) S^nu1        (R = P^T / 4)
+ * on the harmonics of theta, and
+ *   rho_loc = max over the m x m grid theta_i = -pi/2 + pi (i + 1) / m of
+ *             T^low = (-pi/2, pi/2]^2, theta != 0, of the spectral radius of T
+ * (the sup over the continuum is read as this grid maximum).
+ * Eigenvalues: T = D - a b^T (diagonal minus rank one) has the characteristic
+ * polynomial prod(x - d_i) + sum_i a_i b_i prod_{j!=i}(x - d_j); its four roots
+ * are found by Aberth iterations in fp64 (root accuracy ~1e-8 near double roots).
+ * q: HOST array of n queries; rho_out: HOST array of n doubles.  device: CUDA
+ * ordinal; the call blocks.  HH_E_ARG: NULL pointer; HH_E_CONFIG: m < 2 or
+ * > 4096, nu1/nu2 < 0, h <= 0, omega not in (0, 1]. */
+typedef struct {
+  double  k, h, beta, sigma, omega;
+  int32_t nu1, nu2, m;
+  int32_t pad;
+} hh_lfa_query;
+hh_status hh_lfa_rho(const hh_lfa_query* q, int32_t n, int32_t device, double* rho_out);
+
+/* sigma_c = the smallest sigma in [sigma_lo, sigma_hi] with rho_loc(sigma) < 1
+ * (I_conv = [sigma_c, 2], reading G2): bisection to width tol
+ * assuming rho_loc decreases in sigma (a stronger shift damps more), every round
+ * one batched rho_loc evaluation of all queries (q[i].sigma ignored).
+ * sigma_c_out[i] = sigma_lo if rho_loc(sigma_lo) < 1, NaN if rho_loc(sigma_hi) >= 1,
+ * else the upper end of the final bracket.  HOST arrays; blocks. */
+hh_status hh_lfa_sigma_c(const hh_lfa_query* q, int32_t n, int32_t device, double sigma_lo,
+                         double sigma_hi, double tol, double* sigma_c_out);
+
+/* LFA instrumentation since the last reset: st4 = [theta points evaluated,
+ * Aberth iterations, device ms of the rho_loc kernels (CUDA events), kernel
+ * launches]; reset != 0 zeroes them after reading.  st4 may be NULL. */
+hh_status hh_lfa_stats(int32_t reset, double* st4);
+
 hh_status hh_destroy_problem(hh_problem* p);
 
 /* Phase instrumentation for the bench roofline (device events around each

@@ -11,6 +11,8 @@ PAPER.md:252-258  T_hat = S^nu2 K_hat S^nu1,  K_hat = I - I_2h^h L_2h^{-1} I_h^2
 PAPER.md:273-277  symbol of L_h
 PAPER.md:283-289  symbol of L_2h (evaluated at 2 theta)
 PAPER.md:292-306  prolongation / restriction symbols, I_h^2h = (1/4) (I_2h^h)^T
+PAPER.md:343-346  sigma_c = argmin_{sigma in [1,2]} {rho_loc(sigma) < 1} (I_conv = [sigma_c, 2],
+                  reading G2), found by bisection (sigma_c below)
 PAPER.md:327-334  symbol of the damped Jacobi smoother S_h (the symbol is
                   right; the printed S_h *stencil* corners at PAPER.md:157-160
                   are garbled, reading G1 in DESIGN.md)
@@ -82,3 +84,26 @@ def rho_loc(lam, h, omega, nu1, nu2, m=128):
             T = two_grid_symbol(t1, t2, lam, h, omega, nu1, nu2)
             best = max(best, float(np.max(np.abs(np.linalg.eigvals(T)))))
     return best
+
+
+def lam_of(k, beta, sigma):
+    """lambda = k^2 + i beta k^sigma (reading C2)."""
+    return k * k + 1j * beta * k ** sigma
+
+
+def sigma_c(k, h, beta=1.0, omega=0.6, nu1=2, nu2=2, m=64, lo=1.0, hi=2.0, tol=1e-3):
+    """Smallest sigma in [lo, hi] with rho_loc(sigma) < 1, by
+    bisection assuming rho_loc decreases with sigma: lo if rho_loc(lo) < 1, NaN if
+    rho_loc(hi) >= 1, else the upper end of the final bracket (width <= tol)."""
+    r = lambda s: rho_loc(lam_of(k, beta, s), h, omega, nu1, nu2, m)
+    if r(lo) < 1.0:
+        return lo
+    if not r(hi) < 1.0:
+        return float("nan")
+    while hi - lo > tol:
+        mid = 0.5 * (lo + hi)
+        if r(mid) < 1.0:
+            hi = mid
+        else:
+            lo = mid
+    return hi

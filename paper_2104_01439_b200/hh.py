@@ -25,7 +25,8 @@ STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_C
 EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "hh_vcycle",
            "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
            "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
-           "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_last_error", "hh_version"]
+           "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_lfa_rho", "hh_lfa_sigma_c", "hh_lfa_stats",
+           "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -59,6 +60,12 @@ class Sample(C.Structure):
 
 class SearchSample(C.Structure):
     _fields_ = [("id", C.c_int64), ("n_cells", C.c_int32), ("k", C.c_double), ("beta", C.c_double)]
+
+
+class LfaQuery(C.Structure):
+    _fields_ = [("k", C.c_double), ("h", C.c_double), ("beta", C.c_double), ("sigma", C.c_double),
+                ("omega", C.c_double), ("nu1", C.c_int32), ("nu2", C.c_int32), ("m", C.c_int32),
+                ("pad", C.c_int32)]
 
 
 class SearchResult(C.Structure):
@@ -99,6 +106,9 @@ def _load():
         "hh_shift_search": [C.POINTER(ProblemDesc), C.POINTER(FgmresOpts), C.POINTER(SearchSample), i32,
                             C.POINTER(C.c_void_p), C.c_double, C.c_double, C.c_double,
                             C.POINTER(SearchResult)],
+        "hh_lfa_rho": [C.POINTER(LfaQuery), i32, i32, dp],
+        "hh_lfa_sigma_c": [C.POINTER(LfaQuery), i32, i32, C.c_double, C.c_double, C.c_double, dp],
+        "hh_lfa_stats": [i32, dp],
         "hh_apply_op": [vp, i32, vp, vp],
         "hh_vcycle": [vp, vp, vp],
         "hh_coarse_solve": [vp, vp, vp],
@@ -305,6 +315,39 @@ def shift_search(samples, rhs, lo=1.0, hi=2.0, tol=1e-2, o=None, nu_pre=2, nu_po
     _check(lib.hh_shift_search(C.byref(d), C.byref(o), arr, n, ptrs, lo, hi, tol, out))
     del keep
     return [r.as_dict() for r in out]
+
+
+def _lfa_queries(queries):
+    return (LfaQuery * len(queries))(*[LfaQuery(q["k"], q["h"], q.get("beta", 1.0), q.get("sigma", 1.0),
+                                                q.get("omega", 0.6), q.get("nu1", 2), q.get("nu2", 2),
+                                                q.get("m", 128), 0) for q in queries])
+
+
+def lfa_rho(queries, device=None):
+    """hh_lfa_rho: rho_loc of the two-grid symbol for dicts with
+    k, h, beta, sigma, omega, nu1, nu2, m (theta grid m x m of T^low)."""
+    n = len(queries)
+    out = (C.c_double * n)()
+    dev = torch.cuda.current_device() if device is None else device
+    _check(lib.hh_lfa_rho(_lfa_queries(queries), n, dev, out))
+    return list(out)
+
+
+def lfa_sigma_c(queries, lo=1.0, hi=2.0, tol=1e-3, device=None):
+    """hh_lfa_sigma_c: smallest sigma in [lo, hi] with rho_loc < 1
+    by bisection to width tol; NaN when rho_loc(hi) >= 1."""
+    n = len(queries)
+    out = (C.c_double * n)()
+    dev = torch.cuda.current_device() if device is None else device
+    _check(lib.hh_lfa_sigma_c(_lfa_queries(queries), n, dev, lo, hi, tol, out))
+    return list(out)
+
+
+def lfa_stats(reset=False):
+    """hh_lfa_stats: theta evaluations, Aberth iterations, kernel ms, launches."""
+    st = (C.c_double * 4)()
+    _check(lib.hh_lfa_stats(1 if reset else 0, st))
+    return {"evals": st[0], "aberth_iters": st[1], "ms": st[2], "launches": int(st[3])}
 
 
 PHASES = ("pre", "coarse", "post", "krylov")
