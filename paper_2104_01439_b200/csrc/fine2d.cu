@@ -25,6 +25,9 @@
 
 namespace {
 
+#ifndef FINE_DI_GLOBAL
+#define FINE_DI_GLOBAL 1   // heterogeneous D^{-1} read through L1 instead of staged in smem
+#endif
 constexpr int TX = 32;   // tile width  (fine nodes along x, even)
 constexpr int TY = 16;   // tile height (even)
 constexpr int NT = 256;  // threads per CTA
@@ -277,9 +280,9 @@ __global__ void __launch_bounds__(NT) k_apply2d(FineK P, VArg x, VArg y, VArg su
 // D^{-1} at a region node: heterogeneous -> the precomputed copy staged in smem;
 // constant k -> the interior centre coefficient, the element loop at the boundary
 template <bool HET>
-__device__ __forceinline__ cplx dinv_at(const cplx* sDi, int si, const Tile& t, int gx, int gy,
-                                        int n, double h, const double2* sE, double2 kc, cplx di_int) {
-  if (HET) return sDi[si];
+__device__ __forceinline__ cplx dinv_at(const cplx* sDi, const cplx* dg, int si, const Tile& t, int gx,
+                                        int gy, int n, double h, const double2* sE, double2 kc, cplx di_int) {
+  if (HET) return FINE_DI_GLOBAL ? __ldg(&dg[(int64_t)gy * (n + 1) + gx]) : sDi[si];
   if (gx > 0 && gx < n && gy > 0 && gy < n) return di_int;
   return cinv(node_diag<false>(t, gx, gy, n, h, sE, kc));
 }
@@ -303,7 +306,7 @@ __device__ __forceinline__ cplx dinv_at(const cplx* sDi, int si, const Tile& t, 
 // NUC > 0: nu fixed at compile time (region sizes, smem strides and the step
 // loop fold to constants); NUC = 0: nu from P.
 template <bool HET, int NUC>
-__global__ void __launch_bounds__(NT, HET ? 3 : 4) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
+__global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : 4) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
   const int b = blockIdx.z;
   extern __shared__ double4 smem_raw[];
   const int n = P.n, nu = NUC > 0 ? NUC : P.nu;
@@ -316,12 +319,13 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_pre2d(FineK P, VArg f, SArg
   cplx* sF = reinterpret_cast<cplx*>(smem_raw);
   cplx* sA = sF + S;
   cplx* sB = sA + S;
-  cplx* sDi = sB + S;                                   // HET only
-  double2* sE = reinterpret_cast<double2*>(sDi + S);    // HET only
+  cplx* sDi = sB + S;                                   // HET, D^{-1} staged
+  double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
+  const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9 = make_const9(kc, h, true);
   load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
   if (HET) {
-    load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
+    if (!FINE_DI_GLOBAL) load_region(sDi, dg, t, n, 1.0, rlo, rhi);
     load_coef(sE, P.coef + b * P.coef_bs, t, n);
   }
   __syncthreads();
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_pre2d(FineK P, VArg f, SArg
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);   // constant k: interior D = centre coefficient
   FOR_REGION(t.R, {
     cplx v = cmake(0, 0);
-    if (in) v = cscale(cmul(dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega);
+    if (in) v = cscale(cmul(dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega);
     sA[si] = v;
     sB[si] = cmake(0, 0);
   })
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_pre2d(FineK P, VArg f, SArg
     const int hal = t.R - step + 1;
     FOR_REGION(hal, if (in) {
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
-      const cplx di = dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int);
+      const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
       cfma(v, cscale(di, omega), csub(sF[si], ax));
       nxt[si] = v;
@@ -408,8 +412,9 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_post2d(FineK P, VArg f, SAr
   cplx* sA = sF + S;
   cplx* sB = sA + S;
   cplx* sC = sB + S;                                    // coarse block, CW x CH
-  cplx* sDi = sC + CW * CH;                             // HET only
-  double2* sE = reinterpret_cast<double2*>(sDi + S);    // HET only
+  cplx* sDi = sC + CW * CH;                             // HET, D^{-1} staged
+  double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
+  const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9e = make_const9(kc, h, true);
   load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
   load_region(sA, uin.at(b) - vofs, t, n, 1.0, rlo, rhi);
@@ -435,7 +440,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_post2d(FineK P, VArg f, SAr
     }
   }
   if (HET) {
-    load_region(sDi, P.dinv + (int64_t)b * P.stride - vofs, t, n, 1.0, rlo, rhi);
+    if (!FINE_DI_GLOBAL) load_region(sDi, dg, t, n, 1.0, rlo, rhi);
     load_coef(sE, P.coef + b * P.coef_bs, t, n);
   }
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : 4) k_post2d(FineK P, VArg f, SAr
     const int hal = t.R - step;
     FOR_REGION(hal, if (in) {
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e);
-      const cplx di = dinv_at<HET>(sDi, si, t, gx, gy, n, h, sE, kc, di_int);
+      const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
       cfma(v, cscale(di, omega), csub(sF[si], ax));
       nxt[si] = v;
@@ -589,7 +594,7 @@ size_t smem_bytes(int R, int nfields, bool het) {
   return b;
 }
 // pre: f, two iterates (+ D^{-1}, element coefficients if heterogeneous)
-size_t pre_smem(int R, bool het) { return smem_bytes(R, het ? 4 : 3, het); }
+size_t pre_smem(int R, bool het) { return smem_bytes(R, het && !FINE_DI_GLOBAL ? 4 : 3, het); }
 // post: as pre plus the staged coarse block
 size_t post_smem(int R, bool het) {
   return pre_smem(R, het) + (size_t)post_cw(R) * post_ch(R) * sizeof(cplx);
