@@ -26,7 +26,7 @@
 namespace {
 
 #ifndef FINE_DI_GLOBAL
-#define FINE_DI_GLOBAL 1   // heterogeneous D^{-1} read through L1 instead of staged in smem
+#define FINE_DI_GLOBAL 0   // 1: heterogeneous D^{-1} read through L1 instead of staged in smem (measured: no gain)
 #endif
 constexpr int TX = 32;   // tile width  (fine nodes along x, even)
 constexpr int TY = 16;   // tile height (even)
