@@ -39,7 +39,13 @@ struct Q {
   int nu1, nu2, m;
 };
 
-__device__ __forceinline__ cplx cdiv(cplx a, cplx b) { return cmul(a, cinv(b)); }
+// 1/z with the correctly rounded reciprocal instruction sequence (no IEEE
+// division slow path); z is never 0 here except at an exact root, guarded below
+__device__ __forceinline__ cplx crcp(cplx a) {
+  const double d = __drcp_rn(a.x * a.x + a.y * a.y);
+  return make_double2(a.x * d, -a.y * d);
+}
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) { return cmul(a, crcp(b)); }
 __device__ __forceinline__ cplx cpow_int(cplx a, int e) {
   cplx r = cmake(1, 0);
   for (int i = 0; i < e; ++i) r = cmul(r, a);
@@ -118,22 +124,31 @@ __device__ double rho_T(const Q& q, double t1, double t2, int* its) {
     const double r0 = 1e-2 * (sqrt(cabs2(d[k])) + 1e-3);
     z[k] = cadd(d[k], cmake(r0 * cs, r0 * sn));
   }
-  for (int it = 0; it < 200; ++it) {
+  for (int it = 0; it < 200; ++it) {   // simultaneous (Jacobi) Aberth steps
     ++*its;
+    cplx inv[6];                        // 1/(z_a - z_b) for the pairs (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+    inv[0] = crcp(csub(z[0], z[1])); inv[1] = crcp(csub(z[0], z[2])); inv[2] = crcp(csub(z[0], z[3]));
+    inv[3] = crcp(csub(z[1], z[2])); inv[4] = crcp(csub(z[1], z[3])); inv[5] = crcp(csub(z[2], z[3]));
+    cplx sum[4];
+    sum[0] = cadd(cadd(inv[0], inv[1]), inv[2]);
+    sum[1] = csub(cadd(inv[3], inv[4]), inv[0]);
+    sum[2] = csub(inv[5], cadd(inv[1], inv[3]));
+    sum[3] = cmake(-(inv[2].x + inv[4].x + inv[5].x), -(inv[2].y + inv[4].y + inv[5].y));
     double wmax = 0, zmax = 0;
+    cplx w[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       cplx p, dp;
       poly_eval(c, z[k], p, dp);
-      if (cabs2(p) == 0) continue;
+      w[k] = cmake(0, 0);
+      if (cabs2(p) == 0 || cabs2(dp) == 0) continue;
       const cplx N = cdiv(p, dp);
-      cplx sum = cmake(0, 0);
+      w[k] = cdiv(N, csub(cmake(1, 0), cmul(N, sum[k])));
+      wmax = fmax(wmax, cabs2(w[k]));
+    }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j != k) sum = cadd(sum, cinv(csub(z[k], z[j])));
-      const cplx w = cdiv(N, csub(cmake(1, 0), cmul(N, sum)));
-      z[k] = csub(z[k], w);
-      wmax = fmax(wmax, cabs2(w));
+    for (int k = 0; k < 4; ++k) {
+      z[k] = csub(z[k], w[k]);
       zmax = fmax(zmax, cabs2(z[k]));
     }
     if (wmax <= 1e-28 * zmax) break;   // |w| <= 1e-14 |z|: the cubic step already landed

@@ -5,7 +5,7 @@ bounded sample.  Prints one JSON line.
 
 Metric: theta-point symbol evaluations (4 x 4 spectral radius each) per second.
 Roofline: FP64 flops per evaluation = 920 (symbols + characteristic polynomial +
-start) + 556 per Aberth iteration, counted iterations from
+start) + 480 per Aberth iteration, counted iterations from
 hh_lfa_stats; peak = 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz = 37.2 TFLOP/s."""
 import json
 import math
@@ -19,7 +19,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2104_01439_b200.hh as hh  # noqa: E402
 
-F0, F1 = 920.0, 556.0
+F0, F1 = 920.0, 480.0
 PEAK_TFLOPS = 148 * 64 * 2 * 1965e6 / 1e12
 
 
