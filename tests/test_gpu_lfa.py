@@ -66,3 +66,13 @@ def test_lfa_edge_cases():
     with pytest.raises(hh.HHError) as e:
         hh.lfa_sigma_c([dict(k=10.0, h=H, m=8)], lo=2.0, hi=1.0)
     assert e.value.status == 2
+
+
+def test_lfa_many_queries_span_launch_chunks():
+    """More queries than one launch's grid.y (65,535): the host splits them."""
+    n = 70000
+    qs = [dict(k=(0.1 + 0.6 * (i % 7) / 6) / H, h=H, sigma=1.0 + (i % 5) * 0.25, m=4) for i in range(n)]
+    got = hh.lfa_rho(qs)
+    assert len(got) == n
+    for i in (0, 1, 65534, 65535, 65536, n - 1):
+        assert abs(got[i] - _oracle_rho(dict(qs[i], beta=1.0, omega=0.6, nu1=2, nu2=2))) <= 1e-7, i
