@@ -37,3 +37,37 @@ def test_library_exports_every_declared_symbol():
 def test_binding_exports_match_header():
     import paper_2104_01439_b200.hh as hh
     assert sorted(hh.EXPORTS) == declared_symbols()
+
+
+def _lib():
+    import torch  # noqa: F401
+    return ctypes.CDLL(LIB)
+
+
+class _Q(ctypes.Structure):   # hh_lfa_query
+    _fields_ = [("k", ctypes.c_double), ("h", ctypes.c_double), ("beta", ctypes.c_double),
+                ("sigma", ctypes.c_double), ("omega", ctypes.c_double), ("nu1", ctypes.c_int32),
+                ("nu2", ctypes.c_int32), ("m", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+def test_lfa_argument_validation_needs_no_gpu():
+    """hh_lfa_rho / hh_lfa_sigma_c validate before touching the device:
+    n = 0 is OK, NULL arrays are HH_E_ARG (1), bad queries or brackets HH_E_CONFIG (2)."""
+    lib = _lib()
+    out = (ctypes.c_double * 1)()
+    assert lib.hh_lfa_rho(None, 0, 0, None) == 0
+    assert lib.hh_lfa_rho(None, 1, 0, out) == 1
+    bad = [_Q(10.0, 1 / 32, 1.0, 1.0, 0.6, 2, 2, 1, 0),      # m < 2
+           _Q(10.0, 0.0, 1.0, 1.0, 0.6, 2, 2, 8, 0),         # h <= 0
+           _Q(10.0, 1 / 32, 1.0, 1.0, 1.5, 2, 2, 8, 0),      # omega > 1
+           _Q(10.0, 1 / 32, 1.0, 1.0, 0.6, -1, 2, 8, 0)]     # nu < 0
+    for q in bad:
+        assert lib.hh_lfa_rho(ctypes.byref(q), 1, 0, out) == 2
+    ok = _Q(10.0, 1 / 32, 1.0, 1.0, 0.6, 2, 2, 8, 0)
+    f = ctypes.c_double
+    assert lib.hh_lfa_sigma_c(ctypes.byref(ok), 1, 0, f(2.0), f(1.0), f(1e-2), out) == 2   # lo >= hi
+    assert lib.hh_lfa_sigma_c(ctypes.byref(ok), 1, 0, f(1.0), f(2.0), f(0.0), out) == 2    # tol <= 0
+    assert lib.hh_lfa_sigma_c(None, 0, 0, f(1.0), f(2.0), f(1e-2), None) == 0
+    st = (ctypes.c_double * 4)()
+    assert lib.hh_lfa_stats(1, st) == 0 and lib.hh_lfa_stats(0, st) == 0
+    assert list(st) == [0.0, 0.0, 0.0, 0.0]
