@@ -281,19 +281,31 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   const int j = j0 + tx;
   if (j >= f) return;
   const bool jK = (j >= kb && j < kb + nb);
+  // the thread's UT/8 rows at once, k outermost: every R value read from shared
+  // memory feeds UT/8 multiply-adds (the C values are warp broadcasts), so the
+  // update is FP64-bound instead of shared-memory bound; per output the k order
+  // (and so the rounding) is unchanged
+  constexpr int RPT = UT / 8;
+  cplx acc[RPT];
+  bool upd[RPT];
 #pragma unroll
-  for (int r = 0; r < UT / 8; ++r) {
-    const int il = ty + 8 * r;
-    const int i = i0 + il;
+  for (int r = 0; r < RPT; ++r) {
+    const int i = i0 + ty + 8 * r;
+    upd[r] = i < f && !(i >= kb && i < kb + nb);
+    acc[r] = (upd[r] && !jK) ? A[(int64_t)i * f + j] : cmake(0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const cplx rv = Rs[k][tx];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) cfms(acc[r], Cs[ty + 8 * r][k], rv);
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = i0 + ty + 8 * r;
     if (i >= f) continue;
-    if (i >= kb && i < kb + nb) {             // rows K: F[K,K] = P (F[K, not K] scaled by k_nd_piv)
-      if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NB + (j - kb)];
-      continue;
-    }
-    cplx acc = jK ? cmake(0, 0) : A[(int64_t)i * f + j];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) cfms(acc, Cs[il][k], Rs[k][tx]);
-    A[(int64_t)i * f + j] = acc;
+    if (upd[r]) A[(int64_t)i * f + j] = acc[r];
+    else if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NB + (j - kb)];   // rows K: F[K,K] = P
   }
 }
 
