@@ -247,8 +247,12 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
 
 // rank-nb update of all rows outside K:
 //   F[i][j] <- (j in K ? 0 : F[i][j]) - sum_k C[i][k] * F[kb+k][j]
-constexpr int UT = 32;   // update tile (UT x UT outputs per CTA, 256 threads)
-__global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
+constexpr int UT = 32;   // update tile columns (UR x UT outputs per CTA, 256 threads)
+// update tile rows UR (UR / 8 rows per thread): 64 for fronts of order >= 1024
+// (more multiply-adds per shared-memory read; 3 CTAs per SM), 32 below (more CTAs
+// for the many small fronts)
+template <int UR>
+__global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
                                                 int kb, int tiles, cplx* __restrict__ Fall,
                                                 int64_t FE, const cplx* __restrict__ Call,
                                                 int64_t CE, const int64_t* __restrict__ Coff) {
@@ -257,15 +261,15 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   const FrontMeta m = fr[t];
   if (kb >= m.s) return;
   const int f = m.f;
-  const int i0 = (blockIdx.x / tiles) * UT, j0 = (blockIdx.x % tiles) * UT;
+  const int i0 = (blockIdx.x / tiles) * UR, j0 = (blockIdx.x % tiles) * UT;   // tiles = column tiles
   if (i0 >= f || j0 >= f) return;
   const int nb = min(NB, m.s - kb);
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
   const cplx* Pg = C + (int64_t)f * NB;
-  __shared__ cplx Cs[UT][NB + 1];
+  __shared__ cplx Cs[UR][NB + 1];
   __shared__ cplx Rs[NB][UT + 1];
-  for (int idx = threadIdx.x; idx < UT * NB; idx += 256) {
+  for (int idx = threadIdx.x; idx < UR * NB; idx += 256) {
     const int i = idx / NB, k = idx % NB;
     Cs[i][k] = (i0 + i < f && k < nb) ? C[(int64_t)(i0 + i) * NB + k] : cmake(0, 0);
   }
@@ -281,11 +285,11 @@ __global__ void __launch_bounds__(256) k_nd_upd(const FrontMeta* __restrict__ fr
   const int j = j0 + tx;
   if (j >= f) return;
   const bool jK = (j >= kb && j < kb + nb);
-  // the thread's UT/8 rows at once, k outermost: every R value read from shared
-  // memory feeds UT/8 multiply-adds (the C values are warp broadcasts), so the
+  // the thread's UR/8 rows at once, k outermost: every R value read from shared
+  // memory feeds UR/8 multiply-adds (the C values are warp broadcasts), so the
   // update is FP64-bound instead of shared-memory bound; per output the k order
   // (and so the rounding) is unchanged
-  constexpr int RPT = UT / 8;
+  constexpr int RPT = UR / 8;
   cplx acc[RPT];
   bool upd[RPT];
 #pragma unroll
@@ -1578,8 +1582,12 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
       for (int kb = 0; kb < ms; kb += NB) {
         k_nd_piv<<<dim3(cnt, 1, (mf + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
             nd->d_fronts_w, ch.t0, kb, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag);
-        k_nd_upd<<<dim3(tiles * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0, C, 0,
-                                                             nd->d_Coff_w + ch.t0);
+        if (mf >= 1024)
+          k_nd_upd<64><<<dim3((mf + 63) / 64 * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0,
+                                                                             C, 0, nd->d_Coff_w + ch.t0);
+        else
+          k_nd_upd<32><<<dim3((mf + 31) / 32 * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0,
+                                                                             C, 0, nd->d_Coff_w + ch.t0);
       }
       k_nd_copyout<<<dim3(cnt, 64), 256, 0, s>>>(nd->d_fronts_w, nd->d_fronts, nd->d_Soff, ch.t0, W, F, Sst);
       HH_CUDA_TRY(cudaGetLastError());
@@ -1613,9 +1621,12 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
     for (int kb = 0; kb < li.max_s; kb += NB) {
       k_nd_piv<<<dim3(li.count, B, (li.max_f + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
           nd->d_fronts, li.begin, kb, F, FE, cbuf, CE, nd->d_Coff + li.begin, flag);
-      k_nd_upd<<<dim3(tiles * tiles, li.count, B), 256, 0, s>>>(nd->d_fronts, li.begin, kb, tiles,
-                                                                 F, FE, cbuf, CE,
-                                                                 nd->d_Coff + li.begin);
+      if (li.max_f >= 1024)
+        k_nd_upd<64><<<dim3((li.max_f + 63) / 64 * tiles, li.count, B), 256, 0, s>>>(
+            nd->d_fronts, li.begin, kb, tiles, F, FE, cbuf, CE, nd->d_Coff + li.begin);
+      else
+        k_nd_upd<32><<<dim3((li.max_f + 31) / 32 * tiles, li.count, B), 256, 0, s>>>(
+            nd->d_fronts, li.begin, kb, tiles, F, FE, cbuf, CE, nd->d_Coff + li.begin);
     }
     HH_CUDA_TRY(cudaGetLastError());
     if (prof >= 2) {
