@@ -9,7 +9,7 @@
 //    of i*A_eps is eps*M + k*B, positive definite for eps > 0, so every
 //    principal submatrix is non-singular); all fronts of one tree level of all
 //    B samples of a batch in one launch.  Each front is "swept" on its
-//    separator block by partial Gauss-Jordan (block size NB): afterwards the
+//    separator block by partial Gauss-Jordan (block size 16, 32 on large fronts): afterwards the
 //    dense front holds
 //        [ X = F_ss^{-1}      H = F_ss^{-1} F_su ]
 //        [ -H^T               S = F_uu - F_us X F_su ]
@@ -34,7 +34,6 @@
 namespace cg = cooperative_groups;
 
 namespace {
-constexpr int NB = 16;      // pivot block of the partial Gauss-Jordan sweep
 constexpr int PIV_CHUNK = 256;   // rows / columns per k_nd_piv CTA
 constexpr int LEAF = 64;    // max nodes of a leaf box
 #ifndef ND_RB
@@ -170,6 +169,8 @@ __global__ void k_nd_extend_add(const int* __restrict__ list, const FrontMeta* _
 }
 
 // pivot step: P = F[K,K]^{-1}; save column block C = F[:,K]; rows K <- P F[K,:], F[K,K] <- P
+// NBT = pivot block (16, or 32 on large fronts: half the passes over the front)
+template <int NBT>
 __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr, int begin,
                                                 int kb, cplx* __restrict__ Fall, int64_t FE,
                                                 cplx* __restrict__ Call, int64_t CE,
@@ -179,68 +180,94 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
   const int b = blockIdx.y;
   const FrontMeta m = fr[t];
   if (kb >= m.s) return;
-  const int nb = min(NB, m.s - kb);
+  const int nb = min(NBT, m.s - kb);
   const int f = m.f;
   // chunk blockIdx.z of PIV_CHUNK rows (column-block save) / columns (row scaling)
   const int c0 = blockIdx.z * PIV_CHUNK, c1 = min(f, c0 + PIV_CHUNK);
   if (c0 >= f) return;
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.x];
-  cplx* Pg = C + (int64_t)f * NB;   // P for k_nd_upd (the pivot block itself is rewritten there)
-  __shared__ cplx P[NB][NB + 1];
-  const int ti = threadIdx.x / NB, tj = threadIdx.x % NB;   // 16 x 16
-  if (ti < nb && tj < nb) P[ti][tj] = A[(int64_t)(kb + ti) * f + kb + tj];
+  cplx* Pg = C + (int64_t)f * NBT;   // P for k_nd_upd (the pivot block itself is rewritten there)
+  __shared__ cplx P[NBT][NBT + 1];
+  __shared__ cplx rp[NBT], cp[NBT];
+  for (int e = threadIdx.x; e < NBT * NBT; e += 256) {
+    const int ti = e / NBT, tj = e % NBT;
+    if (ti < nb && tj < nb) P[ti][tj] = A[(int64_t)(kb + ti) * f + kb + tj];
+  }
   // save this chunk's rows of the column block (rows outside K only are used later)
-  for (int i = c0 + threadIdx.x / NB; i < c1; i += 256 / NB) {
-    const int k = threadIdx.x % NB;
-    if (k < nb) C[(int64_t)i * NB + k] = A[(int64_t)i * f + kb + k];
+  for (int i = c0 + threadIdx.x / NBT; i < c1; i += 256 / NBT) {
+    const int k = threadIdx.x % NBT;
+    if (k < nb) C[(int64_t)i * NBT + k] = A[(int64_t)i * f + kb + k];
   }
   __syncthreads();
-  // in-place Gauss-Jordan inversion of the nb x nb pivot block (sweep operator)
+  // in-place Gauss-Jordan inversion of the nb x nb pivot block (sweep operator):
+  // row p scaled by 1/P[p][p], column p -> -P[i][p]/P[p][p], the rest
+  // P[i][j] -= P[i][p] * (scaled row p)[j], P[p][p] -> 1/P[p][p]
   for (int p = 0; p < nb; ++p) {
     const cplx piv = P[p][p];
     if (cabs2(piv) == 0.0 && threadIdx.x == 0) atomicExch(flag + b, 1);
     const cplx pinv = cinv(piv);
-    __syncthreads();
-    const bool inrow = (ti == p && tj < nb && tj != p);
-    const cplx rowp = inrow ? cmul(P[p][tj], pinv) : cmake(0, 0);
-    __syncthreads();
-    if (inrow) P[p][tj] = rowp;
-    __syncthreads();
-    cplx newv = cmake(0, 0);
-    bool wr = false;
-    if (ti < nb && tj < nb && ti != p) {
-      const cplx fac = P[ti][p];
-      if (tj != p) {
-        newv = P[ti][tj];
-        cfms(newv, fac, P[p][tj]);
-      } else {
-        newv = cmul(fac, pinv);
-        newv.x = -newv.x; newv.y = -newv.y;
-      }
-      wr = true;
+    if (threadIdx.x < nb) {
+      const int q = threadIdx.x;
+      rp[q] = q == p ? pinv : cmul(P[p][q], pinv);
+      cp[q] = P[q][p];
     }
     __syncthreads();
-    if (wr) P[ti][tj] = newv;
-    if (threadIdx.x == 0) P[p][p] = pinv;
+    for (int e = threadIdx.x; e < NBT * NBT; e += 256) {
+      const int i = e / NBT, j = e % NBT;
+      if (i >= nb || j >= nb) continue;
+      if (i == p) {
+        P[p][j] = rp[j];
+      } else if (j == p) {
+        const cplx v = cmul(cp[i], pinv);
+        P[i][p] = cmake(-v.x, -v.y);
+      } else {
+        cplx v = P[i][j];
+        cfms(v, cp[i], rp[j]);
+        P[i][j] = v;
+      }
+    }
     __syncthreads();
   }
-  if (blockIdx.z == 0 && ti < NB && tj < NB) Pg[ti * NB + tj] = (ti < nb && tj < nb) ? P[ti][tj] : cmake(0, 0);
+  if (blockIdx.z == 0)
+    for (int e = threadIdx.x; e < NBT * NBT; e += 256) {
+      const int ti = e / NBT, tj = e % NBT;
+      Pg[e] = (ti < nb && tj < nb) ? P[ti][tj] : cmake(0, 0);
+    }
   // rows K of this chunk's columns: R[k][j] = sum_l P[k][l] A[kb+l][j] for j not in K
   // (F[K,K] = P is written by k_nd_upd: the pivot block is read by every chunk here)
-  for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
-    if (j >= kb && j < kb + nb) continue;
-    cplx col[NB];
+  if constexpr (NBT == 16) {
+    for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+      if (j >= kb && j < kb + nb) continue;
+      cplx col[NBT];
 #pragma unroll
-    for (int l = 0; l < NB; ++l) col[l] = (l < nb) ? A[(int64_t)(kb + l) * f + j] : cmake(0, 0);
+      for (int l = 0; l < NBT; ++l) col[l] = (l < nb) ? A[(int64_t)(kb + l) * f + j] : cmake(0, 0);
 #pragma unroll
-    for (int k = 0; k < NB; ++k) {
-      if (k >= nb) break;
-      cplx acc = cmake(0, 0);
+      for (int k = 0; k < NBT; ++k) {
+        if (k >= nb) break;
+        cplx acc = cmake(0, 0);
 #pragma unroll
-      for (int l = 0; l < NB; ++l)
-        if (l < nb) cfma(acc, P[k][l], col[l]);
-      A[(int64_t)(kb + k) * f + j] = acc;
+        for (int l = 0; l < NBT; ++l)
+          if (l < nb) cfma(acc, P[k][l], col[l]);
+        A[(int64_t)(kb + k) * f + j] = acc;
+      }
+    }
+  } else {   // 32 columns at a time through shared memory (32 column values per thread would spill)
+    __shared__ cplx colS[NBT][32];
+    for (int js = c0; js < c1; js += 32) {
+      for (int e = threadIdx.x; e < NBT * 32; e += 256) {
+        const int l = e / 32, jj = e % 32;
+        colS[l][jj] = (l < nb && js + jj < c1) ? A[(int64_t)(kb + l) * f + js + jj] : cmake(0, 0);
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < NBT * 32; e += 256) {
+        const int k = e / 32, jj = e % 32, j = js + jj;
+        if (k >= nb || j >= c1 || (j >= kb && j < kb + nb)) continue;
+        cplx acc = cmake(0, 0);
+        for (int l = 0; l < nb; ++l) cfma(acc, P[k][l], colS[l][jj]);
+        A[(int64_t)(kb + k) * f + j] = acc;
+      }
+      __syncthreads();
     }
   }
 }
@@ -248,10 +275,11 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
 // rank-nb update of all rows outside K:
 //   F[i][j] <- (j in K ? 0 : F[i][j]) - sum_k C[i][k] * F[kb+k][j]
 constexpr int UT = 32;   // update tile columns (UR x UT outputs per CTA, 256 threads)
+constexpr int NB_MAX = 32;   // C-buffer layout allows pivot blocks up to this size
 // update tile rows UR (UR / 8 rows per thread): 64 for fronts of order >= 1024
 // (more multiply-adds per shared-memory read; 3 CTAs per SM), 32 below (more CTAs
 // for the many small fronts)
-template <int UR>
+template <int UR, int NBT>
 __global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
                                                 int kb, int tiles, cplx* __restrict__ Fall,
                                                 int64_t FE, const cplx* __restrict__ Call,
@@ -263,21 +291,22 @@ __global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMet
   const int f = m.f;
   const int i0 = (blockIdx.x / tiles) * UR, j0 = (blockIdx.x % tiles) * UT;   // tiles = column tiles
   if (i0 >= f || j0 >= f) return;
-  const int nb = min(NB, m.s - kb);
+  const int nb = min(NBT, m.s - kb);
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
-  const cplx* Pg = C + (int64_t)f * NB;
-  __shared__ cplx Cs[UR][NB + 1];
-  __shared__ cplx Rs[NB][UT + 1];
-  for (int idx = threadIdx.x; idx < UR * NB; idx += 256) {
-    const int i = idx / NB, k = idx % NB;
-    Cs[i][k] = (i0 + i < f && k < nb) ? C[(int64_t)(i0 + i) * NB + k] : cmake(0, 0);
+  const cplx* Pg = C + (int64_t)f * NBT;
+  // unpadded: C is read as warp broadcasts, R rows and both fills are contiguous
+  __shared__ cplx Cs[UR][NBT];
+  __shared__ cplx Rs[NBT][UT];
+  for (int idx = threadIdx.x; idx < UR * NBT; idx += 256) {
+    const int i = idx / NBT, k = idx % NBT;
+    Cs[i][k] = (i0 + i < f && k < nb) ? C[(int64_t)(i0 + i) * NBT + k] : cmake(0, 0);
   }
-  for (int idx = threadIdx.x; idx < NB * UT; idx += 256) {
+  for (int idx = threadIdx.x; idx < NBT * UT; idx += 256) {
     const int k = idx / UT, j = idx % UT;
     const int jj = j0 + j;
     cplx r = cmake(0, 0);
-    if (k < nb && jj < f) r = (jj >= kb && jj < kb + nb) ? Pg[k * NB + (jj - kb)] : A[(int64_t)(kb + k) * f + jj];
+    if (k < nb && jj < f) r = (jj >= kb && jj < kb + nb) ? Pg[k * NBT + (jj - kb)] : A[(int64_t)(kb + k) * f + jj];
     Rs[k][j] = r;
   }
   __syncthreads();
@@ -299,7 +328,7 @@ __global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMet
     acc[r] = (upd[r] && !jK) ? A[(int64_t)i * f + j] : cmake(0, 0);
   }
 #pragma unroll
-  for (int k = 0; k < NB; ++k) {
+  for (int k = 0; k < NBT; ++k) {
     const cplx rv = Rs[k][tx];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) cfms(acc[r], Cs[ty + 8 * r][k], rv);
@@ -309,7 +338,7 @@ __global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMet
     const int i = i0 + ty + 8 * r;
     if (i >= f) continue;
     if (upd[r]) A[(int64_t)i * f + j] = acc[r];
-    else if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NB + (j - kb)];   // rows K: F[K,K] = P
+    else if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NBT + (j - kb)];   // rows K: F[K,K] = P
   }
 }
 
@@ -1289,7 +1318,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   std::vector<int64_t> Coff(nf);
   for (auto& li : nd->levels) {
     int64_t o = 0;
-    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB + NB * NB; }
+    for (int t = li.begin; t < li.begin + li.count; ++t) { Coff[t] = o; o += (int64_t)nd->fronts[t].f * NB_MAX + NB_MAX * NB_MAX; }
     Cmax = std::max(Cmax, o);
   }
   nd->F_entries = Foff; nd->w_entries = posOff; nd->out_entries = outOff; nd->C_entries = Cmax;
@@ -1333,7 +1362,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
           fronts_w[t].Foff = w;
           w += ff;
           Coff_w[t] = co;
-          co += (int64_t)nd->fronts[t].f * NB + NB * NB;
+          co += (int64_t)nd->fronts[t].f * NB_MAX + NB_MAX * NB_MAX;
           ++t;
         }
         ch.t1 = t;
@@ -1550,6 +1579,33 @@ int64_t nd_cbuf_entries(const NDPlan* p) {
   return std::max<int64_t>(1, p->C_entries);
 }
 
+// The partial Gauss-Jordan sweep of `cnt` fronts (x Bn samples) starting at t0:
+// pivot blocks of 32 on fronts of order >= HH_ND_NB32_F (default 1024; half the
+// passes over the front, twice the multiply-adds per byte), 16 below.
+static int nb32_f() {
+  static const int v = getenv("HH_ND_NB32_F") ? atoi(getenv("HH_ND_NB32_F")) : 1024;
+  return v;
+}
+static void pivot_sweep(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, int mf, cplx* F, int64_t FE,
+                        cplx* C, int64_t CE, const int64_t* coff, int* flag, cudaStream_t s) {
+  const int nbt = mf >= nb32_f() ? 32 : 16;
+  const bool big = mf >= 1024;
+  const int tiles = (mf + UT - 1) / UT;
+  const dim3 gp(cnt, Bn, (mf + PIV_CHUNK - 1) / PIV_CHUNK);
+  const dim3 gu((mf + (big ? 63 : 31)) / (big ? 64 : 32) * tiles, cnt, Bn);
+  for (int kb = 0; kb < ms; kb += nbt) {
+    if (nbt == 32) {
+      k_nd_piv<32><<<gp, 256, 0, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
+      if (big) k_nd_upd<64, 32><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+      else k_nd_upd<32, 32><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    } else {
+      k_nd_piv<16><<<gp, 256, 0, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
+      if (big) k_nd_upd<64, 16><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+      else k_nd_upd<32, 16><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    }
+  }
+}
+
 hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
                     cudaStream_t s) {
   const int64_t FE = nd->F_entries, CE = nd_cbuf_entries(nd);
@@ -1578,17 +1634,7 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
                                                                    nd->d_fronts_w, nd->d_Soff, Sst,
                                                                    nd->d_eamap, W);
       }
-      const int tiles = (mf + UT - 1) / UT;
-      for (int kb = 0; kb < ms; kb += NB) {
-        k_nd_piv<<<dim3(cnt, 1, (mf + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
-            nd->d_fronts_w, ch.t0, kb, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag);
-        if (mf >= 1024)
-          k_nd_upd<64><<<dim3((mf + 63) / 64 * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0,
-                                                                             C, 0, nd->d_Coff_w + ch.t0);
-        else
-          k_nd_upd<32><<<dim3((mf + 31) / 32 * tiles, cnt, 1), 256, 0, s>>>(nd->d_fronts_w, ch.t0, kb, tiles, W, 0,
-                                                                             C, 0, nd->d_Coff_w + ch.t0);
-      }
+      pivot_sweep(nd->d_fronts_w, ch.t0, cnt, 1, ms, mf, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag, s);
       k_nd_copyout<<<dim3(cnt, 64), 256, 0, s>>>(nd->d_fronts_w, nd->d_fronts, nd->d_Soff, ch.t0, W, F, Sst);
       HH_CUDA_TRY(cudaGetLastError());
     }
@@ -1617,17 +1663,8 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
       k_nd_extend_add<<<g, 128, 0, s>>>(nd->d_eaList + li.ea_list_off[slot], nd->d_fronts,
                                         nd->d_eamap, F, FE);
     }
-    const int tiles = (li.max_f + UT - 1) / UT;
-    for (int kb = 0; kb < li.max_s; kb += NB) {
-      k_nd_piv<<<dim3(li.count, B, (li.max_f + PIV_CHUNK - 1) / PIV_CHUNK), 256, 0, s>>>(
-          nd->d_fronts, li.begin, kb, F, FE, cbuf, CE, nd->d_Coff + li.begin, flag);
-      if (li.max_f >= 1024)
-        k_nd_upd<64><<<dim3((li.max_f + 63) / 64 * tiles, li.count, B), 256, 0, s>>>(
-            nd->d_fronts, li.begin, kb, tiles, F, FE, cbuf, CE, nd->d_Coff + li.begin);
-      else
-        k_nd_upd<32><<<dim3((li.max_f + 31) / 32 * tiles, li.count, B), 256, 0, s>>>(
-            nd->d_fronts, li.begin, kb, tiles, F, FE, cbuf, CE, nd->d_Coff + li.begin);
-    }
+    pivot_sweep(nd->d_fronts, li.begin, li.count, B, li.max_s, li.max_f, F, FE, cbuf, CE, nd->d_Coff + li.begin,
+                flag, s);
     HH_CUDA_TRY(cudaGetLastError());
     if (prof >= 2) {
       cudaEventRecord(pe1, s);
