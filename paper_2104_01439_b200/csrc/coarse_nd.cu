@@ -188,8 +188,11 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
   cplx* A = Fall + (int64_t)b * FE + m.Foff;
   cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.x];
   cplx* Pg = C + (int64_t)f * NBT;   // P for k_nd_upd (the pivot block itself is rewritten there)
-  __shared__ cplx P[NBT][NBT + 1];
-  __shared__ cplx rp[NBT], cp[NBT];
+  // shared memory (dynamic): P [NBT][NBT + 1], rp, cp [NBT], and for NBT > 16 colS [NBT][32]
+  extern __shared__ double4 smem_raw[];
+  cplx (*P)[NBT + 1] = reinterpret_cast<cplx (*)[NBT + 1]>(smem_raw);
+  cplx* rp = reinterpret_cast<cplx*>(smem_raw) + NBT * (NBT + 1);
+  cplx* cp = rp + NBT;
   for (int e = threadIdx.x; e < NBT * NBT; e += 256) {
     const int ti = e / NBT, tj = e % NBT;
     if (ti < nb && tj < nb) P[ti][tj] = A[(int64_t)(kb + ti) * f + kb + tj];
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
       }
     }
   } else {   // 32 columns at a time through shared memory (32 column values per thread would spill)
-    __shared__ cplx colS[NBT][32];
+    cplx (*colS)[32] = reinterpret_cast<cplx (*)[32]>(cp + NBT);
     for (int js = c0; js < c1; js += 32) {
       for (int e = threadIdx.x; e < NBT * 32; e += 256) {
         const int l = e / 32, jj = e % 32;
@@ -275,12 +278,12 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
 // rank-nb update of all rows outside K:
 //   F[i][j] <- (j in K ? 0 : F[i][j]) - sum_k C[i][k] * F[kb+k][j]
 constexpr int UT = 32;   // update tile columns (UR x UT outputs per CTA, 256 threads)
-constexpr int NB_MAX = 32;   // C-buffer layout allows pivot blocks up to this size
+constexpr int NB_MAX = 32;   // C-buffer layout allows pivot blocks up to this size (64 needs NB_MAX = 64)
 // update tile rows UR (UR / 8 rows per thread): 64 for fronts of order >= 1024
 // (more multiply-adds per shared-memory read; 3 CTAs per SM), 32 below (more CTAs
 // for the many small fronts)
 template <int UR, int NBT>
-__global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
+__global__ void __launch_bounds__(256, UR == 64 ? (NBT == 64 ? 2 : 3) : 5) k_nd_upd(const FrontMeta* __restrict__ fr, int begin,
                                                 int kb, int tiles, cplx* __restrict__ Fall,
                                                 int64_t FE, const cplx* __restrict__ Call,
                                                 int64_t CE, const int64_t* __restrict__ Coff) {
@@ -296,8 +299,9 @@ __global__ void __launch_bounds__(256, UR == 64 ? 3 : 5) k_nd_upd(const FrontMet
   const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
   const cplx* Pg = C + (int64_t)f * NBT;
   // unpadded: C is read as warp broadcasts, R rows and both fills are contiguous
-  __shared__ cplx Cs[UR][NBT];
-  __shared__ cplx Rs[NBT][UT];
+  extern __shared__ double4 smem_raw[];   // Cs [UR][NBT], Rs [NBT][UT]
+  cplx (*Cs)[NBT] = reinterpret_cast<cplx (*)[NBT]>(smem_raw);
+  cplx (*Rs)[UT] = reinterpret_cast<cplx (*)[UT]>(reinterpret_cast<cplx*>(smem_raw) + UR * NBT);
   for (int idx = threadIdx.x; idx < UR * NBT; idx += 256) {
     const int i = idx / NBT, k = idx % NBT;
     Cs[i][k] = (i0 + i < f && k < nb) ? C[(int64_t)(i0 + i) * NBT + k] : cmake(0, 0);
@@ -1580,30 +1584,50 @@ int64_t nd_cbuf_entries(const NDPlan* p) {
 }
 
 // The partial Gauss-Jordan sweep of `cnt` fronts (x Bn samples) starting at t0:
-// pivot blocks of 32 on fronts of order >= HH_ND_NB32_F (default 1024; half the
-// passes over the front, twice the multiply-adds per byte), 16 below.
+// pivot blocks of 32 on fronts of order >= HH_ND_NB32_F (default 1024), 16 below
+// (64 from HH_ND_NB64_F, off by default) -- larger blocks mean fewer passes over
+// the front and more multiply-adds per byte, smaller ones more CTAs.
 static int nb32_f() {
   static const int v = getenv("HH_ND_NB32_F") ? atoi(getenv("HH_ND_NB32_F")) : 1024;
   return v;
 }
-static void pivot_sweep(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, int mf, cplx* F, int64_t FE,
-                        cplx* C, int64_t CE, const int64_t* coff, int* flag, cudaStream_t s) {
-  const int nbt = mf >= nb32_f() ? 32 : 16;
+static int nb64_f() {   // pivot blocks of 64 from this front order (HH_ND_NB64_F; compiled in only
+                        // with NB_MAX = 64: 2 CTAs per SM and the longer serial inversion lost,
+                        // cfg3 372 -> 398-405 ms)
+  static const int v = getenv("HH_ND_NB64_F") ? atoi(getenv("HH_ND_NB64_F")) : (1 << 30);
+  return v;
+}
+template <int NBT>
+static size_t piv_smem() { return ((size_t)NBT * (NBT + 1) + 2 * NBT + (NBT > 16 ? (size_t)NBT * 32 : 0)) * sizeof(cplx); }
+template <int UR, int NBT>
+static size_t upd_smem() { return ((size_t)UR * NBT + (size_t)NBT * UT) * sizeof(cplx); }
+
+template <int NBT>
+static void pivot_sweep_nb(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, int mf, cplx* F, int64_t FE,
+                           cplx* C, int64_t CE, const int64_t* coff, int* flag, cudaStream_t s) {
   const bool big = mf >= 1024;
   const int tiles = (mf + UT - 1) / UT;
   const dim3 gp(cnt, Bn, (mf + PIV_CHUNK - 1) / PIV_CHUNK);
   const dim3 gu((mf + (big ? 63 : 31)) / (big ? 64 : 32) * tiles, cnt, Bn);
-  for (int kb = 0; kb < ms; kb += nbt) {
-    if (nbt == 32) {
-      k_nd_piv<32><<<gp, 256, 0, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
-      if (big) k_nd_upd<64, 32><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
-      else k_nd_upd<32, 32><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
-    } else {
-      k_nd_piv<16><<<gp, 256, 0, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
-      if (big) k_nd_upd<64, 16><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
-      else k_nd_upd<32, 16><<<gu, 256, 0, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+  const size_t sp = piv_smem<NBT>(), su = big ? upd_smem<64, NBT>() : upd_smem<32, NBT>();
+  if (sp > 48 * 1024) smem_attr((const void*)k_nd_piv<NBT>, sp);
+  if (su > 48 * 1024) smem_attr(big ? (const void*)k_nd_upd<64, NBT> : (const void*)k_nd_upd<32, NBT>, su);
+  for (int kb = 0; kb < ms; kb += NBT) {
+    k_nd_piv<NBT><<<gp, 256, sp, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
+    if (big) k_nd_upd<64, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    else k_nd_upd<32, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+  }
+}
+static void pivot_sweep(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, int mf, cplx* F, int64_t FE,
+                        cplx* C, int64_t CE, const int64_t* coff, int* flag, cudaStream_t s) {
+  if constexpr (NB_MAX >= 64) {
+    if (mf >= nb64_f()) {
+      pivot_sweep_nb<64>(fr, t0, cnt, Bn, ms, mf, F, FE, C, CE, coff, flag, s);
+      return;
     }
   }
+  if (mf >= nb32_f()) pivot_sweep_nb<32>(fr, t0, cnt, Bn, ms, mf, F, FE, C, CE, coff, flag, s);
+  else pivot_sweep_nb<16>(fr, t0, cnt, Bn, ms, mf, F, FE, C, CE, coff, flag, s);
 }
 
 hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
