@@ -36,6 +36,9 @@ namespace cg = cooperative_groups;
 namespace {
 constexpr int PIV_CHUNK = 256;   // rows / columns per k_nd_piv CTA
 constexpr int LEAF = 64;    // max nodes of a leaf box
+#ifndef ND_PIV_REG
+#define ND_PIV_REG 0   // 1: 16-pivot row scaling with the column in registers (120 registers; sweep 0.369 -> 0.379 s)
+#endif
 #ifndef ND_RB
 #define ND_RB 2
 #endif
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
     }
   // rows K of this chunk's columns: R[k][j] = sum_l P[k][l] A[kb+l][j] for j not in K
   // (F[K,K] = P is written by k_nd_upd: the pivot block is read by every chunk here)
-  if constexpr (NBT == 16) {
+  if constexpr (NBT == 16 && ND_PIV_REG) {
     for (int j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
       if (j >= kb && j < kb + nb) continue;
       cplx col[NBT];
@@ -1609,7 +1612,7 @@ static void pivot_sweep_nb(const FrontMeta* fr, int t0, int cnt, int Bn, int ms,
   const int tiles = (mf + UT - 1) / UT;
   const dim3 gp(cnt, Bn, (mf + PIV_CHUNK - 1) / PIV_CHUNK);
   const dim3 gu((mf + (big ? 63 : 31)) / (big ? 64 : 32) * tiles, cnt, Bn);
-  const size_t sp = piv_smem<NBT>(), su = big ? upd_smem<64, NBT>() : upd_smem<32, NBT>();
+  const size_t sp = piv_smem<NBT>() + (NBT == 16 && !ND_PIV_REG ? (size_t)NBT * 32 * sizeof(cplx) : 0), su = big ? upd_smem<64, NBT>() : upd_smem<32, NBT>();
   if (sp > 48 * 1024) smem_attr((const void*)k_nd_piv<NBT>, sp);
   if (su > 48 * 1024) smem_attr(big ? (const void*)k_nd_upd<64, NBT> : (const void*)k_nd_upd<32, NBT>, su);
   for (int kb = 0; kb < ms; kb += NBT) {
