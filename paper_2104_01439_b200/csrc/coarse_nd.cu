@@ -1605,10 +1605,14 @@ static size_t piv_smem() { return ((size_t)NBT * (NBT + 1) + 2 * NBT + (NBT > 16
 template <int UR, int NBT>
 static size_t upd_smem() { return ((size_t)UR * NBT + (size_t)NBT * UT) * sizeof(cplx); }
 
+static int ur64_f() {   // 64-row update tiles from this front order (HH_ND_UR64_F)
+  static const int v = getenv("HH_ND_UR64_F") ? atoi(getenv("HH_ND_UR64_F")) : 1024;
+  return v;
+}
 template <int NBT>
 static void pivot_sweep_nb(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, int mf, cplx* F, int64_t FE,
                            cplx* C, int64_t CE, const int64_t* coff, int* flag, cudaStream_t s) {
-  const bool big = mf >= 1024;
+  const bool big = mf >= ur64_f();
   const int tiles = (mf + UT - 1) / UT;
   const dim3 gp(cnt, Bn, (mf + PIV_CHUNK - 1) / PIV_CHUNK);
   const dim3 gu((mf + (big ? 63 : 31)) / (big ? 64 : 32) * tiles, cnt, Bn);
