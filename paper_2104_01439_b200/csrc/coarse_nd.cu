@@ -2020,8 +2020,11 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
       fprintf(stderr, "[hh]   m=%d B=%d cut=%d split=%d: %.1f us\n", nd->m, B, c.sub_cut, c.split, 1e3 * ms / 3);
     if (ms < best_ms) { best_ms = ms; best = c; }
   }
-  // stage 3: dataflow kernels for the per-level range (with and without the cluster top)
-  if (!conc) {
+  // stage 3: dataflow kernels for the per-level range (with and without the cluster top);
+  // for concurrent sweep workers only on trees of at least HH_ND_FLOW_CONC_M coarse
+  // nodes per side (default: never -- waiting CTAs hold SM slots other streams need)
+  static const int flow_conc_m = getenv("HH_ND_FLOW_CONC_M") ? atoi(getenv("HH_ND_FLOW_CONC_M")) : (1 << 30);
+  if (!conc || nd->m >= flow_conc_m) {
     SolveCfg cands[2] = {best, best};
     cands[0].flow = 1;
     cands[1].flow = 1;
