@@ -1647,10 +1647,31 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
     cplx* C = cbuf;
     cplx* W = C + nd->Cw;
     cplx* Sst = W + nd->Wmax;   // packed Schur complements (first-fit offsets, see the plan)
+    static const int lprof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
     for (const Chunk& ch : nd->chunks) {
       const int cnt = ch.t1 - ch.t0;
       int ms = 0, mf = 0;
       for (int t = ch.t0; t < ch.t1; ++t) { ms = std::max(ms, nd->fronts[t].s); mf = std::max(mf, nd->fronts[t].f); }
+      cudaEvent_t ce0 = nullptr, ce1 = nullptr;   // HH_PROFILE_SETUP=2: per-chunk timing (diagnostics)
+      if (lprof >= 2) {
+        cudaEventCreate(&ce0); cudaEventCreate(&ce1);
+        cudaEventRecord(ce0, s);
+      }
+      struct ChunkTimer {
+        cudaEvent_t a, b; cudaStream_t st; const Chunk& c; int n, ms, mf; const NDPlan* p;
+        ~ChunkTimer() {
+          if (!a) return;
+          cudaEventRecord(b, st);
+          cudaEventSynchronize(b);
+          float ms_ = 0;
+          cudaEventElapsedTime(&ms_, a, b);
+          double fl = 0;
+          for (int t = c.t0; t < c.t1; ++t) fl += 8.0 * (double)p->fronts[t].s * p->fronts[t].f * p->fronts[t].f;
+          fprintf(stderr, "[hh factor] lean m=%d level %d chunk: %d fronts max_s=%d max_f=%d %.3f ms %.2f TFLOP/s\n",
+                  p->m, c.level, n, ms, mf, ms_, fl / (ms_ * 1e-3) / 1e12);
+          cudaEventDestroy(a); cudaEventDestroy(b);
+        }
+      } ctimer{ce0, ce1, s, ch, cnt, ms, mf, nd};
       {
         const unsigned gx = (unsigned)std::min<int64_t>(8192, (ch.Wcount + 255) / 256);
         k_nd_zero<<<dim3(gx, 1), 256, 0, s>>>(W, 0, 0, ch.Wcount);
