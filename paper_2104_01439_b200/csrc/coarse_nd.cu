@@ -1845,7 +1845,7 @@ static hh_status flow_launch(const NDPlan* nd, const SolveArgs& A, int B, int L0
 }
 
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                           VArg x, cudaStream_t s, SolveCfg c, bool shareF) {
+                           VArg x, cudaStream_t s, SolveCfg c, bool shareF, bool conc) {
   const int nlev = (int)nd->levels.size();
   // HH_ND_LEVEL_TIMING=1: per-level event timing (diagnostics; synchronises, never in graphs)
   static const bool lt = getenv("HH_ND_LEVEL_TIMING") != nullptr;
@@ -1876,7 +1876,9 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
   A.vmax = nd_vmax();
   static const int pf = getenv("HH_NO_PREFETCH") ? 0 : 1;
-  A.prefetch = pf;
+  // L2 bulk prefetch of the next level's factor rows: pays for a single solve, but
+  // beside other streams it only adds L2/HBM contention (sweep 0.369 -> 0.362 s without)
+  A.prefetch = pf && !conc;
   if (nd->lean) {   // no stored -H^T rows: transposed forward, then the per-level backward
     c.sub_cut = -1;
     c.split = nlev - 1;
@@ -1996,7 +1998,7 @@ hh_status nd_flow_reset(const NDPlan* nd, int B, cplx* work, cudaStream_t s) {
 hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                    VArg x, cudaStream_t s, bool shareF, bool conc) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
-  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B, conc), shareF);
+  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B, conc), shareF, conc);
 }
 
 // Empirical schedule choice on the real factor (called once per (tree, B) at
@@ -2012,9 +2014,9 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   HH_CUDA_TRY(cudaEventCreate(&e0));
   HH_CUDA_TRY(cudaEventCreate(&e1));
   auto run = [&](SolveCfg c, float* ms) -> hh_status {
-    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF));   // warm
+    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));   // warm
     HH_CUDA_TRY(cudaEventRecord(e0, s));
-    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF));
+    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));
     HH_CUDA_TRY(cudaEventRecord(e1, s));
     HH_CUDA_TRY(cudaEventSynchronize(e1));
     HH_CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
