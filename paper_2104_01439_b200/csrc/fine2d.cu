@@ -25,6 +25,9 @@
 
 namespace {
 
+#ifndef FINE_CONST_MINB
+#define FINE_CONST_MINB 4   // CTAs per SM the constant-k smoothers are compiled for
+#endif
 #ifndef FINE_DI_GLOBAL
 #define FINE_DI_GLOBAL 0   // 1: heterogeneous D^{-1} read through L1 instead of staged in smem (measured: no gain)
 #endif
@@ -306,7 +309,7 @@ __device__ __forceinline__ cplx dinv_at(const cplx* sDi, const cplx* dg, int si,
 // NUC > 0: nu fixed at compile time (region sizes, smem strides and the step
 // loop fold to constants); NUC = 0: nu from P.
 template <bool HET, int NUC>
-__global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : 4) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
+__global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MINB) k_pre2d(FineK P, VArg f, SArg fs, VArg uo, VArg rco) {
   const int b = blockIdx.z;
   extern __shared__ double4 smem_raw[];
   const int n = P.n, nu = NUC > 0 ? NUC : P.nu;
@@ -396,7 +399,7 @@ __host__ __device__ constexpr int post_ch(int R) { return TY / 2 + R + CW_EXTRA;
 // ------------------------------------- prolongation + correction + post-smoothing
 // z = S^nu(u + I ec; f); if w: w = A_0 z.  Halo R = nu + (w ? 1 : 0).
 template <bool HET, bool WITH_W, int NUC>
-__global__ void __launch_bounds__(NT, HET ? 3 : 4) k_post2d(FineK P, VArg f, SArg fs, VArg uin, VArg ecin,
+__global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK P, VArg f, SArg fs, VArg uin, VArg ecin,
                                                             VArg zo, VArg wo) {
   const int b = blockIdx.z;
   extern __shared__ double4 smem_raw[];
