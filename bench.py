@@ -3,17 +3,19 @@
 iterations x DOF / s, complex fp64, and HBM GB/s vs peak).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload sweep|cfg0|cfg2|cfg3]
+                  [--workload sweep|search|cfg0|cfg2|cfg3|cfg4]
 
-Workloads (DESIGN.md "Measurement"):
-  sweep (default, BASELINE configs[1]): a step = this rank's fixed share of the
-        3,520-sample shift sweep (sample i goes to residue class i mod 8; rank r
-        of N takes class r, so per-GPU work is fixed and N = 8 covers the whole
-        sweep: weak scaling).  Every sample is set up, its coarse operator
+Workloads:
+  sweep (default, BASELINE configs[1]): a step = the WHOLE 3,520-sample shift
+        sweep.  At N ranks every rank takes a 1/N share: the samples sorted by
+        (grid size, shift strength beta k^sigma) are dealt round-robin, so every
+        rank gets the same mix of sizes and expected iteration counts (strong
+        scaling: total work fixed).  Every sample is set up, its coarse operator
         factored, and solved (point source, FGMRES(100), rtol 1e-6) inside the
-        step, as the paper's end-to-end times do.
-  cfg2 / cfg0 / cfg3: a step = setup + factorisation + one full solve of that
-        config on every rank (replicas; no collective).
+        step, as the paper's end-to-end times do; at N > 1 the
+        per-sample records are gathered to rank 0 inside the step.
+  cfg2 / cfg0 / cfg3 / cfg4: a step = setup + factorisation + one full solve of
+        that config (slab-decomposed over the ranks at N > 1).
 value = sum over ranks of iterations x fine DOFs / max-over-ranks device time.
 No oracle code runs on the product arm except the bounded cpu_baseline leg
 (rank 0, N = 1 only).
@@ -41,7 +43,6 @@ from workloads.configs import sweep_sample_spec  # noqa: E402
 METRIC = "preconditioned FGMRES iterations*DOF/s (complex fp64)"
 SEARCH_COUNT, SEARCH_LEVELS = 48, (4, 5, 6, 7, 8, 9)
 UNIT = "it*DOF/s"
-SHARD = 8   # sweep residue classes
 
 
 def peaks():
@@ -119,12 +120,26 @@ class Clocks:
 
 
 def rank_samples(rank, world):
-    """This rank's fixed share of the sweep: residue class `rank` of the sample id
-    mod 8 (per-GPU work is constant in N; N = 8 covers all 3,520 samples)."""
-    if world > SHARD:
-        raise ValueError(f"the sweep shards over at most {SHARD} ranks")
-    all_s = sweep_samples()
-    return [s for s in all_s if s["id"] % SHARD == rank % SHARD]
+    """This rank's 1/world share of the whole sweep: samples sorted by (grid
+    size n, shift strength beta k^sigma, id) are dealt round-robin, so every
+    rank gets the same mix of grid sizes and (expected) iteration counts;
+    world = 1 is the full 3,520-sample sweep."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    order = sorted(sweep_samples(), key=lambda s: (s["n"], s["beta"] * s["k"] ** s["sigma"], s["id"]))
+    return [s for p, s in enumerate(order) if p % world == rank]
+
+
+def gather_records(res, world):
+    """Per-sample records of every rank, gathered to all ranks (one
+    all_gather_object; the only data exchange of the sweep), sorted by id."""
+    recs = [(r["id"], r["status"], r["iterations"], r["converged"], r["rel_res_true"], r["rho"])
+            for r in res]
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, recs)
+        recs = [x for part in allr for x in part]
+    return sorted(recs)
 
 
 def combine_ranks(dev_ms, dofs, its, world, device):
@@ -163,6 +178,7 @@ def run_ours(args, rank, world, dev):
     if args.workload == "sweep":
         samples = rank_samples(rank, world)
         o = hh.opts(restart=100, rtol=1e-6, max_iters=500)
+        gathered = {"recs": None}
 
         def step():
             res = hh.sweep(samples, o=o)
@@ -171,10 +187,13 @@ def run_ours(args, rank, world, dev):
             bad = [r for r in res if r["status"] != 0]
             if bad:
                 raise RuntimeError(f"sweep sample failed: {bad[0]}")
+            gathered["recs"] = gather_records(res, world)   # inside the step
             return its, dofs, res
 
-        wl = {"workload": "cfg1 shift sweep (BASELINE configs[1])", "samples_per_rank": len(samples),
-              "samples_total": len(samples) * world, "restart": 100, "rtol": 1e-6,
+        wl = {"workload": "cfg1 shift sweep (BASELINE configs[1]), all 3,520 samples",
+              "samples_per_rank": len(samples), "samples_total": len(sweep_samples()),
+              "sharding": "samples sorted by (n, beta k^sigma) dealt round-robin over ranks",
+              "restart": 100, "rtol": 1e-6,
               "l2": "per-sample working sets are L2-resident; L2 flushed (512 MB write) between steps"}
     elif args.workload == "search":
         from workloads.configs import search_rhs, search_samples
@@ -218,7 +237,7 @@ def run_ours(args, rank, world, dev):
                     timers["acc"] = t
                 else:
                     for ph in hh.PHASES:
-                        for key in ("ms", "bytes", "launches", "bytes_all"):
+                        for key in ("ms", "bytes", "launches", "bytes_all", "model", "model_all"):
                             timers["acc"][ph][key] += t[ph][key]
                     timers["acc"]["launches"] += t["launches"]
             gp.close()
@@ -262,6 +281,10 @@ def run_ours(args, rank, world, dev):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     print("step ms: " + " ".join(f"{x:.1f}" for x in step_ms), file=sys.stderr)
     dev_ms = sum(step_ms)
+    rank_ms = [dev_ms]
+    if world > 1:   # per-rank device time (load balance of the shards)
+        rank_ms = [None] * world
+        dist.all_gather_object(rank_ms, dev_ms)
     if args.workload in ("sweep", "search"):
         tm = hh.sweep_timers(0)
     else:
@@ -271,11 +294,25 @@ def run_ours(args, rank, world, dev):
     value = tot_dofs / (dev_ms * 1e-3)
     out = {"value": value, "ms_per_step": dev_ms / args.steps, "wl": wl, "timers": tm,
            "clocks": clocks, "iterations_total": int(tot_its)}
+    if world > 1:
+        wl["rank_ms_per_step"] = [round(x / args.steps, 2) for x in rank_ms]
+    if args.workload == "sweep":
+        recs = gathered["recs"]
+        wl["records_gathered"] = len(recs)
+        wl["records_converged"] = sum(1 for r in recs if r[3])
+        if rank == 0 and args.records:
+            with open(args.records, "w") as fh:
+                for r in recs:
+                    fh.write(json.dumps({"id": r[0], "status": r[1], "iterations": r[2], "converged": r[3],
+                                         "rel_res_true": r[4], "rho": r[5]}) + "\n")
     # e2e: same metric through the public API with host-side inputs/outputs each step
     if args.workload in ("sweep", "search"):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         its, dofs, _ = step()          # hh_sweep / hh_shift_search: host inputs in, host records out
         e2e_s = time.perf_counter() - t0
+        e2e_s, dofs, _ = combine_ranks(e2e_s, dofs, its, world, dev)
         h2d = len(samples) * (40 + 16)
         if args.workload == "search":
             h2d = sum(16 * (x["n"] + 1) ** 2 for x in samples) * 12   # rhs per evaluation
@@ -295,32 +332,103 @@ def run_ours(args, rank, world, dev):
             e2e_s = combine_ranks(e2e_s, 0.0, 0.0, world, dev)[0]
         kb = 0 if spec.k_fine is None else 8 * (spec.k_fine.size + spec.k_coarse.size)
         out["e2e"] = {"value": r["iterations"] * spec.n_nodes / e2e_s, "unit": UNIT,
-                      "h2d_bytes_per_step": 16 * bh.size + kb,
+                      "h2d_bytes_per_step": 32 * bh.size + kb,     # b and x0, k_e arrays
                       "d2h_bytes_per_step": 16 * bh.size}
+    if rank == 0 and world == 1 and not args.no_cold:
+        out["e2e"]["cold"] = cold_probe(args)
     return out
 
 
+def cold_probe(args):
+    """One step of the same workload through the public API in a FRESH process
+    (no ND plans, autotuned schedules, engines or device block caches yet):
+    the first-call end-to-end time a new user sees (CUDA context creation
+    excluded, timed from the first hh call)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--cold-probe", "--workload", args.workload]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+        return json.loads(line)
+    except Exception as e:   # reported, never fatal
+        return {"error": f"{type(e).__name__}: {e}"[:200]}
+
+
+def run_cold_probe(args):
+    import paper_2104_01439_b200.hh as hh
+    torch.cuda.set_device(0)
+    torch.zeros(1, device="cuda")                     # CUDA context outside the timed region
+    torch.cuda.synchronize()
+    if args.workload == "sweep":
+        samples = rank_samples(0, 1)
+        t0 = time.perf_counter()
+        res = hh.sweep(samples, o=hh.opts(restart=100, rtol=1e-6, max_iters=500))
+        dt = time.perf_counter() - t0
+        dofs = sum(r["iterations"] * (s["n"] + 1) ** 2 for r, s in zip(res, samples))
+        what = f"hh_sweep of all {len(samples)} samples, first call in a fresh process"
+    else:
+        spec = config_spec(args.workload)
+        bh = np.ascontiguousarray(spec.rhs())
+        xh = np.zeros_like(bh)
+        t0 = time.perf_counter()
+        gp = hh.Problem.from_spec(spec)
+        r = gp.fgmres_solve_host(bh, xh, hh.opts(restart=spec.restart, rtol=spec.rtol))
+        gp.close()
+        dt = time.perf_counter() - t0
+        dofs = r["iterations"] * spec.n_nodes
+        what = "setup + factor + host-buffer solve, first call in a fresh process"
+    print(json.dumps({"value": dofs / dt, "unit": UNIT, "seconds": dt, "what": what}))
+
+
 # ------------------------------------------------------------------ oracle (CPU)
+def _oracle_sweep_sample(s):
+    """One cfg1 sample through the oracle (a pool worker): setup + LU + solve."""
+    from oracle.solve import OracleProblem
+    _, rep = OracleProblem(sweep_sample_spec(s)).solve()
+    return rep.iterations, rep.iterations * (s["n"] + 1) ** 2
+
+
 def oracle_rate(args, budget_s):
     """The oracle as it stands on this host's cores, on a bounded sample of the
-    same workload: returns (it*DOF/s, description, cores)."""
+    same workload: returns (it*DOF/s, description, cores, seconds)."""
     from oracle.solve import OracleProblem
     cores = len(os.sched_getaffinity(0))
     if args.workload == "sweep":
-        samples = rank_samples(0, 1)
-        order = sorted(samples, key=lambda s: s["n"])[:: max(1, len(samples) // 40)]
+        # sample-parallel over all host cores (one sample per process, SURVEY 8(d)):
+        # every 7th sample of the (n, shift strength)-sorted sweep, in a seeded
+        # shuffled order; samples still running when the budget ends are dropped
+        import multiprocessing as mp
+        order = rank_samples(0, 1)[::7]
+        np.random.default_rng(0).shuffle(order)
+        saved = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+        for k in saved:
+            os.environ[k] = "1"
         t0 = time.perf_counter()
         dofs = its = done = 0
-        for s in order:
-            _, rep = OracleProblem(sweep_sample_spec(s)).solve()
-            dofs += rep.iterations * (s["n"] + 1) ** 2
-            its += rep.iterations
-            done += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        dt = time.perf_counter() - t0
-        return dofs / dt, (f"{done} samples of rank 0's sweep share (size-stratified), "
-                           f"setup+factor+solve each, {its} iterations in {dt:.1f} s"), cores, dt
+        pool = mp.get_context("spawn").Pool(cores)
+        try:
+            it = pool.imap_unordered(_oracle_sweep_sample, order, chunksize=1)
+            while True:
+                left = budget_s - (time.perf_counter() - t0)
+                if left <= 0:
+                    break
+                try:
+                    a, d = it.next(timeout=left)
+                except (StopIteration, mp.TimeoutError):
+                    break
+                its += a
+                dofs += d
+                done += 1
+        finally:
+            dt = time.perf_counter() - t0
+            pool.terminate()
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        return dofs / dt, (f"{done} cfg1 samples (every 7th of the (n, shift)-sorted sweep, shuffled) "
+                           f"finished in {dt:.1f} s by a pool of {cores} single-threaded processes, "
+                           f"setup+factor+solve each, {its} iterations"), cores, dt
     if args.workload == "search":
         from oracle.shift_search import search_sample
         from workloads.configs import search_rhs, search_sample_spec, search_samples
@@ -348,6 +456,67 @@ def oracle_rate(args, budget_s):
                                                  f"({rep.iterations} its) in {dt:.1f} s"), cores, dt
 
 
+PHASE_KERNELS = {"pre": "k_pre2d / k_pre3d (fused 2x Jacobi + residual + I^T restriction)",
+                 "coarse": "nd_solve (k_nd_* forward/backward GEMV sweeps of one coarse solve)",
+                 "post": "k_post2d / k_post3d (fused I e_c + 2x Jacobi + A_0 apply)",
+                 "krylov": "k_mdot + k_update (CGS multi-dot, update + norm + Givens)"}
+
+
+def measured_traffic(workload):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of each phase's
+    kernels for this workload, from the committed capture summary
+    (profiles/r02/traffic.json, written by scripts/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "r02", "traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except Exception:
+        return None
+
+
+def roofline(tm, out, args, peak, peak_kind):
+    """Per-phase HBM rates from the sampled CUDA-event phase timers:
+    algorithmic bytes = SURVEY.md 8(d)'s per-step model ("model": every Jacobi
+    step, transfer and apply a separate pass), next to our fused kernels'
+    compulsory bytes ("fused")."""
+    phases = {}
+    for ph in ("pre", "coarse", "post", "krylov"):
+        d = tm[ph]
+        if d["ms"] > 0 and d["launches"] > 0:
+            sec = d["ms"] * 1e-3
+            phases[ph] = {"ms": d["ms"], "launches": int(d["launches"]), "avg_us": 1e3 * d["ms"] / d["launches"],
+                          "model_bytes_per_launch": d["model"] / d["launches"],
+                          "fused_bytes_per_launch": d["bytes"] / d["launches"],
+                          "achieved_gbs": d["model"] / sec / 1e9, "frac": d["model"] / sec / 1e9 / peak,
+                          "fused_gbs": d["bytes"] / sec / 1e9, "fused_frac": d["bytes"] / sec / 1e9 / peak}
+    if not phases:
+        return None
+    dom = max(phases, key=lambda k: phases[k]["ms"])
+    tot_ms = sum(v["ms"] for v in phases.values())
+    step_s = out["ms_per_step"] * 1e-3
+    for ph, v in phases.items():
+        # concurrent sweep streams overlap launches, so per-launch durations overstate
+        # each kernel's exclusive cost: also split the step's wall time over the phases
+        # in proportion to their summed sampled device time (setup included: a lower bound)
+        ba = tm[ph].get("model_all", 0.0) / args.steps
+        if ba > 0 and tot_ms > 0:
+            v["wall_share_frac"] = ba / (step_s * v["ms"] / tot_ms) / 1e9 / peak
+    ball = sum(tm[ph].get("model_all", 0.0) for ph in phases) / args.steps
+    fall = sum(tm[ph].get("bytes_all", 0.0) for ph in phases) / args.steps
+    agg = {"model_bytes_per_step": ball, "fused_bytes_per_step": fall,
+           "frac": ball / step_s / 1e9 / peak, "fused_frac": fall / step_s / 1e9 / peak,
+           "note": "bytes of every iteration / whole step time (setup and factorisation included)"}
+    tr = measured_traffic(args.workload)
+    p = phases[dom]
+    return {"bound": "hbm", "kernel": PHASE_KERNELS[dom], "phase": dom, "achieved": p["achieved_gbs"],
+            "peak": peak, "unit": "GB/s", "frac": p["frac"],
+            "traffic": (tr or {}).get(dom, {}).get("dram_bytes_per_launch"),
+            "traffic_source": (tr or {}).get("source"),
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+            "bytes_model": "SURVEY.md 8(d) per-step model bytes per launch (fused kernels' compulsory "
+                           "bytes alongside as fused_*); DESIGN.md section 6",
+            "frac_wall_share": p.get("wall_share_frac"), "phases": phases, "aggregate": agg}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -356,7 +525,13 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="sweep", choices=["sweep", "search", "cfg0", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cold", action="store_true", help="skip the fresh-process first-call e2e")
+    ap.add_argument("--records", default=None, help="write the sweep's gathered per-sample records (JSONL)")
+    ap.add_argument("--cold-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cold_probe:
+        run_cold_probe(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -365,7 +540,8 @@ def main():
         # reference arm = the CPU oracle (no installable reference exists)
         if rank != 0:
             return
-        budget = 20.0
+        # each step a bounded sample, sized so that the whole run ends within minutes
+        budget = float(min(20.0, max(5.0, 150.0 / max(1, args.steps + args.warmup))))
         vals = []
         for _ in range(args.warmup):
             oracle_rate(args, budget / 4)
@@ -378,7 +554,7 @@ def main():
         v = float(np.mean(vals))
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
                 "data": "synthetic", "config": {"workload": args.workload, "oracle": "numpy/scipy CPU"},
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                  "sample": desc},
@@ -400,50 +576,11 @@ def main():
     tm = out["timers"]
     roof = None
     if tm:
-        names = {"pre": "k_pre2d (fused 2x Jacobi + residual + I^T restriction)",
-                 "coarse": "nd_solve (k_nd_fwd*/k_nd_bwd* GEMV chain, one coarse solve)",
-                 "post": "k_post2d (fused I e_c + 2x Jacobi + A_0 apply)",
-                 "krylov": "k_mdot + k_update (CGS multi-dot, update + norm + Givens)"}
-        phases = {}
-        for ph in ("pre", "coarse", "post", "krylov"):
-            d = tm[ph]
-            if d["ms"] > 0 and d["launches"] > 0:
-                gbs = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-                phases[ph] = {"ms": d["ms"], "launches": int(d["launches"]),
-                              "avg_us": 1e3 * d["ms"] / d["launches"],
-                              "bytes_per_launch": d["bytes"] / d["launches"],
-                              "achieved_gbs": gbs, "frac": gbs / peak}
-        dom = max(phases, key=lambda k: phases[k]["ms"]) if phases else None
-        ball = sum(tm[ph].get("bytes_all", 0.0) for ph in ("pre", "coarse", "post", "krylov"))
-        agg = None
-        if ball > 0:
-            gbs = ball / (out["ms_per_step"] * args.steps * 1e-3) / 1e9
-            agg = {"bytes_per_step": ball / args.steps, "achieved_gbs": gbs, "frac": gbs / peak,
-                   "note": "all algorithmic bytes of every iteration / whole step time (setup included)"}
-        tot_ms = sum(v["ms"] for v in phases.values())
-        step_s = out["ms_per_step"] * 1e-3
-        for ph, v in phases.items():
-            # concurrent streams overlap launches, so per-launch durations overstate
-            # each kernel's cost: split the step's wall time over the phases in
-            # proportion to their summed sampled device time (setup time is split
-            # over them too, so this is a lower bound on the rate)
-            ba = tm[ph].get("bytes_all", 0.0) / args.steps
-            if ba > 0 and tot_ms > 0:
-                g = ba / (step_s * v["ms"] / tot_ms) / 1e9
-                v["wall_share_gbs"] = g
-                v["wall_share_frac"] = g / peak
-        if dom:
-            p = phases[dom]
-            roof = {"bound": "hbm", "kernel": names[dom], "achieved": p["achieved_gbs"],
-                    "peak": peak, "unit": "GB/s", "frac": p["frac"], "traffic": None,
-                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                    "bytes_model": "algorithmic bytes per launch (DESIGN.md 'Roofline')",
-                    "frac_wall_share": p.get("wall_share_frac"),
-                    "phases": phases, "aggregate": agg}
+        roof = roofline(tm, out, args, peak, peak_kind)
     line = {"metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": out["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "weak" if args.workload == "sweep" or world == 1 else "strong",
+            "scaling": "weak" if args.workload == "search" else "strong",
             "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": out["wl"], "e2e": out["e2e"], "roofline": roof,
             "clocks": out["clocks"], "gpu_launches": int(tm["launches"]) if tm else None,

@@ -97,6 +97,12 @@ typedef struct {
   int32_t fixed_iters;          /* > 0: run exactly this many Arnoldi steps (parity at threshold) */
   double  rtol;                 /* stop when |g_{j+1}| <= rtol * ||b||                      */
   int32_t check_every;          /* host reads the device convergence flag every this many steps (>=1) */
+  /* Orthogonalisation of the Arnoldi step (PAPER.md:357-359 is silent; SURVEY 8(c)
+   * C11): 0 = single-pass classical Gram-Schmidt (default: one
+   * batched multi-dot pass + one update pass); 1 = selective re-orthogonalisation
+   * (DGKS): a second CGS pass whenever ||w'|| < ||w|| / sqrt(2); 2 = always two
+   * passes (CGS2).  Anything else: HH_E_CONFIG.                                  */
+  int32_t reorth;
 } hh_fgmres_opts;
 
 typedef struct {
@@ -157,16 +163,29 @@ hh_status hh_vcycle(hh_problem* p, const void* f, void* z);
 hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e);
 
 /* FGMRES(m) on A_0 x = b with right preconditioner one V-cycle
- * (PAPER.md:357-360).  b: device; x: device, in: ignored (x0 = 0), out:
- * solution.  res_hist: optional HOST array of max_iters+1 doubles receiving
- * |g_{j+1}|/||b|| per iteration (entry 0 = 1).  blocks. */
+ * (PAPER.md:357-360).  b: device; x: device, in: the initial guess x0 (the
+ * paper's u^(0); the BASELINE configs use x0 = 0, so pass zeros),
+ * out: solution.  r_0 = b - A_0 x0; the stopping threshold stays rtol ||b||
+ * and restarts recompute r = b - A_0 x (reading C14).  res_hist: optional HOST
+ * array of max_iters+1 doubles receiving |g_{j+1}|/||b|| per iteration (entry 0
+ * = 1).  Errors: HH_E_CONFIG (restart not in 1..max_restart,
+ * max_iters/fixed_iters out of range, reorth not in 0..2); HH_E_CUDA also when
+ * the coarse solve's dataflow schedule timed out (never a silent wrong
+ * result; the schedule is then disabled for the handle's grid).  blocks. */
 hh_status hh_fgmres_solve(hh_problem* p, const void* b, void* x, const hh_fgmres_opts* o,
                           hh_fgmres_report* r, double* res_hist);
 
-/* Same, with HOST b and x (complex128): the host<->device copies are part of
- * the call (end-to-end path).  blocks. */
+/* Same, with HOST b and x (complex128; x in: x0, out: solution): the
+ * host<->device copies are part of the call (end-to-end path).  blocks. */
 hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, void* x_host,
                                const hh_fgmres_opts* o, hh_fgmres_report* r);
+
+/* Orthogonality of the Arnoldi basis of the LAST cycle of the last solve on
+ * this handle (diagnostic; SURVEY 8(c) "FGMRES" pin):
+ * max_loss = max over a, c <= J of |<v_a, v_c> - delta_ac| for the normalised
+ * basis v_0..v_J (J = Arnoldi steps of that cycle; a zero last vector after a
+ * breakdown is excluded), nvec = J + 1.  HH_E_STATE for slab handles.  blocks. */
+hh_status hh_arnoldi_orthogonality(hh_problem* p, double* max_loss, int32_t* nvec);
 
 typedef struct {
   int64_t id;
@@ -237,19 +256,22 @@ hh_status hh_lfa_stats(int32_t reset, double* st4);
 hh_status hh_destroy_problem(hh_problem* p);
 
 /* Phase instrumentation for the bench roofline (device events around each
- * phase of every FGMRES iteration; enabling it adds one host sync per
- * iteration).  st16 = [ms x4, algorithmic HBM bytes x4, phase launches x4,
- * algorithmic HBM bytes of EVERY iteration x4] (the first three over the timed,
- * i.e. sampled, iterations)
- * for the phases [pre-smooth+restrict, coarse solve, prolong+post-smooth+A_0,
- * Krylov (multi-dot + update)], accumulated since the last reset. */
+ * phase of sampled FGMRES iterations; enabling it adds host syncs).
+ * st24 (24 doubles, caller-owned HOST array) = [ms x4, compulsory HBM bytes x4,
+ * phase launches x4, compulsory HBM bytes of EVERY iteration x4, SURVEY 8(d)
+ * model bytes x4, model bytes of EVERY iteration x4] (ms, bytes, launches,
+ * model over the timed, i.e. sampled, iterations) for the phases
+ * [pre-smooth+restrict, coarse solve, prolong+post-smooth+A_0, Krylov
+ * (multi-dot + update)], accumulated since the last reset.  "Compulsory" = each
+ * fused kernel reads its inputs and writes its outputs once; "model" = every
+ * Jacobi step / transfer / apply as its own pass. */
 hh_status hh_reset_timers(hh_problem* p, int32_t enable);
-hh_status hh_read_timers(hh_problem* p, double* st16, int64_t* launches);
+hh_status hh_read_timers(hh_problem* p, double* st24, int64_t* launches);
 
-/* Sweep-wide phase instrumentation (same st16 layout as hh_read_timers) and
+/* Sweep-wide phase instrumentation (same st24 layout as hh_read_timers) and
  * kernel-launch count since the last reset; reset_enable >= 0 resets and sets
  * timing on (1) / off (0); -1 only reads. */
-hh_status hh_sweep_timers(int32_t reset_enable, double* st16, int64_t* launches);
+hh_status hh_sweep_timers(int32_t reset_enable, double* st24, int64_t* launches);
 
 const char* hh_last_error(void);
 const char* hh_version(void);

@@ -31,6 +31,7 @@
 #include <numeric>
 #include <cooperative_groups.h>
 #include "hh_internal.cuh"
+#include "krylov.cuh"
 namespace cg = cooperative_groups;
 
 namespace {
@@ -78,6 +79,12 @@ struct LevelInfo {
 
 // Solve schedule: levels <= sub_cut run as one-CTA subtree walks, levels
 // (sub_cut, split] as per-level kernels, levels > split inside one cluster kernel.
+// wide backward levels with fronts of order > this (HH_ND_BWDK_F) use the K-split rows
+static int bwdk_f() {
+  static const int v = getenv("HH_ND_BWDK_F") ? atoi(getenv("HH_ND_BWDK_F")) : 1024;
+  return v;
+}
+
 struct SolveCfg { int sub_cut, split, flow = 0; };
 
 struct NDPlan {
@@ -115,6 +122,7 @@ struct NDPlan {
   int* d_lvbeg = nullptr;            // per level: first front
   std::mutex cut_mu;
   std::vector<std::pair<int, SolveCfg>> cfg_cache;   // (B, schedule) chosen by nd_autotune
+  bool flow_disabled = false;                          // a dataflow solve failed (nd_flow_disable)
   // lean storage
   bool lean = false;
   std::vector<Chunk> chunks;
@@ -476,6 +484,7 @@ struct SolveArgs {
   VArg rhs, x;
   int vmax;                        // fronts with f <= vmax stage their vectors in shared memory
   int prefetch;                    // L2 bulk prefetch of the factor rows before the PDL wait
+  int* fail;                       // dataflow failure flag when st == nullptr (see nd_solve)
 };
 
 // Programmatic dependent launch: a level kernel may start while its predecessor
@@ -927,8 +936,13 @@ __global__ void __launch_bounds__(256) k_nd_cluster(SolveArgs A, const int64_t* 
 // increment per finished CTA after a device fence; consumers poll with
 // ld.acquire and read the producers' values through L2 (__ldcg).  The forward
 // counters are cleared by the backward kernel and vice versa, so they are zero
-// again at the start of every solve.  A wait that exceeds ~1 s gives up and
-// raises g_flow_timeout (no hang; the autotuner then rejects the schedule).
+// again at the start of every solve.  A wait that exceeds max_polls polls
+// (~1 s by default; HH_ND_FLOW_POLLS) gives up and marks the SAMPLE failed:
+// st[b] = HHK_NDFAIL (the FGMRES driver then reports an error for it, resets
+// the counters and disables the schedule), or *fail when there is no status
+// array (hh_vcycle / hh_coarse_solve check it before returning; the autotuner
+// passes g_flow_timeout and rejects the schedule).  Later waits of the same
+// sample see the mark and give up at once; other samples are not affected.
 constexpr int FLOW_MAXL = 40;
 struct FlowArgs {
   int L0, nl;                    // flow levels [L0, L0 + nl)
@@ -937,6 +951,7 @@ struct FlowArgs {
   int nch[FLOW_MAXL];            // CTAs per front of level offset j (this direction)
   int64_t cnt_off;               // counters: (int*)(work[b] + cnt_off) (complex entries), [2][nfronts]
   int nfr;
+  unsigned max_polls;            // give up a dependency wait after this many polls
 };
 __device__ int g_flow_timeout = 0;
 
@@ -945,14 +960,22 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void flow_wait(const int* c, int target) {
+__device__ __forceinline__ void flow_wait(const int* c, int target, int* fail, int fail_code,
+                                          unsigned max_polls) {
   if (target <= 0) return;
+  if (max_polls == 0) { atomicExch(fail, fail_code); return; }   // HH_ND_FLOW_POLLS=0: fault injection (tests)
   unsigned polls = 0;
   while (ld_acquire(c) < target) {
+    if (*(volatile int*)fail) break;                                     // this sample already failed
+    if (++polls > max_polls) { atomicExch(fail, fail_code); break; }
     __nanosleep(64);
-    if (++polls > (1u << 24)) { atomicExch(&g_flow_timeout, 1); break; }
-    if ((polls & 1023u) == 0 && *(volatile int*)&g_flow_timeout) break;   // another wait gave up
   }
+}
+// failure flag of sample b: its Krylov status, else the solve's flag
+__device__ __forceinline__ int* flow_fail(const SolveArgs& A, int b, int& code) {
+  if (A.st) { code = HHK_NDFAIL; return const_cast<int*>(A.st) + b; }
+  code = 1;
+  return A.fail ? A.fail : &g_flow_timeout;
 }
 __device__ __forceinline__ int* flow_cnt(const SolveArgs& A, const FlowArgs& W, int b) {
   return reinterpret_cast<int*>(A.work + (int64_t)b * A.WE + W.cnt_off);
@@ -996,7 +1019,9 @@ __global__ void __launch_bounds__(LT) k_nd_flow_fwd(SolveArgs A, FlowArgs W, con
       const int cc = q ? ch.y : ch.x;
       if (cc < 0) continue;
       const int jc = A.fr[cc].level - W.L0;
-      if (jc >= 0) flow_wait(cnt + cc, W.nch[jc]);
+      int code;
+      int* fl = flow_fail(A, b, code);
+      if (jc >= 0) flow_wait(cnt + cc, W.nch[jc], fl, code, W.max_polls);
     }
     __threadfence();
   }
@@ -1045,7 +1070,9 @@ __global__ void __launch_bounds__(LT) k_nd_flow_bwd(SolveArgs A, FlowArgs W, con
     if (c == 0) cnt[t] = 0;                  // forward counter of t, for the next solve's forward
     if (m.parent >= 0) {
       const int jp = A.fr[m.parent].level - W.L0;
-      if (jp < W.nl) flow_wait(cnt + W.nfr + m.parent, W.nch[jp]);
+      int code;
+      int* fl = flow_fail(A, b, code);
+      if (jp < W.nl) flow_wait(cnt + W.nfr + m.parent, W.nch[jp], fl, code, W.max_polls);
     }
     __threadfence();
   }
@@ -1336,7 +1363,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
       Koff[t] = ko;
       ko += (int64_t)((nd->fronts[t].f + 2047) / 2048) * nd->fronts[t].s;
     }
-    if (li.max_f > 1024) nd->Kmax = std::max(nd->Kmax, ko);
+    if (li.max_f > bwdk_f()) nd->Kmax = std::max(nd->Kmax, ko);
   }
   // lean storage for trees whose full fronts would not fit (3D coarse grids of
   // cfg4 size); HH_ND_LEAN=0/1 overrides, HH_ND_WMAX sets the workspace (entries)
@@ -1753,6 +1780,7 @@ static SolveCfg get_cfg(NDPlan* nd, int B, bool conc) {
   if (const char* e = getenv("HH_ND_SPLIT")) c.split = std::min<int>(atoi(e), c.split);
   if (const char* e = getenv("HH_ND_CUT")) c.sub_cut = std::min<int>(atoi(e), c.split);
   if (const char* e = getenv("HH_ND_FLOW")) c.flow = atoi(e);
+  if (nd->flow_disabled) c.flow = 0;
   if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT")) return c;
   SolveCfg cc;
   if (cached_cfg(nd, cfg_key(B, conc), &cc)) return cc;
@@ -1819,6 +1847,10 @@ static hh_status flow_launch(const NDPlan* nd, const SolveArgs& A, int B, int L0
   W.L0 = L0; W.nl = L1 - L0 + 1;
   W.cnt_off = flow_cnt_off(nd);
   W.nfr = (int)nd->fronts.size();
+  {
+    const char* e = getenv("HH_ND_FLOW_POLLS");   // 0: every wait fails (fault injection for tests)
+    W.max_polls = e ? (unsigned)strtoul(e, nullptr, 10) : (1u << 24);
+  }
   int maxf = 1;
   for (int j = 0; j < W.nl; ++j) {
     const LevelInfo& li = nd->levels[L0 + j];
@@ -1845,7 +1877,7 @@ static hh_status flow_launch(const NDPlan* nd, const SolveArgs& A, int B, int L0
 }
 
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                           VArg x, cudaStream_t s, SolveCfg c, bool shareF, bool conc) {
+                           VArg x, cudaStream_t s, SolveCfg c, bool shareF, bool conc, int* fail = nullptr) {
   const int nlev = (int)nd->levels.size();
   // HH_ND_LEVEL_TIMING=1: per-level event timing (diagnostics; synchronises, never in graphs)
   static const bool lt = getenv("HH_ND_LEVEL_TIMING") != nullptr;
@@ -1875,6 +1907,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
   A.F = F; A.FE = shareF ? 0 : nd->F_entries;
   A.work = work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
   A.vmax = nd_vmax();
+  A.fail = fail;
   static const int pf = getenv("HH_NO_PREFETCH") ? 0 : 1;
   // L2 bulk prefetch of the next level's factor rows: pays for a single solve, but
   // beside other streams it only adds L2/HBM contention (sweep 0.369 -> 0.362 s without)
@@ -1955,7 +1988,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
       dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
       HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
-      if (li.max_f > 1024 && !getenv("HH_NO_BWDK")) {   // long rows: K-split over column chunks
+      if (li.max_f > bwdk_f() && !getenv("HH_NO_BWDK")) {   // long rows: K-split over column chunks
         const int ncb = (li.max_f + KC - 1) / KC, nrb = (li.max_s + KR - 1) / KR;
         const int64_t KE = nd->w_entries + nd->out_entries + (nd->lean ? nd->Pmax : 0);
         HH_TRY(launch_pdl(k_nd_bwdK, dim3(nrb * ncb, li.count, B), LT, 0, s, A, li.begin, ncb,
@@ -1996,9 +2029,22 @@ hh_status nd_flow_reset(const NDPlan* nd, int B, cplx* work, cudaStream_t s) {
 }
 
 hh_status nd_solve(const NDPlan* ndc, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s, bool shareF, bool conc) {
+                   VArg x, cudaStream_t s, bool shareF, bool conc, int* fail) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
-  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B, conc), shareF, conc);
+  return solve_cfg(nd, B, st, F, work, rhs, x, s, get_cfg(nd, B, conc), shareF, conc, fail);
+}
+
+bool nd_solve_uses_flow(const NDPlan* ndc, int B, bool conc) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  const SolveCfg c = get_cfg(nd, B, conc);
+  return c.flow && !nd->lean && flow_ok(nd, c.sub_cut, c.split);
+}
+
+void nd_flow_disable(const NDPlan* ndc) {
+  NDPlan* nd = const_cast<NDPlan*>(ndc);
+  std::lock_guard<std::mutex> lk(nd->cut_mu);
+  nd->flow_disabled = true;
+  for (auto& e : nd->cfg_cache) e.second.flow = 0;
 }
 
 // Empirical schedule choice on the real factor (called once per (tree, B) at
@@ -2047,7 +2093,7 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   // for concurrent sweep workers only on trees of at least HH_ND_FLOW_CONC_M coarse
   // nodes per side (default: never -- waiting CTAs hold SM slots other streams need)
   static const int flow_conc_m = getenv("HH_ND_FLOW_CONC_M") ? atoi(getenv("HH_ND_FLOW_CONC_M")) : (1 << 30);
-  if (!conc || nd->m >= flow_conc_m) {
+  if ((!conc || nd->m >= flow_conc_m) && !nd->flow_disabled) {
     SolveCfg cands[2] = {best, best};
     cands[0].flow = 1;
     cands[1].flow = 1;

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <new>
 #include <thread>
+#include <tuple>
 #include <vector>
 #include "hh_internal.cuh"
 #include "krylov.cuh"
@@ -243,15 +244,18 @@ struct Pool {
 };
 
 // ND plans are shared by every engine (tree depends on (dim, m) only)
+// (per device: a plan holds device arrays of the device current at creation)
 std::mutex g_plan_mu;
-std::map<std::pair<int, int>, NDPlan*> g_plans;
+std::map<std::tuple<int, int, int>, NDPlan*> g_plans;   // (device, dim, m)
 hh_status get_plan(int dim, int m, NDPlan** out) {
+  int dev = 0;
+  HH_CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto it = g_plans.find({dim, m});
+  auto it = g_plans.find({dev, dim, m});
   if (it != g_plans.end()) { *out = it->second; return HH_OK; }
   NDPlan* p = nullptr;
   HH_TRY(nd_plan_create(dim, m, &p));
-  g_plans[{dim, m}] = p;
+  g_plans[{dev, dim, m}] = p;
   *out = p;
   return HH_OK;
 }
@@ -326,6 +330,7 @@ struct Engine {
   KArgs ka;
   int* jdev = nullptr;
   int* nd_flag = nullptr;
+  int* flow_fail = nullptr;  // dataflow coarse-solve failure flag of the status-less calls
   double setup_s = 0;
   // graph of one iteration
   cudaGraphExec_t gexec = nullptr;     // plain iteration
@@ -343,6 +348,8 @@ struct Engine {
   double acc_ms[T_NT] = {0, 0, 0, 0};
   double acc_bytes[T_NT] = {0, 0, 0, 0};      // timed (sampled) iterations
   double acc_bytes_all[T_NT] = {0, 0, 0, 0};  // every iteration (aggregate throughput)
+  double acc_model[T_NT] = {0, 0, 0, 0};      // SURVEY 8(d) per-step model bytes, timed iterations
+  double acc_model_all[T_NT] = {0, 0, 0, 0};  // ... every iteration
   double acc_launch[T_NT] = {0, 0, 0, 0};
   int64_t launches = 0;
   int64_t launches_per_iter = 0;
@@ -396,7 +403,8 @@ size_t ksmall_bytes(int B, int m) {
   const size_t ldv = m + 1, ldh = m + 1;
   auto r = [](size_t b) { return (b + 255) / 256 * 256; };
   return r(B * ldv * 8) * 2 + r(B * ldv * 16) * 3 + r((size_t)B * m * ldh * 16) + r(B * 8) * 3 +
-         r(B * 4) * 3 + r(16) + r(B * 4) * 2 + r(B * (ldv + 1) * 16) + r(B * 8);
+         r(B * 4) * 3 + r(16) + r(B * 4) * 2 + r(B * (ldv + 1) * 16) + r(B * 8) + r(B * 8) + r(B * 4) * 2 +
+         r(16);
 }
 
 // Grow the engine's pools to hold batch `sp` (no-op when already large enough).
@@ -566,7 +574,8 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
                o_g = carve(B * ldv * 16), o_y = carve(B * ldv * 16), o_H = carve((size_t)B * m * ldh * 16),
                o_bn = carve(B * 8), o_res = carve(B * 8), o_rt = carve(B * 8), o_st = carve(B * 4),
                o_its = carve(B * 4), o_je = carve(B * 4), o_j = carve(16), o_fl = carve(B * 4),
-               o_cnt = carve(B * 4), o_red = carve(B * (ldv + 1) * 16), o_red2 = carve(B * 8);
+               o_cnt = carve(B * 4), o_red = carve(B * (ldv + 1) * 16), o_red2 = carve(B * 8),
+               o_wn = carve(B * 8), o_reo = carve(B * 4), o_jl = carve(B * 4), o_ff = carve(16);
   HH_TRY(E.ksmall.ensure(off));
   HH_TRY(E.cpart.ensure((size_t)B * E.nblk * (m + 2) * 16));
   HH_TRY(E.dpart.ensure((size_t)B * E.nblk * 8));
@@ -594,7 +603,10 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   A.ks.bnorm = (double*)(base + o_bn); A.ks.res = (double*)(base + o_res);
   A.ks.rtrue = (double*)(base + o_rt); A.ks.status = (int*)(base + o_st);
   A.ks.its = (int*)(base + o_its); A.ks.jend = (int*)(base + o_je); A.ks.hist = E.hist.as<double>();
+  A.ks.jlast = (int*)(base + o_jl);
+  A.wnorm2 = (double*)(base + o_wn); A.reo = (int*)(base + o_reo);
   E.nd_flag = (int*)(base + o_fl);
+  E.flow_fail = (int*)(base + o_ff);
   HH_CUDA_TRY(cudaMemsetAsync(E.ksmall.p, 0, off, E.s));
   prof_mark(E, "pools+coef", tp);
   // precomputed D^{-1} of the heterogeneous fine operator (read by the smoothers)
@@ -633,20 +645,42 @@ VArg vfine(Engine& E, Pool& p) { return varg(p.as<cplx>() + E.FL.pad, E.FL.strid
 bool slab_mode(const Engine& E) { return E.spec.slabmode; }
 // coarse solve on all entries (shared factor in slab mode)
 hh_status coarse_solve_all(Engine& E, const int* st, VArg rhs, VArg x) {
-  return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E), E.conc);
+  return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E), E.conc,
+                  E.flow_fail);
+}
+// after a dataflow coarse-solve failure: zero the counters, never use the schedule again
+hh_status flow_recover(Engine& E) {
+  HH_TRY(nd_flow_reset(E.plan, E.B, E.work.as<cplx>(), E.s));
+  HH_CUDA_TRY(cudaMemsetAsync(E.flow_fail, 0, sizeof(int), E.s));
+  HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  nd_flow_disable(E.plan);
+  E.drop_graphs();
+  return HH_OK;
+}
+// status-less calls (hh_vcycle, hh_coarse_solve): when the dataflow schedule ran,
+// read its failure flag before returning (these calls then block)
+hh_status flow_check(Engine& E, bool used) {
+  if (!used) return HH_OK;
+  int f = 0;
+  HH_CUDA_TRY(cudaMemcpyAsync(&f, E.flow_fail, sizeof(int), cudaMemcpyDeviceToHost, E.s));
+  HH_CUDA_TRY(cudaStreamSynchronize(E.s));
+  if (!f) return HH_OK;
+  HH_TRY(flow_recover(E));
+  hh_set_error("coarse solve: a dataflow dependency wait timed out (schedule disabled; retry the call)");
+  return HH_E_CUDA;
 }
 // Arnoldi reductions of the slab mode: partials -> (NCCL allreduce) -> finish on every entry
-hh_status krylov_mdot_all(Engine& E) {
-  HH_TRY(krylov_mdot(E.ka, E.B, E.s));
+hh_status krylov_mdot_all(Engine& E, int pass) {
+  HH_TRY(krylov_mdot(E.ka, E.B, E.s, pass));
   if (!slab_mode(E)) return HH_OK;
   HH_TRY(slab_allreduce(E.X, (double*)E.ka.red, (size_t)2 * E.ka.ldr * E.B, E.s));
-  return krylov_mdot_fin(E.ka, E.B, E.s);
+  return krylov_mdot_fin(E.ka, E.B, E.s, pass);
 }
-hh_status krylov_update_all(Engine& E) {
-  HH_TRY(krylov_update(E.ka, E.B, E.s));
+hh_status krylov_update_all(Engine& E, int pass) {
+  HH_TRY(krylov_update(E.ka, E.B, E.s, pass));
   if (!slab_mode(E)) return HH_OK;
   HH_TRY(slab_allreduce(E.X, E.ka.red2, (size_t)E.B, E.s));
-  return krylov_update_fin(E.ka, E.B, E.s);
+  return krylov_update_fin(E.ka, E.B, E.s, pass);
 }
 hh_status krylov_norm_all(Engine& E, VArg r, int mode) {
   HH_TRY(krylov_norm(E.ka, E.B, r, mode, E.s));
@@ -677,8 +711,12 @@ hh_status enqueue_iteration(Engine& E, bool timing) {
                    vflat(E.ec, E.Nc), vZ(E), vfine(E, E.w), s));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[5], s, cudaEventRecordExternal));
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[6], s, cudaEventRecordExternal));
-  HH_TRY(krylov_mdot_all(E));
-  HH_TRY(krylov_update_all(E));
+  HH_TRY(krylov_mdot_all(E, 1));
+  HH_TRY(krylov_update_all(E, 1));
+  if (E.ka.reorth) {   // second CGS pass (samples with reo[b] = 1 only)
+    HH_TRY(krylov_mdot_all(E, 2));
+    HH_TRY(krylov_update_all(E, 2));
+  }
   if (timing) HH_CUDA_TRY(cudaEventRecordWithFlags(E.ev[7], s, cudaEventRecordExternal));
   HH_TRY(krylov_advance(E.jdev, -1, s));
   return HH_OK;
@@ -691,7 +729,8 @@ int64_t launches_per_iteration(const Engine& E) {
     const bool multi = E.X.comm && E.X.comm->nranks > 1;
     slab = 2 * ((E.B > 1 ? 1 : 0) + (multi ? 2 : 0)) + (E.B > 1 ? 1 : 0) + 2;
   }
-  return fine + nd_solve_launches(E.plan, E.B, E.conc) + 3 + slab;
+  const int kry = E.ka.reorth ? 4 + (slab_mode(E) ? 2 * (2 + (E.X.comm && E.X.comm->nranks > 1 ? 2 : 0)) : 0) : 0;
+  return fine + nd_solve_launches(E.plan, E.B, E.conc) + 3 + slab + kry;
 }
 
 // two captured variants of one iteration: plain, and with phase events (sampled timing)
@@ -719,28 +758,51 @@ void harvest_timers(Engine& E) {
     else cudaGetLastError();
 }
 
-// algorithmic HBM bytes of one iteration per running sample:
-// each kernel reads its inputs and writes its outputs exactly once
-void phase_bytes(const Engine& E, int j, double* out) {
+// HBM bytes of one iteration per running sample, two counts:
+//  out   = compulsory bytes of OUR fused kernels (each reads its inputs and writes
+//          its outputs once: pre/post are single passes over the fine grid);
+//  model = SURVEY.md 8(d)'s per-step model, in which every Jacobi step, the
+//          residual + restriction, the prolongation + correction and the A_0
+//          apply are separate passes (vectors 16 B/node, coefficients c = 16 B
+//          (A_eps) / c0 = 8 B (A_0) per element when heterogeneous, coarse share
+//          16/2^d B per fine node).  The model counts are the "algorithmic" bytes
+//          of the roofline; the fused kernels move fewer, so their model-byte rate
+//          can exceed what HBM alone would allow.
+void phase_bytes(const Engine& E, int j, double* out, double* model) {
   const double N = (double)E.N, Nc = (double)E.Nc;
-  const double c = E.LF.het ? 16.0 * (double)E.LF.elems : 0.0;
-  out[T_PRE] = 32.0 * N + 16.0 * Nc + c;                   // f, u, r_c (+ coef)
-  out[T_POST] = 64.0 * N + 16.0 * Nc + c;                  // f, u, e_c, z, w (+ coef)
+  const double ce = E.LF.het ? 16.0 * (double)E.LF.elems : 0.0;   // A_eps coefficients
+  const double c0 = E.LF.het ? 8.0 * (double)E.LF.elems : 0.0;    // A_0 coefficients
+  const double cshare = 16.0 * Nc;
+  const int nu1 = E.spec.nu_pre, nu2 = E.spec.nu_post;
+  out[T_PRE] = 32.0 * N + 16.0 * Nc + ce;                  // f, u, r_c (+ coef)
+  out[T_POST] = 64.0 * N + 16.0 * Nc + ce;                 // f, u, e_c, z, w (+ coef)
   out[T_COARSE] = (double)nd_stream_bytes(E.plan) + 32.0 * Nc;
   out[T_KRYLOV] = (2.0 * (j + 1) + 3.0) * 16.0 * N;        // mdot + update
+  if (E.ka.reorth == 2) out[T_KRYLOV] *= 2.0;              // second pass every step
+  // Jacobi from zero 32 + c, Jacobi 48 + c, residual + restrict 32 + c + share
+  model[T_PRE] = (32.0 * N + ce) + (nu1 - 1) * (48.0 * N + ce) + (32.0 * N + ce + cshare);
+  // prolong + correct + Jacobi 48 + c + share, Jacobi 48 + c, apply A_0 32 + c0
+  model[T_POST] = (48.0 * N + ce + cshare) + (nu2 - 1) * (48.0 * N + ce) + (32.0 * N + c0);
+  model[T_COARSE] = out[T_COARSE];
+  model[T_KRYLOV] = (32.0 * (j + 1) + 48.0) * N;           // CGS 32j + 80 B/node (j counted from 1)
+  if (E.ka.reorth == 2) model[T_KRYLOV] *= 2.0;
 }
 void account_bytes(Engine& E, int running, int j) {
-  double pb[T_NT];
-  phase_bytes(E, j, pb);
+  double pb[T_NT], mb[T_NT];
+  phase_bytes(E, j, pb, mb);
   for (int t = 0; t < T_NT; ++t) {
     E.acc_bytes[t] += running * pb[t];
+    E.acc_model[t] += running * mb[t];
     E.acc_launch[t] += 1;
   }
 }
 void account_bytes_all(Engine& E, int running, int j) {
-  double pb[T_NT];
-  phase_bytes(E, j, pb);
-  for (int t = 0; t < T_NT; ++t) E.acc_bytes_all[t] += running * pb[t];
+  double pb[T_NT], mb[T_NT];
+  phase_bytes(E, j, pb, mb);
+  for (int t = 0; t < T_NT; ++t) {
+    E.acc_bytes_all[t] += running * pb[t];
+    E.acc_model_all[t] += running * mb[t];
+  }
 }
 
 int count_running(Engine& E) {
@@ -756,8 +818,10 @@ hh_status sync_status(Engine& E) {
 }
 
 // FGMRES(m) for every sample of the batch: b, x are [B] device vectors
+// use_x0: xvec holds the initial guess x0 (r_0 = b - A_0 x0, PAPER.md:416 u^(0));
+// otherwise x0 = 0 (BASELINE configs) and xvec is cleared.
 hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
-                      std::vector<SampleOut>& out, double* hist_host) {
+                      std::vector<SampleOut>& out, double* hist_host, bool use_x0 = false) {
   const int B = E.B;
   const int m = o.restart;
   if (m < 1 || m > E.m) { hh_set_error("restart %d not in 1..%d", m, E.m); return HH_E_CONFIG; }
@@ -765,17 +829,27 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
     hh_set_error("max_iters/fixed_iters out of range");
     return HH_E_CONFIG;
   }
+  if (o.reorth < 0 || o.reorth > 2) { hh_set_error("reorth must be 0, 1 or 2 (got %d)", o.reorth); return HH_E_CONFIG; }
+  if (!(o.rtol >= 0)) { hh_set_error("rtol must be >= 0"); return HH_E_CONFIG; }
   cudaStream_t s = E.s;
   KArgs& A = E.ka;
   A.rtol = o.rtol;
   A.max_iters = o.max_iters;
   A.fixed_iters = o.fixed_iters;
-  E.drop_graphs();   // KArgs (rtol, caps) are captured by value
+  A.reorth = o.reorth;
+  E.drop_graphs();   // KArgs (rtol, caps, reorth) are captured by value
   const int check = std::max(1, o.check_every);
-  HH_TRY(vset(E.LF, xvec, VArg(), B, 0, 0, nullptr, s));
+  if (!use_x0) HH_TRY(vset(E.LF, xvec, VArg(), B, 0, 0, nullptr, s));
   HH_CUDA_TRY(cudaMemsetAsync(A.H, 0, (size_t)B * A.HB * sizeof(cplx), s));
+  HH_CUDA_TRY(cudaMemsetAsync(A.reo, 0, (size_t)B * sizeof(int), s));
   HH_TRY(vset(E.LF, varg(A.V, A.Vbs), bvec, B, 1, 0, nullptr, s));       // V[0] = b
   HH_TRY(krylov_norm_all(E, bvec, 0));                                    // ||b||, status
+  if (use_x0) {   // V[0] = r_0 = b - A_0 x0; the threshold stays relative to ||b|| (C14)
+    HH_TRY(halo(E, xvec));
+    HH_TRY(fine_apply(E.LF, B, A.ks.status, HH_OP_A0, xvec, varg(A.V, A.Vbs), bvec, s));
+    HH_TRY(krylov_norm_all(E, varg(A.V, A.Vbs), 1));
+    E.launches += 2;
+  }
   HH_TRY(sync_status(E));
   std::vector<int> restarts(B, 0);
   int running = count_running(E);
@@ -832,6 +906,7 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
   HH_CUDA_TRY(cudaMemcpyAsync(stt.data(), A.ks.status, B * 4, cudaMemcpyDeviceToHost, s));
   HH_CUDA_TRY(cudaStreamSynchronize(s));
   out.assign(B, SampleOut());
+  bool ndfail = false;
   for (int b = 0; b < B; ++b) {
     SampleOut& r = out[b];
     r.iterations = its[b];
@@ -841,6 +916,15 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
     r.rho = its[b] > 0 ? std::pow(r.rel_res_true, 1.0 / its[b]) : NAN;
     r.converged = o.fixed_iters > 0 ? (r.rel_res_true <= o.rtol) : (stt[b] == HHK_CONVERGED);
     r.status = stt[b] == HHK_NAN ? HH_E_DIVERGED : (stt[b] == HHK_BREAKDOWN ? HH_E_BREAKDOWN : HH_OK);
+    if (stt[b] == HHK_NDFAIL) {   // never a silent wrong result: the sample fails loudly
+      r.status = HH_E_CUDA;
+      r.converged = 0;
+      ndfail = true;
+    }
+  }
+  if (ndfail) {
+    HH_TRY(flow_recover(E));
+    hh_set_error("coarse solve: a dataflow dependency wait timed out (schedule disabled; rerun the sample)");
   }
   if (hist_host && (B == 1 || slab_mode(E))) {
     std::vector<double> h(its[0] + 1);
@@ -1043,6 +1127,7 @@ extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   HH_TRY(fine_post(E.LF, E.B, nullptr, E.spec.nu_post, E.spec.omega, vfine(E, E.bv), SArg(),
                    vfine(E, E.u), vflat(E.ec, E.Nc), vfine(E, E.xv), VArg(), E.s));
   HH_TRY(user_out(E, E.xv, z));
+  HH_TRY(flow_check(E, nd_solve_uses_flow(E.plan, E.B, E.conc)));
   return leave(E, p->user);
 }
 
@@ -1051,7 +1136,8 @@ extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
   Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
   HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
-                  varg((cplx*)e, 0), E.s, true));
+                  varg((cplx*)e, 0), E.s, true, false, E.flow_fail));
+  HH_TRY(flow_check(E, nd_solve_uses_flow(E.plan, 1, false)));
   return leave(E, p->user);
 }
 
@@ -1078,7 +1164,8 @@ extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, co
   HH_CUDA_TRY(cudaEventRecord(e0, E.s));
   std::vector<SampleOut> out;
   hh_status st = user_in(E, bv, E.bv);
-  if (st == HH_OK) st = batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, res_hist);
+  if (st == HH_OK) st = user_in(E, xv, E.xv);   // x0
+  if (st == HH_OK) st = batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, res_hist, true);
   if (st == HH_OK) st = user_out(E, E.xv, xv);
   HH_CUDA_TRY(cudaEventRecord(e1, E.s));
   HH_CUDA_TRY(cudaEventSynchronize(e1));
@@ -1090,8 +1177,9 @@ extern "C" hh_status hh_fgmres_solve(hh_problem* p, const void* bv, void* xv, co
   fill_report(p, out[0], ms * 1e-3, rep);
   HH_TRY(leave(E, p->user));
   if (out[0].status != HH_OK) {
-    hh_set_error(out[0].status == HH_E_DIVERGED ? "FGMRES: NaN/Inf in the Arnoldi recurrence"
-                                                : "FGMRES: breakdown with residual above tolerance");
+    if (out[0].status != HH_E_CUDA)
+      hh_set_error(out[0].status == HH_E_DIVERGED ? "FGMRES: NaN/Inf in the Arnoldi recurrence"
+                                                  : "FGMRES: breakdown with residual above tolerance");
     return (hh_status)out[0].status;
   }
   return HH_OK;
@@ -1105,14 +1193,28 @@ extern "C" hh_status hh_fgmres_solve_host(hh_problem* p, const void* b_host, voi
   HH_TRY(E.ustage.ensure((size_t)p->n_local * 16));
   HH_CUDA_TRY(cudaMemcpyAsync(E.ustage.p, b_host, p->n_local * 16, cudaMemcpyHostToDevice, E.s));
   HH_TRY(user_in(E, E.ustage.p, E.bv));
+  HH_CUDA_TRY(cudaMemcpyAsync(E.ustage.p, x_host, p->n_local * 16, cudaMemcpyHostToDevice, E.s));
+  HH_TRY(user_in(E, E.ustage.p, E.xv));   // x0
   std::vector<SampleOut> out;
   const double t0 = now_s();
-  HH_TRY(batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, nullptr));
+  HH_TRY(batch_solve(E, vfine(E, E.bv), vfine(E, E.xv), *o, out, nullptr, true));
   HH_TRY(user_out(E, E.xv, E.ustage.p));
   HH_CUDA_TRY(cudaMemcpyAsync(x_host, E.ustage.p, p->n_local * 16, cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   fill_report(p, out[0], now_s() - t0, r);
   return (hh_status)out[0].status;
+}
+
+extern "C" hh_status hh_arnoldi_orthogonality(hh_problem* p, double* max_loss, int32_t* nvec) {
+  if (!p || !max_loss) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  Engine& E = *p->ep;
+  if (slab_mode(E)) { hh_set_error("arnoldi_orthogonality: not available for slab-decomposed handles"); return HH_E_STATE; }
+  HH_CUDA_TRY(cudaSetDevice(E.device));
+  HH_TRY(enter(E, p->user));
+  int nv = 0;
+  HH_TRY(krylov_orth_loss(E.ka, 0, max_loss, &nv, E.s));
+  if (nvec) *nvec = nv;
+  return leave(E, p->user);
 }
 
 extern "C" hh_status hh_destroy_problem(hh_problem* p) {
@@ -1126,7 +1228,9 @@ extern "C" hh_status hh_destroy_problem(hh_problem* p) {
 extern "C" hh_status hh_reset_timers(hh_problem* p, int32_t enable) {
   if (!p) return HH_E_ARG;
   p->ep->timing = enable != 0;
-  for (int i = 0; i < T_NT; ++i) p->ep->acc_ms[i] = p->ep->acc_bytes[i] = p->ep->acc_launch[i] = p->ep->acc_bytes_all[i] = 0;
+  for (int i = 0; i < T_NT; ++i)
+    p->ep->acc_ms[i] = p->ep->acc_bytes[i] = p->ep->acc_launch[i] = p->ep->acc_bytes_all[i] =
+        p->ep->acc_model[i] = p->ep->acc_model_all[i] = 0;
   p->ep->launches = 0;
   return HH_OK;
 }
@@ -1139,6 +1243,8 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
       st12[4 + i] = p->ep->acc_bytes[i];
       st12[8 + i] = p->ep->acc_launch[i];
       st12[12 + i] = p->ep->acc_bytes_all[i];
+      st12[16 + i] = p->ep->acc_model[i];
+      st12[20 + i] = p->ep->acc_model_all[i];
     }
   if (launches) *launches = p->ep->launches;
   return HH_OK;
@@ -1147,14 +1253,23 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
 // ================================================================== sweep
 static std::mutex g_sweep_mu;
 static bool g_sweep_timing = false;
-static double g_sweep_st[4 * T_NT] = {0};
+static double g_sweep_st[6 * T_NT] = {0};
 static int64_t g_sweep_launches = 0;
-static std::vector<std::unique_ptr<Engine>> g_sweep_engines;   // persistent across hh_sweep calls
+// persistent sweep engines per device; a sweep holds its device's lock for the
+// whole call, so concurrent hh_sweep calls never share an engine
+static std::map<int, std::vector<std::unique_ptr<Engine>>> g_sweep_engines;
+static std::map<int, std::unique_ptr<std::mutex>> g_sweep_dev_mu;
+static std::mutex& sweep_device_mutex(int dev) {
+  std::lock_guard<std::mutex> lk(g_sweep_mu);
+  auto& m = g_sweep_dev_mu[dev];
+  if (!m) m.reset(new std::mutex());
+  return *m;
+}
 
 extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t* launches) {
   std::lock_guard<std::mutex> lk(g_sweep_mu);
   if (st12)
-    for (int i = 0; i < 4 * T_NT; ++i) st12[i] = g_sweep_st[i];
+    for (int i = 0; i < 6 * T_NT; ++i) st12[i] = g_sweep_st[i];
   if (launches) *launches = g_sweep_launches;
   if (reset_enable >= 0) {
     g_sweep_timing = reset_enable != 0;
@@ -1171,8 +1286,24 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
                            const hh_sample* smp, int32_t n, const void* const* rhs,
                            hh_sample_result* out) {
   if (!common || !o || (n && (!smp || !out))) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  if (n < 0) { hh_set_error("negative sample count"); return HH_E_ARG; }
   if (n == 0) return HH_OK;
-  const int m = std::max(o->restart, common->max_restart > 0 ? std::min(common->max_restart, 127) : o->restart);
+  // the checks of hh_setup_problem (the Krylov kernels stage restart + 1 coefficients)
+  if (o->restart < 1 || o->restart > KMAX_RESTART) {
+    hh_set_error("restart must be in 1..%d (got %d)", KMAX_RESTART, o->restart);
+    return HH_E_CONFIG;
+  }
+  if (common->max_restart > KMAX_RESTART) {
+    hh_set_error("max_restart must be <= %d (got %d)", KMAX_RESTART, common->max_restart);
+    return HH_E_CONFIG;
+  }
+  if (!(common->omega > 0 && common->omega <= 1)) { hh_set_error("omega must be in (0,1] (got %g)", common->omega); return HH_E_CONFIG; }
+  if (common->nu_pre < 1 || common->nu_pre > 4 || common->nu_post < 1 || common->nu_post > 4) {
+    hh_set_error("nu_pre/nu_post must be in 1..4");
+    return HH_E_CONFIG;
+  }
+  if (common->shift_map < 0 || common->shift_map > 3) { hh_set_error("shift_map must be 0..3"); return HH_E_CONFIG; }
+  const int m = std::max(o->restart, common->max_restart > 0 ? common->max_restart : o->restart);
   for (int i = 0; i < n; ++i) {
     memset(&out[i], 0, sizeof(out[i]));
     out[i].id = smp[i].id;
@@ -1183,6 +1314,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     }
   }
   HH_CUDA_TRY(cudaSetDevice(common->device));
+  std::lock_guard<std::mutex> dev_lock(sweep_device_mutex(common->device));
   // group by grid size; within a group, order by shift strength eps = beta k^sigma
   // (stronger shift -> more FGMRES iterations) so samples of
   // similar iteration counts share a lockstep batch; batches are bounded by a
@@ -1253,11 +1385,12 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   std::vector<Engine*> engines;
   {
     std::lock_guard<std::mutex> lk(g_sweep_mu);
-    while ((int)g_sweep_engines.size() < nt) {
-      g_sweep_engines.emplace_back(new Engine());
-      HH_TRY(engine_init(*g_sweep_engines.back(), common->device));
+    auto& pool = g_sweep_engines[common->device];
+    while ((int)pool.size() < nt) {
+      pool.emplace_back(new Engine());
+      HH_TRY(engine_init(*pool.back(), common->device));
     }
-    for (int t = 0; t < nt; ++t) engines.push_back(g_sweep_engines[t].get());
+    for (int t = 0; t < nt; ++t) engines.push_back(pool[t].get());
   }
   for (Engine* E : engines) E->conc = nt > 1;
   for (Engine* E : engines)
@@ -1289,6 +1422,8 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     for (double& a : E.acc_ms) a = 0;
     for (double& a : E.acc_bytes) a = 0;
     for (double& a : E.acc_bytes_all) a = 0;
+    for (double& a : E.acc_model) a = 0;
+    for (double& a : E.acc_model_all) a = 0;
     for (double& a : E.acc_launch) a = 0;
     E.launches = 0;
     if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
@@ -1353,6 +1488,8 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
       g_sweep_st[4 + t] += E.acc_bytes[t];
       g_sweep_st[12 + t] += E.acc_bytes_all[t];
       g_sweep_st[8 + t] += E.acc_launch[t];
+      g_sweep_st[16 + t] += E.acc_model[t];
+      g_sweep_st[20 + t] += E.acc_model_all[t];
     }
     g_sweep_launches += E.launches;
   };

@@ -15,6 +15,10 @@
 // ---------------------------------------------------------------- complex fp64
 typedef double2 cplx;   // (re, im), 16 B: same bytes as torch.complex128
 
+// largest FGMRES restart length m (hh_problem_desc.max_restart, hh_fgmres_opts.restart):
+// the Krylov kernels stage m + 1 coefficients in fixed shared arrays
+constexpr int KMAX_RESTART = 127;
+
 __host__ __device__ __forceinline__ cplx cmake(double r, double i) { return make_double2(r, i); }
 __host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
 __host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -150,8 +154,17 @@ hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* 
 // conc: the solve shares the GPU with other streams (concurrent sweep workers):
 // schedules are tuned and cached separately, and the dataflow kernels (whose
 // waiting CTAs hold SM slots) are not used
+// Dataflow schedule failure (a dependency wait that exceeded HH_ND_FLOW_POLLS polls):
+// the waiting CTA marks sample b failed -- st[b] = HHK_NDFAIL when the Krylov
+// status array is given, else *fail = 1 (a caller-owned device int) -- and every
+// later wait of that sample gives up; the caller must then report an error,
+// nd_flow_reset the counters and nd_flow_disable the schedule.
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
-                   VArg x, cudaStream_t s, bool shareF = false, bool conc = false);
+                   VArg x, cudaStream_t s, bool shareF = false, bool conc = false, int* fail = nullptr);
+// true if nd_solve(p, B, ..., conc) runs the dataflow kernels
+bool nd_solve_uses_flow(const NDPlan* p, int B, bool conc);
+// never use the dataflow schedule for this tree again (after a failure)
+void nd_flow_disable(const NDPlan* p);
 // choose the solve schedule for batch size B by timing candidates on the real factor
 hh_status nd_autotune(const NDPlan* p, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
                       cudaStream_t s, bool shareF = false, bool conc = false);

@@ -12,11 +12,14 @@
 // V[i] is stored UNNORMALISED; vscale[i] = 1 / ||V[i]|| is applied by every
 // consumer (the V-cycle reads f = vscale[j] V[j]), which saves a full
 // read+write pass per iteration.
+#include <algorithm>
+#include <vector>
 #include "hh_internal.cuh"
 #include "krylov.cuh"
 
 namespace {
 constexpr int KT = 256;     // threads per CTA
+constexpr int KMAX_CF = KMAX_RESTART + 8;   // Arnoldi coefficients staged per pass (>= m + 1)
 
 __device__ __forceinline__ cplx block_sum(cplx v, cplx* sh) {
 #pragma unroll
@@ -66,16 +69,21 @@ __device__ __forceinline__ void owned_view(const KArgs& A, int b, int64_t& off, 
 // flight (no serial tail loop); unit partials are combined in shared memory in
 // a fixed order (deterministic).
 constexpr int MD_UNITS = 1024;   // max units per CTA (nv <= 128, sub-chunks <= 8)
-__global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
+// pass 2 (reorth): w = V[j+1] (the first pass's w'), result h2 -> y (folded into
+// H column j by the second update's tail); reorth = 1: ||w||^2 rides along as
+// the extra column nv of the partials (DGKS criterion).
+__global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A, int pass) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
+  if (pass == 2 && !A.reo[b]) return;
   const int j = *A.jdev;
   const int nv = j + 1;
+  const bool wn = pass == 1 && A.reorth == 1;
   int64_t off, N;
   owned_view(A, b, off, N);
   const int64_t NS = A.Nst;
   const cplx* V = A.V + (int64_t)b * A.Vbs + off;
-  const cplx* w = A.w + (int64_t)b * NS + off;
+  const cplx* w = pass == 2 ? V + (int64_t)(j + 1) * NS : A.w + (int64_t)b * NS + off;
   cplx* part = A.cpart + ((int64_t)b * gridDim.x + blockIdx.x) * A.ldp;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
@@ -84,8 +92,21 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
   cplx* usum = reinterpret_cast<cplx*>(smem_raw);   // [MD_UNITS]
   cplx* ws = usum + MD_UNITS;                       // this CTA's chunk of w
   const int len = hi > lo ? (int)(hi - lo) : 0;
-  for (int t = threadIdx.x; t < len; t += KT) ws[t] = w[lo + t];
+  double wsq = 0;
+  for (int t = threadIdx.x; t < len; t += KT) {
+    const cplx a = w[lo + t];
+    ws[t] = a;
+    wsq += a.x * a.x + a.y * a.y;
+  }
+  if (wn) {   // ||w||^2 partial of this CTA: warp shuffles, then warps in a fixed order
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wsq += __shfl_xor_sync(0xffffffffu, wsq, o);
+    if (lane == 0) usum[MD_UNITS - 1 - warp] = cmake(wsq, 0);
+  }
   __syncthreads();
+  double wsum = 0;
+  if (wn && threadIdx.x == 0)
+    for (int q = 0; q < KT / 32; ++q) wsum += usum[MD_UNITS - 1 - q].x;
   const int S = max(1, min(8, (4 * (KT / 32) + nv - 1) / nv));   // sub-chunks per vector
   const int sl = (len + S - 1) / S;
   const int units = nv * S;
@@ -122,11 +143,13 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
     for (int sub = 0; sub < S; ++sub) acc = cadd(acc, usum[q * S + sub]);
     part[q] = acc;
   }
+  if (wn && threadIdx.x == 0) part[nv] = cmake(wsum, 0);
   if (last_block(A.counter + b)) {
     // column sums over the CTAs: one warp per entry, lanes stride the CTAs, fixed-order shuffle
     cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
     const cplx* P0 = A.cpart + (int64_t)b * gridDim.x * A.ldp;
-    for (int q = warp; q < nv; q += KT / 32) {
+    cplx* y = A.y + (int64_t)b * A.ldv;
+    for (int q = warp; q < nv + (wn ? 1 : 0); q += KT / 32) {
       cplx s0 = cmake(0, 0), s1 = cmake(0, 0);
       int k = lane;
       for (; k + 32 < (int)gridDim.x; k += 64) {
@@ -142,6 +165,8 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
       }
       if (lane == 0) {
         if (A.slabred) A.red[(int64_t)b * A.ldr + q] = s;
+        else if (q == nv) A.wnorm2[b] = s.x;
+        else if (pass == 2) y[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
         else Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
       }
     }
@@ -150,39 +175,47 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A) {
 }
 
 // slabred: H column j = vscale * (sum over the entries of the partials)
-__global__ void k_mdot_fin(KArgs A, int B) {
+__global__ void k_mdot_fin(KArgs A, int B, int pass) {
   const int b = blockIdx.x;
   if (A.ks.status[b]) return;
+  if (pass == 2 && !A.reo[b]) return;
   const int j = *A.jdev;
+  const bool wn = pass == 1 && A.reorth == 1;
   cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
-  for (int q = threadIdx.x; q <= j; q += blockDim.x) {
+  cplx* y = A.y + (int64_t)b * A.ldv;
+  for (int q = threadIdx.x; q <= j + (wn ? 1 : 0); q += blockDim.x) {
     cplx s = cmake(0, 0);
     for (int e = 0; e < B; ++e) s = cadd(s, A.red[(int64_t)e * A.ldr + q]);
-    Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+    if (q == j + 1) A.wnorm2[b] = s.x;
+    else if (pass == 2) y[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+    else Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
   }
 }
 
 __device__ void givens_tail(const KArgs& A, int b, int j, double ssum);
+__device__ void update_tail(const KArgs& A, int b, int j, double ssum, int pass);
 
 // w' = w - sum_i (H_i vscale_i) V_i -> V[j+1] ; ||w'||^2 ; last block:
 // h_{j+1,j} = ||w'||, vscale_{j+1}, Givens on column j, status.
-__global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
+// pass 2 (reorth): V[j+1] <- V[j+1] - sum_i (y_i vscale_i) V_i in place, with y = h2.
+__global__ void __launch_bounds__(KT, 5) k_update(KArgs A, int pass) {
   const int b = blockIdx.y;
   if (A.ks.status[b]) return;
-  __shared__ cplx cf[136];
+  if (pass == 2 && !A.reo[b]) return;
+  __shared__ cplx cf[KMAX_CF];
   __shared__ cplx sh[KT / 32];
   const int j = *A.jdev;
   const int nv = j + 1;
   int64_t off, N;
   owned_view(A, b, off, N);
   const int64_t NS = A.Nst;
-  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+  const cplx* hsrc = pass == 2 ? A.y + (int64_t)b * A.ldv : A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
   const double* vs = A.vscale + (int64_t)b * A.ldv;
-  for (int q = threadIdx.x; q < 136; q += KT) cf[q] = q < nv ? cscale(Hcol[q], vs[q]) : cmake(0, 0);
+  for (int q = threadIdx.x; q < KMAX_CF; q += KT) cf[q] = q < nv ? cscale(hsrc[q], vs[q]) : cmake(0, 0);
   __syncthreads();
   const cplx* V = A.V + (int64_t)b * A.Vbs + off;
-  const cplx* w = A.w + (int64_t)b * NS + off;
   cplx* Vout = A.V + (int64_t)b * A.Vbs + (int64_t)(j + 1) * NS + off;
+  const cplx* w = pass == 2 ? Vout : A.w + (int64_t)b * NS + off;
   const int64_t chunk = (N + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(N, lo + chunk);
   double nrm = 0.0;
@@ -210,16 +243,37 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A) {
   if (threadIdx.x != 0) return;
   A.counter[b] = 0u;
   if (A.slabred) { A.red2[b] = ssum; return; }
-  givens_tail(A, b, j, ssum);
+  update_tail(A, b, j, ssum, pass);
 }
 
 // slabred: ||w'||^2 = sum over the entries, then the Givens tail
-__global__ void k_update_fin(KArgs A, int B) {
+__global__ void k_update_fin(KArgs A, int B, int pass) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B || A.ks.status[b]) return;
+  if (pass == 2 && !A.reo[b]) return;
   double ssum = 0;
   for (int e = 0; e < B; ++e) ssum += A.red2[e];
-  givens_tail(A, b, *A.jdev, ssum);
+  update_tail(A, b, *A.jdev, ssum, pass);
+}
+
+// after the update pass: reorth = 1 decides the second pass by the DGKS
+// criterion ||w'|| < ||w|| / sqrt 2 (oracle fgmres.py), reorth = 2
+// always takes it; the second pass folds h2 into H column j, then Givens.
+__device__ void update_tail(const KArgs& A, int b, int j, double ssum, int pass) {
+  if (pass == 2) {
+    cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+    const cplx* y = A.y + (int64_t)b * A.ldv;
+    for (int q = 0; q <= j; ++q) Hcol[q] = cadd(Hcol[q], y[q]);
+    A.reo[b] = 0;
+    givens_tail(A, b, j, ssum);
+    return;
+  }
+  if (A.reorth == 2 || (A.reorth == 1 && ssum < 0.5 * A.wnorm2[b])) {
+    A.reo[b] = 1;   // the second pass finishes this step
+    return;
+  }
+  if (A.reorth) A.reo[b] = 0;
+  givens_tail(A, b, j, ssum);
 }
 
 // h_{j+1,j} = sqrt(ssum), vscale_{j+1}, Givens rotations on column j, status
@@ -287,7 +341,7 @@ __global__ void k_trisolve(KArgs A) {
   const int b = blockIdx.x;
   const int k = A.ks.jend[b];
   if (k <= 0) return;
-  __shared__ cplx rhs[128];
+  __shared__ cplx rhs[KMAX_RESTART];
   const cplx* H = A.H + (int64_t)b * A.HB;
   const cplx* g = A.g + (int64_t)b * A.ldv;
   cplx* y = A.y + (int64_t)b * A.ldv;
@@ -306,7 +360,7 @@ __global__ void __launch_bounds__(KT) k_xupdate(KArgs A, VArg xv) {
   const int b = blockIdx.y;
   const int k = A.ks.jend[b];
   if (k <= 0) return;
-  __shared__ cplx ys[128];
+  __shared__ cplx ys[KMAX_RESTART];
   for (int q = threadIdx.x; q < k; q += KT) ys[q] = A.y[(int64_t)b * A.ldv + q];
   __syncthreads();
   int64_t off, N;
@@ -373,22 +427,49 @@ __device__ void norm_tail(const KArgs& A, int b, int mode, double t) {
 
 __global__ void k_clear_jend(KArgs A, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < B) A.ks.jend[b] = 0;
+  if (b >= B) return;
+  if (A.ks.jend[b] > 0) A.ks.jlast[b] = A.ks.jend[b];
+  A.ks.jend[b] = 0;
+}
+
+// |<v_a, v_c> - delta_ac| for every pair a <= c <= nv - 1 of entry b's basis
+// (v_q = vscale_q V_q), one CTA per pair, fixed-order reduction
+__global__ void __launch_bounds__(KT) k_orth(KArgs A, int b, int nv, double* out) {
+  __shared__ cplx sh[KT / 32];
+  int p = blockIdx.x, a = 0;
+  while (p >= nv - a) { p -= nv - a; ++a; }
+  const int c = a + p;
+  int64_t off, N;
+  owned_view(A, b, off, N);
+  const cplx* Va = A.V + (int64_t)b * A.Vbs + (int64_t)a * A.Nst + off;
+  const cplx* Vc = A.V + (int64_t)b * A.Vbs + (int64_t)c * A.Nst + off;
+  cplx acc = cmake(0, 0);
+  for (int64_t i = threadIdx.x; i < N; i += KT) {
+    const cplx x = Va[i], y = Vc[i];
+    acc.x = fma(x.x, y.x, fma(x.y, y.y, acc.x));
+    acc.y = fma(x.x, y.y, fma(-x.y, y.x, acc.y));
+  }
+  const cplx s = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    const double* vs = A.vscale + (int64_t)b * A.ldv;
+    const cplx g = cscale(s, vs[a] * vs[c]);
+    out[blockIdx.x] = sqrt(cabs2(cmake(g.x - (a == c ? 1.0 : 0.0), g.y)));
+  }
 }
 
 }  // namespace
 
 // ================================================================ host side
-hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s) {
+hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s, int pass) {
   const size_t sm = (size_t)(MD_UNITS + (A.Nst + A.nblk - 1) / A.nblk) * sizeof(cplx);
   if (sm > 48 * 1024)
     HH_CUDA_TRY(smem_attr((const void*)k_mdot, sm));
-  k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A);
+  k_mdot<<<dim3(A.nblk, B), KT, sm, s>>>(A, pass);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-hh_status krylov_update(const KArgs& A, int B, cudaStream_t s) {
-  k_update<<<dim3(A.nblk, B), KT, 0, s>>>(A);
+hh_status krylov_update(const KArgs& A, int B, cudaStream_t s, int pass) {
+  k_update<<<dim3(A.nblk, B), KT, 0, s>>>(A, pass);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
@@ -409,18 +490,44 @@ hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s) {
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s) {
-  k_mdot_fin<<<B, 128, 0, s>>>(A, B);
+hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s, int pass) {
+  k_mdot_fin<<<B, 128, 0, s>>>(A, B, pass);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s) {
-  k_update_fin<<<(B + 31) / 32, 32, 0, s>>>(A, B);
+hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s, int pass) {
+  k_update_fin<<<(B + 31) / 32, 32, 0, s>>>(A, B, pass);
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
 hh_status krylov_norm_fin(const KArgs& A, int B, int mode, cudaStream_t s) {
   k_norm_fin<<<(B + 31) / 32, 32, 0, s>>>(A, B, mode);
   HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
+hh_status krylov_orth_loss(const KArgs& A, int b, double* loss, int* nvec, cudaStream_t s) {
+  int jl = 0;
+  HH_CUDA_TRY(cudaMemcpyAsync(&jl, A.ks.jlast + b, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<double> vs(jl + 1, 0.0);
+  if (jl > 0)
+    HH_CUDA_TRY(cudaMemcpy(vs.data(), A.vscale + (int64_t)b * A.ldv, (jl + 1) * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+  int nv = jl + 1;
+  while (nv > 0 && vs[nv - 1] == 0.0) --nv;   // a zero last vector (breakdown) is not a basis vector
+  *nvec = nv;
+  *loss = 0;
+  if (nv <= 0) return HH_OK;
+  const int np = nv * (nv + 1) / 2;
+  double* d = nullptr;
+  HH_CUDA_TRY(cudaMallocAsync(&d, np * sizeof(double), s));
+  k_orth<<<np, KT, 0, s>>>(A, b, nv, d);
+  HH_CUDA_TRY(cudaGetLastError());
+  std::vector<double> h(np);
+  HH_CUDA_TRY(cudaMemcpyAsync(h.data(), d, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HH_CUDA_TRY(cudaFreeAsync(d, s));
+  HH_CUDA_TRY(cudaStreamSynchronize(s));
+  for (double v : h) *loss = std::max(*loss, v);
   return HH_OK;
 }

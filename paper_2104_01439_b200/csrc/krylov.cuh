@@ -2,7 +2,8 @@
 #pragma once
 #include "hh_internal.cuh"
 
-enum { HHK_RUN = 0, HHK_CONVERGED = 1, HHK_MAXIT = 2, HHK_BREAKDOWN = 3, HHK_NAN = 4, HHK_FIXED = 5 };
+enum { HHK_RUN = 0, HHK_CONVERGED = 1, HHK_MAXIT = 2, HHK_BREAKDOWN = 3, HHK_NAN = 4, HHK_FIXED = 5,
+       HHK_NDFAIL = 6 /* the coarse solve's dataflow schedule timed out (nd_solve) */ };
 
 struct KState {              // per-sample device arrays, [B] each (hist: [B][hist_len])
   double* bnorm = nullptr;   // ||b||
@@ -11,6 +12,7 @@ struct KState {              // per-sample device arrays, [B] each (hist: [B][hi
   int* status = nullptr;     // HHK_*
   int* its = nullptr;        // preconditioner applications so far
   int* jend = nullptr;       // Arnoldi steps of the current cycle
+  int* jlast = nullptr;      // Arnoldi steps of the last finished cycle (orthogonality diagnostic)
   double* hist = nullptr;    // |g_{j+1}| / ||b|| per iteration
 };
 
@@ -43,14 +45,24 @@ struct KArgs {
   int slabred = 0;
   cplx* red = nullptr; int ldr = 0;     // [B][ldr] multi-dot partials (slabred)
   double* red2 = nullptr;               // [B] norm partials (slabred)
+  // re-orthogonalisation (hh_fgmres_opts.reorth, reading C11): 0 none (single-pass
+  // CGS), 1 selective (DGKS: second CGS pass when ||w'|| < ||w|| / sqrt 2), 2 always
+  int reorth = 0;
+  double* wnorm2 = nullptr;             // [B] ||w||^2 before the first pass (reorth = 1)
+  int* reo = nullptr;                   // [B] 1: the second pass runs for this sample / step
 };
 
-hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s);
-hh_status krylov_update(const KArgs& A, int B, cudaStream_t s);
+// pass 1: h = V_j^H w, w' = w - V_j h (-> V[j+1]); pass 2 (reorth): the second
+// CGS pass on V[j+1] for the samples whose pass 1 asked for it (reo[b] = 1)
+hh_status krylov_mdot(const KArgs& A, int B, cudaStream_t s, int pass = 1);
+hh_status krylov_update(const KArgs& A, int B, cudaStream_t s, int pass = 1);
 hh_status krylov_advance(int* jdev, int v, cudaStream_t s);    // v < 0: ++j, else j = v
 hh_status krylov_cycle_end(const KArgs& A, int B, VArg x, cudaStream_t s);
 hh_status krylov_norm(const KArgs& A, int B, VArg r, int mode, cudaStream_t s);
 // slabred: finish a reduction after the partials were combined across processes
-hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s);
-hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s);
+hh_status krylov_mdot_fin(const KArgs& A, int B, cudaStream_t s, int pass = 1);
+hh_status krylov_update_fin(const KArgs& A, int B, cudaStream_t s, int pass = 1);
+// max over pairs (a, c) of the last cycle's basis v_0..v_jlast of |<v_a, v_c> - delta_ac|
+// for entry b (blocks; diagnostic of the Arnoldi orthogonality)
+hh_status krylov_orth_loss(const KArgs& A, int b, double* loss, int* nvec, cudaStream_t s);
 hh_status krylov_norm_fin(const KArgs& A, int B, int mode, cudaStream_t s);

@@ -26,7 +26,7 @@ EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "h
            "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
            "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
            "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_lfa_rho", "hh_lfa_sigma_c", "hh_lfa_stats",
-           "hh_last_error", "hh_version"]
+           "hh_arnoldi_orthogonality", "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -41,7 +41,7 @@ class ProblemDesc(C.Structure):
 
 class FgmresOpts(C.Structure):
     _fields_ = [("restart", C.c_int32), ("max_iters", C.c_int32), ("fixed_iters", C.c_int32),
-                ("rtol", C.c_double), ("check_every", C.c_int32)]
+                ("rtol", C.c_double), ("check_every", C.c_int32), ("reorth", C.c_int32)]
 
 
 class FgmresReport(C.Structure):
@@ -117,6 +117,7 @@ def _load():
         "hh_sweep": [C.POINTER(ProblemDesc), C.POINTER(FgmresOpts), C.POINTER(Sample), i32,
                      C.POINTER(SampleResult)],
         "hh_destroy_problem": [vp],
+        "hh_arnoldi_orthogonality": [vp, dp, C.POINTER(C.c_int32)],
         "hh_reset_timers": [vp, i32],
         "hh_read_timers": [vp, dp, C.POINTER(C.c_int64)],
         "hh_sweep_timers": [i32, dp, C.POINTER(C.c_int64)],
@@ -150,8 +151,9 @@ def _ptr(t: torch.Tensor, n: int, name: str):
     return C.c_void_p(t.data_ptr())
 
 
-def opts(restart=100, max_iters=500, fixed_iters=0, rtol=1e-6, check_every=1):
-    return FgmresOpts(restart, max_iters, fixed_iters, rtol, check_every)
+def opts(restart=100, max_iters=500, fixed_iters=0, rtol=1e-6, check_every=1, reorth=0):
+    """hh_fgmres_opts; reorth: 0 single-pass CGS, 1 selective (DGKS), 2 always (C11)."""
+    return FgmresOpts(restart, max_iters, fixed_iters, rtol, check_every, reorth)
 
 
 class Problem:
@@ -235,6 +237,7 @@ class Problem:
         return e
 
     def fgmres_solve(self, b, x=None, o=None, history=False):
+        """x: the initial guess x0 on entry (zeros if None), the solution on exit."""
         x = self.new_vector() if x is None else x
         o = o or opts()
         rep = FgmresReport()
@@ -255,11 +258,17 @@ class Problem:
                                         C.c_void_p(x_host.ctypes.data), C.byref(o), C.byref(rep)))
         return rep.as_dict()
 
+    def arnoldi_orthogonality(self):
+        """(max |<v_a, v_c> - delta_ac|, number of basis vectors) of the last Arnoldi cycle."""
+        loss, nv = C.c_double(), C.c_int32()
+        _check(lib.hh_arnoldi_orthogonality(self.handle, C.byref(loss), C.byref(nv)))
+        return loss.value, nv.value
+
     def reset_timers(self, enable=True):
         _check(lib.hh_reset_timers(self.handle, int(enable)))
 
     def read_timers(self):
-        st = (C.c_double * 16)()
+        st = (C.c_double * 24)()
         nl = C.c_int64()
         _check(lib.hh_read_timers(self.handle, st, C.byref(nl)))
         return _phase_dict(st, nl.value)
@@ -356,12 +365,13 @@ PHASES = ("pre", "coarse", "post", "krylov")
 def _phase_dict(st, launches):
     d = {"launches": launches}
     for i, ph in enumerate(PHASES):
-        d[ph] = {"ms": st[i], "bytes": st[4 + i], "launches": st[8 + i], "bytes_all": st[12 + i]}
+        d[ph] = {"ms": st[i], "bytes": st[4 + i], "launches": st[8 + i], "bytes_all": st[12 + i],
+                 "model": st[16 + i], "model_all": st[20 + i]}
     return d
 
 
 def sweep_timers(reset_enable=-1):
-    st = (C.c_double * 16)()
+    st = (C.c_double * 24)()
     nl = C.c_int64()
     _check(lib.hh_sweep_timers(reset_enable, st, C.byref(nl)))
     return _phase_dict(st, nl.value)

@@ -94,3 +94,61 @@ def test_flow_batched_sweep(monkeypatch):
     for a, c in zip(res, ref):
         assert a["status"] == 0 and a["iterations"] == c["iterations"]
         assert abs(a["rel_res_true"] - c["rel_res_true"]) <= 1e-8 * max(c["rel_res_true"], 1e-300) + 1e-14
+
+
+# ---------------------------------------------------------------- failure path
+# HH_ND_FLOW_POLLS=0 makes every dataflow dependency wait fail (fault injection).
+# A failed wait must surface as an error (never a silent wrong coarse correction),
+# and the handle must recover: counters reset, the schedule disabled for that
+# tree.  Each case uses its own grid size, because the disable is per tree.
+FORCE_FLOW = ("1", "-1", "99")
+
+
+def test_flow_failure_fgmres_raises_then_recovers(monkeypatch):
+    spec = config_spec("cfg0", n=96)
+    gp = hh.Problem.from_spec(spec)
+    b = spec.rhs()
+    _set(monkeypatch, FORCE_FLOW)
+    monkeypatch.setenv("HH_ND_FLOW_POLLS", "0")
+    with pytest.raises(hh.HHError) as e:
+        gp.fgmres_solve(_dev(b), o=hh.opts(restart=spec.restart, rtol=spec.rtol))
+    assert e.value.status == 4 and "dataflow" in str(e.value)
+    monkeypatch.delenv("HH_ND_FLOW_POLLS")
+    xo, ro = OracleProblem(spec).solve(b)
+    x, r = gp.fgmres_solve(_dev(b), o=hh.opts(restart=spec.restart, rtol=spec.rtol,
+                                              fixed_iters=ro.iterations))
+    assert _rel(_host(x), xo) <= 1e-8
+    gp.close()
+
+
+def test_flow_failure_coarse_solve_raises_then_recovers(monkeypatch):
+    spec = config_spec("cfg0", n=80)
+    gp = hh.Problem.from_spec(spec)
+    orc = OracleProblem(spec)
+    r = _rand(spec.n_coarse_nodes, 7)
+    _set(monkeypatch, FORCE_FLOW)
+    monkeypatch.setenv("HH_ND_FLOW_POLLS", "0")
+    with pytest.raises(hh.HHError) as e:
+        gp.coarse_solve(_dev(r))
+    assert e.value.status == 4
+    monkeypatch.delenv("HH_ND_FLOW_POLLS")
+    e2 = _host(gp.coarse_solve(_dev(r)))
+    assert _rel(e2, orc.tg.coarse.solve(r)) <= 1e-10
+    gp.close()
+
+
+def test_flow_failure_in_sweep_is_a_per_sample_error(monkeypatch):
+    monkeypatch.setenv("HH_SWEEP_STREAMS", "1")
+    _set(monkeypatch, FORCE_FLOW)
+    monkeypatch.setenv("HH_ND_FLOW_POLLS", "0")
+    samples = [{"id": i, "dim": 2, "n": 72, "k": 8.0 + i, "kh_target": 0.6, "sigma": 1.5,
+                "beta": 0.5} for i in range(3)]
+    res = hh.sweep(samples)
+    assert all(r["status"] == 4 and r["converged"] == 0 for r in res), res
+    monkeypatch.delenv("HH_ND_FLOW_POLLS")
+    res = hh.sweep(samples)
+    from workloads.configs import sweep_sample_spec
+    for s, r in zip(samples, res):
+        assert r["status"] == 0
+        ro = OracleProblem(sweep_sample_spec(s)).solve()[1]
+        assert abs(r["iterations"] - ro.iterations) <= 1

@@ -12,16 +12,23 @@ import bench
 from workloads import sweep_samples
 
 
-def test_residue_shards_partition_the_sweep():
-    allids = {s["id"] for s in sweep_samples()}
-    seen = []
-    for r in range(8):
-        seen += [s["id"] for s in bench.rank_samples(r, 8)]
-    assert sorted(seen) == sorted(allids) and len(seen) == 3520
-    sizes = [len(bench.rank_samples(r, 8)) for r in range(8)]
-    assert sizes == [440] * 8                       # weak scaling: fixed work per rank
+def test_shards_partition_the_sweep():
+    """Every N: the ranks' shares tile all 3,520 samples, sizes differ by at most
+    one, and every rank gets the same mix of grid sizes (strong scaling)."""
+    allids = sorted(s["id"] for s in sweep_samples())
+    assert len(allids) == 3520
+    assert sorted(s["id"] for s in bench.rank_samples(0, 1)) == allids      # N = 1: the whole sweep
+    for world in (2, 3, 4, 8):
+        shares = [bench.rank_samples(r, world) for r in range(world)]
+        seen = sorted(s["id"] for sh in shares for s in sh)
+        assert seen == allids
+        sizes = [len(sh) for sh in shares]
+        assert max(sizes) - min(sizes) <= 1
+        # balance of the dominant cost (fine nodes): within 2% of the mean
+        work = [sum((s["n"] + 1) ** 2 for s in sh) for sh in shares]
+        assert max(work) <= 1.02 * sum(work) / world
     with pytest.raises(ValueError):
-        bench.rank_samples(0, 9)
+        bench.rank_samples(2, 2)
 
 
 def _free_port():
@@ -42,7 +49,11 @@ def _worker(rank, world, port, q):
     t, d, i = bench.combine_ranks(ms, dofs, len(mine), world, torch.device("cpu"))
     ids = [None] * world
     dist.all_gather_object(ids, [s["id"] for s in mine])
-    q.put((rank, t, d, i, ids))
+    # the per-sample record gather of the sweep step (fake results)
+    res = [{"id": s["id"], "status": 0, "iterations": 10 + s["id"] % 7, "converged": 1,
+            "rel_res_true": 1e-7, "rho": 0.2} for s in mine]
+    recs = bench.gather_records(res, world)
+    q.put((rank, t, d, i, ids, recs))
     dist.destroy_process_group()
 
 
@@ -59,10 +70,13 @@ def test_two_rank_gloo_reduction():
         p.join(timeout=60)
         assert p.exitcode == 0
     want_dofs = sum((s["n"] + 1) ** 2 for r in range(world) for s in bench.rank_samples(r, world))
-    for rank, t, d, i, ids in out:
+    for rank, t, d, i, ids, recs in out:
         assert t == 150.0                       # max over ranks
-        assert d == want_dofs and i == 880      # sum over ranks
+        assert d == want_dofs and i == 3520     # sum over ranks: the whole sweep
         assert not set(ids[0]) & set(ids[1])    # disjoint shards
+        # every rank holds all 3,520 records, sorted by id, with the values sent
+        assert [r[0] for r in recs] == list(range(3520))
+        assert all(r[2] == 10 + r[0] % 7 for r in recs)
 
 
 # ------------------------------------------------------------------ slab decomposition host logic
