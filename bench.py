@@ -216,11 +216,15 @@ def run_ours(args, rank, world, dev):
         slabkw = {}
         rhs = spec.rhs()
         if world > 1:
-            # one solve, slab-decomposed over the ranks (NCCL halos + allreduces)
+            # one solve, slab-decomposed over the ranks (NCCL halos + allreduces); the
+            # coarse factor replicated (SURVEY 8(e) first version) or distributed
+            # over the slabs (--coarse dist: HH_COARSE_ND_DIST)
             nid = share_nccl_id(hh.nccl_unique_id, rank, dev)
             z = hh.slab_bounds(spec.n, world)
             rhs = slab_part(rhs, spec.n, spec.dim, z, rank)
             slabkw = {"nccl_id": nid, "rank": rank, "nranks": world}
+            if args.coarse == "dist":
+                slabkw["coarse_solver"] = hh.HH_COARSE_ND_DIST
 
         b_dev = torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
         timers = {"on": False, "acc": None}
@@ -247,7 +251,9 @@ def run_ours(args, rank, world, dev):
         wl = {"workload": f"{args.workload} (BASELINE configs[{args.workload[-1]}])",
               "n_cells": spec.n, "dim": spec.dim, "restart": spec.restart, "rtol": spec.rtol,
               "l2": "Krylov basis > L2 (126 MB); L2 flushed between steps",
-              "parallelism": f"slab{world}" if world > 1 else "single"}
+              "parallelism": f"slab{world}" if world > 1 else "single",
+              "coarse": ("distributed slab-aligned ND" if args.coarse == "dist" else "replicated ND")
+              if world > 1 else "ND"}
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
     clk = Clocks(dev) if rank == 0 and not os.environ.get("HH_BENCH_NO_CLOCKS") else None
     for _ in range(args.warmup):
@@ -526,6 +532,8 @@ def main():
     ap.add_argument("--workload", default="sweep", choices=["sweep", "search", "cfg0", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cold", action="store_true", help="skip the fresh-process first-call e2e")
+    ap.add_argument("--coarse", choices=["replicated", "dist"], default="replicated",
+                    help="coarse factor of a slab-decomposed single solve (N > 1)")
     ap.add_argument("--records", default=None, help="write the sweep's gathered per-sample records (JSONL)")
     ap.add_argument("--cold-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()

@@ -55,8 +55,22 @@ typedef struct hh_problem hh_problem;   /* opaque */
 /* operator selector for hh_apply_op */
 enum { HH_OP_A0 = 0, HH_OP_AEPS = 1, HH_OP_AEPS_COARSE = 2 };
 
-/* coarse direct solver (Alg. 1 line 3) */
-enum { HH_COARSE_AUTO = 0, HH_COARSE_ND = 1 };
+/* coarse direct solver (Alg. 1 line 3; factored once per setup,
+ * PAPER.md:511-512):
+ *  HH_COARSE_AUTO / HH_COARSE_ND: nested-dissection LDL^T-type factor (no pivoting,
+ *    reading C18); with a slab decomposition every rank holds the whole factor
+ *    and solves redundantly (SURVEY.md 8(e) "first version");
+ *  HH_COARSE_ND_DIST (slab decompositions only): distributed exact solve --
+ *    slab-aligned nested dissection whose top separators are the P-1 coarse
+ *    interface planes at the slab boundaries, eliminated middle-first over the
+ *    chain of slabs (block cyclic reduction of the block-tridiagonal interface
+ *    Schur complement); rank r factors and solves only its slab interior and the
+ *    interface plane it owns, Schur complements / update vectors move to the
+ *    parent's owner and the interface solutions are broadcast (NCCL, or device
+ *    copies between in-process slabs).  Needs >= 2 coarse planes per slab.
+ *    (The paper's own distributed step is parallel MUMPS LU, PAPER.md:511,
+ *    1463-1466.)                                                            */
+enum { HH_COARSE_AUTO = 0, HH_COARSE_ND = 1, HH_COARSE_ND_DIST = 2 };
 
 typedef struct {
   int32_t dim;                  /* 2 | 3                                                    */
@@ -272,6 +286,12 @@ hh_status hh_read_timers(hh_problem* p, double* st24, int64_t* launches);
  * kernel-launch count since the last reset; reset_enable >= 0 resets and sets
  * timing on (1) / off (0); -1 only reads. */
 hh_status hh_sweep_timers(int32_t reset_enable, double* st24, int64_t* launches);
+
+/* FP64 FMA throughput of the device (microbenchmark: independent DFMA chains on
+ * every SM, best of 5 timed launches, 2 flops per DFMA): the measured peak the
+ * coarse factorisation's TFLOP/s are quoted against.
+ * tflops: out; sm_mhz: out (nullable), the device's nominal SM clock.  blocks. */
+hh_status hh_fp64_peak(int32_t device, double* tflops, double* sm_mhz);
 
 const char* hh_last_error(void);
 const char* hh_version(void);

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhh.so")
-SOURCES = ["hh_api.cu", "fine2d.cu", "fine3d.cu", "coarse_nd.cu", "krylov.cu", "comm.cu", "lfa.cu"]
+SOURCES = ["hh_api.cu", "fine2d.cu", "fine3d.cu", "coarse_nd.cu", "krylov.cu", "comm.cu", "lfa.cu", "peak.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "shared", "--expt-relaxed-constexpr",

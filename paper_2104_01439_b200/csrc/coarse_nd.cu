@@ -135,6 +135,18 @@ struct NDPlan {
   // K-split backward of long rows (3D): per front ceil(f / KC) x s partial sums
   int64_t Kmax = 0;
   int64_t* d_Koff = nullptr;
+  // distributed (slab-aligned) plan: the view of rank `rank` of a P-rank tree
+  // (nd_plan_create_dist).  Fronts are ordered by (level, owner), so `levels`
+  // holds this rank's contiguous range of every level; the storage offsets
+  // (Foff, Poff) cover its own fronts only, the work layout and the packed-S
+  // offsets are global (identical on every rank: exchanged blocks land at the
+  // same place on both sides).
+  int P = 1, rank = 0;
+  std::vector<int> owner;                 // per front
+  std::vector<std::vector<int>> xcross;   // per level: fronts whose parent has another owner
+  std::vector<std::vector<int>> xtop;     // per level: fronts spanning several ranks (interface planes)
+  std::vector<int64_t> Soff_h;            // packed-S offsets (host copy)
+  int64_t top_sep_max = 0;                // largest sum of top-front separators of one level
 };
 
 // ============================================================ device kernels
@@ -1139,6 +1151,8 @@ struct HostFront {
   int parent = -1;
   std::vector<int> children;
   int level = 0;
+  int owner = 0;        // rank owning the front (distributed plans)
+  bool top = false;     // interface-plane front of a distributed plan
 };
 
 int64_t box_count(const Box& b, int dim) {
@@ -1185,19 +1199,80 @@ void build_tree(const Box& b, int dim, int m, int parent, std::vector<HostFront>
   out[id].children.push_back(rid);
 }
 
+// Slab-aligned nested dissection (distributed coarse solve, SURVEY.md 8(e)
+// "second version" / 8(f) row 2): the coarse planes Zc[1..P-1] of the slowest
+// axis (the slab boundaries of the fine decomposition, halved) are the top
+// separators, taken middle-first over the chain of slabs [r0, r1), so the
+// interface planes form a binary tree above the P slab interiors; each slab
+// interior [Zc[r] + 1, Zc[r+1]) (rank 0: [0, Zc[1])) is an ordinary
+// geometric ND subtree owned by rank r.  Interface plane Zc[k] is owned by rank
+// k (the slab that restricts onto it: fine plane 2 Zc[k] belongs to slab k).
+void build_tree_dist(const Box& b, int dim, int m, int parent, std::vector<HostFront>& out,
+                     const std::vector<int>& Zc, int r0, int r1) {
+  if (r1 - r0 == 1) {
+    const size_t first = out.size();
+    build_tree(b, dim, m, parent, out);
+    for (size_t i = first; i < out.size(); ++i) out[i].owner = r0;
+    return;
+  }
+  const int k = (r0 + r1) / 2;   // plane Zc[k]: ranks [r0, k) below, [k, r1) above
+  const int ax = dim - 1;
+  const int id = (int)out.size();
+  out.push_back(HostFront());
+  out[id].box = b;
+  out[id].parent = parent;
+  out[id].owner = k;
+  out[id].top = true;
+  Box sp = b; sp.lo[ax] = Zc[k]; sp.hi[ax] = Zc[k] + 1;
+  push_box_nodes(sp, dim, m, out[id].sep);
+  Box l = b; l.hi[ax] = Zc[k];
+  Box r = b; r.lo[ax] = Zc[k] + 1;
+  const int lid = (int)out.size();
+  build_tree_dist(l, dim, m, id, out, Zc, r0, k);
+  out[id].children.push_back(lid);
+  const int rid = (int)out.size();
+  build_tree_dist(r, dim, m, id, out, Zc, k, r1);
+  out[id].children.push_back(rid);
+}
+
 }  // namespace
 
 // ============================================================ host API
-hh_status nd_plan_create(int dim, int m, NDPlan** out) {
+static hh_status plan_build(int dim, int m, const std::vector<int>* Zc, int rank, NDPlan** out);
+
+hh_status nd_plan_create(int dim, int m, NDPlan** out) { return plan_build(dim, m, nullptr, 0, out); }
+
+hh_status nd_plan_create_dist(int dim, int m, const std::vector<int>& Zc, int rank, NDPlan** out) {
+  const int P = (int)Zc.size() - 1;
+  if (P < 2 || rank < 0 || rank >= P || Zc[0] != 0 || Zc[P] != m) {
+    hh_set_error("nd dist: bad plane bounds / rank");
+    return HH_E_CONFIG;
+  }
+  for (int k = 0; k < P; ++k)
+    if (Zc[k + 1] - Zc[k] < 2) {
+      hh_set_error("nd dist: slab %d has %d coarse planes (need >= 2)", k, Zc[k + 1] - Zc[k]);
+      return HH_E_CONFIG;
+    }
+  return plan_build(dim, m, &Zc, rank, out);
+}
+
+static hh_status plan_build(int dim, int m, const std::vector<int>* Zc, int rank, NDPlan** out) {
   NDPlan* nd = new NDPlan();
   nd->dim = dim; nd->m = m;
   nd->N = 1;
   for (int d = 0; d < dim; ++d) nd->N *= m;
   nd->S = dim == 2 ? 9 : 27;
+  const bool dist = Zc != nullptr;
   std::vector<HostFront> tf;
   Box root;
   for (int d = 0; d < 3; ++d) { root.lo[d] = 0; root.hi[d] = (d < dim) ? m : 1; }
-  build_tree(root, dim, m, -1, tf);
+  if (dist) {
+    nd->P = (int)Zc->size() - 1;
+    nd->rank = rank;
+    build_tree_dist(root, dim, m, -1, tf, *Zc, 0, nd->P);
+  } else {
+    build_tree(root, dim, m, -1, tf);
+  }
   const int nf = (int)tf.size();
   // halo rings + levels (height above the leaves)
   for (int t = nf - 1; t >= 0; --t) {
@@ -1222,7 +1297,9 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   // order fronts by level (stable)
   std::vector<int> order(nf);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tf[a].level < tf[b].level; });
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {   // by level, then owner
+    return tf[a].level != tf[b].level ? tf[a].level < tf[b].level : tf[a].owner < tf[b].owner;
+  });
   std::vector<int> newid(nf);
   for (int i = 0; i < nf; ++i) newid[order[i]] = i;
   const int nlev = tf[order[nf - 1]].level + 1;
@@ -1365,6 +1442,41 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
     }
     if (li.max_f > bwdk_f()) nd->Kmax = std::max(nd->Kmax, ko);
   }
+  // distributed plan: keep the global level ranges for the packed-S offsets,
+  // narrow `levels` to this rank's fronts, and record the exchange lists
+  const std::vector<LevelInfo> glevels = nd->levels;
+  if (dist) {
+    nd->owner.resize(nf);
+    for (int i = 0; i < nf; ++i) nd->owner[i] = tf[order[i]].owner;
+    nd->xcross.assign(nlev, {});
+    nd->xtop.assign(nlev, {});
+    for (int L = 0; L < nlev; ++L) {
+      LevelInfo& li = nd->levels[L];
+      const int gb = li.begin, ge = li.begin + li.count;
+      int b0 = gb;
+      while (b0 < ge && nd->owner[b0] < rank) ++b0;
+      int b1 = b0;
+      while (b1 < ge && nd->owner[b1] == rank) ++b1;
+      li.begin = b0;
+      li.count = b1 - b0;
+      li.max_s = li.max_u = li.max_f = 0;
+      for (int t = b0; t < b1; ++t) {
+        li.max_s = std::max(li.max_s, nd->fronts[t].s);
+        li.max_u = std::max(li.max_u, nd->fronts[t].u);
+        li.max_f = std::max(li.max_f, nd->fronts[t].f);
+      }
+      int64_t topsum = 0;
+      for (int t = gb; t < ge; ++t) {
+        const int p = nd->fronts[t].parent;
+        if (p >= 0 && nd->owner[p] != nd->owner[t]) nd->xcross[L].push_back(t);
+        if (tf[order[t]].top) {
+          nd->xtop[L].push_back(t);
+          topsum += nd->fronts[t].s;
+        }
+      }
+      nd->top_sep_max = std::max(nd->top_sep_max, topsum);
+    }
+  }
   // lean storage for trees whose full fronts would not fit (3D coarse grids of
   // cfg4 size); HH_ND_LEAN=0/1 overrides, HH_ND_WMAX sets the workspace (entries)
   std::vector<FrontMeta> fronts_w;
@@ -1372,7 +1484,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   std::vector<int> eaListC;
   {
     const char* el = getenv("HH_ND_LEAN");
-    nd->lean = el ? atoi(el) != 0 : 16.0 * (double)Foff > 24e9;
+    nd->lean = dist || (el ? atoi(el) != 0 : 16.0 * (double)Foff > 24e9);   // distributed: always lean
   }
   if (nd->lean) {
     const int64_t Wlim = getenv("HH_ND_WMAX") ? atoll(getenv("HH_ND_WMAX")) : (int64_t)750000000;
@@ -1454,28 +1566,53 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
         if (pv->first + pv->second == it->first) { pv->second += it->second; freel.erase(it); }
       }
     };
+    // distributed plans: only the S blocks this rank touches get a place -- its own
+    // fronts' (sent on after their level when the parent lives elsewhere) and the
+    // ones its fronts receive from children of other owners; every rank places
+    // them in its own store (the transfers use each side's own offsets)
+    auto own = [&](int q) { return !dist || nd->owner[q] == rank; };
+    auto touches = [&](int q) {
+      const int p = nd->fronts[q].parent;
+      return p >= 0 && (own(q) || own(p));
+    };
+    std::vector<int> sent_prev;   // own fronts of the previous level whose S went to another rank
     for (int L = 0; L < nlev; ++L) {
-      const LevelInfo& li = nd->levels[L];
+      const LevelInfo& li = glevels[L];
       for (int q = li.begin; q < li.begin + li.count; ++q) {
         const FrontMeta& fm = nd->fronts[q];
-        Soff[q] = fm.parent >= 0 ? alloc((int64_t)fm.u * (fm.u + 1) / 2) : 0;
+        Soff[q] = touches(q) ? alloc((int64_t)fm.u * (fm.u + 1) / 2) : 0;
       }
-      for (int q = li.begin; q < li.begin + li.count; ++q)
-        for (int c : tf[order[q]].children) {
+      for (int q = li.begin; q < li.begin + li.count; ++q) {
+        if (!own(q)) continue;
+        for (int c : tf[order[q]].children) {   // consumed by this level's extend-add
           const FrontMeta& fc = nd->fronts[newid[c]];
           release(Soff[newid[c]], (int64_t)fc.u * (fc.u + 1) / 2);
         }
+      }
+      for (int q : sent_prev) {
+        const FrontMeta& fc = nd->fronts[q];
+        release(Soff[q], (int64_t)fc.u * (fc.u + 1) / 2);
+      }
+      sent_prev.clear();
+      for (int q = li.begin; q < li.begin + li.count; ++q)
+        if (dist && own(q) && touches(q) && !own(nd->fronts[q].parent)) sent_prev.push_back(q);
     }
     nd->Smax[0] = std::max<int64_t>(1, top);
     nd->Smax[1] = 0;
   }
   int64_t sb = 0;
-  for (auto& fm : nd->fronts) sb += (int64_t)fm.s * fm.f + (int64_t)fm.u * fm.s;
+  for (int t = 0; t < nf; ++t) {
+    if (dist && nd->owner[t] != rank) continue;   // distributed: this rank's fronts only
+    const FrontMeta& fm = nd->fronts[t];
+    sb += (int64_t)fm.s * fm.f + (int64_t)fm.u * fm.s;
+  }
   nd->stream_bytes = sb * (int64_t)sizeof(cplx);
+  nd->Soff_h = Soff;
 
-  // bottom-subtree decompositions for every cut level
+  // bottom-subtree decompositions for every cut level (not for distributed plans:
+  // they always run the per-level lean schedule)
   std::vector<int> sptr_all, slist_all;
-  {
+  if (!dist) {
     std::vector<std::vector<int>> kids(nf);
     for (int i = 0; i < nf; ++i)
       if (nd->fronts[i].parent >= 0) kids[nd->fronts[i].parent].push_back(i);
@@ -1524,6 +1661,7 @@ hh_status nd_plan_create(int dim, int m, NDPlan** out) {
   nd->level_bytes.assign(nlev, 0.0);
   for (int L = 0; L < nlev; ++L) {
     const LevelInfo& li = nd->levels[L];
+    if (li.count == 0) continue;
     const FrontMeta& f0 = nd->fronts[li.begin];
     const FrontMeta& fl = nd->fronts[li.begin + li.count - 1];
     lvr[6 * L] = f0.sepOff;
@@ -1664,6 +1802,58 @@ static void pivot_sweep(const FrontMeta* fr, int t0, int cnt, int Bn, int ms, in
   else pivot_sweep_nb<16>(fr, t0, cnt, Bn, ms, mf, F, FE, C, CE, coff, flag, s);
 }
 
+// one chunk of the lean factorisation: zero the workspace, assemble the coarse
+// stencil entries, extend-add the children's packed Schur complements, Gauss-Jordan
+// sweep, copy [X | H] and the packed S out
+// C: pivot columns (nd->Cw entries), W: workspace (nd->Wmax), Sst: packed Schur
+// complements (first-fit offsets, see the plan; nd->Smax[0] entries)
+static hh_status lean_chunk(const NDPlan* nd, const Chunk& ch, const cplx* st, cplx* F, cplx* C, cplx* W,
+                            cplx* Sst, int* flag, cudaStream_t s) {
+  const int64_t stS = nd->N * nd->S;
+  static const int lprof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
+  const int cnt = ch.t1 - ch.t0;
+  int ms = 0, mf = 0;
+  for (int t = ch.t0; t < ch.t1; ++t) { ms = std::max(ms, nd->fronts[t].s); mf = std::max(mf, nd->fronts[t].f); }
+  cudaEvent_t ce0 = nullptr, ce1 = nullptr;   // HH_PROFILE_SETUP=2: per-chunk timing (diagnostics)
+  if (lprof >= 2) {
+    cudaEventCreate(&ce0); cudaEventCreate(&ce1);
+    cudaEventRecord(ce0, s);
+  }
+  struct ChunkTimer {
+    cudaEvent_t a, b; cudaStream_t st; const Chunk& c; int n, ms, mf; const NDPlan* p;
+    ~ChunkTimer() {
+      if (!a) return;
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms_ = 0;
+      cudaEventElapsedTime(&ms_, a, b);
+      double fl = 0;
+      for (int t = c.t0; t < c.t1; ++t) fl += 8.0 * (double)p->fronts[t].s * p->fronts[t].f * p->fronts[t].f;
+      fprintf(stderr, "[hh factor] lean m=%d level %d chunk: %d fronts max_s=%d max_f=%d %.3f ms %.2f TFLOP/s\n",
+              p->m, c.level, n, ms, mf, ms_, fl / (ms_ * 1e-3) / 1e12);
+      cudaEventDestroy(a); cudaEventDestroy(b);
+    }
+  } ctimer{ce0, ce1, s, ch, cnt, ms, mf, nd};
+  {
+    const unsigned gx = (unsigned)std::min<int64_t>(8192, (ch.Wcount + 255) / 256);
+    k_nd_zero<<<dim3(gx, 1), 256, 0, s>>>(W, 0, 0, ch.Wcount);
+  }
+  if (ch.asmCount) {
+    k_nd_assemble<<<dim3((unsigned)((ch.asmCount + 255) / 256), 1), 256, 0, s>>>(
+        nd->d_asm + ch.asmBegin, ch.asmCount, nd->d_fronts_w, st, stS, W, 0);
+  }
+  for (int slot = 0; slot < 2; ++slot) {
+    if (!ch.ea_count[slot]) continue;
+    k_nd_ea_packed<<<dim3(ch.ea_count[slot], 64), 128, 0, s>>>(nd->d_eaListC + ch.ea_list_off[slot],
+                                                               nd->d_fronts_w, nd->d_Soff, Sst,
+                                                               nd->d_eamap, W);
+  }
+  pivot_sweep(nd->d_fronts_w, ch.t0, cnt, 1, ms, mf, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag, s);
+  k_nd_copyout<<<dim3(cnt, 64), 256, 0, s>>>(nd->d_fronts_w, nd->d_fronts, nd->d_Soff, ch.t0, W, F, Sst);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
 hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf, int* flag,
                     cudaStream_t s) {
   const int64_t FE = nd->F_entries, CE = nd_cbuf_entries(nd);
@@ -1671,52 +1861,8 @@ hh_status nd_factor(const NDPlan* nd, int B, const cplx* st, cplx* F, cplx* cbuf
   HH_CUDA_TRY(cudaMemsetAsync(flag, 0, B * sizeof(int), s));
   if (nd->lean) {
     if (B != 1) { hh_set_error("lean ND storage needs one problem per factorisation"); return HH_E_CONFIG; }
-    cplx* C = cbuf;
-    cplx* W = C + nd->Cw;
-    cplx* Sst = W + nd->Wmax;   // packed Schur complements (first-fit offsets, see the plan)
-    static const int lprof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
-    for (const Chunk& ch : nd->chunks) {
-      const int cnt = ch.t1 - ch.t0;
-      int ms = 0, mf = 0;
-      for (int t = ch.t0; t < ch.t1; ++t) { ms = std::max(ms, nd->fronts[t].s); mf = std::max(mf, nd->fronts[t].f); }
-      cudaEvent_t ce0 = nullptr, ce1 = nullptr;   // HH_PROFILE_SETUP=2: per-chunk timing (diagnostics)
-      if (lprof >= 2) {
-        cudaEventCreate(&ce0); cudaEventCreate(&ce1);
-        cudaEventRecord(ce0, s);
-      }
-      struct ChunkTimer {
-        cudaEvent_t a, b; cudaStream_t st; const Chunk& c; int n, ms, mf; const NDPlan* p;
-        ~ChunkTimer() {
-          if (!a) return;
-          cudaEventRecord(b, st);
-          cudaEventSynchronize(b);
-          float ms_ = 0;
-          cudaEventElapsedTime(&ms_, a, b);
-          double fl = 0;
-          for (int t = c.t0; t < c.t1; ++t) fl += 8.0 * (double)p->fronts[t].s * p->fronts[t].f * p->fronts[t].f;
-          fprintf(stderr, "[hh factor] lean m=%d level %d chunk: %d fronts max_s=%d max_f=%d %.3f ms %.2f TFLOP/s\n",
-                  p->m, c.level, n, ms, mf, ms_, fl / (ms_ * 1e-3) / 1e12);
-          cudaEventDestroy(a); cudaEventDestroy(b);
-        }
-      } ctimer{ce0, ce1, s, ch, cnt, ms, mf, nd};
-      {
-        const unsigned gx = (unsigned)std::min<int64_t>(8192, (ch.Wcount + 255) / 256);
-        k_nd_zero<<<dim3(gx, 1), 256, 0, s>>>(W, 0, 0, ch.Wcount);
-      }
-      if (ch.asmCount) {
-        k_nd_assemble<<<dim3((unsigned)((ch.asmCount + 255) / 256), 1), 256, 0, s>>>(
-            nd->d_asm + ch.asmBegin, ch.asmCount, nd->d_fronts_w, st, stS, W, 0);
-      }
-      for (int slot = 0; slot < 2; ++slot) {
-        if (!ch.ea_count[slot]) continue;
-        k_nd_ea_packed<<<dim3(ch.ea_count[slot], 64), 128, 0, s>>>(nd->d_eaListC + ch.ea_list_off[slot],
-                                                                   nd->d_fronts_w, nd->d_Soff, Sst,
-                                                                   nd->d_eamap, W);
-      }
-      pivot_sweep(nd->d_fronts_w, ch.t0, cnt, 1, ms, mf, W, 0, C, 0, nd->d_Coff_w + ch.t0, flag, s);
-      k_nd_copyout<<<dim3(cnt, 64), 256, 0, s>>>(nd->d_fronts_w, nd->d_fronts, nd->d_Soff, ch.t0, W, F, Sst);
-      HH_CUDA_TRY(cudaGetLastError());
-    }
+    for (const Chunk& ch : nd->chunks)
+      HH_TRY(lean_chunk(nd, ch, st, F, cbuf, cbuf + nd->Cw, cbuf + nd->Cw + nd->Wmax, flag, s));
     return HH_OK;
   }
   static const int prof = getenv("HH_PROFILE_SETUP") ? atoi(getenv("HH_PROFILE_SETUP")) : 0;
@@ -1876,6 +2022,52 @@ static hh_status flow_launch(const NDPlan* nd, const SolveArgs& A, int B, int L0
   return launch_pdl(k_nd_flow_bwd, dim3((unsigned)tot), LT, sm, s, A, W, (const int*)nd->d_lvbeg, B);
 }
 
+// one level of the forward solve on lean storage: gather w_t, then the update
+// vectors upd_t = w_t[halo] - H^T z_s from the transposed [X | H] rows
+static hh_status lean_fwd_level(const NDPlan* nd, const SolveArgs& A, const LevelInfo& li, int B, cudaStream_t s) {
+  if (li.count == 0) return HH_OK;   // (distributed plans: no front of this rank on the level)
+  dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
+  HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
+  if (li.max_u == 0) return HH_OK;
+  const int ncb = (li.max_u + FT_COLS - 1) / FT_COLS, nrc = (li.max_s + FT_ROWS - 1) / FT_ROWS;
+  const int64_t PE = nd->w_entries + nd->out_entries;
+  HH_TRY(launch_pdl(k_nd_fwdT, dim3(ncb * nrc, li.count, B), FT_COLS, 0, s, A, li.begin,
+                    (const int64_t*)nd->d_Poff, ncb, PE));
+  HH_TRY(launch_pdl(k_nd_fwdT_red, dim3((li.max_u + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
+                    (const int64_t*)nd->d_Poff, PE));
+  return HH_OK;
+}
+
+// one level of the backward solve: x[sep] = [X | H] [z_s ; -x[halo]]
+static hh_status bwd_level(const NDPlan* nd, const SolveArgs& A, const LevelInfo& li, int B, cudaStream_t s) {
+  if (li.count == 0) return HH_OK;
+  if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
+    dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
+    HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
+    if (li.max_f > bwdk_f() && !getenv("HH_NO_BWDK")) {   // long rows: K-split over column chunks
+      const int ncb = (li.max_f + KC - 1) / KC, nrb = (li.max_s + KR - 1) / KR;
+      const int64_t KE = nd->w_entries + nd->out_entries + (nd->lean ? nd->Pmax : 0);
+      HH_TRY(launch_pdl(k_nd_bwdK, dim3(nrb * ncb, li.count, B), LT, 0, s, A, li.begin, ncb,
+                        (const int64_t*)nd->d_Koff, KE));
+      HH_TRY(launch_pdl(k_nd_bwdK_red, dim3((li.max_s + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
+                        (const int64_t*)nd->d_Koff, KE));
+      return HH_OK;
+    }
+    // fronts whose vector does not fit read it from L2: no shared memory then (occupancy)
+    const size_t sm = li.max_f > A.vmax ? 0 : (size_t)li.max_f * sizeof(cplx);
+    if (sm > 48 * 1024)
+      HH_CUDA_TRY(smem_attr((const void*)k_nd_rows_wide<1>, sm));
+    dim3 g(li.count, (li.max_s + WIDE_RPC - 1) / WIDE_RPC, B);
+    HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
+    return HH_OK;
+  }
+  const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
+  if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_bwd, sm));
+  dim3 g(li.count, level_split(li.max_s, li.count, B, li.max_f), B);
+  HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
+  return HH_OK;
+}
+
 static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                            VArg x, cudaStream_t s, SolveCfg c, bool shareF, bool conc, int* fail = nullptr) {
   const int nlev = (int)nd->levels.size();
@@ -1933,15 +2125,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     tick();
     struct Tk { decltype(tock)& f; int L; ~Tk() { f("fwd", L); } } tk_{tock, L};
     if (nd->lean) {
-      dim3 gg(li.count, std::max(1, std::min(64, (li.max_f + 255) / 256)), B);
-      HH_TRY(launch_pdl(k_nd_gather, gg, 256, 0, s, A, li.begin));
-      if (li.max_u == 0) continue;
-      const int ncb = (li.max_u + FT_COLS - 1) / FT_COLS, nrc = (li.max_s + FT_ROWS - 1) / FT_ROWS;
-      const int64_t PE = nd->w_entries + nd->out_entries;
-      HH_TRY(launch_pdl(k_nd_fwdT, dim3(ncb * nrc, li.count, B), FT_COLS, 0, s, A, li.begin,
-                        (const int64_t*)nd->d_Poff, ncb, PE));
-      HH_TRY(launch_pdl(k_nd_fwdT_red, dim3((li.max_u + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
-                        (const int64_t*)nd->d_Poff, PE));
+      HH_TRY(lean_fwd_level(nd, A, li, B, s));
       continue;
     }
     if (li.max_f > A.vmax || (li.max_u >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
@@ -1985,30 +2169,7 @@ static hh_status solve_cfg(NDPlan* nd, int B, const int* st, const cplx* F, cplx
     const LevelInfo& li = nd->levels[L];
     tick();
     struct Tk { decltype(tock)& f; int L; ~Tk() { f("bwd", L); } } tk_{tock, L};
-    if (li.max_f > A.vmax || (li.max_s >= wide_rows() && (nd->dim == 3 || li.max_f >= wide_f()))) {
-      dim3 gg(li.count, std::max(1, std::min(64, (li.max_u + 255) / 256)), B);
-      HH_TRY(launch_pdl(k_nd_bwd_stage, gg, 256, 0, s, A, li.begin));
-      if (li.max_f > bwdk_f() && !getenv("HH_NO_BWDK")) {   // long rows: K-split over column chunks
-        const int ncb = (li.max_f + KC - 1) / KC, nrb = (li.max_s + KR - 1) / KR;
-        const int64_t KE = nd->w_entries + nd->out_entries + (nd->lean ? nd->Pmax : 0);
-        HH_TRY(launch_pdl(k_nd_bwdK, dim3(nrb * ncb, li.count, B), LT, 0, s, A, li.begin, ncb,
-                          (const int64_t*)nd->d_Koff, KE));
-        HH_TRY(launch_pdl(k_nd_bwdK_red, dim3((li.max_s + 255) / 256, li.count, B), 256, 0, s, A, li.begin,
-                          (const int64_t*)nd->d_Koff, KE));
-        continue;
-      }
-      // fronts whose vector does not fit read it from L2: no shared memory then (occupancy)
-      const size_t sm = li.max_f > A.vmax ? 0 : (size_t)li.max_f * sizeof(cplx);
-      if (sm > 48 * 1024)
-        HH_CUDA_TRY(smem_attr((const void*)k_nd_rows_wide<1>, sm));
-      dim3 g(li.count, (li.max_s + WIDE_RPC - 1) / WIDE_RPC, B);
-      HH_TRY(launch_pdl(k_nd_rows_wide<1>, g, LT, sm, s, A, li.begin, (int)(sm / sizeof(cplx))));
-      continue;
-    }
-    const size_t sm = (size_t)std::min(li.max_f, A.vmax) * sizeof(cplx);
-    if (sm > 48 * 1024) HH_CUDA_TRY(smem_attr((const void*)k_nd_bwd, sm));
-    dim3 g(li.count, level_split(li.max_s, li.count, B, li.max_f), B);
-    HH_TRY(launch_pdl(k_nd_bwd, g, LT, sm, s, A, li.begin));
+    HH_TRY(bwd_level(nd, A, li, B, s));
   }
   if (cut >= 0) {
     const size_t sm = (size_t)nd->sub_maxf[cut] * sizeof(cplx);
@@ -2050,7 +2211,7 @@ void nd_flow_disable(const NDPlan* ndc) {
 // Empirical schedule choice on the real factor (called once per (tree, B) at
 // setup, outside graph capture): time the candidate schedules with CUDA events.
 hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s, bool shareF, bool conc) {
+                      cudaStream_t s, bool shareF, bool conc, const std::vector<NDTuneCtx>* multi) {
   NDPlan* nd = const_cast<NDPlan*>(ndc);
   SolveCfg have;
   if (getenv("HH_ND_SPLIT") || getenv("HH_ND_CUT") || cached_cfg(nd, cfg_key(B, conc), &have) || nd->lean)
@@ -2059,11 +2220,39 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   cudaEvent_t e0, e1;
   HH_CUDA_TRY(cudaEventCreate(&e0));
   HH_CUDA_TRY(cudaEventCreate(&e1));
+  std::vector<cudaEvent_t> ej;
+  if (multi)
+    for (size_t k = 0; k < multi->size(); ++k) {
+      cudaEvent_t e;
+      HH_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ej.push_back(e);
+    }
+  // isolated: the latency of one solve on an idle GPU; multi (concurrent sweep
+  // workers): the makespan of one solve on EVERY worker stream at once, i.e. the
+  // schedule's throughput when the streams share the SMs
   auto run = [&](SolveCfg c, float* ms) -> hh_status {
-    HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));   // warm
-    HH_CUDA_TRY(cudaEventRecord(e0, s));
-    for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));
-    HH_CUDA_TRY(cudaEventRecord(e1, s));
+    if (!multi) {
+      HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));   // warm
+      HH_CUDA_TRY(cudaEventRecord(e0, s));
+      for (int r = 0; r < 3; ++r) HH_TRY(solve_cfg(nd, B, nullptr, F, work, rhs, x, s, c, shareF, conc));
+      HH_CUDA_TRY(cudaEventRecord(e1, s));
+    } else {
+      const std::vector<NDTuneCtx>& M = *multi;
+      cudaStream_t s0 = M[0].s;
+      for (int pass = 0; pass < 2; ++pass) {   // pass 0 warms up
+        HH_CUDA_TRY(cudaEventRecord(e0, s0));
+        for (size_t k = 1; k < M.size(); ++k) HH_CUDA_TRY(cudaStreamWaitEvent(M[k].s, e0, 0));
+        for (size_t k = 0; k < M.size(); ++k)
+          for (int r = 0; r < (pass ? 3 : 1); ++r)
+            HH_TRY(solve_cfg(nd, B, nullptr, M[k].F, M[k].work, M[k].rhs, M[k].x, M[k].s, c, shareF, conc));
+        for (size_t k = 1; k < M.size(); ++k) {
+          HH_CUDA_TRY(cudaEventRecord(ej[k], M[k].s));
+          HH_CUDA_TRY(cudaStreamWaitEvent(s0, ej[k], 0));
+        }
+        HH_CUDA_TRY(cudaEventRecord(e1, s0));
+        HH_CUDA_TRY(cudaEventSynchronize(e1));
+      }
+    }
     HH_CUDA_TRY(cudaEventSynchronize(e1));
     HH_CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
     return HH_OK;
@@ -2093,7 +2282,7 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   // for concurrent sweep workers only on trees of at least HH_ND_FLOW_CONC_M coarse
   // nodes per side (default: never -- waiting CTAs hold SM slots other streams need)
   static const int flow_conc_m = getenv("HH_ND_FLOW_CONC_M") ? atoi(getenv("HH_ND_FLOW_CONC_M")) : (1 << 30);
-  if ((!conc || nd->m >= flow_conc_m) && !nd->flow_disabled) {
+  if ((!conc || nd->m >= flow_conc_m) && !nd->flow_disabled && !multi) {
     SolveCfg cands[2] = {best, best};
     cands[0].flow = 1;
     cands[1].flow = 1;
@@ -2123,6 +2312,7 @@ hh_status nd_autotune(const NDPlan* ndc, int B, const cplx* F, cplx* work, VArg 
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  for (cudaEvent_t e : ej) cudaEventDestroy(e);
   std::lock_guard<std::mutex> lk(nd->cut_mu);
   nd->cfg_cache.push_back({cfg_key(B, conc), best});
   if (getenv("HH_DEBUG"))
@@ -2150,3 +2340,194 @@ int nd_solve_launches(const NDPlan* ndc, int B, bool conc) {
   }
   return n;
 }
+
+// ============================================================ distributed coarse solve
+// SURVEY.md 8(e) "second version" / 8(f) row 2 (the paper ran this step as a
+// parallel MUMPS LU).  The slab-aligned tree of
+// nd_plan_create_dist is factored and solved by its owners: rank r eliminates its
+// slab interior (an ordinary ND subtree) and the interface planes it owns; the
+// only exchanges are
+//   factor  : the packed Schur complement S_t of a front whose parent is owned by
+//             another rank -> the parent's owner (same packed-S offset on both);
+//   forward : the update vector upd_t of such a front -> the parent's owner;
+//   backward: the solution on every interface plane -> every rank (the halos of
+//             the fronts below it reach into the planes of all their ancestors).
+// The views of one process are either all P ranks (in-process slabs: the
+// exchanges are device copies) or one rank with an NCCL communicator.
+namespace {
+__global__ void k_nd_sep_copy(const int* __restrict__ sep, int n, const cplx* __restrict__ x,
+                              cplx* __restrict__ y, cplx* __restrict__ buf, int mode) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int g = sep[i];
+    if (mode == 0) buf[i] = x[g];            // pack
+    else if (mode == 1) y[g] = buf[i];       // unpack
+    else y[g] = x[g];                        // direct (in-process)
+  }
+}
+
+SolveArgs dist_args(const NDPlan* nd, const NDDistView& v, const int* st, VArg rhs, VArg x) {
+  SolveArgs A;
+  A.fr = nd->d_fronts; A.st = st; A.sep = nd->d_sep; A.halo = nd->d_halo; A.gmap = nd->d_gmap;
+  A.F = v.F; A.FE = 0;
+  A.work = v.work; A.WE = nd_work_entries(nd); A.updE = nd->w_entries; A.rhs = rhs; A.x = x;
+  A.vmax = nd_vmax();
+  A.prefetch = 0;
+  A.fail = nullptr;
+  return A;
+}
+
+int view_of(const std::vector<NDDistView>& V, int rank) {
+  for (size_t k = 0; k < V.size(); ++k)
+    if (V[k].plan->rank == rank) return (int)k;
+  return -1;
+}
+
+// move the blocks of `list` (fronts whose parent has another owner) from the
+// child's owner to the parent's owner: kind 0 = packed S (cbuf), 1 = upd (work)
+hh_status dist_xfer(std::vector<NDDistView>& V, Comm* comm, const std::vector<int>& list, int kind,
+                    cudaStream_t s) {
+  if (list.empty()) return HH_OK;
+  const NDPlan* g = V[0].plan;
+  auto where = [&](const NDDistView& v, int t, int64_t* cnt) -> cplx* {
+    const FrontMeta& fm = g->fronts[t];
+    if (kind == 0) {
+      *cnt = (int64_t)fm.u * (fm.u + 1) / 2;
+      return v.S + v.plan->Soff_h[t];   // each rank's own placement
+    }
+    *cnt = fm.u;
+    return v.work + g->w_entries + fm.outOff;
+  };
+  if (!comm) {
+    for (int t : list) {
+      const int a = view_of(V, g->owner[t]), b = view_of(V, g->owner[g->fronts[t].parent]);
+      if (a < 0 || b < 0) { hh_set_error("nd dist: rank view missing"); return HH_E_STATE; }
+      int64_t cnt = 0;
+      cplx* src = where(V[a], t, &cnt);
+      cplx* dst = where(V[b], t, &cnt);
+      if (cnt) HH_CUDA_TRY(cudaMemcpyAsync(dst, src, cnt * sizeof(cplx), cudaMemcpyDeviceToDevice, s));
+    }
+    return HH_OK;
+  }
+  const int me = V[0].plan->rank;
+  HH_TRY(comm_group(true));
+  for (int t : list) {
+    const int a = g->owner[t], b = g->owner[g->fronts[t].parent];
+    int64_t cnt = 0;
+    cplx* buf = where(V[0], t, &cnt);
+    if (!cnt) continue;
+    if (a == me) HH_TRY(comm_send(comm, buf, cnt * sizeof(cplx), b, s));
+    if (b == me) HH_TRY(comm_recv(comm, buf, cnt * sizeof(cplx), a, s));
+  }
+  return comm_group(false);
+}
+
+// the solution on the interface planes of `list` (level L) -> every rank
+hh_status dist_bcast_top(std::vector<NDDistView>& V, Comm* comm, const std::vector<int>& list, VArg x,
+                         cplx* stage, cudaStream_t s) {
+  if (list.empty()) return HH_OK;
+  const NDPlan* g = V[0].plan;
+  if (!comm) {
+    for (int t : list) {
+      const FrontMeta& fm = g->fronts[t];
+      const int a = view_of(V, g->owner[t]);
+      for (size_t b = 0; b < V.size(); ++b) {
+        if ((int)b == a) continue;
+        k_nd_sep_copy<<<std::min(1024, (fm.s + 255) / 256), 256, 0, s>>>(
+            g->d_sep + fm.sepOff, fm.s, x.p + (int64_t)a * x.bs, x.p + (int64_t)b * x.bs, nullptr, 2);
+      }
+    }
+    HH_CUDA_TRY(cudaGetLastError());
+    return HH_OK;
+  }
+  const int me = V[0].plan->rank;
+  int64_t off = 0;
+  for (int t : list) {   // pack the planes this rank owns
+    const FrontMeta& fm = g->fronts[t];
+    if (g->owner[t] == me)
+      k_nd_sep_copy<<<std::min(1024, (fm.s + 255) / 256), 256, 0, s>>>(g->d_sep + fm.sepOff, fm.s, x.p,
+                                                                        nullptr, stage + off, 0);
+    off += fm.s;
+  }
+  HH_CUDA_TRY(cudaGetLastError());
+  HH_TRY(comm_group(true));
+  off = 0;
+  for (int t : list) {
+    const FrontMeta& fm = g->fronts[t];
+    HH_TRY(comm_bcast(comm, stage + off, (size_t)fm.s * sizeof(cplx), g->owner[t], s));
+    off += fm.s;
+  }
+  HH_TRY(comm_group(false));
+  off = 0;
+  for (int t : list) {   // unpack the others'
+    const FrontMeta& fm = g->fronts[t];
+    if (g->owner[t] != me)
+      k_nd_sep_copy<<<std::min(1024, (fm.s + 255) / 256), 256, 0, s>>>(g->d_sep + fm.sepOff, fm.s, nullptr,
+                                                                        x.p, stage + off, 1);
+    off += fm.s;
+  }
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+}  // namespace
+
+int64_t nd_dist_stage_entries(const NDPlan* p) { return std::max<int64_t>(1, p->top_sep_max); }
+
+int nd_dist_levels(const NDPlan* p) { return (int)p->levels.size(); }
+
+hh_status nd_dist_factor(std::vector<NDDistView>& V, const cplx* st, Comm* comm, cudaStream_t s) {
+  if (V.empty()) return HH_OK;
+  const NDPlan* g = V[0].plan;
+  const int nlev = (int)g->levels.size();
+  std::vector<size_t> next(V.size(), 0);
+  for (auto& v : V) HH_CUDA_TRY(cudaMemsetAsync(v.flag, 0, sizeof(int), s));
+  for (int L = 0; L < nlev; ++L) {
+    for (size_t k = 0; k < V.size(); ++k) {
+      const NDPlan* p = V[k].plan;
+      while (next[k] < p->chunks.size() && p->chunks[next[k]].level == L)
+        HH_TRY(lean_chunk(p, p->chunks[next[k]++], st, V[k].F, V[k].scratch, V[k].scratch + p->Cw, V[k].S,
+                          V[k].flag, s));
+    }
+    HH_TRY(dist_xfer(V, comm, g->xcross[L], 0, s));
+  }
+  return HH_OK;
+}
+
+hh_status nd_dist_solve(std::vector<NDDistView>& V, const int* st, VArg rhs, VArg x, Comm* comm, cplx* stage,
+                        cudaStream_t s) {
+  if (V.empty()) return HH_OK;
+  const NDPlan* g = V[0].plan;
+  const int nlev = (int)g->levels.size();
+  std::vector<SolveArgs> A;
+  for (size_t k = 0; k < V.size(); ++k)
+    A.push_back(dist_args(V[k].plan, V[k], st ? st + k : nullptr, varg(rhs.p + (int64_t)k * rhs.bs, rhs.bs),
+                          varg(x.p + (int64_t)k * x.bs, x.bs)));
+  for (int L = 0; L < nlev; ++L) {
+    for (size_t k = 0; k < V.size(); ++k) HH_TRY(lean_fwd_level(V[k].plan, A[k], V[k].plan->levels[L], 1, s));
+    HH_TRY(dist_xfer(V, comm, g->xcross[L], 1, s));
+  }
+  for (int L = nlev - 1; L >= 0; --L) {
+    for (size_t k = 0; k < V.size(); ++k) HH_TRY(bwd_level(V[k].plan, A[k], V[k].plan->levels[L], 1, s));
+    HH_TRY(dist_bcast_top(V, comm, g->xtop[L], x, stage, s));
+  }
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
+int nd_dist_launches(const std::vector<NDDistView>& V) {
+  int n = 0;
+  for (const NDDistView& v : V)
+    for (const LevelInfo& li : v.plan->levels) {
+      if (!li.count) continue;
+      n += 1 + (li.max_u > 0 ? 2 : 0);                                    // forward
+      n += (li.max_f > nd_vmax() || li.max_s >= wide_rows()) ? (li.max_f > bwdk_f() ? 3 : 2) : 1;   // backward
+    }
+  const NDPlan* g = V[0].plan;
+  for (size_t L = 0; L < g->levels.size(); ++L)
+    n += (int)(g->xcross[L].size() + g->xtop[L].size() * (V.size() > 1 ? V.size() - 1 : 2));
+  return n;
+}
+
+// scratch (pivot columns + workspace: reusable across the views of one process,
+// which run one after another) and packed-S (per view) sizes of a rank view
+int64_t nd_dist_scratch_entries(const NDPlan* p) { return p->Cw + p->Wmax; }
+int64_t nd_dist_s_entries(const NDPlan* p) { return std::max<int64_t>(1, p->Smax[0] + p->Smax[1]); }

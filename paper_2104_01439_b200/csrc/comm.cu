@@ -260,3 +260,23 @@ hh_status slab_user_copy(const SlabCtx& X, VArg ent, void* user, int to_user, cu
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
+
+// ------------------------------------------------------------------ distributed coarse solve transport
+hh_status comm_group(bool start) {
+  NcclApi& a = nccl();
+  if (!a.ok) { hh_set_error("%s", a.err.c_str()); return HH_E_NCCL; }
+  HH_NCCL_TRY(start ? a.GroupStart() : a.GroupEnd());
+  return HH_OK;
+}
+hh_status comm_send(Comm* c, const void* buf, size_t bytes, int peer, cudaStream_t s) {
+  HH_NCCL_TRY(nccl().Send(buf, bytes / 8, ncclFloat64, peer, (ncclComm_t)c->comm, s));
+  return HH_OK;
+}
+hh_status comm_recv(Comm* c, void* buf, size_t bytes, int peer, cudaStream_t s) {
+  HH_NCCL_TRY(nccl().Recv(buf, bytes / 8, ncclFloat64, peer, (ncclComm_t)c->comm, s));
+  return HH_OK;
+}
+hh_status comm_bcast(Comm* c, void* buf, size_t bytes, int root, cudaStream_t s) {
+  HH_NCCL_TRY(nccl().Broadcast(buf, buf, bytes / 8, ncclFloat64, root, (ncclComm_t)c->comm, s));
+  return HH_OK;
+}

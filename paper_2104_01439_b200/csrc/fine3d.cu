@@ -14,6 +14,8 @@
 // Round-1 3D design: one thread per node, neighbours through L1/L2 (__ldg), one
 // kernel per Jacobi step (the 3D two-grid is dominated by the coarse solve,
 // SURVEY 8(d)); temporal blocking as in 2D is future work.
+#include <algorithm>
+#include <cstdlib>
 #include "hh_internal.cuh"
 
 namespace {
@@ -351,6 +353,311 @@ __global__ void k_stencil3d(F3 P, cplx* __restrict__ stv) {
   for (int o = 0; o < 27; ++o) st[o] = e[o];
 }
 
+// ------------------------------------------------------------ z-marching kernels
+// 2.5D tiles: a CTA owns a 32 x 8 column tile of nodes of one entry and marches
+// through a range of z planes.  The input field x (with a 1-node halo in x, y) is
+// staged plane by plane in a 4-plane shared-memory ring, the element
+// coefficients (k_e, eps_e) in a 3-plane ring; the next plane's global loads are
+// issued into registers before the current plane is computed (one barrier per
+// plane), so load latency overlaps the arithmetic.
+//
+// Interior nodes use the assembled forms, evaluated with in-plane pair sums:
+// per plane z' the centre c, the 4 edge-adjacent e, the 4 diagonal d values and
+// the quadrant sums P(sx,sy) = 4c + 2x(sx) + 2y(sy) + xy(sx,sy);
+//   K u   = 8h/3 c_z - h/6 (d_z + e_{z-1} + e_{z+1}) - h/12 (d_{z-1} + d_{z+1})
+//   M_l u = h^3/216 sum_q [2 (lb_q + la_q) P_z(q) + lb_q P_{z-1}(q) + la_q P_{z+1}(q)]
+// (lb / la: lambda of the quadrant-q element below / above the node plane; a
+// constant lambda gives the assembled mass 64 / 16 / 4 / 1), D = 8h/3 -
+// h^3/27 sum_e lambda_e computed on the fly.  Boundary nodes take the element
+// loop (+ boundary faces) on the staged values.  (SURVEY.md 8(d) kernel notes.)
+constexpr int MTX = 32, MTY = 8, MT = MTX * MTY;
+constexpr int NPX = MTX + 2, NPY = MTY + 2, NPL = NPX * NPY;   // node plane with halo
+constexpr int EPX = MTX + 1, EPY = MTY + 1, EPL = EPX * EPY;   // element plane
+constexpr int NRING = 4, ERING = 3;
+enum { M_APPLY = 0, M_JAC = 1, M_JACP = 2, M_RES = 3 };
+
+struct MarchSmem {
+  cplx u[NRING][NPL];
+  double2 c[ERING][EPL];
+};
+
+// boundary node of the z-marching kernels (element loop + boundary faces of
+// row3 / diag3 on the staged planes; kept out of line: it is rare and would
+// otherwise raise the register count of the interior path)
+template <bool HET>
+__device__ __noinline__ void boundary3(const cplx* U0, const cplx* U1, const cplx* U2, const double2* Cb,
+                                       const double2* Ca, int ci, int gx, int gy, int t, int x0, int y0, int n,
+                                       double h, int eps, double2 kc, cplx& ax, cplx& dg) {
+  const double hm = h * h * h / 216.0;
+  const cplx xc = U1[ci];
+  auto X = [&](int dx, int dy, int dz) {
+    const cplx* U = dz < 0 ? U0 : (dz > 0 ? U2 : U1);
+    return U[ci + dy * NPX + dx];
+  };
+  auto LAM = [&](int ex, int ey, int ez) -> double2 {   // (k_e, eps_e) of element (ex, ey, ez) or 0
+    if (ex < 0 || ex >= n || ey < 0 || ey >= n || ez < 0 || ez >= n) return make_double2(0, 0);
+    if (!HET) return kc;
+    const double2* C = ez < t ? Cb : Ca;
+    return C[(ey - (y0 - 1)) * EPX + ex - (x0 - 1)];
+  };
+  const double hk = h / 36.0;
+  ax = cmake(0, 0);
+  dg = cmake(0, 0);
+  for (int o = 0; o < 8; ++o) {
+    const int dx = (o & 1) ? 1 : -1, dy = (o & 2) ? 1 : -1, dz = (o & 4) ? 1 : -1;
+    const int ex = gx + (dx < 0 ? -1 : 0), ey = gy + (dy < 0 ? -1 : 0), ez = t + (dz < 0 ? -1 : 0);
+    if (ex < 0 || ex >= n || ey < 0 || ey >= n || ez < 0 || ez >= n) continue;
+    const cplx a1x = X(dx, 0, 0), a1y = X(0, dy, 0), a1z = X(0, 0, dz);
+    const cplx a2xy = X(dx, dy, 0), a2xz = X(dx, 0, dz), a2yz = X(0, dy, dz);
+    const cplx a3 = X(dx, dy, dz);
+    const cplx s1 = cmake(a1x.x + a1y.x + a1z.x, a1x.y + a1y.y + a1z.y);
+    const cplx s2 = cmake(a2xy.x + a2xz.x + a2yz.x, a2xy.y + a2xz.y + a2yz.y);
+    const cplx kp = cmake(hk * (12.0 * xc.x - 3.0 * s2.x - 3.0 * a3.x), hk * (12.0 * xc.y - 3.0 * s2.y - 3.0 * a3.y));
+    const cplx mp = cmake(hm * (8.0 * xc.x + 4.0 * s1.x + 2.0 * s2.x + a3.x),
+                          hm * (8.0 * xc.y + 4.0 * s1.y + 2.0 * s2.y + a3.y));
+    const double2 c = LAM(ex, ey, ez);
+    const cplx lam = cmake(c.x * c.x, eps ? c.y : 0.0);
+    ax = cadd(ax, kp);
+    cfms(ax, lam, mp);
+    dg.x += h / 3.0 - 8.0 * hm * lam.x;
+    dg.y -= 8.0 * hm * lam.y;
+  }
+  const double hb = h * h / 36.0;
+  const int g3[3] = {gx, gy, t};
+  for (int a = 0; a < 3; ++a) {
+    if (g3[a] != 0 && g3[a] != n) continue;
+    const int ea = g3[a] == 0 ? 0 : n - 1;
+    const int u = (a + 1) % 3, v = (a + 2) % 3;
+    for (int q = 0; q < 4; ++q) {
+      const int du = (q & 1) ? 1 : -1, dv = (q & 2) ? 1 : -1;
+      const int eu = g3[u] + (du < 0 ? -1 : 0), ev = g3[v] + (dv < 0 ? -1 : 0);
+      if (eu < 0 || eu >= n || ev < 0 || ev >= n) continue;
+      int e3i[3], d_u[3] = {0, 0, 0}, d_v[3] = {0, 0, 0};
+      e3i[a] = ea; e3i[u] = eu; e3i[v] = ev;
+      d_u[u] = du; d_v[v] = dv;
+      const double k = LAM(e3i[0], e3i[1], e3i[2]).x;
+      const cplx xu = X(d_u[0], d_u[1], d_u[2]), xv = X(d_v[0], d_v[1], d_v[2]);
+      const cplx xd = X(d_u[0] + d_v[0], d_u[1] + d_v[1], d_u[2] + d_v[2]);
+      const cplx sb = cmake(hb * (4.0 * xc.x + 2.0 * (xu.x + xv.x) + xd.x),
+                            hb * (4.0 * xc.y + 2.0 * (xu.y + xv.y) + xd.y));
+      ax.x += k * sb.y;   // -i k B
+      ax.y -= k * sb.x;
+      dg.y -= 4.0 * hb * k;
+    }
+  }
+}
+
+template <bool HET, int MODE, int MINB>
+__global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out,
+                                                   int eps, int zlen, int nzc) {
+  extern __shared__ double4 smem_raw[];
+  MarchSmem& S = *reinterpret_cast<MarchSmem*>(smem_raw);
+  const int n = P.n, N1 = P.N1;
+  const int tid = threadIdx.x, tx = tid % MTX, ty = tid / MTX;
+  const int x0 = blockIdx.x * MTX, y0 = blockIdx.y * MTY;
+  const int b = blockIdx.z / nzc, chunk = blockIdx.z % nzc;
+  if (P.st && P.st[b]) return;
+  const int2 sl = slab_of(P.slab, b, n);
+  const int zlo = max(0, sl.x - P.ext), zhi = min(N1, sl.y + P.ext);
+  const int zs = zlo + chunk * zlen, ze = min(zhi, zs + zlen);
+  if (zs >= ze) return;
+  const int64_t vo = (int64_t)(sl.x - P.G) * N1 * N1;
+  const cplx* xb = x.at(b) - vo;
+  const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const int NC1 = n / 2 + 1;
+  const cplx* eb = MODE == M_JACP ? ec.at(b) : nullptr;
+  // ---- staging: node plane gz (x or x + I e_c) and element plane ez
+  cplx rn[2];
+  double2 rc[2];
+  auto fetch = [&](int gz, int ez) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * MT;
+      rn[k] = cmake(0, 0);
+      if (q < NPL && gz >= 0 && gz <= n) {
+        const int gx = x0 - 1 + q % NPX, gy = y0 - 1 + q / NPX;
+        if (gx >= 0 && gx <= n && gy >= 0 && gy <= n) {
+          cplx v = __ldg(&xb[((int64_t)gz * N1 + gy) * N1 + gx]);
+          if (MODE == M_JACP) {   // trilinear prolongation of the coarse correction (Alg. 1 line 4)
+            const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
+            const double w = ((gx & 1) ? 0.5 : 1.0) * ((gy & 1) ? 0.5 : 1.0) * ((gz & 1) ? 0.5 : 1.0);
+            for (int kk = 0; kk <= (gz & 1); ++kk)
+              for (int j = 0; j <= (gy & 1); ++j)
+                for (int i = 0; i <= (gx & 1); ++i) {
+                  const cplx c = __ldg(&eb[((int64_t)(cz0 + kk) * NC1 + cy0 + j) * NC1 + cx0 + i]);
+                  v.x += w * c.x;
+                  v.y += w * c.y;
+                }
+          }
+          rn[k] = v;
+        }
+      }
+      if (HET) {
+        rc[k] = make_double2(0, 0);
+        if (q < EPL && ez >= 0 && ez < n) {
+          const int ex = x0 - 1 + q % EPX, ey = y0 - 1 + q / EPX;
+          if (ex >= 0 && ex < n && ey >= 0 && ey < n) rc[k] = __ldg(&cf[((int64_t)ez * n + ey) * n + ex]);
+        }
+      }
+    }
+  };
+  auto commit = [&](int gz, int ez) {   // node plane gz, element plane ez (between ez and ez + 1)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * MT;
+      if (q < NPL) S.u[(gz + NRING) % NRING][q] = rn[k];
+      if (HET && q < EPL) S.c[(ez + ERING) % ERING][q] = rc[k];
+    }
+  };
+  // prologue: node planes zs - 1, zs and element plane zs - 1 in shared memory,
+  // node plane zs + 1 / element plane zs in registers
+  fetch(zs - 1, zs - 1);
+  commit(zs - 1, zs - 1);
+  fetch(zs, -1);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int q = tid + k * MT;
+    if (q < NPL) S.u[(zs + NRING) % NRING][q] = rn[k];
+  }
+  fetch(zs + 1, zs);
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool act = gx <= n && gy <= n;
+  const bool icol = gx > 0 && gx < n && gy > 0 && gy < n;   // interior column
+  const double h = P.h, hm = h * h * h / 216.0;
+  const double kc0 = 8.0 * h / 3.0, ke = -h / 6.0, kk = -h / 12.0;
+  const int ci = (ty + 1) * NPX + tx + 1;    // this node in a node plane
+  const int e0 = ty * EPX + tx;              // element (gx - 1, gy - 1) in an element plane
+  const cplx lamc = HET ? cmake(0, 0) : cmake(kc.x * kc.x, eps ? kc.y : 0.0);
+  // Per node plane z (interior columns): centre c, K_in = 8h/3 c - h/6 d (its role as
+  // the node's own plane), K_off = -h/6 e - h/12 d (as the plane above / below);
+  // HET: quadrant sums P(q); constant k: the mass folded in (A_in / A_off).
+  struct PlaneQ { cplx c, kin, koff, Pq[4]; };
+  auto planeq = [&](int z, PlaneQ& Q) {
+    const cplx* U = S.u[(z + NRING) % NRING];
+    const cplx c = U[ci], xm = U[ci - 1], xp = U[ci + 1], ym = U[ci - NPX], yp = U[ci + NPX];
+    const cplx mm = U[ci - NPX - 1], pm = U[ci - NPX + 1], mp = U[ci + NPX - 1], pp = U[ci + NPX + 1];
+    const cplx e = cmake(xm.x + xp.x + ym.x + yp.x, xm.y + xp.y + ym.y + yp.y);
+    const cplx d = cmake(mm.x + pm.x + mp.x + pp.x, mm.y + pm.y + mp.y + pp.y);
+    Q.c = c;
+    Q.kin = cmake(kc0 * c.x + ke * d.x, kc0 * c.y + ke * d.y);
+    Q.koff = cmake(ke * e.x + kk * d.x, ke * e.y + kk * d.y);
+    if (HET) {   // quadrants q = (sx > 0) + 2 (sy > 0)
+      Q.Pq[0] = cmake(4 * c.x + 2 * (xm.x + ym.x) + mm.x, 4 * c.y + 2 * (xm.y + ym.y) + mm.y);
+      Q.Pq[1] = cmake(4 * c.x + 2 * (xp.x + ym.x) + pm.x, 4 * c.y + 2 * (xp.y + ym.y) + pm.y);
+      Q.Pq[2] = cmake(4 * c.x + 2 * (xm.x + yp.x) + mp.x, 4 * c.y + 2 * (xm.y + yp.y) + mp.y);
+      Q.Pq[3] = cmake(4 * c.x + 2 * (xp.x + yp.x) + pp.x, 4 * c.y + 2 * (xp.y + yp.y) + pp.y);
+    } else {
+      const cplx in = cmake(64 * c.x + 16 * e.x + 4 * d.x, 64 * c.y + 16 * e.y + 4 * d.y);
+      const cplx of = cmake(16 * c.x + 4 * e.x + d.x, 16 * c.y + 4 * e.y + d.y);
+      cfms(Q.kin, cscale(lamc, hm), in);
+      cfms(Q.koff, cscale(lamc, hm), of);
+    }
+  };
+  // element plane ez (between node planes ez, ez + 1), HET: mass of the lower node
+  // (weights 2 P_lo + P_hi), of the upper node (2 P_hi + P_lo), and sum of lambda
+  auto eplane = [&](int ez, const cplx* Plo, const cplx* Phi, cplx& mlo, cplx& mhi, cplx& ls) {
+    const double2* C = S.c[(ez + ERING) % ERING];
+    mlo = mhi = ls = cmake(0, 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double2 cq = C[e0 + (q & 1) + (q >> 1) * EPX];
+      const cplx l = cmake(cq.x * cq.x, eps ? cq.y : 0.0);
+      ls = cadd(ls, l);
+      cfma(mlo, l, cmake(2 * Plo[q].x + Phi[q].x, 2 * Plo[q].y + Phi[q].y));
+      cfma(mhi, l, cmake(2 * Phi[q].x + Plo[q].x, 2 * Phi[q].y + Plo[q].y));
+    }
+  };
+  // f (or sub) of the node of plane t, loaded one plane ahead (its latency hides
+  // under the previous plane's arithmetic)
+  const bool needf = MODE != M_APPLY;
+  const cplx* fb = needf ? f.at(b) - vo : (sub.p ? sub.at(b) - vo : nullptr);
+  auto ldf = [&](int z) -> cplx {
+    if (!act || !fb || z >= ze) return cmake(0, 0);
+    return __ldg(&fb[((int64_t)z * N1 + gy) * N1 + gx]);
+  };
+  cplx fnext = ldf(zs);
+  // carried along z (interior columns): node t's partial operator row acc, its
+  // lambda sum below, plane t's P, K_off (const: A_off) and centre
+  cplx acc = cmake(0, 0), lsb = cmake(0, 0), koff_t = cmake(0, 0), c_t = cmake(0, 0);
+  cplx Pt[4] = {cmake(0, 0), cmake(0, 0), cmake(0, 0), cmake(0, 0)};
+  for (int t = zs; t < ze; ++t) {
+    commit(t + 1, t);              // node plane t + 1, element plane t
+    __syncthreads();
+    if (t + 2 <= ze) fetch(t + 2, t + 1);
+    const cplx fcur = fnext;
+    fnext = ldf(t + 1);
+    if (!act) continue;
+    const cplx* U0 = S.u[(t - 1 + NRING) % NRING];
+    const cplx* U1 = S.u[t % NRING];
+    const cplx* U2 = S.u[(t + 1) % NRING];
+    const double2* Cb = S.c[(t - 1 + ERING) % ERING];   // elements below the node plane
+    const double2* Ca = S.c[t % ERING];                  // above
+    const int64_t gi = ((int64_t)t * N1 + gy) * N1 + gx;
+    cplx ax = cmake(0, 0), dg = cmake(0, 0);
+    cplx xc = U1[ci];
+    if (icol) {
+      if (t == zs) {   // start of the march: planes zs - 1, zs and element plane zs - 1
+        PlaneQ Qm, Q0;
+        planeq(t - 1, Qm);
+        planeq(t, Q0);
+        acc = cadd(Q0.kin, Qm.koff);
+        if (HET) {
+          cplx mlo, mhi, ls;
+          eplane(t - 1, Qm.Pq, Q0.Pq, mlo, mhi, ls);
+          cfms(acc, cmake(hm, 0), mhi);
+          lsb = ls;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) Pt[q] = Q0.Pq[q];
+        }
+        koff_t = Q0.koff;
+        c_t = Q0.c;
+      }
+      PlaneQ Q1;
+      planeq(t + 1, Q1);
+      ax = cadd(acc, Q1.koff);
+      xc = c_t;
+      if (HET) {
+        cplx mlo, mhi, ls;
+        eplane(t, Pt, Q1.Pq, mlo, mhi, ls);
+        cfms(ax, cmake(hm, 0), mlo);
+        dg = cmake(kc0 - 8.0 * hm * (lsb.x + ls.x), -8.0 * hm * (lsb.y + ls.y));
+        acc = cadd(Q1.kin, koff_t);        // node t + 1
+        cfms(acc, cmake(hm, 0), mhi);
+        lsb = ls;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Pt[q] = Q1.Pq[q];
+      } else {
+        dg = cmake(kc0 - 64.0 * hm * lamc.x, -64.0 * hm * lamc.y);
+        acc = cadd(Q1.kin, koff_t);
+      }
+      koff_t = Q1.koff;
+      c_t = Q1.c;
+    }
+    if (icol && t > 0 && t < n) {
+      // interior node: ax, dg from the carried plane quantities
+    } else {
+      // boundary node: element loop + boundary faces on the staged values
+      boundary3<HET>(U0, U1, U2, Cb, Ca, ci, gx, gy, t, x0, y0, n, h, eps, kc, ax, dg);
+    }
+    cplx* ob = out.at(b) - vo;
+    if (MODE == M_APPLY) {
+      if (sub.p) ax = csub(fcur, ax);
+      ob[gi] = ax;
+    } else {
+      const cplx fv = cscale(fcur, fs.at(b));
+      const cplx r = csub(fv, ax);
+      if (MODE == M_RES) {
+        ob[gi] = r;
+      } else {
+        cplx v = xc;
+        cfma(v, cscale(cinv(dg), P.omega), r);
+        ob[gi] = v;
+      }
+    }
+  }
+}
+
 F3 make3(const Level& L, double omega, const int* st, int ext) {
   F3 P;
   P.n = L.n; P.h = L.h; P.omega = omega; P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc;
@@ -365,9 +672,43 @@ dim3 grid3(const F3& P, int B) {
 
 }  // namespace
 
+// z-marching launch: CTAs per entry = x tiles x y tiles x z chunks, with enough
+// z chunks to put ~4 CTAs on every SM
+static bool g_march = getenv("HH_3D_NAIVE") == nullptr;   // HH_3D_NAIVE=1: the one-node-per-thread kernels
+template <int MODE>
+static hh_status march3(const Level& L, const F3& P, int B, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out,
+                        bool eps, cudaStream_t s) {
+  const int tx = (P.N1 + MTX - 1) / MTX, ty = (P.N1 + MTY - 1) / MTY;
+  const int span = std::min(P.N1, P.maxloc + 2 * P.ext);
+  const int want = std::max(1, (4 * 148 + tx * ty * B - 1) / (tx * ty * B));
+  const int nzc = std::max(1, std::min(span, want));
+  const int zlen = (span + nzc - 1) / nzc;
+  const size_t sm = sizeof(MarchSmem);
+  const dim3 g(tx, ty, nzc * B);
+  // register budget: 3 CTAs per SM (80 registers, some spills) or 2 (128, none);
+  // HH_3D_MINB selects, default = the measured faster one
+  static const int minb = getenv("HH_3D_MINB") ? atoi(getenv("HH_3D_MINB")) : 3;
+  if (L.het && minb == 2) {
+    HH_CUDA_TRY(smem_attr((const void*)k_march3d<true, MODE, 2>, sm));
+    k_march3d<true, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+  } else if (L.het) {
+    HH_CUDA_TRY(smem_attr((const void*)k_march3d<true, MODE, 3>, sm));
+    k_march3d<true, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+  } else if (minb == 2) {
+    HH_CUDA_TRY(smem_attr((const void*)k_march3d<false, MODE, 2>, sm));
+    k_march3d<false, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+  } else {
+    HH_CUDA_TRY(smem_attr((const void*)k_march3d<false, MODE, 3>, sm));
+    k_march3d<false, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+  }
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
 hh_status fine_apply3d(const Level& L, int B, const int* st, int op, VArg x, VArg y, VArg sub,
                        cudaStream_t s) {
   const F3 P = make3(L, 0, st, 0);
+  if (g_march) return march3<M_APPLY>(L, P, B, x, VArg(), SArg(), VArg(), sub, y, op != HH_OP_A0, s);
   const dim3 g = grid3(P, B), bl(BX, BY);
   if (L.het) {
     if (op == HH_OP_A0) k_apply3d<true, false><<<g, bl, 0, s>>>(P, x, y, sub);
@@ -382,6 +723,7 @@ hh_status fine_apply3d(const Level& L, int B, const int* st, int op, VArg x, VAr
 
 static hh_status jac3(const Level& L, const F3& P, int B, VArg f, SArg fs, VArg u, VArg uo,
                       cudaStream_t s) {
+  if (g_march && u.p) return march3<M_JAC>(L, P, B, u, f, fs, VArg(), VArg(), uo, true, s);
   const dim3 g = grid3(P, B), bl(BX, BY);
   if (L.het) k_jacobi3d<true><<<g, bl, 0, s>>>(P, f, fs, u, uo);
   else k_jacobi3d<false><<<g, bl, 0, s>>>(P, f, fs, u, uo);
@@ -408,7 +750,8 @@ hh_status fine_pre3d(const Level& L, int B, const int* st, int nu, double omega,
   }
   const F3 Pr = make3(L, omega, st, std::max(L.G - nu, 0));
   const dim3 g = grid3(Pr, B), bl(BX, BY);
-  if (L.het) k_resid3d<true><<<g, bl, 0, s>>>(Pr, f, fs, u, t1);
+  if (g_march) HH_TRY(march3<M_RES>(L, Pr, B, u, f, fs, VArg(), VArg(), t1, true, s));
+  else if (L.het) k_resid3d<true><<<g, bl, 0, s>>>(Pr, f, fs, u, t1);
   else k_resid3d<false><<<g, bl, 0, s>>>(Pr, f, fs, u, t1);
   const int NC1 = L.n / 2 + 1;
   const int cspan = L.maxloc / 2 + 1;
@@ -429,6 +772,19 @@ hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega
   const dim3 bl(BX, BY);
   // the nu post-steps must end in z: pick the prolongation target accordingly
   VArg bufs[2] = {t0, z};
+  if (g_march) {
+    // prolongation fused into the first post-smoothing step (x + I e_c formed on load)
+    int cur = (nu % 2 == 1) ? 1 : 0;   // first destination: the nu steps end in z
+    HH_TRY(march3<M_JACP>(L, make3(L, omega, st, std::max(e0 - 1, 0)), B, u, f, fs, ec, VArg(), bufs[cur],
+                          true, s));
+    for (int k = 2; k <= nu; ++k) {
+      HH_TRY(jac3(L, make3(L, omega, st, std::max(e0 - k, 0)), B, f, fs, bufs[cur], bufs[cur ^ 1], s));
+      cur ^= 1;
+    }
+    if (w.p) HH_TRY(fine_apply3d(L, B, st, HH_OP_A0, z, w, VArg(), s));
+    HH_CUDA_TRY(cudaGetLastError());
+    return HH_OK;
+  }
   int cur = (nu % 2 == 0) ? 1 : 0;
   k_prolong3d<<<grid3(Pp, B), bl, 0, s>>>(Pp, u, ec, bufs[cur]);
   for (int k = 1; k <= nu; ++k) {

@@ -260,6 +260,22 @@ hh_status get_plan(int dim, int m, NDPlan** out) {
   return HH_OK;
 }
 
+// rank views of distributed (slab-aligned) coarse trees, per (device, dim, m, bounds, rank)
+std::map<std::tuple<int, int, int, std::vector<int>, int>, NDPlan*> g_dplans;
+hh_status get_dist_plan(int dim, int m, const std::vector<int>& Zc, int rank, NDPlan** out) {
+  int dev = 0;
+  HH_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto key = std::make_tuple(dev, dim, m, Zc, rank);
+  auto it = g_dplans.find(key);
+  if (it != g_dplans.end()) { *out = it->second; return HH_OK; }
+  NDPlan* p = nullptr;
+  HH_TRY(nd_plan_create_dist(dim, m, Zc, rank, &p));
+  g_dplans[key] = p;
+  *out = p;
+  return HH_OK;
+}
+
 enum { T_PRE = 0, T_COARSE, T_POST, T_KRYLOV, T_NT };
 
 struct BatchSpec {
@@ -274,6 +290,7 @@ struct BatchSpec {
   int slabs_total = 1, slab_first = 0;
   Comm* comm = nullptr;
   int shift_map = 0;                     // > 0: sigma = sigma_p(k_e, log2 n) of Table 1 row p
+  bool dist = false;                     // slab mode: distributed coarse solve (HH_COARSE_ND_DIST)
 };
 
 // fine-vector layout of a batch: G ghost planes, entry stride, slab bounds
@@ -315,7 +332,10 @@ struct Engine {
   bool conc = false;         // runs beside other sweep workers (ND schedule choice)
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
-      cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp;
+      cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp, dscratch, dflag, dstage;
+  // distributed coarse solve: one rank view per entry (factor, packed S, work per view)
+  std::vector<NDDistView> dviews;
+  std::vector<Pool> dF, dS, dW;
   int* h_status = nullptr;   // pinned
   int h_cap = 0;
   // batch
@@ -357,14 +377,16 @@ struct Engine {
   // return every pool to the device block cache (the engine itself is reused)
   void release_pools() {
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
-                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp};
+                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp,
+                   &dscratch, &dflag, &dstage};
     for (Pool* p : all) p->release();
+    for (auto* vp : {&dF, &dS, &dW})
+      for (Pool& p : *vp) p.release();
+    dviews.clear();
   }
   ~Engine() {
     drop_graphs();
-    Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
-                   &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp};
-    for (Pool* p : all) p->release();
+    release_pools();
     if (h_status) cudaFreeHost(h_status);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (s) cudaStreamDestroy(s);
@@ -416,7 +438,7 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   const int64_t N = FL.stride, Nc = ipow(n / 2 + 1, dim);
   const int Bf = sp.slabmode ? 1 : B;
   NDPlan* P = nullptr;
-  HH_TRY(get_plan(dim, n / 2 + 1, &P));
+  if (!sp.dist) HH_TRY(get_plan(dim, n / 2 + 1, &P));   // distributed: rank views (dist_setup)
   const int S = dim == 2 ? 9 : 27;
   const int nblk = krylov_blocks((int64_t)FL.maxloc * FL.plane);
   // fine vectors: B entries of N (ghosted, padded) nodes + 16 nodes of slack for the lead pad
@@ -430,12 +452,14 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   HH_TRY(E.rc.ensure((size_t)B * Nc * 16));
   HH_TRY(E.ec.ensure((size_t)B * Nc * 16));
   HH_TRY(E.stc.ensure((size_t)Bf * Nc * S * 16));
-  HH_TRY(E.F.ensure((size_t)Bf * nd_front_entries(P) * 16));
-  HH_TRY(E.cbuf.ensure((size_t)Bf * nd_cbuf_entries(P) * 16));
+  if (P) HH_TRY(E.F.ensure((size_t)Bf * nd_front_entries(P) * 16));
+  if (P) HH_TRY(E.cbuf.ensure((size_t)Bf * nd_cbuf_entries(P) * 16));
   HH_TRY(E.slabp.ensure((size_t)B * sizeof(int2)));
   if (sp.comm) HH_TRY(E.hstage.ensure((size_t)4 * FL.G * FL.plane * 16));
-  HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
-  HH_TRY(nd_flow_reset(P, B, E.work.as<cplx>(), E.s));
+  if (P) {
+    HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
+    HH_TRY(nd_flow_reset(P, B, E.work.as<cplx>(), E.s));
+  }
   HH_TRY(E.kcf.ensure((size_t)B * 16));
   HH_TRY(E.kcc.ensure((size_t)B * 16));
   HH_TRY(E.cpart.ensure((size_t)B * nblk * (m + 2) * 16));
@@ -461,6 +485,50 @@ static void prof_mark(Engine& E, const char* what, double& t) {
   t = t1;
 }
 
+// distributed coarse solve: the rank views of this process' entries (slab k =
+// rank slab_first + k) of the slab-aligned tree over the coarse planes of the
+// fine slab bounds, with their factor / packed-S / work pools; the pivot-column
+// + workspace scratch is shared by the views (they run one after another)
+hh_status dist_setup(Engine& E, const BatchSpec& sp) {
+  const int m = sp.n / 2 + 1, P = sp.slabs_total;
+  const std::vector<int> z = slab_bounds(sp.n, P);
+  std::vector<int> Zc(P + 1);
+  for (int k = 0; k < P; ++k) Zc[k] = z[k] / 2;
+  Zc[P] = m;
+  E.dviews.assign(sp.B, NDDistView());
+  E.dF.resize(sp.B);
+  E.dS.resize(sp.B);
+  E.dW.resize(sp.B);
+  int64_t scratch = 1, stage = 1;
+  for (int b = 0; b < sp.B; ++b) {
+    NDPlan* p = nullptr;
+    HH_TRY(get_dist_plan(sp.dim, m, Zc, sp.slab_first + b, &p));
+    scratch = std::max(scratch, nd_dist_scratch_entries(p));
+    stage = std::max(stage, nd_dist_stage_entries(p));
+    HH_TRY(E.dF[b].ensure((size_t)std::max<int64_t>(1, nd_front_entries(p)) * 16));
+    HH_TRY(E.dS[b].ensure((size_t)nd_dist_s_entries(p) * 16));
+    HH_TRY(E.dW[b].ensure((size_t)nd_work_entries(p) * 16));
+    E.dviews[b].plan = p;
+    if (getenv("HH_DEBUG"))
+      fprintf(stderr, "[hh dist] rank %d/%d: factor %.3f GB, packed S %.3f GB, work %.3f GB, scratch %.3f GB\n",
+              sp.slab_first + b, P, 16e-9 * nd_front_entries(p), 16e-9 * nd_dist_s_entries(p),
+              16e-9 * nd_work_entries(p), 16e-9 * nd_dist_scratch_entries(p));
+  }
+  HH_TRY(E.dscratch.ensure((size_t)scratch * 16));
+  HH_TRY(E.dstage.ensure((size_t)stage * 16));
+  HH_TRY(E.dflag.ensure((size_t)sp.B * sizeof(int)));
+  for (int b = 0; b < sp.B; ++b) {
+    NDDistView& v = E.dviews[b];
+    v.F = E.dF[b].as<cplx>();
+    v.S = E.dS[b].as<cplx>();
+    v.work = E.dW[b].as<cplx>();
+    v.scratch = E.dscratch.as<cplx>();
+    v.flag = E.dflag.as<int>() + b;
+  }
+  E.plan = E.dviews[0].plan;
+  return HH_OK;
+}
+
 hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   const double t0 = now_s();
   double tp = t0;
@@ -482,7 +550,8 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
                      n, sp.slabs_total);
         return HH_E_CONFIG;
       }
-  HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
+  if (sp.dist) HH_TRY(dist_setup(E, sp));
+  else HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
   const NDPlan* P = E.plan;
   // pools
   HH_TRY(reserve_pools(E, sp));
@@ -618,15 +687,30 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   }
   // coarse operator + factorisation (slab mode: one copy, shared by the slabs)
   HH_TRY(coarse_stencil(E.LC, E.Bf, E.stc.as<cplx>(), E.s));
-  HH_TRY(nd_factor(P, E.Bf, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
-  prof_mark(E, "factor", tp);
-  HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
-  HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
-                     varg(E.ec.as<cplx>(), Nc), E.s, sp.slabmode, E.conc));
-  prof_mark(E, "autotune", tp);
-  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, E.nd_flag, E.Bf * sizeof(int), cudaMemcpyDeviceToHost, E.s));
+  int nflag = E.Bf;
+  const int* flags = E.nd_flag;
+  if (sp.dist) {   // each rank view factors its own fronts; S blocks move to the parents' owners
+    HH_TRY(nd_dist_factor(E.dviews, E.stc.as<cplx>(), sp.comm, E.s));
+    nflag = B;
+    flags = E.dflag.as<int>();
+    prof_mark(E, "factor", tp);
+  } else {
+    HH_TRY(nd_factor(P, E.Bf, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
+    prof_mark(E, "factor", tp);
+    HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)B * Nc * 16, E.s));
+    HH_TRY(nd_autotune(P, B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
+                       varg(E.ec.as<cplx>(), Nc), E.s, sp.slabmode, E.conc));
+    prof_mark(E, "autotune", tp);
+  }
+  if (E.h_cap < nflag) {
+    if (E.h_status) cudaFreeHost(E.h_status);
+    E.h_status = nullptr;
+    HH_CUDA_TRY(cudaMallocHost(&E.h_status, nflag * sizeof(int)));
+    E.h_cap = nflag;
+  }
+  HH_CUDA_TRY(cudaMemcpyAsync(E.h_status, flags, nflag * sizeof(int), cudaMemcpyDeviceToHost, E.s));
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
-  for (int b = 0; b < E.Bf; ++b)
+  for (int b = 0; b < nflag; ++b)
     if (E.h_status[b]) {
       hh_set_error("zero pivot in the coarse factorisation (sample %d: k=%g, beta=%g, sigma=%g, h=%g)",
                    b, sp.k.empty() ? 0.0 : sp.k[b], sp.beta[b], sp.sigma[b], E.LC.h);
@@ -645,6 +729,10 @@ VArg vfine(Engine& E, Pool& p) { return varg(p.as<cplx>() + E.FL.pad, E.FL.strid
 bool slab_mode(const Engine& E) { return E.spec.slabmode; }
 // coarse solve on all entries (shared factor in slab mode)
 hh_status coarse_solve_all(Engine& E, const int* st, VArg rhs, VArg x) {
+  if (E.spec.dist) {   // distributed: each entry solves its own fronts, then the owned planes go round
+    HH_TRY(nd_dist_solve(E.dviews, st, rhs, x, E.spec.comm, E.dstage.as<cplx>(), E.s));
+    return slab_coarse_allgather(E.X, x, E.s);
+  }
   return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E), E.conc,
                   E.flow_fail);
 }
@@ -730,7 +818,8 @@ int64_t launches_per_iteration(const Engine& E) {
     slab = 2 * ((E.B > 1 ? 1 : 0) + (multi ? 2 : 0)) + (E.B > 1 ? 1 : 0) + 2;
   }
   const int kry = E.ka.reorth ? 4 + (slab_mode(E) ? 2 * (2 + (E.X.comm && E.X.comm->nranks > 1 ? 2 : 0)) : 0) : 0;
-  return fine + nd_solve_launches(E.plan, E.B, E.conc) + 3 + slab + kry;
+  const int nd = E.spec.dist ? nd_dist_launches(E.dviews) + 2 : nd_solve_launches(E.plan, E.B, E.conc);
+  return fine + nd + 3 + slab + kry;
 }
 
 // two captured variants of one iteration: plain, and with phase events (sampled timing)
@@ -776,7 +865,12 @@ void phase_bytes(const Engine& E, int j, double* out, double* model) {
   const int nu1 = E.spec.nu_pre, nu2 = E.spec.nu_post;
   out[T_PRE] = 32.0 * N + 16.0 * Nc + ce;                  // f, u, r_c (+ coef)
   out[T_POST] = 64.0 * N + 16.0 * Nc + ce;                 // f, u, e_c, z, w (+ coef)
-  out[T_COARSE] = (double)nd_stream_bytes(E.plan) + 32.0 * Nc;
+  double nb = 0;
+  if (E.spec.dist)   // every view streams its own fronts (per problem: the sum over the ranks)
+    for (const NDDistView& v : E.dviews) nb += (double)nd_stream_bytes(v.plan);
+  else
+    nb = (double)nd_stream_bytes(E.plan);
+  out[T_COARSE] = nb + 32.0 * Nc;
   out[T_KRYLOV] = (2.0 * (j + 1) + 3.0) * 16.0 * N;        // mdot + update
   if (E.ka.reorth == 2) out[T_KRYLOV] *= 2.0;              // second pass every step
   // Jacobi from zero 32 + c, Jacobi 48 + c, residual + restrict 32 + c + share
@@ -1027,8 +1121,16 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   if (d->max_restart < 1 || d->max_restart > 127) { hh_set_error("max_restart must be in 1..127"); return HH_E_CONFIG; }
   if (!(d->beta >= 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
   if (d->shift_map < 0 || d->shift_map > 3) { hh_set_error("shift_map must be 0..3"); return HH_E_CONFIG; }
+  if (d->coarse_solver < HH_COARSE_AUTO || d->coarse_solver > HH_COARSE_ND_DIST) {
+    hh_set_error("coarse_solver must be HH_COARSE_AUTO, HH_COARSE_ND or HH_COARSE_ND_DIST");
+    return HH_E_CONFIG;
+  }
   const int nloc = std::max(1, d->nslabs_local);
   const bool use_nccl = d->nccl_id != nullptr;
+  if (d->coarse_solver == HH_COARSE_ND_DIST && !(use_nccl ? d->nranks > 1 : nloc > 1)) {
+    hh_set_error("HH_COARSE_ND_DIST needs a slab decomposition (nslabs_local > 1 or nranks > 1)");
+    return HH_E_CONFIG;
+  }
   if (use_nccl && (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks || nloc != 1)) {
     hh_set_error("NCCL slab mode needs 0 <= rank < nranks and nslabs_local <= 1");
     return HH_E_CONFIG;
@@ -1060,6 +1162,7 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
     sp.k.assign(sp.B, d->k_const); sp.beta.assign(sp.B, d->beta); sp.sigma.assign(sp.B, d->sigma);
     sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
     sp.shift_map = d->shift_map;
+    sp.dist = d->coarse_solver == HH_COARSE_ND_DIST;
     st = enter(*p->ep, p->user);
     if (st == HH_OK) st = batch_setup(*p->ep, sp);
   }
@@ -1127,7 +1230,7 @@ extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   HH_TRY(fine_post(E.LF, E.B, nullptr, E.spec.nu_post, E.spec.omega, vfine(E, E.bv), SArg(),
                    vfine(E, E.u), vflat(E.ec, E.Nc), vfine(E, E.xv), VArg(), E.s));
   HH_TRY(user_out(E, E.xv, z));
-  HH_TRY(flow_check(E, nd_solve_uses_flow(E.plan, E.B, E.conc)));
+  HH_TRY(flow_check(E, !E.spec.dist && nd_solve_uses_flow(E.plan, E.B, E.conc)));
   return leave(E, p->user);
 }
 
@@ -1135,6 +1238,13 @@ extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
   if (!p || !r || !e) { hh_set_error("NULL argument"); return HH_E_ARG; }
   Engine& E = *p->ep;
   HH_TRY(enter(E, p->user));
+  if (E.spec.dist) {   // r -> every entry, distributed solve + owned-plane allgather, entry 0 -> e
+    for (int b = 0; b < E.B; ++b)
+      HH_CUDA_TRY(cudaMemcpyAsync(E.rc.as<cplx>() + (int64_t)b * E.Nc, r, E.Nc * 16, cudaMemcpyDeviceToDevice, E.s));
+    HH_TRY(coarse_solve_all(E, nullptr, vflat(E.rc, E.Nc), vflat(E.ec, E.Nc)));
+    HH_CUDA_TRY(cudaMemcpyAsync(e, E.ec.p, E.Nc * 16, cudaMemcpyDeviceToDevice, E.s));
+    return leave(E, p->user);
+  }
   HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
                   varg((cplx*)e, 0), E.s, true, false, E.flow_fail));
   HH_TRY(flow_check(E, nd_solve_uses_flow(E.plan, 1, false)));
@@ -1327,7 +1437,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   const char* eb = getenv("HH_SWEEP_MAX_BATCH");
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
   const char* en = getenv("HH_SWEEP_NODES");
-  const double node_budget = en ? atof(en) : 1.2e6;
+  const double node_budget = en ? atof(en) : 2.4e6;   // A/B: 1.2e6 -> 2.4e6 = +1.5% (profiles/r02/sweep_ab)
   // device memory size, queried once per device (cudaMemGetInfo takes driver locks
   // that can stall for tens of ms)
   static std::mutex tot_mu;
@@ -1397,16 +1507,29 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     for (const BatchSpec& sp : specs) HH_TRY(reserve_pools(*E, sp));
   // ND solve schedule per (grid, batch size), timed once on an idle GPU (zero
   // factor: the schedule depends on sizes only), then cached in the shared tree
+  // (HH_ND_TUNE_CONC=1: time the candidates on all worker streams at once --
+  // throughput under concurrency -- instead of in isolation; measured slower:
+  // 2.97 vs 2.80 s per sweep step)
   {
+    static const bool tune_conc = getenv("HH_ND_TUNE_CONC") && atoi(getenv("HH_ND_TUNE_CONC")) != 0;
     Engine& E = *engines[0];
     for (const BatchSpec& sp : specs) {
       NDPlan* P = nullptr;
       HH_TRY(get_plan(2, sp.n / 2 + 1, &P));
       const int64_t Nc = ipow(sp.n / 2 + 1, 2);
-      HH_CUDA_TRY(cudaMemsetAsync(E.F.p, 0, (size_t)sp.B * nd_front_entries(P) * 16, E.s));
-      HH_CUDA_TRY(cudaMemsetAsync(E.rc.p, 0, (size_t)sp.B * Nc * 16, E.s));
+      std::vector<NDTuneCtx> multi;
+      for (Engine* Ek : engines) {
+        HH_CUDA_TRY(cudaMemsetAsync(Ek->F.p, 0, (size_t)sp.B * nd_front_entries(P) * 16, Ek->s));
+        HH_CUDA_TRY(cudaMemsetAsync(Ek->rc.p, 0, (size_t)sp.B * Nc * 16, Ek->s));
+        HH_TRY(nd_flow_reset(P, sp.B, Ek->work.as<cplx>(), Ek->s));
+        multi.push_back({Ek->F.as<cplx>(), Ek->work.as<cplx>(), varg(Ek->rc.as<cplx>(), Nc),
+                         varg(Ek->ec.as<cplx>(), Nc), Ek->s});
+        if (!(tune_conc && E.conc)) break;
+      }
+      for (Engine* Ek : engines) HH_CUDA_TRY(cudaStreamSynchronize(Ek->s));
       HH_TRY(nd_autotune(P, sp.B, E.F.as<cplx>(), E.work.as<cplx>(), varg(E.rc.as<cplx>(), Nc),
-                         varg(E.ec.as<cplx>(), Nc), E.s, false, E.conc));
+                         varg(E.ec.as<cplx>(), Nc), E.s, false, E.conc,
+                         (tune_conc && E.conc && multi.size() > 1) ? &multi : nullptr));
     }
     HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   }

@@ -161,10 +161,44 @@ hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* 
 // nd_flow_reset the counters and nd_flow_disable the schedule.
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                    VArg x, cudaStream_t s, bool shareF = false, bool conc = false, int* fail = nullptr);
+// ---- distributed coarse solve (slab-aligned ND; SURVEY.md 8(e) second version)
+struct Comm;
+struct NDDistView {            // one rank's part, held by this process
+  NDPlan* plan = nullptr;      // rank view (nd_plan_create_dist)
+  cplx* F = nullptr;           // nd_front_entries(plan): this rank's [X | H] rows
+  cplx* scratch = nullptr;     // nd_dist_scratch_entries(plan): pivot columns | workspace (shareable)
+  cplx* S = nullptr;           // nd_dist_s_entries(plan): packed Schur complements
+  cplx* work = nullptr;        // nd_work_entries(plan): solve vectors
+  int* flag = nullptr;         // zero-pivot flag
+};
+// Zc: P + 1 coarse plane bounds of the slowest axis (slab k owns [Zc[k], Zc[k+1]))
+hh_status nd_plan_create_dist(int dim, int m, const std::vector<int>& Zc, int rank, NDPlan** out);
+// V: the rank views of this process (all P in-process, or one with an NCCL comm);
+// st: the coarse stencil of the whole grid (each rank assembles its own fronts)
+hh_status nd_dist_factor(std::vector<NDDistView>& V, const cplx* st, Comm* comm, cudaStream_t s);
+// rhs / x: entry k = view k (full coarse vectors, rhs complete in every entry); on
+// return x holds the solution on view k's own fronts and on every interface plane,
+// i.e. on its own coarse planes [Zc[r], Zc[r+1]).  stage: nd_dist_stage_entries.
+hh_status nd_dist_solve(std::vector<NDDistView>& V, const int* st, VArg rhs, VArg x, Comm* comm, cplx* stage,
+                        cudaStream_t s);
+int64_t nd_dist_stage_entries(const NDPlan* p);
+int64_t nd_dist_scratch_entries(const NDPlan* p);
+int64_t nd_dist_s_entries(const NDPlan* p);
+int nd_dist_launches(const std::vector<NDDistView>& V);
+// transport of the distributed solve (comm.cu): grouped NCCL point-to-point / broadcast
+hh_status comm_group(bool start);
+hh_status comm_send(Comm* c, const void* buf, size_t bytes, int peer, cudaStream_t s);
+hh_status comm_recv(Comm* c, void* buf, size_t bytes, int peer, cudaStream_t s);
+hh_status comm_bcast(Comm* c, void* buf, size_t bytes, int root, cudaStream_t s);
+
 // true if nd_solve(p, B, ..., conc) runs the dataflow kernels
 bool nd_solve_uses_flow(const NDPlan* p, int B, bool conc);
 // never use the dataflow schedule for this tree again (after a failure)
 void nd_flow_disable(const NDPlan* p);
-// choose the solve schedule for batch size B by timing candidates on the real factor
+// choose the solve schedule for batch size B by timing candidates on the real factor;
+// multi != NULL (concurrent sweep workers): time every candidate on all the given
+// streams at once (throughput under concurrency instead of isolated latency)
+struct NDTuneCtx { const cplx* F; cplx* work; VArg rhs, x; cudaStream_t s; };
 hh_status nd_autotune(const NDPlan* p, int B, const cplx* F, cplx* work, VArg rhs, VArg x,
-                      cudaStream_t s, bool shareF = false, bool conc = false);
+                      cudaStream_t s, bool shareF = false, bool conc = false,
+                      const std::vector<NDTuneCtx>* multi = nullptr);

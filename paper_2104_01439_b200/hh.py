@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")
 
 HH_OP_A0, HH_OP_AEPS, HH_OP_AEPS_COARSE = 0, 1, 2
-HH_COARSE_AUTO, HH_COARSE_ND = 0, 1
+HH_COARSE_AUTO, HH_COARSE_ND, HH_COARSE_ND_DIST = 0, 1, 2
 STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_CUDA",
           5: "HH_E_NCCL", 6: "HH_E_OOM", 7: "HH_E_SINGULAR", 8: "HH_E_BREAKDOWN",
           9: "HH_E_DIVERGED", 10: "HH_E_STATE"}
@@ -26,7 +26,7 @@ EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "h
            "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
            "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
            "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_lfa_rho", "hh_lfa_sigma_c", "hh_lfa_stats",
-           "hh_arnoldi_orthogonality", "hh_last_error", "hh_version"]
+           "hh_arnoldi_orthogonality", "hh_fp64_peak", "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -118,6 +118,7 @@ def _load():
                      C.POINTER(SampleResult)],
         "hh_destroy_problem": [vp],
         "hh_arnoldi_orthogonality": [vp, dp, C.POINTER(C.c_int32)],
+        "hh_fp64_peak": [i32, dp, dp],
         "hh_reset_timers": [vp, i32],
         "hh_read_timers": [vp, dp, C.POINTER(C.c_int64)],
         "hh_sweep_timers": [i32, dp, C.POINTER(C.c_int64)],
@@ -161,11 +162,13 @@ class Problem:
 
     def __init__(self, dim, n_cells, k_const=0.0, k_elem=None, k_elem_coarse=None, beta=1.0,
                  sigma=1.5, nu_pre=2, nu_post=2, omega=0.6, max_restart=100, device=None,
-                 nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None, shift_map=0):
+                 nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None, shift_map=0,
+                 coarse_solver=HH_COARSE_ND):
         """nslabs_local > 1: the solve is cut into that many slabs held by this
         process; nccl_id (from nccl_unique_id(), shared by all ranks): this
         process holds slab `rank` of `nranks` (one GPU per process).  Vectors
-        then hold this handle's owned planes (local_layout())."""
+        then hold this handle's owned planes (local_layout()).  coarse_solver =
+        HH_COARSE_ND_DIST distributes the coarse factor over the slabs."""
         self.handle = C.c_void_p()
         dev = torch.cuda.current_device() if device is None else device
         d = ProblemDesc()
@@ -180,7 +183,7 @@ class Problem:
             d.k_elem = kf.ctypes.data_as(C.POINTER(C.c_double))
             d.k_elem_coarse = kc.ctypes.data_as(C.POINTER(C.c_double))
         d.beta, d.sigma, d.nu_pre, d.nu_post, d.omega = beta, sigma, nu_pre, nu_post, omega
-        d.coarse_solver = HH_COARSE_ND
+        d.coarse_solver = coarse_solver
         d.device = dev
         d.stream = _stream()
         d.max_restart = max_restart
@@ -375,6 +378,14 @@ def sweep_timers(reset_enable=-1):
     nl = C.c_int64()
     _check(lib.hh_sweep_timers(reset_enable, st, C.byref(nl)))
     return _phase_dict(st, nl.value)
+
+
+def fp64_peak(device=None):
+    """(measured FP64 TFLOP/s, nominal SM MHz) from the DFMA microbenchmark."""
+    t, mhz = C.c_double(), C.c_double()
+    dev = torch.cuda.current_device() if device is None else device
+    _check(lib.hh_fp64_peak(dev, C.byref(t), C.byref(mhz)))
+    return t.value, mhz.value
 
 
 def version():
