@@ -55,14 +55,38 @@ __device__ __forceinline__ double2 coef3(const F3& P, const double2* cf, double2
 }
 
 // row of A x at node (gx, gy, gz) reading x from global memory
-template <bool HET, bool EPS>
-__device__ cplx row3(const F3& P, const cplx* __restrict__ x, const double2* cf, double2 kc,
-                     int gx, int gy, int gz) {
+// x values through an accessor: plain loads, or (first post-smoothing step of the
+// z-marching path's boundary nodes) u + I e_c formed on the fly
+struct LdgAcc {
+  const cplx* x;
+  __device__ __forceinline__ cplx operator()(int64_t i, int, int, int) const { return __ldg(&x[i]); }
+};
+struct ProlongAcc {   // u + I e_c at fine node (gx, gy, gz) (trilinear I, weights 1, 1/2, 1/4, 1/8)
+  const cplx* u;
+  const cplx* ec;
+  int NC1;
+  __device__ __forceinline__ cplx operator()(int64_t i, int gx, int gy, int gz) const {
+    cplx v = __ldg(&u[i]);
+    const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
+    const double w = ((gx & 1) ? 0.5 : 1.0) * ((gy & 1) ? 0.5 : 1.0) * ((gz & 1) ? 0.5 : 1.0);
+    for (int k = 0; k <= (gz & 1); ++k)
+      for (int j = 0; j <= (gy & 1); ++j)
+        for (int q = 0; q <= (gx & 1); ++q) {
+          const cplx c = __ldg(&ec[((int64_t)(cz0 + k) * NC1 + cy0 + j) * NC1 + cx0 + q]);
+          v.x += w * c.x;
+          v.y += w * c.y;
+        }
+    return v;
+  }
+};
+
+template <bool HET, bool EPS, typename ACC = LdgAcc>
+__device__ cplx row3(const F3& P, ACC acc, const double2* cf, double2 kc, int gx, int gy, int gz) {
   const int n = P.n, N1 = P.N1;
   const double h = P.h;
   const int64_t gi = ((int64_t)gz * N1 + gy) * N1 + gx;
   auto X = [&](int dx, int dy, int dz) {
-    return __ldg(&x[gi + ((int64_t)dz * N1 + dy) * N1 + dx]);
+    return acc(gi + ((int64_t)dz * N1 + dy) * N1 + dx, gx + dx, gy + dy, gz + dz);
   };
   const cplx xp = X(0, 0, 0);
   const double hk = h / 36.0, hm = h * h * h / 216.0;
@@ -185,7 +209,7 @@ __global__ void __launch_bounds__(BX * BY) k_apply3d(F3 P, VArg x, VArg y, VArg 
   if (P.st && P.st[b]) return;
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
-  cplx ax = row3<HET, EPS>(P, x.at(b) - vo, cf, kc, gx, gy, gz);
+  cplx ax = row3<HET, EPS>(P, LdgAcc{x.at(b) - vo}, cf, kc, gx, gy, gz);
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
   if (sub.p) ax = csub((sub.at(b) - vo)[gi], ax);
   (y.at(b) - vo)[gi] = ax;
@@ -207,7 +231,7 @@ __global__ void __launch_bounds__(BX * BY) k_jacobi3d(F3 P, VArg f, SArg fs, VAr
   cplx v;
   if (u.p) {
     const cplx* ub = u.at(b) - vo;
-    const cplx ax = row3<HET, true>(P, ub, cf, kc, gx, gy, gz);
+    const cplx ax = row3<HET, true>(P, LdgAcc{ub}, cf, kc, gx, gy, gz);
     v = ub[gi];
     cfma(v, cscale(di, P.omega), csub(fv, ax));
   } else {
@@ -226,7 +250,7 @@ __global__ void __launch_bounds__(BX * BY) k_resid3d(F3 P, VArg f, SArg fs, VArg
   const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const int64_t gi = ((int64_t)gz * P.N1 + gy) * P.N1 + gx;
-  const cplx ax = row3<HET, true>(P, u.at(b) - vo, cf, kc, gx, gy, gz);
+  const cplx ax = row3<HET, true>(P, LdgAcc{u.at(b) - vo}, cf, kc, gx, gy, gz);
   (r.at(b) - vo)[gi] = csub(cscale(__ldg(&(f.at(b) - vo)[gi]), fs.at(b)), ax);
 }
 
@@ -374,6 +398,15 @@ constexpr int MTX = 32, MTY = 8, MT = MTX * MTY;
 constexpr int NPX = MTX + 2, NPY = MTY + 2, NPL = NPX * NPY;   // node plane with halo
 constexpr int EPX = MTX + 1, EPY = MTY + 1, EPL = EPX * EPY;   // element plane
 constexpr int NRING = 4, ERING = 3;
+
+// 16-byte asynchronous global -> shared copy (zero-fill when !valid)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 enum { M_APPLY = 0, M_JAC = 1, M_JACP = 2, M_RES = 3 };
 
 struct MarchSmem {
@@ -381,84 +414,22 @@ struct MarchSmem {
   double2 c[ERING][EPL];
 };
 
-// boundary node of the z-marching kernels (element loop + boundary faces of
-// row3 / diag3 on the staged planes; kept out of line: it is rare and would
-// otherwise raise the register count of the interior path)
-template <bool HET>
-__device__ __noinline__ void boundary3(const cplx* U0, const cplx* U1, const cplx* U2, const double2* Cb,
-                                       const double2* Ca, int ci, int gx, int gy, int t, int x0, int y0, int n,
-                                       double h, int eps, double2 kc, cplx& ax, cplx& dg) {
-  const double hm = h * h * h / 216.0;
-  const cplx xc = U1[ci];
-  auto X = [&](int dx, int dy, int dz) {
-    const cplx* U = dz < 0 ? U0 : (dz > 0 ? U2 : U1);
-    return U[ci + dy * NPX + dx];
-  };
-  auto LAM = [&](int ex, int ey, int ez) -> double2 {   // (k_e, eps_e) of element (ex, ey, ez) or 0
-    if (ex < 0 || ex >= n || ey < 0 || ey >= n || ez < 0 || ez >= n) return make_double2(0, 0);
-    if (!HET) return kc;
-    const double2* C = ez < t ? Cb : Ca;
-    return C[(ey - (y0 - 1)) * EPX + ex - (x0 - 1)];
-  };
-  const double hk = h / 36.0;
-  ax = cmake(0, 0);
-  dg = cmake(0, 0);
-  for (int o = 0; o < 8; ++o) {
-    const int dx = (o & 1) ? 1 : -1, dy = (o & 2) ? 1 : -1, dz = (o & 4) ? 1 : -1;
-    const int ex = gx + (dx < 0 ? -1 : 0), ey = gy + (dy < 0 ? -1 : 0), ez = t + (dz < 0 ? -1 : 0);
-    if (ex < 0 || ex >= n || ey < 0 || ey >= n || ez < 0 || ez >= n) continue;
-    const cplx a1x = X(dx, 0, 0), a1y = X(0, dy, 0), a1z = X(0, 0, dz);
-    const cplx a2xy = X(dx, dy, 0), a2xz = X(dx, 0, dz), a2yz = X(0, dy, dz);
-    const cplx a3 = X(dx, dy, dz);
-    const cplx s1 = cmake(a1x.x + a1y.x + a1z.x, a1x.y + a1y.y + a1z.y);
-    const cplx s2 = cmake(a2xy.x + a2xz.x + a2yz.x, a2xy.y + a2xz.y + a2yz.y);
-    const cplx kp = cmake(hk * (12.0 * xc.x - 3.0 * s2.x - 3.0 * a3.x), hk * (12.0 * xc.y - 3.0 * s2.y - 3.0 * a3.y));
-    const cplx mp = cmake(hm * (8.0 * xc.x + 4.0 * s1.x + 2.0 * s2.x + a3.x),
-                          hm * (8.0 * xc.y + 4.0 * s1.y + 2.0 * s2.y + a3.y));
-    const double2 c = LAM(ex, ey, ez);
-    const cplx lam = cmake(c.x * c.x, eps ? c.y : 0.0);
-    ax = cadd(ax, kp);
-    cfms(ax, lam, mp);
-    dg.x += h / 3.0 - 8.0 * hm * lam.x;
-    dg.y -= 8.0 * hm * lam.y;
-  }
-  const double hb = h * h / 36.0;
-  const int g3[3] = {gx, gy, t};
-  for (int a = 0; a < 3; ++a) {
-    if (g3[a] != 0 && g3[a] != n) continue;
-    const int ea = g3[a] == 0 ? 0 : n - 1;
-    const int u = (a + 1) % 3, v = (a + 2) % 3;
-    for (int q = 0; q < 4; ++q) {
-      const int du = (q & 1) ? 1 : -1, dv = (q & 2) ? 1 : -1;
-      const int eu = g3[u] + (du < 0 ? -1 : 0), ev = g3[v] + (dv < 0 ? -1 : 0);
-      if (eu < 0 || eu >= n || ev < 0 || ev >= n) continue;
-      int e3i[3], d_u[3] = {0, 0, 0}, d_v[3] = {0, 0, 0};
-      e3i[a] = ea; e3i[u] = eu; e3i[v] = ev;
-      d_u[u] = du; d_v[v] = dv;
-      const double k = LAM(e3i[0], e3i[1], e3i[2]).x;
-      const cplx xu = X(d_u[0], d_u[1], d_u[2]), xv = X(d_v[0], d_v[1], d_v[2]);
-      const cplx xd = X(d_u[0] + d_v[0], d_u[1] + d_v[1], d_u[2] + d_v[2]);
-      const cplx sb = cmake(hb * (4.0 * xc.x + 2.0 * (xu.x + xv.x) + xd.x),
-                            hb * (4.0 * xc.y + 2.0 * (xu.y + xv.y) + xd.y));
-      ax.x += k * sb.y;   // -i k B
-      ax.y -= k * sb.x;
-      dg.y -= 4.0 * hb * k;
-    }
-  }
-}
-
+// Interior nodes only (x, y, z in 1..n-1): the tiles start at x0 = 1 + 32 i,
+// y0 = 1 + 8 j and march the interior planes of the entry's range; the domain
+// boundary faces (2-3% of the nodes: the absorbing-boundary terms and the
+// partial element sets) are computed by k_bnd3d below.
 template <bool HET, int MODE, int MINB>
 __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out,
-                                                   int eps, int zlen, int nzc) {
+                                                     int eps, int zlen, int nzc) {
   extern __shared__ double4 smem_raw[];
   MarchSmem& S = *reinterpret_cast<MarchSmem*>(smem_raw);
   const int n = P.n, N1 = P.N1;
   const int tid = threadIdx.x, tx = tid % MTX, ty = tid / MTX;
-  const int x0 = blockIdx.x * MTX, y0 = blockIdx.y * MTY;
+  const int x0 = 1 + blockIdx.x * MTX, y0 = 1 + blockIdx.y * MTY;
   const int b = blockIdx.z / nzc, chunk = blockIdx.z % nzc;
   if (P.st && P.st[b]) return;
   const int2 sl = slab_of(P.slab, b, n);
-  const int zlo = max(0, sl.x - P.ext), zhi = min(N1, sl.y + P.ext);
+  const int zlo = max(1, sl.x - P.ext), zhi = min(n, sl.y + P.ext);   // interior planes
   const int zs = zlo + chunk * zlen, ze = min(zhi, zs + zlen);
   if (zs >= ze) return;
   const int64_t vo = (int64_t)(sl.x - P.G) * N1 * N1;
@@ -467,74 +438,106 @@ __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg
   const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
   const int NC1 = n / 2 + 1;
   const cplx* eb = MODE == M_JACP ? ec.at(b) : nullptr;
-  // ---- staging: node plane gz (x or x + I e_c) and element plane ez
-  cplx rn[2];
-  double2 rc[2];
-  auto fetch = [&](int gz, int ez) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int q = tid + k * MT;
-      rn[k] = cmake(0, 0);
-      if (q < NPL && gz >= 0 && gz <= n) {
-        const int gx = x0 - 1 + q % NPX, gy = y0 - 1 + q / NPX;
-        if (gx >= 0 && gx <= n && gy >= 0 && gy <= n) {
-          cplx v = __ldg(&xb[((int64_t)gz * N1 + gy) * N1 + gx]);
-          if (MODE == M_JACP) {   // trilinear prolongation of the coarse correction (Alg. 1 line 4)
-            const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
-            const double w = ((gx & 1) ? 0.5 : 1.0) * ((gy & 1) ? 0.5 : 1.0) * ((gz & 1) ? 0.5 : 1.0);
-            for (int kk = 0; kk <= (gz & 1); ++kk)
-              for (int j = 0; j <= (gy & 1); ++j)
-                for (int i = 0; i <= (gx & 1); ++i) {
-                  const cplx c = __ldg(&eb[((int64_t)(cz0 + kk) * NC1 + cy0 + j) * NC1 + cx0 + i]);
-                  v.x += w * c.x;
-                  v.y += w * c.y;
-                }
-          }
-          rn[k] = v;
-        }
-      }
-      if (HET) {
-        rc[k] = make_double2(0, 0);
-        if (q < EPL && ez >= 0 && ez < n) {
-          const int ex = x0 - 1 + q % EPX, ey = y0 - 1 + q / EPX;
-          if (ex >= 0 && ex < n && ey >= 0 && ey < n) rc[k] = __ldg(&cf[((int64_t)ez * n + ey) * n + ex]);
-        }
-      }
-    }
-  };
-  auto commit = [&](int gz, int ez) {   // node plane gz, element plane ez (between ez and ez + 1)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int q = tid + k * MT;
-      if (q < NPL) S.u[(gz + NRING) % NRING][q] = rn[k];
-      if (HET && q < EPL) S.c[(ez + ERING) % ERING][q] = rc[k];
-    }
-  };
-  // prologue: node planes zs - 1, zs and element plane zs - 1 in shared memory,
-  // node plane zs + 1 / element plane zs in registers
-  fetch(zs - 1, zs - 1);
-  commit(zs - 1, zs - 1);
-  fetch(zs, -1);
+  // ---- staging: node plane gz (x or x + I e_c) and element plane ez.  Every
+  // thread stages the same <= 2 node / element slots of each plane: their plane
+  // offsets are computed once, so a plane costs one 64-bit add per load.
+  const int64_t NN = (int64_t)N1 * N1, EE = (int64_t)n * n;
+  int64_t noff[2], eoff[2];
+  int ngx[2], ngy[2];
+  bool nok[2], eok[2];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int q = tid + k * MT;
-    if (q < NPL) S.u[(zs + NRING) % NRING][q] = rn[k];
+    const int qx = q % NPX, qy = q / NPX;
+    ngx[k] = x0 - 1 + qx;
+    ngy[k] = y0 - 1 + qy;
+    nok[k] = q < NPL && ngx[k] <= n && ngy[k] <= n;   // >= 0 by construction
+    noff[k] = (int64_t)ngy[k] * N1 + ngx[k];
+    const int ex = x0 - 1 + q % EPX, ey = y0 - 1 + q / EPX;
+    eok[k] = HET && q < EPL && ex < n && ey < n;
+    eoff[k] = (int64_t)ey * n + ex;
   }
-  fetch(zs + 1, zs);
+  cplx rn[2];
+  double2 rc[2];
+  auto fetch = [&](int gz, int ez) {
+    const cplx* xp = xb + gz * NN;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      rn[k] = cmake(0, 0);
+      if (nok[k]) {
+        cplx v = __ldg(xp + noff[k]);
+        if (MODE == M_JACP) {   // trilinear prolongation of the coarse correction (Alg. 1 line 4)
+          const int gx = ngx[k], gy = ngy[k];
+          const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
+          const double w = ((gx & 1) ? 0.5 : 1.0) * ((gy & 1) ? 0.5 : 1.0) * ((gz & 1) ? 0.5 : 1.0);
+          for (int kk = 0; kk <= (gz & 1); ++kk)
+            for (int j = 0; j <= (gy & 1); ++j)
+              for (int i = 0; i <= (gx & 1); ++i) {
+                const cplx c = __ldg(&eb[((int64_t)(cz0 + kk) * NC1 + cy0 + j) * NC1 + cx0 + i]);
+                v.x += w * c.x;
+                v.y += w * c.y;
+              }
+        }
+        rn[k] = v;
+      }
+      if (HET) rc[k] = eok[k] ? __ldg(cf + ez * EE + eoff[k]) : make_double2(0, 0);
+    }
+  };
+  auto commit = [&](cplx* un, double2* ce) {   // -> node plane slot un, element plane slot ce
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * MT;
+      if (q < NPL) un[q] = rn[k];
+      if (HET && q < EPL) ce[q] = rc[k];
+    }
+  };
+  // Asynchronous staging (every mode but JACP, whose staged values need the
+  // prolongation added): cp.async copies global -> shared directly (no
+  // registers), out-of-range slots are zero-filled (src-size 0).
+  constexpr bool ASYNC = MODE != M_JACP;
+  auto issue = [&](int gz, int ez, cplx* un, double2* ce, bool elem) {
+    const cplx* xp = xb + gz * NN;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * MT;
+      if (q < NPL) cp_async16(&un[q], nok[k] ? xp + noff[k] : xb, nok[k]);
+      if (HET && elem && q < EPL) cp_async16(&ce[q], eok[k] ? cf + ez * EE + eoff[k] : cf, eok[k]);
+    }
+    cp_async_commit();
+  };
+  // ring slots (rotated, no modulo in the loop): node planes t-1, t, t+1, t+2;
+  // element planes t-1, t, t+1
+  cplx* Un[NRING] = {S.u[0], S.u[1], S.u[2], S.u[3]};
+  double2* Ce[ERING] = {S.c[0], S.c[1], S.c[2]};
+  // prologue: node planes zs - 1, zs and element plane zs - 1 in shared memory,
+  // node plane zs + 1 / element plane zs in flight (registers or cp.async)
+  if (ASYNC) {
+    issue(zs - 1, zs - 1, Un[0], Ce[0], true);
+    issue(zs, zs, Un[1], Ce[0], false);
+    issue(zs + 1, zs, Un[2], Ce[1], true);
+  } else {
+    fetch(zs - 1, zs - 1);
+    commit(Un[0], Ce[0]);
+    fetch(zs, zs);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * MT;
+      if (q < NPL) Un[1][q] = rn[k];
+    }
+    fetch(zs + 1, zs);
+  }
   const int gx = x0 + tx, gy = y0 + ty;
-  const bool act = gx <= n && gy <= n;
-  const bool icol = gx > 0 && gx < n && gy > 0 && gy < n;   // interior column
+  const bool act = gx < n && gy < n;
   const double h = P.h, hm = h * h * h / 216.0;
   const double kc0 = 8.0 * h / 3.0, ke = -h / 6.0, kk = -h / 12.0;
   const int ci = (ty + 1) * NPX + tx + 1;    // this node in a node plane
   const int e0 = ty * EPX + tx;              // element (gx - 1, gy - 1) in an element plane
   const cplx lamc = HET ? cmake(0, 0) : cmake(kc.x * kc.x, eps ? kc.y : 0.0);
-  // Per node plane z (interior columns): centre c, K_in = 8h/3 c - h/6 d (its role as
-  // the node's own plane), K_off = -h/6 e - h/12 d (as the plane above / below);
-  // HET: quadrant sums P(q); constant k: the mass folded in (A_in / A_off).
+  // Per node plane z: centre c, K_in = 8h/3 c - h/6 d (its role as the node's own
+  // plane), K_off = -h/6 e - h/12 d (as the plane above / below); HET: quadrant
+  // sums P(q); constant k: the mass folded in (A_in / A_off).
   struct PlaneQ { cplx c, kin, koff, Pq[4]; };
-  auto planeq = [&](int z, PlaneQ& Q) {
-    const cplx* U = S.u[(z + NRING) % NRING];
+  auto planeq = [&](const cplx* U, PlaneQ& Q) {
     const cplx c = U[ci], xm = U[ci - 1], xp = U[ci + 1], ym = U[ci - NPX], yp = U[ci + NPX];
     const cplx mm = U[ci - NPX - 1], pm = U[ci - NPX + 1], mp = U[ci + NPX - 1], pp = U[ci + NPX + 1];
     const cplx e = cmake(xm.x + xp.x + ym.x + yp.x, xm.y + xp.y + ym.y + yp.y);
@@ -556,8 +559,7 @@ __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg
   };
   // element plane ez (between node planes ez, ez + 1), HET: mass of the lower node
   // (weights 2 P_lo + P_hi), of the upper node (2 P_hi + P_lo), and sum of lambda
-  auto eplane = [&](int ez, const cplx* Plo, const cplx* Phi, cplx& mlo, cplx& mhi, cplx& ls) {
-    const double2* C = S.c[(ez + ERING) % ERING];
+  auto eplane = [&](const double2* C, const cplx* Plo, const cplx* Phi, cplx& mlo, cplx& mhi, cplx& ls) {
     mlo = mhi = ls = cmake(0, 0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -568,43 +570,43 @@ __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg
       cfma(mhi, l, cmake(2 * Phi[q].x + Plo[q].x, 2 * Phi[q].y + Plo[q].y));
     }
   };
-  // f (or sub) of the node of plane t, loaded one plane ahead (its latency hides
-  // under the previous plane's arithmetic)
-  const bool needf = MODE != M_APPLY;
-  const cplx* fb = needf ? f.at(b) - vo : (sub.p ? sub.at(b) - vo : nullptr);
-  auto ldf = [&](int z) -> cplx {
-    if (!act || !fb || z >= ze) return cmake(0, 0);
-    return __ldg(&fb[((int64_t)z * N1 + gy) * N1 + gx]);
-  };
-  cplx fnext = ldf(zs);
-  // carried along z (interior columns): node t's partial operator row acc, its
-  // lambda sum below, plane t's P, K_off (const: A_off) and centre
+  // f (or sub) of this node at plane t, loaded one plane ahead
+  const cplx* fb = MODE != M_APPLY ? f.at(b) - vo : (sub.p ? sub.at(b) - vo : nullptr);
+  const int64_t nodeoff = (int64_t)gy * N1 + gx;
+  const cplx* fp = (act && fb) ? fb + zs * NN + nodeoff : nullptr;   // advanced by one plane per step
+  const double fsc = MODE != M_APPLY ? fs.at(b) : 1.0;
+  cplx fnext = fp ? __ldg(fp) : cmake(0, 0);
+  // carried along z: node t's partial operator row acc and its lambda sum below;
+  // plane t's P, K_off (const: A_off) and centre
   cplx acc = cmake(0, 0), lsb = cmake(0, 0), koff_t = cmake(0, 0), c_t = cmake(0, 0);
   cplx Pt[4] = {cmake(0, 0), cmake(0, 0), cmake(0, 0), cmake(0, 0)};
-  for (int t = zs; t < ze; ++t) {
-    commit(t + 1, t);              // node plane t + 1, element plane t
-    __syncthreads();
-    if (t + 2 <= ze) fetch(t + 2, t + 1);
+  cplx* op = out.at(b) - vo + zs * NN + nodeoff;
+  for (int t = zs; t < ze; ++t, op += NN) {
+    // slots this step: node planes t-1 = Un[0], t = Un[1], t+1 = Un[2] (being
+    // committed), t+2 = Un[3] (next); element planes t-1 = Ce[0], t = Ce[1]
+    if (ASYNC) {
+      cp_async_wait_all();         // node plane t + 1, element plane t landed
+      __syncthreads();
+      if (t + 2 <= ze) issue(t + 2, t + 1, Un[3], Ce[2], true);
+    } else {
+      commit(Un[2], Ce[1]);        // node plane t + 1, element plane t
+      __syncthreads();
+      if (t + 2 <= ze) fetch(t + 2, t + 1);
+    }
     const cplx fcur = fnext;
-    fnext = ldf(t + 1);
-    if (!act) continue;
-    const cplx* U0 = S.u[(t - 1 + NRING) % NRING];
-    const cplx* U1 = S.u[t % NRING];
-    const cplx* U2 = S.u[(t + 1) % NRING];
-    const double2* Cb = S.c[(t - 1 + ERING) % ERING];   // elements below the node plane
-    const double2* Ca = S.c[t % ERING];                  // above
-    const int64_t gi = ((int64_t)t * N1 + gy) * N1 + gx;
-    cplx ax = cmake(0, 0), dg = cmake(0, 0);
-    cplx xc = U1[ci];
-    if (icol) {
+    if (fp && t + 1 < ze) {
+      fp += NN;
+      fnext = __ldg(fp);
+    }
+    if (act) {
       if (t == zs) {   // start of the march: planes zs - 1, zs and element plane zs - 1
         PlaneQ Qm, Q0;
-        planeq(t - 1, Qm);
-        planeq(t, Q0);
+        planeq(Un[0], Qm);
+        planeq(Un[1], Q0);
         acc = cadd(Q0.kin, Qm.koff);
         if (HET) {
           cplx mlo, mhi, ls;
-          eplane(t - 1, Qm.Pq, Q0.Pq, mlo, mhi, ls);
+          eplane(Ce[0], Qm.Pq, Q0.Pq, mlo, mhi, ls);
           cfms(acc, cmake(hm, 0), mhi);
           lsb = ls;
 #pragma unroll
@@ -614,12 +616,12 @@ __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg
         c_t = Q0.c;
       }
       PlaneQ Q1;
-      planeq(t + 1, Q1);
-      ax = cadd(acc, Q1.koff);
-      xc = c_t;
+      planeq(Un[2], Q1);
+      cplx ax = cadd(acc, Q1.koff), dg;
+      const cplx xc = c_t;
       if (HET) {
         cplx mlo, mhi, ls;
-        eplane(t, Pt, Q1.Pq, mlo, mhi, ls);
+        eplane(Ce[1], Pt, Q1.Pq, mlo, mhi, ls);
         cfms(ax, cmake(hm, 0), mlo);
         dg = cmake(kc0 - 8.0 * hm * (lsb.x + ls.x), -8.0 * hm * (lsb.y + ls.y));
         acc = cadd(Q1.kin, koff_t);        // node t + 1
@@ -633,25 +635,80 @@ __global__ void __launch_bounds__(MT, MINB) k_march3d(F3 P, VArg x, VArg f, SArg
       }
       koff_t = Q1.koff;
       c_t = Q1.c;
+      if (MODE == M_APPLY) {
+        *op = fb ? csub(fcur, ax) : ax;
+      } else {
+        const cplx r = csub(cscale(fcur, fsc), ax);
+        if (MODE == M_RES) {
+          *op = r;
+        } else {
+          cplx v = xc;
+          cfma(v, cscale(cinv(dg), P.omega), r);
+          *op = v;
+        }
+      }
     }
-    if (icol && t > 0 && t < n) {
-      // interior node: ax, dg from the carried plane quantities
+    // rotate the rings
+    cplx* u0 = Un[0];
+    Un[0] = Un[1]; Un[1] = Un[2]; Un[2] = Un[3]; Un[3] = u0;
+    double2* c0 = Ce[0];
+    Ce[0] = Ce[1]; Ce[1] = Ce[2]; Ce[2] = c0;
+  }
+}
+
+// Domain-boundary nodes of the marching kernels' operations: planes z = 0, n
+// entirely, the perimeter of every other plane of the entry's range; one thread
+// per node, the element loop + boundary faces of row3 / diag3 from global memory.
+template <bool HET, int MODE, bool EPS>
+__global__ void __launch_bounds__(256) k_bnd3d(F3 P, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out) {
+  const int n = P.n, N1 = P.N1;
+  const int b = blockIdx.z;
+  if (P.st && P.st[b]) return;
+  const int2 sl = slab_of(P.slab, b, n);
+  const int zlo = max(0, sl.x - P.ext), zhi = min(N1, sl.y + P.ext);
+  // flattened: the perimeters (4n nodes) of all planes of the range, then the
+  // interiors ((n-1)^2 nodes) of the planes z = 0 and z = n if in the range
+  const int span = zhi - zlo, per = 4 * n, in2 = (n - 1) * (n - 1);
+  const bool f0 = zlo == 0, f1 = zhi == N1;
+  const int64_t total = (int64_t)span * per + (int64_t)((f0 ? 1 : 0) + (f1 ? 1 : 0)) * in2;
+  const int64_t vo = (int64_t)(sl.x - P.G) * N1 * N1;
+  const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int gx, gy, z;
+    if (i < (int64_t)span * per) {   // perimeter: (r, 0), (n, r), (n - r, n), (0, n - r), r in 0..n-1
+      z = zlo + (int)(i / per);
+      const int j = (int)(i % per), side = j / n, r = j % n;
+      gx = side == 0 ? r : (side == 1 ? n : (side == 2 ? n - r : 0));
+      gy = side == 0 ? 0 : (side == 1 ? r : (side == 2 ? n : n - r));
     } else {
-      // boundary node: element loop + boundary faces on the staged values
-      boundary3<HET>(U0, U1, U2, Cb, Ca, ci, gx, gy, t, x0, y0, n, h, eps, kc, ax, dg);
+      const int64_t j = i - (int64_t)span * per;
+      z = (j < in2 && f0) ? 0 : n;
+      const int r = (int)(j % in2);
+      gx = 1 + r % (n - 1);
+      gy = 1 + r / (n - 1);
+    }
+    const int64_t gi = ((int64_t)z * N1 + gy) * N1 + gx;
+    cplx ax, xc;
+    if (MODE == M_JACP) {
+      const ProlongAcc acc{x.at(b) - vo, ec.at(b), n / 2 + 1};
+      ax = row3<HET, EPS>(P, acc, cf, kc, gx, gy, z);
+      xc = acc(gi, gx, gy, z);
+    } else {
+      const LdgAcc acc{x.at(b) - vo};
+      ax = row3<HET, EPS>(P, acc, cf, kc, gx, gy, z);
+      xc = acc(gi, gx, gy, z);
     }
     cplx* ob = out.at(b) - vo;
     if (MODE == M_APPLY) {
-      if (sub.p) ax = csub(fcur, ax);
-      ob[gi] = ax;
+      ob[gi] = sub.p ? csub(__ldg(&(sub.at(b) - vo)[gi]), ax) : ax;
     } else {
-      const cplx fv = cscale(fcur, fs.at(b));
-      const cplx r = csub(fv, ax);
+      const cplx r = csub(cscale(__ldg(&(f.at(b) - vo)[gi]), fs.at(b)), ax);
       if (MODE == M_RES) {
         ob[gi] = r;
       } else {
         cplx v = xc;
-        cfma(v, cscale(cinv(dg), P.omega), r);
+        cfma(v, cscale(cinv(diag3<HET>(P, cf, kc, gx, gy, z)), P.omega), r);
         ob[gi] = v;
       }
     }
@@ -678,28 +735,42 @@ static bool g_march = getenv("HH_3D_NAIVE") == nullptr;   // HH_3D_NAIVE=1: the 
 template <int MODE>
 static hh_status march3(const Level& L, const F3& P, int B, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out,
                         bool eps, cudaStream_t s) {
-  const int tx = (P.N1 + MTX - 1) / MTX, ty = (P.N1 + MTY - 1) / MTY;
+  const int ni = P.n - 1;   // interior nodes per side
+  const int tx = (ni + MTX - 1) / MTX, ty = (ni + MTY - 1) / MTY;
   const int span = std::min(P.N1, P.maxloc + 2 * P.ext);
   const int want = std::max(1, (4 * 148 + tx * ty * B - 1) / (tx * ty * B));
   const int nzc = std::max(1, std::min(span, want));
   const int zlen = (span + nzc - 1) / nzc;
   const size_t sm = sizeof(MarchSmem);
   const dim3 g(tx, ty, nzc * B);
-  // register budget: 3 CTAs per SM (80 registers, some spills) or 2 (128, none);
-  // HH_3D_MINB selects, default = the measured faster one
-  static const int minb = getenv("HH_3D_MINB") ? atoi(getenv("HH_3D_MINB")) : 3;
+  // register budget: 3 CTAs per SM (80 registers) or 2 (128); HH_3D_MINB selects,
+  // default = the measured faster one
+  static const int minb_env = getenv("HH_3D_MINB") ? atoi(getenv("HH_3D_MINB")) : 0;
+  const int minb = minb_env ? minb_env : (L.het ? 2 : 3);   // spill-free budgets
+  const int e = eps ? 1 : 0;
   if (L.het && minb == 2) {
     HH_CUDA_TRY(smem_attr((const void*)k_march3d<true, MODE, 2>, sm));
-    k_march3d<true, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+    k_march3d<true, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, e, zlen, nzc);
   } else if (L.het) {
     HH_CUDA_TRY(smem_attr((const void*)k_march3d<true, MODE, 3>, sm));
-    k_march3d<true, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+    k_march3d<true, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, e, zlen, nzc);
   } else if (minb == 2) {
     HH_CUDA_TRY(smem_attr((const void*)k_march3d<false, MODE, 2>, sm));
-    k_march3d<false, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+    k_march3d<false, MODE, 2><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, e, zlen, nzc);
   } else {
     HH_CUDA_TRY(smem_attr((const void*)k_march3d<false, MODE, 3>, sm));
-    k_march3d<false, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, eps ? 1 : 0, zlen, nzc);
+    k_march3d<false, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, e, zlen, nzc);
+  }
+  HH_CUDA_TRY(cudaGetLastError());
+  // the boundary faces (same stream, disjoint nodes)
+  const int64_t nb = (int64_t)span * 4 * P.n + 2LL * (P.n - 1) * (P.n - 1);   // boundary nodes per entry (max)
+  const dim3 gb((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (nb + 255) / 256)), 1, B);
+  if (L.het) {
+    if (eps) k_bnd3d<true, MODE, true><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
+    else k_bnd3d<true, MODE, false><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
+  } else {
+    if (eps) k_bnd3d<false, MODE, true><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
+    else k_bnd3d<false, MODE, false><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
   }
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
@@ -772,7 +843,11 @@ hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega
   const dim3 bl(BX, BY);
   // the nu post-steps must end in z: pick the prolongation target accordingly
   VArg bufs[2] = {t0, z};
-  if (g_march) {
+  // the prolongation fused into the first post-smoothing step (staged through
+  // registers with the prolongation added) or a separate pointwise kernel followed
+  // by the cp.async-staged steps; HH_3D_JACP=1 selects the fused one (A/B)
+  static const bool fuse_p = getenv("HH_3D_JACP") && atoi(getenv("HH_3D_JACP")) != 0;
+  if (g_march && fuse_p) {
     // prolongation fused into the first post-smoothing step (x + I e_c formed on load)
     int cur = (nu % 2 == 1) ? 1 : 0;   // first destination: the nu steps end in z
     HH_TRY(march3<M_JACP>(L, make3(L, omega, st, std::max(e0 - 1, 0)), B, u, f, fs, ec, VArg(), bufs[cur],

@@ -1,0 +1,10 @@
+#!/bin/bash
+# round 2: interior-only z-marching 3D kernels (+ boundary-face kernel): A/B + parity
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/r02h
+mkdir -p $O
+timeout 600 python scripts/probe_3d.py > $O/probe_march.json 2> $O/probe_march.err; echo "m=$?" >> $O/status.txt
+timeout 600 env HH_3D_MINB=3 python scripts/probe_3d.py > $O/probe_march3.json 2> $O/probe_march3.err; echo "m3=$?" >> $O/status.txt
+timeout 600 env HH_3D_NAIVE=1 python scripts/probe_3d.py > $O/probe_naive.json 2> $O/probe_naive.err; echo "naive=$?" >> $O/status.txt
+timeout 1500 python -m pytest -x -q -p no:cacheprovider tests/test_gpu_parity.py tests/test_gpu_slabs.py tests/test_gpu_nd_forced.py tests/test_gpu_fullsize.py tests/test_gpu_dist_coarse.py -k "not fullsize or cfg2" > $O/pytest_3d.log 2>&1; echo "par=$?" >> $O/status.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_march3d -s 2 -c 1 -o $O/full_march_cfg4 python scripts/probe_3d.py cfg4 > $O/ncu.log 2>&1; echo "ncu=$?" >> $O/status.txt
