@@ -16,6 +16,8 @@
 // SURVEY 8(d)); temporal blocking as in 2D is future work.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include "hh_internal.cuh"
 
 namespace {
@@ -715,6 +717,83 @@ __global__ void __launch_bounds__(256) k_bnd3d(F3 P, VArg x, VArg f, SArg fs, VA
   }
 }
 
+// Pointwise steps as streaming kernels (grid-stride over the entry's planes, two
+// nodes in flight per thread): MODE 0 = the first Jacobi step from u = 0,
+// uo = omega D^{-1} f fs (D^{-1}: the precomputed copy (heterogeneous), the
+// interior constant / diag3 at the boundary (constant k)); MODE 1 = prolongation
+// and correction uo = u + I e_c.
+template <bool HET, int MODE>
+__global__ void __launch_bounds__(256) k_pw3d(F3 P, VArg f, SArg fs, VArg u, VArg ec, VArg uo) {
+  const int n = P.n, N1 = P.N1;
+  const int b = blockIdx.y;
+  if (P.st && P.st[b]) return;
+  const int2 sl = slab_of(P.slab, b, n);
+  const int zlo = max(0, sl.x - P.ext), zhi = min(N1, sl.y + P.ext);
+  const int64_t NN = (int64_t)N1 * N1, i0 = zlo * NN, i1 = zhi * NN;
+  const int64_t vo = (int64_t)(sl.x - P.G) * NN;
+  cplx* ob = uo.at(b) - vo;
+  const double2* cf = HET ? P.coef + b * P.coef_bs : nullptr;
+  const double2 kc = HET ? make_double2(0, 0) : P.kc[b];
+  const int NC1 = n / 2 + 1;
+  const cplx* fb = MODE == 0 ? f.at(b) - vo : nullptr;
+  const double fsc = MODE == 0 ? fs.at(b) : 1.0;
+  const cplx* ub = MODE == 1 ? u.at(b) - vo : nullptr;
+  const cplx* eb = MODE == 1 ? ec.at(b) : nullptr;
+  const cplx* dib = (MODE == 0 && HET) ? P.dinv + (int64_t)b * P.stride - vo : nullptr;
+  const double hm = P.h * P.h * P.h / 216.0;
+  const cplx di_int = HET ? cmake(0, 0)   // constant k: interior D = 8h/3 - 64 h^3/216 lambda
+                          : cinv(cmake(8.0 * P.h / 3.0 - 64.0 * hm * kc.x * kc.x, -64.0 * hm * kc.y));
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < i1; i += 2 * step) {
+    const int64_t j = i + step;
+    const bool two = j < i1;
+    if (MODE == 0) {
+      const cplx f0 = __ldg(&fb[i]), f1 = two ? __ldg(&fb[j]) : cmake(0, 0);
+      cplx d0, d1;
+      if (HET) {
+        d0 = __ldg(&dib[i]);
+        d1 = two ? __ldg(&dib[j]) : cmake(0, 0);
+      } else {
+        auto dg = [&](int64_t k) {
+          const int gx = (int)(k % N1), gy = (int)((k / N1) % N1), gz = (int)(k / NN);
+          const bool inter = gx > 0 && gx < n && gy > 0 && gy < n && gz > 0 && gz < n;
+          return inter ? di_int : cinv(diag3<false>(P, nullptr, kc, gx, gy, gz));
+        };
+        d0 = dg(i);
+        d1 = two ? dg(j) : cmake(0, 0);
+      }
+      ob[i] = cscale(cmul(d0, cscale(f0, fsc)), P.omega);
+      if (two) ob[j] = cscale(cmul(d1, cscale(f1, fsc)), P.omega);
+    } else {
+      const cplx u0 = __ldg(&ub[i]), u1 = two ? __ldg(&ub[j]) : cmake(0, 0);
+      auto pro = [&](int64_t k, cplx v) {
+        const int gx = (int)(k % N1), gy = (int)((k / N1) % N1), gz = (int)(k / NN);
+        const int cx0 = gx >> 1, cy0 = gy >> 1, cz0 = gz >> 1;
+        const double w = ((gx & 1) ? 0.5 : 1.0) * ((gy & 1) ? 0.5 : 1.0) * ((gz & 1) ? 0.5 : 1.0);
+        for (int kk = 0; kk <= (gz & 1); ++kk)
+          for (int jj = 0; jj <= (gy & 1); ++jj)
+            for (int ii = 0; ii <= (gx & 1); ++ii) {
+              const cplx c = __ldg(&eb[((int64_t)(cz0 + kk) * NC1 + cy0 + jj) * NC1 + cx0 + ii]);
+              v.x += w * c.x;
+              v.y += w * c.y;
+            }
+        return v;
+      };
+      ob[i] = pro(i, u0);
+      if (two) ob[j] = pro(j, u1);
+    }
+  }
+}
+
+template <bool HET, int MODE>
+static hh_status pw3(const F3& P, int B, VArg f, SArg fs, VArg u, VArg ec, VArg uo, cudaStream_t s) {
+  const int64_t nodes = (int64_t)std::min(P.N1, P.maxloc + 2 * P.ext) * P.N1 * P.N1;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8 / std::max(1, B) + 1, (nodes + 511) / 512));
+  k_pw3d<HET, MODE><<<dim3(gx, B), 256, 0, s>>>(P, f, fs, u, ec, uo);
+  HH_CUDA_TRY(cudaGetLastError());
+  return HH_OK;
+}
+
 F3 make3(const Level& L, double omega, const int* st, int ext) {
   F3 P;
   P.n = L.n; P.h = L.h; P.omega = omega; P.coef = L.coef; P.coef_bs = L.coef_bs; P.kc = L.kc;
@@ -732,9 +811,39 @@ dim3 grid3(const F3& P, int B) {
 // z-marching launch: CTAs per entry = x tiles x y tiles x z chunks, with enough
 // z chunks to put ~4 CTAs on every SM
 static bool g_march = getenv("HH_3D_NAIVE") == nullptr;   // HH_3D_NAIVE=1: the one-node-per-thread kernels
+// side stream of the boundary-face kernel (runs beside the marching kernel:
+// disjoint nodes), one per device; the fork / join sequence is serialised so
+// concurrent callers never interleave their event records
+struct Side { cudaStream_t s = nullptr; cudaEvent_t a = nullptr, b = nullptr; };
+static std::mutex g_side_mu;
+static hh_status side_of(Side** out) {
+  static std::map<int, Side> sides;
+  int dev = 0;
+  HH_CUDA_TRY(cudaGetDevice(&dev));
+  Side& sd = sides[dev];
+  if (!sd.s) {
+    HH_CUDA_TRY(cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking));
+    HH_CUDA_TRY(cudaEventCreateWithFlags(&sd.a, cudaEventDisableTiming));
+    HH_CUDA_TRY(cudaEventCreateWithFlags(&sd.b, cudaEventDisableTiming));
+  }
+  *out = &sd;
+  return HH_OK;
+}
+static const bool g_side = getenv("HH_3D_NOSIDE") == nullptr;
+
 template <int MODE>
 static hh_status march3(const Level& L, const F3& P, int B, VArg x, VArg f, SArg fs, VArg ec, VArg sub, VArg out,
                         bool eps, cudaStream_t s) {
+  std::unique_lock<std::mutex> lk(g_side_mu, std::defer_lock);
+  Side* sd = nullptr;
+  cudaStream_t sb = s;   // stream of the boundary-face kernel
+  if (g_side) {
+    lk.lock();
+    HH_TRY(side_of(&sd));
+    HH_CUDA_TRY(cudaEventRecord(sd->a, s));
+    HH_CUDA_TRY(cudaStreamWaitEvent(sd->s, sd->a, 0));
+    sb = sd->s;
+  }
   const int ni = P.n - 1;   // interior nodes per side
   const int tx = (ni + MTX - 1) / MTX, ty = (ni + MTY - 1) / MTY;
   const int span = std::min(P.N1, P.maxloc + 2 * P.ext);
@@ -762,17 +871,21 @@ static hh_status march3(const Level& L, const F3& P, int B, VArg x, VArg f, SArg
     k_march3d<false, MODE, 3><<<g, MT, sm, s>>>(P, x, f, fs, ec, sub, out, e, zlen, nzc);
   }
   HH_CUDA_TRY(cudaGetLastError());
-  // the boundary faces (same stream, disjoint nodes)
+  // the boundary faces (side stream, disjoint nodes), joined back into s
   const int64_t nb = (int64_t)span * 4 * P.n + 2LL * (P.n - 1) * (P.n - 1);   // boundary nodes per entry (max)
   const dim3 gb((unsigned)std::max<int64_t>(1, std::min<int64_t>(2048, (nb + 255) / 256)), 1, B);
   if (L.het) {
-    if (eps) k_bnd3d<true, MODE, true><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
-    else k_bnd3d<true, MODE, false><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
+    if (eps) k_bnd3d<true, MODE, true><<<gb, 256, 0, sb>>>(P, x, f, fs, ec, sub, out);
+    else k_bnd3d<true, MODE, false><<<gb, 256, 0, sb>>>(P, x, f, fs, ec, sub, out);
   } else {
-    if (eps) k_bnd3d<false, MODE, true><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
-    else k_bnd3d<false, MODE, false><<<gb, 256, 0, s>>>(P, x, f, fs, ec, sub, out);
+    if (eps) k_bnd3d<false, MODE, true><<<gb, 256, 0, sb>>>(P, x, f, fs, ec, sub, out);
+    else k_bnd3d<false, MODE, false><<<gb, 256, 0, sb>>>(P, x, f, fs, ec, sub, out);
   }
   HH_CUDA_TRY(cudaGetLastError());
+  if (sd) {
+    HH_CUDA_TRY(cudaEventRecord(sd->b, sd->s));
+    HH_CUDA_TRY(cudaStreamWaitEvent(s, sd->b, 0));
+  }
   return HH_OK;
 }
 
@@ -795,6 +908,8 @@ hh_status fine_apply3d(const Level& L, int B, const int* st, int op, VArg x, VAr
 static hh_status jac3(const Level& L, const F3& P, int B, VArg f, SArg fs, VArg u, VArg uo,
                       cudaStream_t s) {
   if (g_march && u.p) return march3<M_JAC>(L, P, B, u, f, fs, VArg(), VArg(), uo, true, s);
+  if (g_march)   // the first step from u = 0: pointwise
+    return L.het ? pw3<true, 0>(P, B, f, fs, VArg(), VArg(), uo, s) : pw3<false, 0>(P, B, f, fs, VArg(), VArg(), uo, s);
   const dim3 g = grid3(P, B), bl(BX, BY);
   if (L.het) k_jacobi3d<true><<<g, bl, 0, s>>>(P, f, fs, u, uo);
   else k_jacobi3d<false><<<g, bl, 0, s>>>(P, f, fs, u, uo);
@@ -861,7 +976,8 @@ hh_status fine_post3d(const Level& L, int B, const int* st, int nu, double omega
     return HH_OK;
   }
   int cur = (nu % 2 == 0) ? 1 : 0;
-  k_prolong3d<<<grid3(Pp, B), bl, 0, s>>>(Pp, u, ec, bufs[cur]);
+  if (g_march) HH_TRY((pw3<false, 1>(Pp, B, VArg(), SArg(), u, ec, bufs[cur], s)));
+  else k_prolong3d<<<grid3(Pp, B), bl, 0, s>>>(Pp, u, ec, bufs[cur]);
   for (int k = 1; k <= nu; ++k) {
     HH_TRY(jac3(L, make3(L, omega, st, std::max(e0 - k, 0)), B, f, fs, bufs[cur], bufs[cur ^ 1], s));
     cur ^= 1;

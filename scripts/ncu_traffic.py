@@ -17,6 +17,7 @@ import re
 import sys
 
 PHASE = [("coarse", r"^k_nd_(fwd|bwd|gather|rows_wide|fwdT|bwdK|bwd_stage|cluster|flow|fwd_sub|bwd_sub)"),
+         ("fine3d", r"^k_march3d|^k_bnd3d|^k_pw3d|^k_prolong3d"),   # 3D: shared by pre / post / A_0
          ("setup", r"^k_nd_|^k_coef|^k_stencil|^k_dinv|^k_cstencil"),
          ("pre", r"^k_pre|^k_jacobi|^k_resid|^k_restrict"),
          ("post", r"^k_post|^k_prolong|^k_apply"),
@@ -73,6 +74,17 @@ def main():
         res[ph] = {"dram_bytes_per_launch": by / n, "model_bytes_per_launch": tm[ph]["model"] / n,
                    "fused_bytes_per_launch": tm[ph]["bytes"] / n, "kernels": k, "phase_launches": int(n),
                    "ncu_us_per_launch": 1e6 * t / n, "ncu_dram_gbs": by / t / 1e9 if t > 0 else None}
+    if "fine3d" in agg:   # 3D: the marching kernels serve pre, post and the A_0 apply
+        k, by, t = agg["fine3d"]
+        n = tm["pre"]["launches"]
+        pre, post = res.get("pre", {}), res.get("post", {})
+        by += pre.get("dram_bytes_per_launch", 0) * n + post.get("dram_bytes_per_launch", 0) * n
+        t += 1e-6 * n * (pre.get("ncu_us_per_launch", 0) + post.get("ncu_us_per_launch", 0))
+        res["fine3d_pre_post"] = {"dram_bytes_per_iteration": by / n,
+                                  "model_bytes_per_iteration": (tm["pre"]["model"] + tm["post"]["model"]) / n,
+                                  "ncu_us_per_iteration": 1e6 * t / n, "ncu_dram_gbs": by / t / 1e9}
+        res.pop("pre", None)
+        res.pop("post", None)
     res["setup"] = {"kernels": agg["setup"][0], "dram_bytes": agg["setup"][1], "ncu_ms": 1e3 * agg["setup"][2]}
     tot_t = sum(a[2] for a in agg.values())
     res["time_share"] = {ph: round(a[2] / tot_t, 4) for ph, a in agg.items()} if tot_t else {}
