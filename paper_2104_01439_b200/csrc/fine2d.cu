@@ -191,6 +191,19 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     }                                                                          \
   }
 
+#ifndef FINE_ASYNC
+#define FINE_ASYNC 1   // 1: stage the smoothers' inputs with cp.async (all in flight at once, no registers)
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 // g = virtual global base of the entry's vector; rows outside [rlo, rhi] read as 0.
 // Flat index over the region, 4 loads issued per thread before any is used.
 __device__ __forceinline__ void load_region(cplx* sX, const cplx* __restrict__ g, const Tile& t,
@@ -234,6 +247,30 @@ __device__ __forceinline__ void load_coef(double2* sE, const double2* __restrict
       const int idx = base + k * NT;
       if (idx < total) sE[idx] = v[k];
     }
+  }
+}
+
+// cp.async variants: unscaled copies, zero-filled outside the grid / slab rows;
+// the caller waits (cp_async_wait_all) before its barrier
+__device__ __forceinline__ void load_region_async(cplx* sX, const cplx* __restrict__ g, const Tile& t, int n, int rlo,
+                                                  int rhi) {
+  const int N1 = n + 1;
+  const int total = t.SX * t.SY;
+  for (int idx = threadIdx.x; idx < total; idx += NT) {
+    const int sy = idx / t.SX, sx = idx - sy * t.SX;
+    const int gy = t.gy(sy), gx = t.gx(sx);
+    const bool ok = gy >= rlo && gy <= rhi && gx >= 0 && gx <= n;
+    cp_async16(&sX[idx], ok ? g + (int64_t)gy * N1 + gx : g + (int64_t)rlo * N1, ok);
+  }
+}
+__device__ __forceinline__ void load_coef_async(double2* sE, const double2* __restrict__ coef, const Tile& t, int n) {
+  const int EX = t.SX + 1, EY = t.SY + 1;
+  const int total = EX * EY;
+  for (int idx = threadIdx.x; idx < total; idx += NT) {
+    const int ey0 = idx / EX, ex0 = idx - ey0 * EX;
+    const int ey = t.Y0 - t.R - 1 + ey0, ex = t.X0 - t.R - 1 + ex0;
+    const bool ok = ex >= 0 && ex < n && ey >= 0 && ey < n;
+    cp_async16(&sE[idx], ok ? coef + (int64_t)ey * n + ex : coef, ok);
   }
 }
 
@@ -326,17 +363,28 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
   double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
   const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9 = make_const9(kc, h, true);
-  load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
-  if (HET) {
-    if (!FINE_DI_GLOBAL) load_region(sDi, dg, t, n, 1.0, rlo, rhi);
-    load_coef(sE, P.coef + b * P.coef_bs, t, n);
+  // f staged unscaled with cp.async (the Krylov scale fsc is applied where it is read)
+  const double fsa = FINE_ASYNC ? fsc : 1.0;
+  if (FINE_ASYNC) {
+    load_region_async(sF, fg - vofs, t, n, rlo, rhi);
+    if (HET) {
+      if (!FINE_DI_GLOBAL) load_region_async(sDi, dg, t, n, rlo, rhi);
+      load_coef_async(sE, P.coef + b * P.coef_bs, t, n);
+    }
+    cp_async_wait_all();
+  } else {
+    load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
+    if (HET) {
+      if (!FINE_DI_GLOBAL) load_region(sDi, dg, t, n, 1.0, rlo, rhi);
+      load_coef(sE, P.coef + b * P.coef_bs, t, n);
+    }
   }
   __syncthreads();
   // the first step from u = 0 (pointwise) on the full region
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);   // constant k: interior D = centre coefficient
   FOR_REGION(t.R, {
     cplx v = cmake(0, 0);
-    if (in) v = cscale(cmul(dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega);
+    if (in) v = cscale(cmul(dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega * fsa);
     sA[si] = v;
     sB[si] = cmake(0, 0);
   })
@@ -349,7 +397,7 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
       const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
-      cfma(v, cscale(di, omega), csub(sF[si], ax));
+      cfma(v, cscale(di, omega), csub(cscale(sF[si], fsa), ax));
       nxt[si] = v;
     })
     __syncthreads();
@@ -359,7 +407,7 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
   cplx* ub = uo.at(b) - vofs;
   FOR_REGION(1, if (in) {
     const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
-    nxt[si] = csub(sF[si], ax);
+    nxt[si] = csub(cscale(sF[si], fsa), ax);
     if (sx >= t.R && sx < t.R + TX && sy >= t.R && sy < t.R + TY && gy < sl.y)
       ub[(int64_t)gy * (n + 1) + gx] = cur[si];
   })
@@ -419,8 +467,18 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
   double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
   const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9e = make_const9(kc, h, true);
-  load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
-  load_region(sA, uin.at(b) - vofs, t, n, 1.0, rlo, rhi);
+  const double fsa = FINE_ASYNC ? fsc : 1.0;
+  if (FINE_ASYNC) {
+    load_region_async(sF, fg - vofs, t, n, rlo, rhi);
+    load_region_async(sA, uin.at(b) - vofs, t, n, rlo, rhi);
+    if (HET) {
+      if (!FINE_DI_GLOBAL) load_region_async(sDi, dg, t, n, rlo, rhi);
+      load_coef_async(sE, P.coef + b * P.coef_bs, t, n);
+    }
+  } else {
+    load_region(sF, fg - vofs, t, n, fsc, rlo, rhi);
+    load_region(sA, uin.at(b) - vofs, t, n, 1.0, rlo, rhi);
+  }
   // coarse nodes under the region: cx in [cx0, cx0 + CW), cy in [cy0, cy0 + CH)
   const int nc = n / 2, NC1 = nc + 1;
   const int cx0 = (t.X0 - t.R) >> 1, cy0 = (t.Y0 - t.R) >> 1;
@@ -442,10 +500,11 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
         if (base + k * NT < total) sC[base + k * NT] = v[k];
     }
   }
-  if (HET) {
+  if (HET && !FINE_ASYNC) {
     if (!FINE_DI_GLOBAL) load_region(sDi, dg, t, n, 1.0, rlo, rhi);
     load_coef(sE, P.coef + b * P.coef_bs, t, n);
   }
+  if (FINE_ASYNC) cp_async_wait_all();
   const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);
   __syncthreads();
   // u + I ec on the full region (bilinear interpolation from the staged block)
@@ -486,7 +545,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
       const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e);
       const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
-      cfma(v, cscale(di, omega), csub(sF[si], ax));
+      cfma(v, cscale(di, omega), csub(cscale(sF[si], fsa), ax));
       nxt[si] = v;
     })
     __syncthreads();
