@@ -369,6 +369,107 @@ __global__ void __launch_bounds__(256, UR == 64 ? (NBT == 64 ? 2 : 3) : 5) k_nd_
   }
 }
 
+// The same rank-nb update on the FP64 tensor path (mma.sync m8n8k4 f64, DMMA):
+// the CTA's 64 x 32 complex tile is split over 8 warps as 16 x 16 complex warp
+// tiles, i.e. 2 x 2 blocks of 8 x 8 real and imaginary accumulators; per k step
+// of 4 the complex product takes four real MMAs (Re -= Cr Rr - Ci Ri, Im -= Cr Ri +
+// Ci Rr).  Same inputs / outputs / special cases as k_nd_upd<64, NBT>; only the
+// summation order inside the MMA differs.  (Measured on this B200: DMMA 37.2
+// TFLOP/s, DFMA chains 36.3: the win is fewer issued instructions and
+// shared-memory reads per multiply-add, not a higher peak.)
+constexpr int MU_R = 64, MU_C = 32;
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+template <int NBT>
+__global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restrict__ fr, int begin, int kb, int tiles,
+                                                     cplx* __restrict__ Fall, int64_t FE, const cplx* __restrict__ Call,
+                                                     int64_t CE, const int64_t* __restrict__ Coff) {
+  const int t = begin + blockIdx.y;
+  const int b = blockIdx.z;
+  const FrontMeta m = fr[t];
+  if (kb >= m.s) return;
+  const int f = m.f;
+  const int i0 = (blockIdx.x / tiles) * MU_R, j0 = (blockIdx.x % tiles) * MU_C;
+  if (i0 >= f || j0 >= f) return;
+  const int nb = min(NBT, m.s - kb);
+  cplx* A = Fall + (int64_t)b * FE + m.Foff;
+  const cplx* C = Call + (int64_t)b * CE + Coff[blockIdx.y];
+  const cplx* Pg = C + (int64_t)f * NBT;
+  constexpr int CSX = NBT + 1, RSX = MU_C + 1;   // padded strides
+  extern __shared__ double4 smem_raw[];
+  cplx* Cs = reinterpret_cast<cplx*>(smem_raw);   // [MU_R][CSX]
+  cplx* Rs = Cs + MU_R * CSX;                     // [NBT][RSX]
+  for (int idx = threadIdx.x; idx < MU_R * NBT; idx += 256) {
+    const int i = idx / NBT, k = idx % NBT;
+    Cs[i * CSX + k] = (i0 + i < f && k < nb) ? C[(int64_t)(i0 + i) * NBT + k] : cmake(0, 0);
+  }
+  for (int idx = threadIdx.x; idx < NBT * MU_C; idx += 256) {
+    const int k = idx / MU_C, j = idx % MU_C;
+    const int jj = j0 + j;
+    cplx r = cmake(0, 0);
+    if (k < nb && jj < f) r = (jj >= kb && jj < kb + nb) ? Pg[k * NBT + (jj - kb)] : A[(int64_t)(kb + k) * f + jj];
+    Rs[k * RSX + j] = r;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
+  double re[2][2][2], im[2][2][2];
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb) {
+    const int i = i0 + wr * 16 + rb * 8 + g;
+    const bool upd = i < f && !(i >= kb && i < kb + nb);
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + wc * 16 + cb * 8 + 2 * q + e;
+        const bool jK = j >= kb && j < kb + nb;
+        cplx v = cmake(0, 0);
+        if (upd && j < f && !jK) v = A[(int64_t)i * f + j];
+        re[rb][cb][e] = v.x;
+        im[rb][cb][e] = v.y;
+      }
+  }
+#pragma unroll
+  for (int ks = 0; ks < NBT / 4; ++ks) {
+    const int k = ks * 4 + q;
+    cplx av[2], bv[2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) av[rb] = Cs[(wr * 16 + rb * 8 + g) * CSX + k];
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb) bv[cb] = Rs[k * RSX + wc * 16 + cb * 8 + g];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        dmma884(re[rb][cb][0], re[rb][cb][1], -av[rb].x, bv[cb].x);   // Re -= Cr Rr
+        dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].y, bv[cb].y);    // Re += Ci Ri
+        dmma884(im[rb][cb][0], im[rb][cb][1], -av[rb].x, bv[cb].y);   // Im -= Cr Ri
+        dmma884(im[rb][cb][0], im[rb][cb][1], -av[rb].y, bv[cb].x);   // Im -= Ci Rr
+      }
+  }
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb) {
+    const int i = i0 + wr * 16 + rb * 8 + g;
+    if (i >= f) continue;
+    const bool upd = !(i >= kb && i < kb + nb);
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + wc * 16 + cb * 8 + 2 * q + e;
+        if (j >= f) continue;
+        const bool jK = j >= kb && j < kb + nb;
+        if (upd) A[(int64_t)i * f + j] = cmake(re[rb][cb][e], im[rb][cb][e]);
+        else if (jK) A[(int64_t)i * f + j] = Pg[(i - kb) * NBT + (j - kb)];   // rows K: F[K,K] = P
+      }
+  }
+}
+template <int NBT>
+constexpr size_t upd_mma_smem() { return (size_t)(MU_R * (NBT + 1) + NBT * (MU_C + 1)) * sizeof(cplx); }
+
 // ------------------------------------------------------------ lean storage kernels
 // extend-add of packed child Schur complements into the parents' workspace
 __global__ void k_nd_ea_packed(const int* __restrict__ list, const FrontMeta* __restrict__ frw,
@@ -1784,9 +1885,15 @@ static void pivot_sweep_nb(const FrontMeta* fr, int t0, int cnt, int Bn, int ms,
   const size_t sp = piv_smem<NBT>() + (NBT == 16 && !ND_PIV_REG ? (size_t)NBT * 32 * sizeof(cplx) : 0), su = big ? upd_smem<64, NBT>() : upd_smem<32, NBT>();
   if (sp > 48 * 1024) smem_attr((const void*)k_nd_piv<NBT>, sp);
   if (su > 48 * 1024) smem_attr(big ? (const void*)k_nd_upd<64, NBT> : (const void*)k_nd_upd<32, NBT>, su);
+  // FP64 tensor-core (DMMA) update on the 64-row tiles (HH_ND_MMA=0: the FMA kernel)
+  static const bool use_mma = !getenv("HH_ND_MMA") || atoi(getenv("HH_ND_MMA")) != 0;
+  const bool mma = big && use_mma && NBT >= 4 && NBT % 4 == 0;
+  const size_t sm_mma = upd_mma_smem<NBT>();
+  if (mma && sm_mma > 48 * 1024) smem_attr((const void*)k_nd_upd_mma<NBT>, sm_mma);
   for (int kb = 0; kb < ms; kb += NBT) {
     k_nd_piv<NBT><<<gp, 256, sp, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
-    if (big) k_nd_upd<64, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    if (mma) k_nd_upd_mma<NBT><<<gu, 256, sm_mma, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    else if (big) k_nd_upd<64, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
     else k_nd_upd<32, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
   }
 }
