@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(256) k_nd_piv(const FrontMeta* __restrict__ fr
 // rank-nb update of all rows outside K:
 //   F[i][j] <- (j in K ? 0 : F[i][j]) - sum_k C[i][k] * F[kb+k][j]
 constexpr int UT = 32;   // update tile columns (UR x UT outputs per CTA, 256 threads)
-constexpr int NB_MAX = 32;   // C-buffer layout allows pivot blocks up to this size (64 needs NB_MAX = 64)
+constexpr int NB_MAX = 32;   // C-buffer layout allows pivot blocks up to this size (64 needs NB_MAX = 64; measured slower, also with DMMA)
 // update tile rows UR (UR / 8 rows per thread): 64 for fronts of order >= 1024
 // (more multiply-adds per shared-memory read; 3 CTAs per SM), 32 below (more CTAs
 // for the many small fronts)

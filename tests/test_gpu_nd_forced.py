@@ -10,7 +10,9 @@ tests/nd_forced_check.py in a subprocess:
   * the same with the K-split off (k_nd_rows_wide<1> on the long rows);
   * lean storage (transposed forward k_nd_fwdT + k_nd_fwdT_red, chunked
     factorisation with packed Schur complements) with a tiny workspace
-    (HH_ND_LEAN=1, HH_ND_WMAX=20000) plus the wide levels.
+    (HH_ND_LEAN=1, HH_ND_WMAX=20000) plus the wide levels;
+  * the factorisation's large-front update paths (64-row tiles, pivot blocks
+    of 32, DMMA or FMA update kernel) on every front of order >= 48.
 Bars: coarse solve <= 1e-10 (residual <= 1e-11), V-cycle <= 1e-10, FGMRES
 iterations +-1 and solution <= 1e-8 at equal counts (BASELINE north_star)."""
 import json
@@ -28,6 +30,10 @@ VARIANTS = {
     "wide_vmax_bwdk": {"HH_ND_WIDE": "4", "HH_ND_VMAX": "40", "HH_ND_BWDK_F": "64"},
     "wide_no_bwdk": {"HH_ND_WIDE": "4", "HH_ND_VMAX": "40", "HH_NO_BWDK": "1"},
     "lean_wide": {"HH_ND_LEAN": "1", "HH_ND_WMAX": "20000", "HH_ND_WIDE": "4", "HH_ND_BWDK_F": "64"},
+    # the factorisation's large-front paths on small fronts: 64-row update tiles and
+    # 32-pivot blocks on the FP64 tensor path (DMMA) and with the FMA update kernel
+    "mma_nb32": {"HH_ND_UR64_F": "48", "HH_ND_NB32_F": "48"},
+    "fma_ur64": {"HH_ND_MMA": "0", "HH_ND_UR64_F": "48", "HH_ND_NB32_F": "48"},
 }
 
 
