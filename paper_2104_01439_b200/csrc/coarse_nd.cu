@@ -377,13 +377,14 @@ __global__ void __launch_bounds__(256, UR == 64 ? (NBT == 64 ? 2 : 3) : 5) k_nd_
 // summation order inside the MMA differs.  (Measured on this B200: DMMA 37.2
 // TFLOP/s, DFMA chains 36.3: the win is fewer issued instructions and
 // shared-memory reads per multiply-add, not a higher peak.)
-constexpr int MU_R = 64, MU_C = 32;
+constexpr int MU_C = 32;
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
-template <int NBT>
-__global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restrict__ fr, int begin, int kb, int tiles,
+// UR = 64: 4 x 2 warps of 16 x 16 complex; UR = 32: 2 x 4 warps of 16 x 8 complex
+template <int UR, int NBT>
+__global__ void __launch_bounds__(256, UR == 64 ? 3 : 4) k_nd_upd_mma(const FrontMeta* __restrict__ fr, int begin, int kb, int tiles,
                                                      cplx* __restrict__ Fall, int64_t FE, const cplx* __restrict__ Call,
                                                      int64_t CE, const int64_t* __restrict__ Coff) {
   const int t = begin + blockIdx.y;
@@ -391,6 +392,7 @@ __global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restri
   const FrontMeta m = fr[t];
   if (kb >= m.s) return;
   const int f = m.f;
+  constexpr int MU_R = UR, WC = 8 / (UR / 16), CBN = MU_C / WC / 8;   // warp grid, 8-col blocks per warp
   const int i0 = (blockIdx.x / tiles) * MU_R, j0 = (blockIdx.x % tiles) * MU_C;
   if (i0 >= f || j0 >= f) return;
   const int nb = min(NBT, m.s - kb);
@@ -414,17 +416,18 @@ __global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restri
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wr = warp >> 1, wc = warp & 1, g = lane >> 2, q = lane & 3;
-  double re[2][2][2], im[2][2][2];
+  const int wr = warp / WC, wc = warp % WC, g = lane >> 2, q = lane & 3;
+  const int wcol = wc * (MU_C / WC);
+  double re[2][CBN][2], im[2][CBN][2];
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb) {
     const int i = i0 + wr * 16 + rb * 8 + g;
     const bool upd = i < f && !(i >= kb && i < kb + nb);
 #pragma unroll
-    for (int cb = 0; cb < 2; ++cb)
+    for (int cb = 0; cb < CBN; ++cb)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int j = j0 + wc * 16 + cb * 8 + 2 * q + e;
+        const int j = j0 + wcol + cb * 8 + 2 * q + e;
         const bool jK = j >= kb && j < kb + nb;
         cplx v = cmake(0, 0);
         if (upd && j < f && !jK) v = A[(int64_t)i * f + j];
@@ -435,15 +438,15 @@ __global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restri
 #pragma unroll
   for (int ks = 0; ks < NBT / 4; ++ks) {
     const int k = ks * 4 + q;
-    cplx av[2], bv[2];
+    cplx av[2], bv[CBN];
 #pragma unroll
     for (int rb = 0; rb < 2; ++rb) av[rb] = Cs[(wr * 16 + rb * 8 + g) * CSX + k];
 #pragma unroll
-    for (int cb = 0; cb < 2; ++cb) bv[cb] = Rs[k * RSX + wc * 16 + cb * 8 + g];
+    for (int cb = 0; cb < CBN; ++cb) bv[cb] = Rs[k * RSX + wcol + cb * 8 + g];
 #pragma unroll
     for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
-      for (int cb = 0; cb < 2; ++cb) {
+      for (int cb = 0; cb < CBN; ++cb) {
         dmma884(re[rb][cb][0], re[rb][cb][1], -av[rb].x, bv[cb].x);   // Re -= Cr Rr
         dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].y, bv[cb].y);    // Re += Ci Ri
         dmma884(im[rb][cb][0], im[rb][cb][1], -av[rb].x, bv[cb].y);   // Im -= Cr Ri
@@ -456,10 +459,10 @@ __global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restri
     if (i >= f) continue;
     const bool upd = !(i >= kb && i < kb + nb);
 #pragma unroll
-    for (int cb = 0; cb < 2; ++cb)
+    for (int cb = 0; cb < CBN; ++cb)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int j = j0 + wc * 16 + cb * 8 + 2 * q + e;
+        const int j = j0 + wcol + cb * 8 + 2 * q + e;
         if (j >= f) continue;
         const bool jK = j >= kb && j < kb + nb;
         if (upd) A[(int64_t)i * f + j] = cmake(re[rb][cb][e], im[rb][cb][e]);
@@ -467,8 +470,8 @@ __global__ void __launch_bounds__(256, 3) k_nd_upd_mma(const FrontMeta* __restri
       }
   }
 }
-template <int NBT>
-constexpr size_t upd_mma_smem() { return (size_t)(MU_R * (NBT + 1) + NBT * (MU_C + 1)) * sizeof(cplx); }
+template <int UR, int NBT>
+constexpr size_t upd_mma_smem() { return (size_t)(UR * (NBT + 1) + NBT * (MU_C + 1)) * sizeof(cplx); }
 
 // ------------------------------------------------------------ lean storage kernels
 // extend-add of packed child Schur complements into the parents' workspace
@@ -1885,14 +1888,17 @@ static void pivot_sweep_nb(const FrontMeta* fr, int t0, int cnt, int Bn, int ms,
   const size_t sp = piv_smem<NBT>() + (NBT == 16 && !ND_PIV_REG ? (size_t)NBT * 32 * sizeof(cplx) : 0), su = big ? upd_smem<64, NBT>() : upd_smem<32, NBT>();
   if (sp > 48 * 1024) smem_attr((const void*)k_nd_piv<NBT>, sp);
   if (su > 48 * 1024) smem_attr(big ? (const void*)k_nd_upd<64, NBT> : (const void*)k_nd_upd<32, NBT>, su);
-  // FP64 tensor-core (DMMA) update on the 64-row tiles (HH_ND_MMA=0: the FMA kernel)
-  static const bool use_mma = !getenv("HH_ND_MMA") || atoi(getenv("HH_ND_MMA")) != 0;
-  const bool mma = big && use_mma && NBT >= 4 && NBT % 4 == 0;
-  const size_t sm_mma = upd_mma_smem<NBT>();
-  if (mma && sm_mma > 48 * 1024) smem_attr((const void*)k_nd_upd_mma<NBT>, sm_mma);
+  // FP64 tensor-core (DMMA) update (HH_ND_MMA: 0 = FMA kernels, 1 = DMMA on the 64-row
+  // tiles only, 2 (default) = DMMA on all tiles)
+  static const int use_mma = getenv("HH_ND_MMA") ? atoi(getenv("HH_ND_MMA")) : 2;
+  const bool mma = (big ? use_mma >= 1 : use_mma >= 2) && NBT % 4 == 0;
+  const size_t sm_mma = big ? upd_mma_smem<64, NBT>() : upd_mma_smem<32, NBT>();
+  if (mma && sm_mma > 48 * 1024)
+    smem_attr(big ? (const void*)k_nd_upd_mma<64, NBT> : (const void*)k_nd_upd_mma<32, NBT>, sm_mma);
   for (int kb = 0; kb < ms; kb += NBT) {
     k_nd_piv<NBT><<<gp, 256, sp, s>>>(fr, t0, kb, F, FE, C, CE, coff, flag);
-    if (mma) k_nd_upd_mma<NBT><<<gu, 256, sm_mma, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    if (mma && big) k_nd_upd_mma<64, NBT><<<gu, 256, sm_mma, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
+    else if (mma) k_nd_upd_mma<32, NBT><<<gu, 256, sm_mma, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
     else if (big) k_nd_upd<64, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
     else k_nd_upd<32, NBT><<<gu, 256, su, s>>>(fr, t0, kb, tiles, F, FE, C, CE, coff);
   }
