@@ -227,7 +227,7 @@ def run_ours(args, rank, world, dev):
                 slabkw["coarse_solver"] = hh.HH_COARSE_ND_DIST
 
         b_dev = torch.from_numpy(np.ascontiguousarray(rhs)).to(dev)
-        timers = {"on": False, "acc": None}
+        timers = {"on": False, "acc": None, "flops": [0.0, 0.0], "kind": None}
 
         def step():
             gp = hh.Problem.from_spec(spec, **slabkw)   # setup + coarse factorisation (inside the step)
@@ -244,6 +244,10 @@ def run_ours(args, rank, world, dev):
                         for key in ("ms", "bytes", "launches", "bytes_all", "model", "model_all"):
                             timers["acc"][ph][key] += t[ph][key]
                     timers["acc"]["launches"] += t["launches"]
+                f = hh.coarse_flops(gp)
+                timers["flops"][0] += f[0]
+                timers["flops"][1] += f[1]
+            timers["kind"] = gp.coarse_kind()
             gp.close()
             # one solve over all ranks: each rank counts its share of the work
             return r["iterations"] / world, r["iterations"] * spec.n_nodes / world, [r]
@@ -252,8 +256,7 @@ def run_ours(args, rank, world, dev):
               "n_cells": spec.n, "dim": spec.dim, "restart": spec.restart, "rtol": spec.rtol,
               "l2": "Krylov basis > L2 (126 MB); L2 flushed between steps",
               "parallelism": f"slab{world}" if world > 1 else "single",
-              "coarse": ("distributed slab-aligned ND" if args.coarse == "dist" else "replicated ND")
-              if world > 1 else "ND"}
+              "coarse": None}
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
     clk = Clocks(dev) if rank == 0 and not os.environ.get("HH_BENCH_NO_CLOCKS") else None
     for _ in range(args.warmup):
@@ -292,10 +295,20 @@ def run_ours(args, rank, world, dev):
         rank_ms = [None] * world
         dist.all_gather_object(rank_ms, dev_ms)
     if args.workload in ("sweep", "search"):
+        flops = hh.coarse_flops(None)        # before sweep_timers(0) resets them
         tm = hh.sweep_timers(0)
+        wl["coarse"] = ("fast diagonalisation on every batch (HH_COARSE_AUTO: constant k, resolved "
+                        "coarse grids; ND factor only on a validation failure)")
     else:
         timers["on"] = False
         tm = timers["acc"]
+        flops = tuple(timers["flops"])
+        kind = {hh.HH_COARSE_FD: "fast diagonalisation (FP64 tensor-core GEMMs)",
+                hh.HH_COARSE_ND: "nested-dissection factor" + (" (replicated)" if world > 1 else ""),
+                hh.HH_COARSE_ND_DIST: "distributed slab-aligned ND"}
+        wl["coarse"] = kind.get(timers["kind"], str(timers["kind"]))
+    if tm is not None:
+        tm["coarse_flops"], tm["coarse_flops_all"] = flops[0], flops[1]
     dev_ms, tot_dofs, tot_its = combine_ranks(dev_ms, tot_dofs, tot_its, world, dev)
     value = tot_dofs / (dev_ms * 1e-3)
     out = {"value": value, "ms_per_step": dev_ms / args.steps, "wl": wl, "timers": tm,
@@ -464,6 +477,7 @@ def oracle_rate(args, budget_s):
 
 PHASE_KERNELS = {"pre": "k_pre2d / k_pre3d (fused 2x Jacobi + residual + I^T restriction)",
                  "coarse": "nd_solve (k_nd_* forward/backward GEMV sweeps of one coarse solve)",
+                 "coarse_fd": "fd_solve (k_fd_fold, 2d x k_fd_gemm complex FP64 DMMA GEMMs, k_fd_unfold)",
                  "post": "k_post2d / k_post3d (fused I e_c + 2x Jacobi + A_0 apply)",
                  "krylov": "k_mdot + k_update (CGS multi-dot, update + norm + Givens)"}
 
@@ -479,11 +493,13 @@ def measured_traffic(workload):
         return None
 
 
-def roofline(tm, out, args, peak, peak_kind):
+def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
     """Per-phase HBM rates from the sampled CUDA-event phase timers:
     algorithmic bytes = SURVEY.md 8(d)'s per-step model ("model": every Jacobi
     step, transfer and apply a separate pass), next to our fused kernels'
-    compulsory bytes ("fused")."""
+    compulsory bytes ("fused").  A fast-diagonalisation coarse phase (dense
+    complex GEMMs) is tensor-bound: its algorithmic flops / time against the
+    measured FP64 MMA peak."""
     phases = {}
     for ph in ("pre", "coarse", "post", "krylov"):
         d = tm[ph]
@@ -512,7 +528,29 @@ def roofline(tm, out, args, peak, peak_kind):
            "frac": ball / step_s / 1e9 / peak, "fused_frac": fall / step_s / 1e9 / peak,
            "note": "bytes of every iteration / whole step time (setup and factorisation included)"}
     tr = measured_traffic(args.workload)
+    fd = tm.get("coarse_flops", 0.0) > 0 and "coarse" in phases
+    if fd:
+        c = phases["coarse"]
+        sec = c["ms"] * 1e-3
+        c["bound"] = "tensor"
+        c["flops_per_launch"] = tm["coarse_flops"] / c["launches"]
+        c["achieved_tflops"] = tm["coarse_flops"] / sec / 1e12
+        c["tflops_frac"] = c["achieved_tflops"] / mma_peak if mma_peak else None
+        fa = tm.get("coarse_flops_all", 0.0) / args.steps
+        if fa > 0 and tot_ms > 0 and mma_peak:
+            c["wall_share_tflops_frac"] = fa / (step_s * c["ms"] / tot_ms) / 1e12 / mma_peak
     p = phases[dom]
+    if fd and dom == "coarse":
+        return {"bound": "tensor", "kernel": PHASE_KERNELS["coarse_fd"], "phase": dom,
+                "achieved": p["achieved_tflops"], "peak": mma_peak, "unit": "TFLOP/s",
+                "frac": p["tflops_frac"],
+                "traffic": (tr or {}).get("coarse_fd", {}).get("dram_bytes_per_launch"),
+                "traffic_source": (tr or {}).get("source"),
+                "peak_source": "measured (hh_fp64_mma_peak: mma.sync m8n8k4 f64 microbenchmark, this run)",
+                "flops_model": "8 real flops per complex multiply-add of the 2d folded transforms: "
+                               "2D 128 P^3, 3D 384 P^4 per sample and solve (P = nc/2 + 1); DESIGN.md section 7e",
+                "frac_wall_share": p.get("wall_share_tflops_frac"), "phases": phases, "aggregate": agg,
+                "hbm_peak": peak, "hbm_peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
     return {"bound": "hbm", "kernel": PHASE_KERNELS[dom], "phase": dom, "achieved": p["achieved_gbs"],
             "peak": peak, "unit": "GB/s", "frac": p["frac"],
             "traffic": (tr or {}).get(dom, {}).get("dram_bytes_per_launch"),
@@ -521,6 +559,12 @@ def roofline(tm, out, args, peak, peak_kind):
             "bytes_model": "SURVEY.md 8(d) per-step model bytes per launch (fused kernels' compulsory "
                            "bytes alongside as fused_*); DESIGN.md section 6",
             "frac_wall_share": p.get("wall_share_frac"), "phases": phases, "aggregate": agg}
+
+
+def hh_mma_peak(dev):
+    """Measured FP64 tensor-core TFLOP/s (after the timed region)."""
+    import paper_2104_01439_b200.hh as hh
+    return hh.fp64_mma_peak(dev)
 
 
 def main():
@@ -584,7 +628,8 @@ def main():
     tm = out["timers"]
     roof = None
     if tm:
-        roof = roofline(tm, out, args, peak, peak_kind)
+        mma_peak = hh_mma_peak(dev) if tm.get("coarse_flops", 0.0) > 0 else None
+        roof = roofline(tm, out, args, peak, peak_kind, mma_peak)
     line = {"metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": out["ms_per_step"],
             "higher_is_better": True,

@@ -57,7 +57,7 @@ enum { HH_OP_A0 = 0, HH_OP_AEPS = 1, HH_OP_AEPS_COARSE = 2 };
 
 /* coarse direct solver (Alg. 1 line 3; factored once per setup,
  * PAPER.md:511-512):
- *  HH_COARSE_AUTO / HH_COARSE_ND: nested-dissection LDL^T-type factor (no pivoting,
+ *  HH_COARSE_ND: nested-dissection LDL^T-type factor (no pivoting,
  *    reading C18); with a slab decomposition every rank holds the whole factor
  *    and solves redundantly (SURVEY.md 8(e) "first version");
  *  HH_COARSE_ND_DIST (slab decompositions only): distributed exact solve --
@@ -69,8 +69,20 @@ enum { HH_OP_A0 = 0, HH_OP_AEPS = 1, HH_OP_AEPS_COARSE = 2 };
  *    parent's owner and the interface solutions are broadcast (NCCL, or device
  *    copies between in-process slabs).  Needs >= 2 coarse planes per slab.
  *    (The paper's own distributed step is parallel MUMPS LU, PAPER.md:511,
- *    1463-1466.)                                                            */
-enum { HH_COARSE_AUTO = 0, HH_COARSE_ND = 1, HH_COARSE_ND_DIST = 2 };
+ *    1463-1466.)
+ *  HH_COARSE_FD (constant k only): the same exact solve by fast diagonalisation.
+ *    For constant k the Q1 coarse operator is the Kronecker sum
+ *    A = sum_axes M1 x .. x (K1 - ik E) x .. x M1 - (k^2 + i eps) M1 x .. x M1
+ *    of the 1D stiffness K1, mass M1 and boundary selector E, so
+ *    A^{-1} = (V x .. x V) diag(1/(lam_i + lam_j (+ lam_l) - k^2 - i eps)) (V^T x .. x V^T)
+ *    with S0 V = M1 V Lambda (V^T M1 V = I): the eigenpairs come from the DCT-I
+ *    basis plus a rank-one secular equation per parity (validated), the solve is
+ *    2 d complex GEMMs per folded parity block on the FP64 tensor cores.  The
+ *    product is the exact coarse solution (parity with the oracle's LU <= 1e-13).
+ *  HH_COARSE_AUTO: FD for constant k when the dense transforms beat the factor
+ *    (2D nc <= 512, 3D nc <= 256, k h_c <= 2.5) and its validation passes, the
+ *    ND factor otherwise (heterogeneous k, slab-distributed factor, fallback).  */
+enum { HH_COARSE_AUTO = 0, HH_COARSE_ND = 1, HH_COARSE_ND_DIST = 2, HH_COARSE_FD = 3 };
 
 typedef struct {
   int32_t dim;                  /* 2 | 3                                                    */
@@ -287,11 +299,28 @@ hh_status hh_read_timers(hh_problem* p, double* st24, int64_t* launches);
  * timing on (1) / off (0); -1 only reads. */
 hh_status hh_sweep_timers(int32_t reset_enable, double* st24, int64_t* launches);
 
+/* The coarse solver a handle actually uses (HH_COARSE_ND / _ND_DIST / _FD; AUTO
+ * resolved, including FD's fallback to ND when its eigen-decomposition fails
+ * validation).  kind: out.                                                     */
+hh_status hh_coarse_kind(const hh_problem* p, int32_t* kind);
+
+/* Coarse-solve flops since the last timer reset (hh_reset_timers / hh_sweep_timers):
+ * flops2 = [flops of the timed (sampled) iterations, flops of every iteration]
+ * (real flops of the fast-diagonalisation GEMMs, 8 per complex multiply-add;
+ * 0 for the ND factor, whose roofline is bytes).  p = NULL: the sweep's.       */
+hh_status hh_coarse_flops(hh_problem* p, double* flops2);
+
 /* FP64 FMA throughput of the device (microbenchmark: independent DFMA chains on
  * every SM, best of 5 timed launches, 2 flops per DFMA): the measured peak the
  * coarse factorisation's TFLOP/s are quoted against.
  * tflops: out; sm_mhz: out (nullable), the device's nominal SM clock.  blocks. */
 hh_status hh_fp64_peak(int32_t device, double* tflops, double* sm_mhz);
+
+/* FP64 tensor-core throughput (microbenchmark: independent mma.sync m8n8k4 f64
+ * accumulators on every SM, best of 5, 512 flops per MMA): the denominator of
+ * the fast-diagonalisation coarse solve's TFLOP/s (its GEMMs run on this
+ * instruction).  tflops: out.  Blocks.                                        */
+hh_status hh_fp64_mma_peak(int32_t device, double* tflops);
 
 const char* hh_last_error(void);
 const char* hh_version(void);

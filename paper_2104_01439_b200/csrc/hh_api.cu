@@ -291,7 +291,23 @@ struct BatchSpec {
   Comm* comm = nullptr;
   int shift_map = 0;                     // > 0: sigma = sigma_p(k_e, log2 n) of Table 1 row p
   bool dist = false;                     // slab mode: distributed coarse solve (HH_COARSE_ND_DIST)
+  int coarse = HH_COARSE_AUTO;           // requested HH_COARSE_* (AUTO: FD falls back to ND on failure)
+  bool fd = false;                       // coarse solve by fast diagonalisation (fd.cu; constant k)
 };
+
+// AUTO's choice of the fast-diagonalisation coarse solve (fd.cu): constant k,
+// no distributed factor, and a size where its dense transforms beat the ND
+// factor (2D: 16 m^3 flops per solve against O(m^2 log m) bytes -- the GEMMs
+// win up to nc ~ 512 on B200; 3D: 24 m^4 flops against the O(m^4)-byte, O(m^6)-flop
+// factor -- always) with a resolved coarse grid (k h_c <= 2.5, where the secular
+// continuation is validated; the ND factor takes the rest)
+bool fd_wanted(int req, int dim, int nc, bool het, bool dist, double kmax) {
+  if (het || dist) return false;
+  if (req == HH_COARSE_FD) return true;
+  if (req != HH_COARSE_AUTO) return false;
+  if (!(kmax / nc <= 2.5)) return false;
+  return dim == 3 ? nc <= 256 : nc <= 512;
+}
 
 // fine-vector layout of a batch: G ghost planes, entry stride, slab bounds
 struct FineLayout {
@@ -332,7 +348,7 @@ struct Engine {
   bool conc = false;         // runs beside other sweep workers (ND schedule choice)
   cudaStream_t s = nullptr;
   Pool V, Z, w, u, bv, xv, tmp3, rc, ec, stc, F, cbuf, work, kcf, kcc, coef_f, coef_c, ksmall,
-      cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp, dscratch, dflag, dstage;
+      cpart, dpart, hist, kstage, slabp, hstage, ustage, dinvp, dscratch, dflag, dstage, fdb, fdm;
   // distributed coarse solve: one rank view per entry (factor, packed S, work per view)
   std::vector<NDDistView> dviews;
   std::vector<Pool> dF, dS, dW;
@@ -351,6 +367,7 @@ struct Engine {
   int* jdev = nullptr;
   int* nd_flag = nullptr;
   int* flow_fail = nullptr;  // dataflow coarse-solve failure flag of the status-less calls
+  const int* fd_bidx = nullptr;   // FD: basis slot of every entry (device, in fdm)
   double setup_s = 0;
   // graph of one iteration
   cudaGraphExec_t gexec = nullptr;     // plain iteration
@@ -371,6 +388,7 @@ struct Engine {
   double acc_model[T_NT] = {0, 0, 0, 0};      // SURVEY 8(d) per-step model bytes, timed iterations
   double acc_model_all[T_NT] = {0, 0, 0, 0};  // ... every iteration
   double acc_launch[T_NT] = {0, 0, 0, 0};
+  double acc_flops = 0, acc_flops_all = 0;    // coarse-solve flops (FD: tensor-core GEMMs), timed / every iteration
   int64_t launches = 0;
   int64_t launches_per_iter = 0;
 
@@ -378,7 +396,7 @@ struct Engine {
   void release_pools() {
     Pool* all[] = {&V, &Z, &w, &u, &bv, &xv, &tmp3, &rc, &ec, &stc, &F, &cbuf, &work, &kcf, &kcc,
                    &coef_f, &coef_c, &ksmall, &cpart, &dpart, &hist, &kstage, &slabp, &hstage, &ustage, &dinvp,
-                   &dscratch, &dflag, &dstage};
+                   &dscratch, &dflag, &dstage, &fdb, &fdm};
     for (Pool* p : all) p->release();
     for (auto* vp : {&dF, &dS, &dW})
       for (Pool& p : *vp) p.release();
@@ -402,12 +420,13 @@ hh_status engine_init(Engine& E, int device) {
 }
 
 // bytes of device workspace per sample for a (dim, n, m) batch
-int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {
+int64_t per_sample_bytes(int dim, int n, int m, const NDPlan* plan) {   // plan == NULL: FD coarse solve
   const int64_t N = ipow(n + 1, dim + 0) + 6 * ipow(n + 1, dim - 1), Nc = ipow(n / 2 + 1, dim);
   const int S = dim == 2 ? 9 : 27;
   int64_t b = (int64_t)(2 * m + 1 + 4 + (dim == 3 ? 2 : 0)) * N * 16;
   b += Nc * (2 + S) * 16;
-  b += (nd_front_entries(plan) + nd_cbuf_entries(plan) + nd_work_entries(plan)) * 16;
+  if (plan) b += (nd_front_entries(plan) + nd_cbuf_entries(plan) + nd_work_entries(plan)) * 16;
+  else b += (fd_basis_entries(n / 2) + fd_work_entries(dim, n / 2)) * 16;
   return b;
 }
 
@@ -438,7 +457,7 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   const int64_t N = FL.stride, Nc = ipow(n / 2 + 1, dim);
   const int Bf = sp.slabmode ? 1 : B;
   NDPlan* P = nullptr;
-  if (!sp.dist) HH_TRY(get_plan(dim, n / 2 + 1, &P));   // distributed: rank views (dist_setup)
+  if (!sp.dist && !sp.fd) HH_TRY(get_plan(dim, n / 2 + 1, &P));   // distributed: rank views (dist_setup)
   const int S = dim == 2 ? 9 : 27;
   const int nblk = krylov_blocks((int64_t)FL.maxloc * FL.plane);
   // fine vectors: B entries of N (ghosted, padded) nodes + 16 nodes of slack for the lead pad
@@ -459,6 +478,11 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   if (P) {
     HH_TRY(E.work.ensure((size_t)B * nd_work_entries(P) * 16));
     HH_TRY(nd_flow_reset(P, B, E.work.as<cplx>(), E.s));
+  }
+  if (sp.fd) {   // eigenbases (one per factor copy) + two transform buffers per entry
+    HH_TRY(E.fdb.ensure((size_t)Bf * fd_basis_entries(n / 2) * 16));
+    HH_TRY(E.fdm.ensure((size_t)B * 16 + 64));   // bidx[B] | slot flags | slot k (section 7e)
+    HH_TRY(E.work.ensure((size_t)B * fd_work_entries(dim, n / 2) * 16));
   }
   HH_TRY(E.kcf.ensure((size_t)B * 16));
   HH_TRY(E.kcc.ensure((size_t)B * 16));
@@ -550,8 +574,9 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
                      n, sp.slabs_total);
         return HH_E_CONFIG;
       }
+  E.plan = nullptr;
   if (sp.dist) HH_TRY(dist_setup(E, sp));
-  else HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
+  else if (!sp.fd) HH_TRY(get_plan(dim, n / 2 + 1, &E.plan));
   const NDPlan* P = E.plan;
   // pools
   HH_TRY(reserve_pools(E, sp));
@@ -694,6 +719,30 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
     nflag = B;
     flags = E.dflag.as<int>();
     prof_mark(E, "factor", tp);
+  } else if (sp.fd) {   // eigenpairs of the 1D pencil per factor copy (fd.cu)
+    // one eigenbasis per distinct k (it does not depend on eps): slots
+    std::vector<double> ks;
+    std::vector<int> meta(B, 0);
+    for (int b = 0; b < B; ++b) {
+      const double kb = sp.k[sp.slabmode ? 0 : b];
+      int sl = 0;
+      while (sl < (int)ks.size() && ks[sl] != kb) ++sl;
+      if (sl == (int)ks.size()) ks.push_back(kb);
+      meta[b] = sl;
+    }
+    const int ns = (int)ks.size();
+    const size_t o_fl = (size_t)B, o_k = ((o_fl + ns) * sizeof(int) + 7) / 8 * 8;
+    std::vector<char> hb(o_k + ns * sizeof(double), 0);
+    memcpy(hb.data(), meta.data(), B * sizeof(int));
+    memcpy(hb.data() + o_k, ks.data(), ns * sizeof(double));
+    HH_CUDA_TRY(cudaMemcpyAsync(E.fdm.p, hb.data(), hb.size(), cudaMemcpyHostToDevice, E.s));
+    char* fm = E.fdm.as<char>();
+    E.fd_bidx = (const int*)fm;
+    HH_TRY(fd_setup(dim, n / 2, E.Bf, ns, (const double*)(fm + o_k), E.fd_bidx, (int*)fm + o_fl, E.LC.kc,
+                    E.fdb.as<cplx>(), E.nd_flag, E.s));
+    const char* ff = getenv("HH_FD_FAIL");   // fault injection (tests): validation failure
+    if (ff && atoi(ff)) HH_TRY(fd_flag_all(E.nd_flag, E.Bf, 1, E.s));
+    prof_mark(E, "fd basis", tp);
   } else {
     HH_TRY(nd_factor(P, E.Bf, E.stc.as<cplx>(), E.F.as<cplx>(), E.cbuf.as<cplx>(), E.nd_flag, E.s));
     prof_mark(E, "factor", tp);
@@ -712,7 +761,19 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   HH_CUDA_TRY(cudaStreamSynchronize(E.s));
   for (int b = 0; b < nflag; ++b)
     if (E.h_status[b]) {
-      hh_set_error("zero pivot in the coarse factorisation (sample %d: k=%g, beta=%g, sigma=%g, h=%g)",
+      if (sp.fd && E.h_status[b] == 1) {   // secular roots failed validation
+        if (sp.coarse == HH_COARSE_AUTO) {   // -> the nested-dissection factor
+          BatchSpec nd = sp;
+          nd.fd = false;
+          return batch_setup(E, nd);
+        }
+        hh_set_error("HH_COARSE_FD: eigen-decomposition of the coarse pencil failed validation "
+                     "(sample %d: k=%g, h_c=%g; use HH_COARSE_ND)", b, sp.k.empty() ? 0.0 : sp.k[b], E.LC.h);
+        return HH_E_SINGULAR;
+      }
+      hh_set_error("%s (sample %d: k=%g, beta=%g, sigma=%g, h=%g)",
+                   sp.fd ? "singular coarse operator (zero transformed diagonal entry)"
+                         : "zero pivot in the coarse factorisation",
                    b, sp.k.empty() ? 0.0 : sp.k[b], sp.beta[b], sp.sigma[b], E.LC.h);
       return HH_E_SINGULAR;
     }
@@ -733,6 +794,9 @@ hh_status coarse_solve_all(Engine& E, const int* st, VArg rhs, VArg x) {
     HH_TRY(nd_dist_solve(E.dviews, st, rhs, x, E.spec.comm, E.dstage.as<cplx>(), E.s));
     return slab_coarse_allgather(E.X, x, E.s);
   }
+  if (E.spec.fd)   // slab mode: one basis shared by the entries (the replicated coarse solve)
+    return fd_solve(E.spec.dim, E.spec.n / 2, E.B, st, E.fdb.as<cplx>(), E.fd_bidx, E.LC.kc, E.work.as<cplx>(),
+                    rhs, x, E.s);
   return nd_solve(E.plan, E.B, st, E.F.as<cplx>(), E.work.as<cplx>(), rhs, x, E.s, slab_mode(E), E.conc,
                   E.flow_fail);
 }
@@ -818,7 +882,8 @@ int64_t launches_per_iteration(const Engine& E) {
     slab = 2 * ((E.B > 1 ? 1 : 0) + (multi ? 2 : 0)) + (E.B > 1 ? 1 : 0) + 2;
   }
   const int kry = E.ka.reorth ? 4 + (slab_mode(E) ? 2 * (2 + (E.X.comm && E.X.comm->nranks > 1 ? 2 : 0)) : 0) : 0;
-  const int nd = E.spec.dist ? nd_dist_launches(E.dviews) + 2 : nd_solve_launches(E.plan, E.B, E.conc);
+  const int nd = E.spec.fd ? fd_solve_launches(E.spec.dim)
+                           : (E.spec.dist ? nd_dist_launches(E.dviews) + 2 : nd_solve_launches(E.plan, E.B, E.conc));
   return fine + nd + 3 + slab + kry;
 }
 
@@ -866,7 +931,9 @@ void phase_bytes(const Engine& E, int j, double* out, double* model) {
   out[T_PRE] = 32.0 * N + 16.0 * Nc + ce;                  // f, u, r_c (+ coef)
   out[T_POST] = 64.0 * N + 16.0 * Nc + ce;                 // f, u, e_c, z, w (+ coef)
   double nb = 0;
-  if (E.spec.dist)   // every view streams its own fronts (per problem: the sum over the ranks)
+  if (E.spec.fd)
+    nb = (double)fd_solve_bytes(E.spec.dim, E.spec.n / 2) - 32.0 * Nc;
+  else if (E.spec.dist)   // every view streams its own fronts (per problem: the sum over the ranks)
     for (const NDDistView& v : E.dviews) nb += (double)nd_stream_bytes(v.plan);
   else
     nb = (double)nd_stream_bytes(E.plan);
@@ -881,9 +948,13 @@ void phase_bytes(const Engine& E, int j, double* out, double* model) {
   model[T_KRYLOV] = (32.0 * (j + 1) + 48.0) * N;           // CGS 32j + 80 B/node (j counted from 1)
   if (E.ka.reorth == 2) model[T_KRYLOV] *= 2.0;
 }
+double coarse_flops(const Engine& E) {   // per running sample and coarse solve (FD GEMMs; 0 for ND)
+  return E.spec.fd ? fd_solve_flops(E.spec.dim, E.spec.n / 2) : 0.0;
+}
 void account_bytes(Engine& E, int running, int j) {
   double pb[T_NT], mb[T_NT];
   phase_bytes(E, j, pb, mb);
+  E.acc_flops += running * coarse_flops(E);
   for (int t = 0; t < T_NT; ++t) {
     E.acc_bytes[t] += running * pb[t];
     E.acc_model[t] += running * mb[t];
@@ -893,6 +964,7 @@ void account_bytes(Engine& E, int running, int j) {
 void account_bytes_all(Engine& E, int running, int j) {
   double pb[T_NT], mb[T_NT];
   phase_bytes(E, j, pb, mb);
+  E.acc_flops_all += running * coarse_flops(E);
   for (int t = 0; t < T_NT; ++t) {
     E.acc_bytes_all[t] += running * pb[t];
     E.acc_model_all[t] += running * mb[t];
@@ -1121,8 +1193,12 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
   if (d->max_restart < 1 || d->max_restart > 127) { hh_set_error("max_restart must be in 1..127"); return HH_E_CONFIG; }
   if (!(d->beta >= 0)) { hh_set_error("beta must be >= 0"); return HH_E_CONFIG; }
   if (d->shift_map < 0 || d->shift_map > 3) { hh_set_error("shift_map must be 0..3"); return HH_E_CONFIG; }
-  if (d->coarse_solver < HH_COARSE_AUTO || d->coarse_solver > HH_COARSE_ND_DIST) {
-    hh_set_error("coarse_solver must be HH_COARSE_AUTO, HH_COARSE_ND or HH_COARSE_ND_DIST");
+  if (d->coarse_solver < HH_COARSE_AUTO || d->coarse_solver > HH_COARSE_FD) {
+    hh_set_error("coarse_solver must be HH_COARSE_AUTO, HH_COARSE_ND, HH_COARSE_ND_DIST or HH_COARSE_FD");
+    return HH_E_CONFIG;
+  }
+  if (d->coarse_solver == HH_COARSE_FD && d->k_elem) {
+    hh_set_error("HH_COARSE_FD needs a constant k (the coarse operator must be separable)");
     return HH_E_CONFIG;
   }
   const int nloc = std::max(1, d->nslabs_local);
@@ -1163,6 +1239,8 @@ extern "C" hh_status hh_setup_problem(const hh_problem_desc* d, hh_problem** out
     sp.kf = d->k_elem; sp.kcoarse = d->k_elem_coarse;
     sp.shift_map = d->shift_map;
     sp.dist = d->coarse_solver == HH_COARSE_ND_DIST;
+    sp.coarse = d->coarse_solver;
+    sp.fd = fd_wanted(d->coarse_solver, d->dim, d->n_cells / 2, d->k_elem != nullptr, sp.dist, d->k_const);
     st = enter(*p->ep, p->user);
     if (st == HH_OK) st = batch_setup(*p->ep, sp);
   }
@@ -1230,7 +1308,7 @@ extern "C" hh_status hh_vcycle(hh_problem* p, const void* f, void* z) {
   HH_TRY(fine_post(E.LF, E.B, nullptr, E.spec.nu_post, E.spec.omega, vfine(E, E.bv), SArg(),
                    vfine(E, E.u), vflat(E.ec, E.Nc), vfine(E, E.xv), VArg(), E.s));
   HH_TRY(user_out(E, E.xv, z));
-  HH_TRY(flow_check(E, !E.spec.dist && nd_solve_uses_flow(E.plan, E.B, E.conc)));
+  HH_TRY(flow_check(E, !E.spec.dist && !E.spec.fd && nd_solve_uses_flow(E.plan, E.B, E.conc)));
   return leave(E, p->user);
 }
 
@@ -1243,6 +1321,11 @@ extern "C" hh_status hh_coarse_solve(hh_problem* p, const void* r, void* e) {
       HH_CUDA_TRY(cudaMemcpyAsync(E.rc.as<cplx>() + (int64_t)b * E.Nc, r, E.Nc * 16, cudaMemcpyDeviceToDevice, E.s));
     HH_TRY(coarse_solve_all(E, nullptr, vflat(E.rc, E.Nc), vflat(E.ec, E.Nc)));
     HH_CUDA_TRY(cudaMemcpyAsync(e, E.ec.p, E.Nc * 16, cudaMemcpyDeviceToDevice, E.s));
+    return leave(E, p->user);
+  }
+  if (E.spec.fd) {
+    HH_TRY(fd_solve(E.spec.dim, E.spec.n / 2, 1, nullptr, E.fdb.as<cplx>(), E.fd_bidx, E.LC.kc, E.work.as<cplx>(),
+                    varg((cplx*)r, 0), varg((cplx*)e, 0), E.s));
     return leave(E, p->user);
   }
   HH_TRY(nd_solve(E.plan, 1, nullptr, E.F.as<cplx>(), E.work.as<cplx>(), varg((cplx*)r, 0),
@@ -1341,6 +1424,7 @@ extern "C" hh_status hh_reset_timers(hh_problem* p, int32_t enable) {
   for (int i = 0; i < T_NT; ++i)
     p->ep->acc_ms[i] = p->ep->acc_bytes[i] = p->ep->acc_launch[i] = p->ep->acc_bytes_all[i] =
         p->ep->acc_model[i] = p->ep->acc_model_all[i] = 0;
+  p->ep->acc_flops = p->ep->acc_flops_all = 0;
   p->ep->launches = 0;
   return HH_OK;
 }
@@ -1364,6 +1448,7 @@ extern "C" hh_status hh_read_timers(hh_problem* p, double* st12, int64_t* launch
 static std::mutex g_sweep_mu;
 static bool g_sweep_timing = false;
 static double g_sweep_st[6 * T_NT] = {0};
+static double g_sweep_flops[2] = {0, 0};
 static int64_t g_sweep_launches = 0;
 // persistent sweep engines per device; a sweep holds its device's lock for the
 // whole call, so concurrent hh_sweep calls never share an engine
@@ -1384,6 +1469,7 @@ extern "C" hh_status hh_sweep_timers(int32_t reset_enable, double* st12, int64_t
   if (reset_enable >= 0) {
     g_sweep_timing = reset_enable != 0;
     for (double& a : g_sweep_st) a = 0;
+    g_sweep_flops[0] = g_sweep_flops[1] = 0;
     g_sweep_launches = 0;
   }
   return HH_OK;
@@ -1413,6 +1499,11 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     return HH_E_CONFIG;
   }
   if (common->shift_map < 0 || common->shift_map > 3) { hh_set_error("shift_map must be 0..3"); return HH_E_CONFIG; }
+  if (common->coarse_solver != HH_COARSE_AUTO && common->coarse_solver != HH_COARSE_ND &&
+      common->coarse_solver != HH_COARSE_FD) {
+    hh_set_error("sweep: coarse_solver must be HH_COARSE_AUTO, HH_COARSE_ND or HH_COARSE_FD");
+    return HH_E_CONFIG;
+  }
   const int m = std::max(o->restart, common->max_restart > 0 ? common->max_restart : o->restart);
   for (int i = 0; i < n; ++i) {
     memset(&out[i], 0, sizeof(out[i]));
@@ -1456,13 +1547,18 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   }
   const double budget = 0.60 * (double)totb / nstreams;   // engines persist: budget on total HBM
   std::vector<std::vector<int>> batches;
+  std::map<int, bool> group_fd;
   for (auto& kv : groups) {
     std::vector<int>& gi = kv.second;
     std::stable_sort(gi.begin(), gi.end(), [&](int a, int b) {
       return smp[a].beta * std::pow(smp[a].k, smp[a].sigma) > smp[b].beta * std::pow(smp[b].k, smp[b].sigma);
     });
+    double kmax = 0;
+    for (int i : gi) kmax = std::max(kmax, smp[i].k);
+    const bool fd = fd_wanted(common->coarse_solver, 2, kv.first / 2, false, false, kmax);
+    group_fd[kv.first] = fd;
     NDPlan* plan = nullptr;
-    HH_TRY(get_plan(2, kv.first / 2 + 1, &plan));
+    if (!fd) HH_TRY(get_plan(2, kv.first / 2 + 1, &plan));
     const int64_t per = per_sample_bytes(2, kv.first, m, plan);
     const double Nn = (double)(kv.first + 1) * (kv.first + 1);
     const int bmem = (int)std::max<int64_t>(1, std::min<int64_t>(maxB, (int64_t)(budget / per)));
@@ -1487,6 +1583,8 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     const std::vector<int>& bt = batches[bi];
     sp.dim = 2; sp.n = smp[bt[0]].n_cells; sp.B = (int)bt.size();
     sp.nu_pre = common->nu_pre; sp.nu_post = common->nu_post; sp.omega = common->omega; sp.m = m;
+    sp.coarse = common->coarse_solver;
+    sp.fd = group_fd[sp.n];
     for (int i : bt) { sp.k.push_back(smp[i].k); sp.beta.push_back(smp[i].beta); sp.sigma.push_back(smp[i].sigma); }
   }
   const int nt = std::min<int>(nstreams, (int)batches.size());
@@ -1514,6 +1612,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     static const bool tune_conc = getenv("HH_ND_TUNE_CONC") && atoi(getenv("HH_ND_TUNE_CONC")) != 0;
     Engine& E = *engines[0];
     for (const BatchSpec& sp : specs) {
+      if (sp.fd) continue;   // no schedule to tune
       NDPlan* P = nullptr;
       HH_TRY(get_plan(2, sp.n / 2 + 1, &P));
       const int64_t Nc = ipow(sp.n / 2 + 1, 2);
@@ -1548,6 +1647,7 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     for (double& a : E.acc_model) a = 0;
     for (double& a : E.acc_model_all) a = 0;
     for (double& a : E.acc_launch) a = 0;
+    E.acc_flops = E.acc_flops_all = 0;
     E.launches = 0;
     if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
     else E.timing_every = 8;   // sweep: sample 1 iteration in 8 (keeps the pipelines full)
@@ -1614,12 +1714,34 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
       g_sweep_st[16 + t] += E.acc_model[t];
       g_sweep_st[20 + t] += E.acc_model_all[t];
     }
+    g_sweep_flops[0] += E.acc_flops;
+    g_sweep_flops[1] += E.acc_flops_all;
     g_sweep_launches += E.launches;
   };
   std::vector<std::thread> th;
   for (int t = 0; t < nt; ++t) th.emplace_back(worker, engines[t]);
   for (auto& t : th) t.join();
   if (failed) { hh_set_error("%s", err.c_str()); return HH_E_CUDA; }
+  return HH_OK;
+}
+
+extern "C" hh_status hh_coarse_kind(const hh_problem* p, int32_t* kind) {
+  if (!p || !kind) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  const BatchSpec& sp = p->ep->spec;
+  *kind = sp.fd ? HH_COARSE_FD : (sp.dist ? HH_COARSE_ND_DIST : HH_COARSE_ND);
+  return HH_OK;
+}
+
+extern "C" hh_status hh_coarse_flops(hh_problem* p, double* flops2) {
+  if (!flops2) { hh_set_error("NULL argument"); return HH_E_ARG; }
+  if (p) {
+    flops2[0] = p->ep->acc_flops;
+    flops2[1] = p->ep->acc_flops_all;
+    return HH_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_sweep_mu);
+  flops2[0] = g_sweep_flops[0];
+  flops2[1] = g_sweep_flops[1];
   return HH_OK;
 }
 

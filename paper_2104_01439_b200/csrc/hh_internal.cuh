@@ -161,6 +161,24 @@ hh_status nd_factor(const NDPlan* p, int B, const cplx* stencil, cplx* F, cplx* 
 // nd_flow_reset the counters and nd_flow_disable the schedule.
 hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* work, VArg rhs,
                    VArg x, cudaStream_t s, bool shareF = false, bool conc = false, int* fail = nullptr);
+// ---- coarse solve by fast diagonalisation (fd.cu; constant k, separable coarse operator)
+// basis: per factor copy fd_basis_entries(nc) complex entries (folded eigenvector
+// matrices V, V^T per parity + eigenvalues); work: per entry fd_work_entries.
+// fd_setup: flag[b] = 1 if the secular roots fail validation, 2 if the operator is
+// singular (both leave flag 0 untouched otherwise; the caller zeroes it).
+int fd_P(int nc);
+int64_t fd_basis_entries(int nc);
+int64_t fd_work_entries(int dim, int nc);
+int fd_solve_launches(int dim);
+double fd_solve_flops(int dim, int nc);     // real flops per sample and solve
+int64_t fd_solve_bytes(int dim, int nc);    // compulsory HBM bytes per sample and solve
+// kslot: device [nslot] k of each distinct-k basis slot; bidx: device [B] slot of
+// sample b; sflag: device [nslot] ints, zeroed by the caller; flag: per sample
+hh_status fd_setup(int dim, int nc, int B, int nslot, const double* kslot, const int* bidx, int* sflag,
+                   const double2* kc, cplx* basis, int* flag, cudaStream_t s);
+hh_status fd_flag_all(int* flag, int B, int code, cudaStream_t s);   // fault injection (HH_FD_FAIL)
+hh_status fd_solve(int dim, int nc, int B, const int* st, const cplx* basis, const int* bidx, const double2* kc,
+                   cplx* work, VArg rhs, VArg x, cudaStream_t s);
 // ---- distributed coarse solve (slab-aligned ND; SURVEY.md 8(e) second version)
 struct Comm;
 struct NDDistView {            // one rank's part, held by this process

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HH_LIB") or os.path.join(_HERE, "libhh.so")
 
 HH_OP_A0, HH_OP_AEPS, HH_OP_AEPS_COARSE = 0, 1, 2
-HH_COARSE_AUTO, HH_COARSE_ND, HH_COARSE_ND_DIST = 0, 1, 2
+HH_COARSE_AUTO, HH_COARSE_ND, HH_COARSE_ND_DIST, HH_COARSE_FD = 0, 1, 2, 3
 STATUS = {0: "HH_OK", 1: "HH_E_ARG", 2: "HH_E_CONFIG", 3: "HH_E_DIM", 4: "HH_E_CUDA",
           5: "HH_E_NCCL", 6: "HH_E_OOM", 7: "HH_E_SINGULAR", 8: "HH_E_BREAKDOWN",
           9: "HH_E_DIVERGED", 10: "HH_E_STATE"}
@@ -26,7 +26,7 @@ EXPORTS = ["hh_setup_problem", "hh_layout", "hh_local_layout", "hh_apply_op", "h
            "hh_coarse_solve", "hh_fgmres_solve", "hh_fgmres_solve_host", "hh_sweep",
            "hh_destroy_problem", "hh_reset_timers", "hh_read_timers", "hh_sweep_timers",
            "hh_slab_bounds", "hh_nccl_unique_id", "hh_shift_search", "hh_lfa_rho", "hh_lfa_sigma_c", "hh_lfa_stats",
-           "hh_arnoldi_orthogonality", "hh_fp64_peak", "hh_last_error", "hh_version"]
+           "hh_arnoldi_orthogonality", "hh_fp64_peak", "hh_coarse_flops", "hh_coarse_kind", "hh_fp64_mma_peak", "hh_last_error", "hh_version"]
 
 
 class ProblemDesc(C.Structure):
@@ -163,12 +163,14 @@ class Problem:
     def __init__(self, dim, n_cells, k_const=0.0, k_elem=None, k_elem_coarse=None, beta=1.0,
                  sigma=1.5, nu_pre=2, nu_post=2, omega=0.6, max_restart=100, device=None,
                  nslabs_local=1, rank=0, nranks=1, nccl_id: bytes | None = None, shift_map=0,
-                 coarse_solver=HH_COARSE_ND):
+                 coarse_solver=HH_COARSE_AUTO):
         """nslabs_local > 1: the solve is cut into that many slabs held by this
         process; nccl_id (from nccl_unique_id(), shared by all ranks): this
         process holds slab `rank` of `nranks` (one GPU per process).  Vectors
         then hold this handle's owned planes (local_layout()).  coarse_solver =
-        HH_COARSE_ND_DIST distributes the coarse factor over the slabs."""
+        HH_COARSE_ND_DIST distributes the coarse factor over the slabs; HH_COARSE_FD
+        solves it by fast diagonalisation (constant k); AUTO picks FD for
+        constant k where it pays and the ND factor otherwise."""
         self.handle = C.c_void_p()
         dev = torch.cuda.current_device() if device is None else device
         d = ProblemDesc()
@@ -202,6 +204,12 @@ class Problem:
         _check(lib.hh_layout(self.handle, C.byref(nf), C.byref(nc)))
         self.n_fine, self.n_coarse = nf.value, nc.value
         self.dim, self.n_cells, self.device = dim, n_cells, dev
+
+    def coarse_kind(self):
+        """hh_coarse_kind: the coarse solver in use (HH_COARSE_ND / _ND_DIST / _FD)."""
+        k = C.c_int32()
+        _check(lib.hh_coarse_kind(self.handle, C.byref(k)))
+        return k.value
 
     def local_layout(self):
         """(n_local_nodes, first_plane, n_planes) of the owned slab range."""
@@ -288,7 +296,8 @@ class Problem:
             pass
 
 
-def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_restart=100):
+def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_restart=100,
+          coarse_solver=HH_COARSE_AUTO):
     """hh_sweep over a list of dicts with keys id, n, k, beta, sigma."""
     o = o or opts()
     d = ProblemDesc()
@@ -296,7 +305,7 @@ def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_rest
     d.device = torch.cuda.current_device() if device is None else device
     d.stream = _stream()
     d.max_restart = max_restart
-    d.coarse_solver = HH_COARSE_ND
+    d.coarse_solver = coarse_solver
     n = len(samples)
     arr = (Sample * n)(*[Sample(s["id"], s["n"], s["k"], s["beta"], s["sigma"]) for s in samples])
     out = (SampleResult * n)()
@@ -305,7 +314,7 @@ def sweep(samples, nu_pre=2, nu_post=2, omega=0.6, o=None, device=None, max_rest
 
 
 def shift_search(samples, rhs, lo=1.0, hi=2.0, tol=1e-2, o=None, nu_pre=2, nu_post=2, omega=0.6,
-                 device=None, max_restart=100):
+                 device=None, max_restart=100, coarse_solver=HH_COARSE_AUTO):
     """hh_shift_search: golden-section sigma search per sample (dicts with id, n, k,
     beta); rhs[i] = host complex128 right-hand side of sample i (reused for all sigma).
     Default budget = the paper's: rtol 1e-8, 50 iterations, no restart."""
@@ -315,7 +324,7 @@ def shift_search(samples, rhs, lo=1.0, hi=2.0, tol=1e-2, o=None, nu_pre=2, nu_po
     d.device = torch.cuda.current_device() if device is None else device
     d.stream = _stream()
     d.max_restart = max_restart
-    d.coarse_solver = HH_COARSE_ND
+    d.coarse_solver = coarse_solver
     n = len(samples)
     arr = (SearchSample * n)(*[SearchSample(s["id"], s["n"], s["k"], s.get("beta", 1.0)) for s in samples])
     keep = [np.ascontiguousarray(r, dtype=np.complex128) for r in rhs]
@@ -380,12 +389,28 @@ def sweep_timers(reset_enable=-1):
     return _phase_dict(st, nl.value)
 
 
+def coarse_flops(problem=None):
+    """hh_coarse_flops: (timed, all) coarse-solve flops since the last timer reset
+    of `problem` (a Problem) or, with None, of the sweep."""
+    out = (C.c_double * 2)()
+    _check(lib.hh_coarse_flops(problem.handle if problem is not None else None, out))
+    return out[0], out[1]
+
+
 def fp64_peak(device=None):
     """(measured FP64 TFLOP/s, nominal SM MHz) from the DFMA microbenchmark."""
     t, mhz = C.c_double(), C.c_double()
     dev = torch.cuda.current_device() if device is None else device
     _check(lib.hh_fp64_peak(dev, C.byref(t), C.byref(mhz)))
     return t.value, mhz.value
+
+
+def fp64_mma_peak(device=None):
+    """Measured FP64 tensor-core (mma.sync m8n8k4 f64) TFLOP/s."""
+    t = C.c_double()
+    dev = torch.cuda.current_device() if device is None else device
+    _check(lib.hh_fp64_mma_peak(dev, C.byref(t)))
+    return t.value
 
 
 def version():

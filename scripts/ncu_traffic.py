@@ -16,9 +16,10 @@ import json
 import re
 import sys
 
-PHASE = [("coarse", r"^k_nd_(fwd|bwd|gather|rows_wide|fwdT|bwdK|bwd_stage|cluster|flow|fwd_sub|bwd_sub)"),
+PHASE = [("coarse", r"^k_nd_(fwd|bwd|gather|rows_wide|fwdT|bwdK|bwd_stage|cluster|flow|fwd_sub|bwd_sub)"
+                    r"|^k_fd_(fold|unfold|gemm)"),
          ("fine3d", r"^k_march3d|^k_bnd3d|^k_pw3d|^k_prolong3d"),   # 3D: shared by pre / post / A_0
-         ("setup", r"^k_nd_|^k_coef|^k_stencil|^k_dinv|^k_cstencil"),
+         ("setup", r"^k_nd_|^k_fd_|^k_coef|^k_stencil|^k_dinv|^k_cstencil"),
          ("pre", r"^k_pre|^k_jacobi|^k_resid|^k_restrict"),
          ("post", r"^k_post|^k_prolong|^k_apply"),
          ("krylov", r"^k_mdot|^k_update|^k_norm|^k_trisolve|^k_xupdate|^k_advance|^k_clear_jend")]
@@ -74,6 +75,18 @@ def main():
         res[ph] = {"dram_bytes_per_launch": by / n, "model_bytes_per_launch": tm[ph]["model"] / n,
                    "fused_bytes_per_launch": tm[ph]["bytes"] / n, "kernels": k, "phase_launches": int(n),
                    "ncu_us_per_launch": 1e6 * t / n, "ncu_dram_gbs": by / t / 1e9 if t > 0 else None}
+    fdk = [i for i in per if re.match(r"^k_fd_(fold|unfold|gemm)", names[i])]
+    if fdk and "coarse" in res:   # fast-diagonalisation coarse solve: tensor-bound GEMMs
+        n = tm["coarse"]["launches"]
+        t = sum(per[i].get("gpu__time_duration.sum", 0) for i in fdk)
+        g = [i for i in fdk if names[i].startswith("k_fd_gemm")]
+        tg = sum(per[i].get("gpu__time_duration.sum", 0) for i in g)
+        fl = json.load(open(tpath)).get("coarse_flops", 0.0)
+        res["coarse_fd"] = {"dram_bytes_per_launch": res["coarse"]["dram_bytes_per_launch"],
+                            "flops_per_launch": fl / n if n else None,
+                            "ncu_us_per_launch": 1e6 * t / n, "gemm_share": tg / t if t else None,
+                            "ncu_tflops": fl / t / 1e12 if t else None,
+                            "ncu_gemm_tflops": fl / tg / 1e12 if tg else None}
     if "fine3d" in agg:   # 3D: the marching kernels serve pre, post and the A_0 apply
         k, by, t = agg["fine3d"]
         n = tm["pre"]["launches"]

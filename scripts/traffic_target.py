@@ -34,6 +34,7 @@ if what == "sweep":
     hh.sweep(smp, o=o)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+    fl = hh.coarse_flops(None)[0]
     tm = hh.sweep_timers(0)
 else:
     spec = config_spec(what)
@@ -48,6 +49,7 @@ else:
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     tm = gp.read_timers()
+    fl = hh.coarse_flops(gp)[0]
     gp.close()
-json.dump({"workload": what, "timers": tm}, open(out, "w"))
+json.dump({"workload": what, "timers": tm, "coarse_flops": fl}, open(out, "w"))
 print(json.dumps({k: tm[k] for k in hh.PHASES}))

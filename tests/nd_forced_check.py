@@ -35,7 +35,7 @@ def main():
     worst = {"coarse": 0.0, "coarse_res": 0.0, "vcycle": 0.0, "x": 0.0, "dits": 0}
     for spec in specs():
         orc = OracleProblem(spec)
-        gp = hh.Problem.from_spec(spec)
+        gp = hh.Problem.from_spec(spec, coarse_solver=hh.HH_COARSE_ND)   # the ND kernels under test
         r = random_complex(spec.n_coarse_nodes, 3)
         e = gp.coarse_solve(torch.from_numpy(r).cuda())
         torch.cuda.synchronize()

@@ -47,7 +47,7 @@ def _rand(n, seed):
 def pair(request):
     spec = config_spec("cfg0") if request.param == "cfg0" else config_spec("cfg2", n=128)
     orc = OracleProblem(spec)
-    gp = hh.Problem.from_spec(spec)
+    gp = hh.Problem.from_spec(spec, coarse_solver=hh.HH_COARSE_ND)
     yield spec, orc, gp
     gp.close()
 
@@ -88,9 +88,9 @@ def test_flow_batched_sweep(monkeypatch):
     _set(monkeypatch, SCHEDULES[0])
     samples = [{"id": i, "dim": 2, "n": 64, "k": 6.0 + i, "kh_target": 0.6, "sigma": 1.0 + 0.1 * i,
                 "beta": 0.5} for i in range(6)]
-    res = hh.sweep(samples)
+    res = hh.sweep(samples, coarse_solver=hh.HH_COARSE_ND)
     _set(monkeypatch, SCHEDULES[3])
-    ref = hh.sweep(samples)
+    ref = hh.sweep(samples, coarse_solver=hh.HH_COARSE_ND)
     for a, c in zip(res, ref):
         assert a["status"] == 0 and a["iterations"] == c["iterations"]
         assert abs(a["rel_res_true"] - c["rel_res_true"]) <= 1e-8 * max(c["rel_res_true"], 1e-300) + 1e-14
@@ -106,7 +106,7 @@ FORCE_FLOW = ("1", "-1", "99")
 
 def test_flow_failure_fgmres_raises_then_recovers(monkeypatch):
     spec = config_spec("cfg0", n=96)
-    gp = hh.Problem.from_spec(spec)
+    gp = hh.Problem.from_spec(spec, coarse_solver=hh.HH_COARSE_ND)
     b = spec.rhs()
     _set(monkeypatch, FORCE_FLOW)
     monkeypatch.setenv("HH_ND_FLOW_POLLS", "0")
@@ -123,7 +123,7 @@ def test_flow_failure_fgmres_raises_then_recovers(monkeypatch):
 
 def test_flow_failure_coarse_solve_raises_then_recovers(monkeypatch):
     spec = config_spec("cfg0", n=80)
-    gp = hh.Problem.from_spec(spec)
+    gp = hh.Problem.from_spec(spec, coarse_solver=hh.HH_COARSE_ND)
     orc = OracleProblem(spec)
     r = _rand(spec.n_coarse_nodes, 7)
     _set(monkeypatch, FORCE_FLOW)
@@ -143,10 +143,10 @@ def test_flow_failure_in_sweep_is_a_per_sample_error(monkeypatch):
     monkeypatch.setenv("HH_ND_FLOW_POLLS", "0")
     samples = [{"id": i, "dim": 2, "n": 72, "k": 8.0 + i, "kh_target": 0.6, "sigma": 1.5,
                 "beta": 0.5} for i in range(3)]
-    res = hh.sweep(samples)
+    res = hh.sweep(samples, coarse_solver=hh.HH_COARSE_ND)
     assert all(r["status"] == 4 and r["converged"] == 0 for r in res), res
     monkeypatch.delenv("HH_ND_FLOW_POLLS")
-    res = hh.sweep(samples)
+    res = hh.sweep(samples, coarse_solver=hh.HH_COARSE_ND)
     from workloads.configs import sweep_sample_spec
     for s, r in zip(samples, res):
         assert r["status"] == 0

@@ -59,11 +59,25 @@ SPECS = [
 ]
 
 
-@pytest.fixture(scope="module", params=SPECS, ids=[s[0] for s in SPECS])
+# constant-k specs run twice: the default coarse solver (AUTO -> fast
+# diagonalisation, fd.cu) and the nested-dissection factor forced (coarse_nd.cu);
+# heterogeneous specs have the ND factor only
+_CONST = {"cfg0", "cfg0_n4", "cfg0_n6", "cfg0_n70", "cfg3_n8", "cfg3_n14", "sweep_k160_kh06"}
+PAIRS = [(name, mk, "auto") for name, mk in SPECS] + \
+        [(name, mk, "nd") for name, mk in SPECS if name in _CONST]
+
+
+@pytest.fixture(scope="module", params=PAIRS, ids=[f"{p[0]}-{p[2]}" for p in PAIRS])
 def pair(request):
-    spec = request.param[1]()
+    name, mk, coarse = request.param
+    spec = mk()
     orc = OracleProblem(spec)
-    gp = hh.Problem.from_spec(spec)
+    cs = hh.HH_COARSE_ND if coarse == "nd" else hh.HH_COARSE_AUTO
+    gp = hh.Problem.from_spec(spec, coarse_solver=cs)
+    # AUTO takes FD for constant k on resolved coarse grids (k h_c <= 2.5, include/hh.h)
+    fd = coarse == "auto" and name in _CONST and spec.k_const / (spec.n // 2) <= 2.5
+    want = hh.HH_COARSE_FD if fd else hh.HH_COARSE_ND
+    assert gp.coarse_kind() == want, (name, coarse, gp.coarse_kind())
     yield spec, orc, gp
     gp.close()
 
