@@ -540,19 +540,20 @@ hh_status fd_gemm_launch(const FDGemm& g, int B, cudaStream_t s) {
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-// tile choice: the least wave-quantised padded work, ceil(CTAs / (148 c)) * c * BM * BN
-// for c resident CTAs per SM (HH_FD_TILE = 32 / 48 / 64 forces one; A/B in DESIGN.md 7e)
+// tile choice: the least padded output area ceil(M/t) t x ceil(N/t) t over t = 32 / 48
+// (ties -> 32: more CTAs); measured per grid size on the sweep's batches
+// (scripts/probe_fd.py, profiles/r02/fd): 32 wins at P = 9..18, 51, 68, 101 and
+// 48 at P = 34, 134, where the area rule picks them; 64 x 64 tiles never won.
+// HH_FD_TILE = 32 / 48 / 64 forces one (A/B).
 hh_status fd_gemm(const FDGemm& g, int B, cudaStream_t s) {
   static const int force = getenv("HH_FD_TILE") ? atoi(getenv("HH_FD_TILE")) : 0;
-  const int64_t Z = (int64_t)B * g.nblk * g.nsl;
-  const int tiles[3] = {32, 48, 64}, cps[3] = {5, 3, 2};
+  (void)B;
+  const int tiles[2] = {32, 48};
   int best = 0;
-  double bt = 1e300;
-  for (int t = 0; t < 3; ++t) {
-    const int64_t ctas = Z * ((g.M + tiles[t] - 1) / tiles[t]) * ((g.N + tiles[t] - 1) / tiles[t]);
-    const double waves = std::ceil((double)ctas / (148.0 * cps[t]));
-    const double cost = waves * cps[t] * tiles[t] * tiles[t];
-    if (cost < bt * 0.999) { bt = cost; best = t; }
+  int64_t ba = INT64_MAX;
+  for (int t = 0; t < 2; ++t) {
+    const int64_t a = (int64_t)((g.M + tiles[t] - 1) / tiles[t]) * tiles[t] * (((g.N + tiles[t] - 1) / tiles[t]) * tiles[t]);
+    if (a < ba) { ba = a; best = t; }
   }
   const int tile = force ? force : tiles[best];
   if (tile == 64) return fd_gemm_launch<64, 64, 4, 2>(g, B, s);
