@@ -177,11 +177,11 @@ def run_ours(args, rank, world, dev):
     stream = torch.cuda.current_stream()
     if args.workload == "sweep":
         samples = rank_samples(rank, world)
-        o = hh.opts(restart=100, rtol=1e-6, max_iters=500)
+        o = hh.opts(restart=100, rtol=1e-6, max_iters=500, check_every=args.check_every)
         gathered = {"recs": None}
 
         def step():
-            res = hh.sweep(samples, o=o)
+            res = hh.sweep(samples, o=o, coarse_solver=COARSE[args.coarse_solver])
             its = sum(r["iterations"] for r in res)
             dofs = sum(r["iterations"] * (s["n"] + 1) ** 2 for r, s in zip(res, samples))
             bad = [r for r in res if r["status"] != 0]
@@ -273,6 +273,9 @@ def run_ours(args, rank, world, dev):
     ev = []
     tot_its = tot_dofs = 0
     results = []
+    prof = bool(os.environ.get("HH_BENCH_PROFILE"))   # ncu --profile-from-start off: the timed steps only
+    if prof:
+        torch.cuda.profiler.start()
     for _ in range(args.steps):
         flush.fill_(1.0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -284,6 +287,8 @@ def run_ours(args, rank, world, dev):
         tot_dofs += dofs
         results = res
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.profiler.stop()
     if world > 1:
         dist.barrier()
     clocks = clk.stop() if clk else None
@@ -561,6 +566,9 @@ def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
             "frac_wall_share": p.get("wall_share_frac"), "phases": phases, "aggregate": agg}
 
 
+COARSE = {"auto": 0, "nd": 1, "fd": 3}   # HH_COARSE_AUTO / _ND / _FD (include/hh.h)
+
+
 def hh_mma_peak(dev):
     """Measured FP64 tensor-core TFLOP/s (after the timed region)."""
     import paper_2104_01439_b200.hh as hh
@@ -578,6 +586,10 @@ def main():
     ap.add_argument("--no-cold", action="store_true", help="skip the fresh-process first-call e2e")
     ap.add_argument("--coarse", choices=["replicated", "dist"], default="replicated",
                     help="coarse factor of a slab-decomposed single solve (N > 1)")
+    ap.add_argument("--coarse-solver", choices=["auto", "nd", "fd"], default="auto",
+                    help="sweep coarse solver (HH_COARSE_AUTO / _ND / _FD)")
+    ap.add_argument("--check-every", type=int, default=1,
+                    help="host reads the device convergence flags every this many iterations")
     ap.add_argument("--records", default=None, help="write the sweep's gathered per-sample records (JSONL)")
     ap.add_argument("--cold-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()

@@ -417,6 +417,9 @@ __device__ __forceinline__ const cplx* fd_operand(const FDGemm& g, const FDOp& o
 }
 
 constexpr int FD_BK = 16;
+#ifndef FD_3M
+#define FD_3M 1
+#endif
 template <int BM, int BN, int WR, int WC>
 struct FDTile {
   static constexpr int NT = 32 * WR * WC;
@@ -428,7 +431,7 @@ struct FDTile {
 };
 
 template <int BM, int BN, int WR, int WC>
-__global__ void __launch_bounds__(32 * WR * WC) k_fd_gemm(FDGemm g) {
+__global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? 3 : 2)) k_fd_gemm(FDGemm g) {
   using T = FDTile<BM, BN, WR, WC>;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int i0 = (blockIdx.x / tiles_n) * BM, j0 = (blockIdx.x % tiles_n) * BN;
@@ -459,11 +462,15 @@ __global__ void __launch_bounds__(32 * WR * WC) k_fd_gemm(FDGemm g) {
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wr = warp / WC, wc = warp % WC, gq = lane >> 2, q = lane & 3;
-  double re[T::RB][T::CB][2], im[T::RB][T::CB][2];
+  // FD_3M: Gauss's three-multiplication complex product -- t1 = Ar Br, t2 = Ai Bi,
+  // t3 = (Ar + Ai)(Br + Bi), Re = t1 - t2, Im = t3 - t1 - t2 -- 3 DMMAs per
+  // complex multiply-add instead of 4 (FD_3M = 0: the 4-product form)
+  double re[T::RB][T::CB][2], im[T::RB][T::CB][2], t3[T::RB][T::CB][2];
 #pragma unroll
   for (int rb = 0; rb < T::RB; ++rb)
 #pragma unroll
-    for (int cb = 0; cb < T::CB; ++cb) re[rb][cb][0] = re[rb][cb][1] = im[rb][cb][0] = im[rb][cb][1] = 0.0;
+    for (int cb = 0; cb < T::CB; ++cb)
+      re[rb][cb][0] = re[rb][cb][1] = im[rb][cb][0] = im[rb][cb][1] = t3[rb][cb][0] = t3[rb][cb][1] = 0.0;
   const int nk = (g.K + FD_BK - 1) / FD_BK;
   load_stage(0, 0);
   for (int kt = 0; kt < nk; ++kt) {
@@ -488,10 +495,16 @@ __global__ void __launch_bounds__(32 * WR * WC) k_fd_gemm(FDGemm g) {
       for (int rb = 0; rb < T::RB; ++rb)
 #pragma unroll
         for (int cb = 0; cb < T::CB; ++cb) {
-          dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].x, bv[cb].x);    // Re += Ar Br
-          dmma884(re[rb][cb][0], re[rb][cb][1], -av[rb].y, bv[cb].y);   // Re -= Ai Bi
-          dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].x, bv[cb].y);    // Im += Ar Bi
-          dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].y, bv[cb].x);    // Im += Ai Br
+          if (FD_3M) {
+            dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].x, bv[cb].x);                       // t1
+            dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].y, bv[cb].y);                       // t2
+            dmma884(t3[rb][cb][0], t3[rb][cb][1], av[rb].x + av[rb].y, bv[cb].x + bv[cb].y);  // t3
+          } else {
+            dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].x, bv[cb].x);    // Re += Ar Br
+            dmma884(re[rb][cb][0], re[rb][cb][1], -av[rb].y, bv[cb].y);   // Re -= Ai Bi
+            dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].x, bv[cb].y);    // Im += Ar Bi
+            dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].y, bv[cb].x);    // Im += Ai Br
+          }
         }
     }
     __syncthreads();
@@ -513,7 +526,8 @@ __global__ void __launch_bounds__(32 * WR * WC) k_fd_gemm(FDGemm g) {
       for (int e = 0; e < 2; ++e) {
         const int j = j0 + wc * T::WN + cb * 8 + 2 * q + e;
         if (j >= g.N) continue;
-        cplx v = cmake(re[rb][cb][e], im[rb][cb][e]);
+        cplx v = FD_3M ? cmake(re[rb][cb][e] - im[rb][cb][e], t3[rb][cb][e] - re[rb][cb][e] - im[rb][cb][e])
+                       : cmake(re[rb][cb][e], im[rb][cb][e]);
         if (g.dmode) {
           cplx D = csub(li, shift);
           if (g.dmode == 1) {

@@ -1524,7 +1524,10 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   std::map<int, std::vector<int>> groups;
   for (int i = 0; i < n; ++i) groups[smp[i].n_cells].push_back(i);
   const char* es = getenv("HH_SWEEP_STREAMS");
-  const int nstreams = std::max(1, es ? atoi(es) : 8);
+  // 3 engine streams: the same throughput as 4, 8 or 12 (1.62-1.65 s per sweep step with
+  // the FD coarse solve; 1 stream 1.82-2.02 s, 2 streams 1.68-1.72 s: profiles/r02/fd/ab)
+  // with the least time-sharing inflation of the per-launch phase timers
+  const int nstreams = std::max(1, es ? atoi(es) : 3);
   const char* eb = getenv("HH_SWEEP_MAX_BATCH");
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
   const char* en = getenv("HH_SWEEP_NODES");
