@@ -517,7 +517,19 @@ def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
                           "fused_gbs": d["bytes"] / sec / 1e9, "fused_frac": d["bytes"] / sec / 1e9 / peak}
     if not phases:
         return None
-    dom = max(phases, key=lambda k: phases[k]["ms"])
+    # dominant phase: the largest share of the serialised ncu time of the same workload
+    # (profiles/r02/traffic.json time_share) when committed -- concurrent engine streams
+    # time-share the SMs, so live per-launch event times overstate every phase by
+    # different factors -- else the largest summed event time
+    tr = measured_traffic(args.workload)
+    ts = (tr or {}).get("time_share", {})
+    if all(ph in ts for ph in phases):
+        dom = max(phases, key=lambda k: ts[k])
+        dom_by = "ncu serialised time share (profiles/r02/traffic.json): " + \
+                 ", ".join(f"{k} {ts[k]:.3f}" for k in phases)
+    else:
+        dom = max(phases, key=lambda k: phases[k]["ms"])
+        dom_by = "largest summed per-launch event time"
     tot_ms = sum(v["ms"] for v in phases.values())
     step_s = out["ms_per_step"] * 1e-3
     for ph, v in phases.items():
@@ -532,7 +544,6 @@ def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
     agg = {"model_bytes_per_step": ball, "fused_bytes_per_step": fall,
            "frac": ball / step_s / 1e9 / peak, "fused_frac": fall / step_s / 1e9 / peak,
            "note": "bytes of every iteration / whole step time (setup and factorisation included)"}
-    tr = measured_traffic(args.workload)
     fd = tm.get("coarse_flops", 0.0) > 0 and "coarse" in phases
     if fd:
         c = phases["coarse"]
@@ -554,7 +565,8 @@ def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
                 "peak_source": "measured (hh_fp64_mma_peak: mma.sync m8n8k4 f64 microbenchmark, this run)",
                 "flops_model": "8 real flops per complex multiply-add of the 2d folded transforms: "
                                "2D 128 P^3, 3D 384 P^4 per sample and solve (P = nc/2 + 1); DESIGN.md section 7e",
-                "frac_wall_share": p.get("wall_share_tflops_frac"), "phases": phases, "aggregate": agg,
+                "frac_wall_share": p.get("wall_share_tflops_frac"), "dominant_by": dom_by,
+                "phases": phases, "aggregate": agg,
                 "hbm_peak": peak, "hbm_peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
     return {"bound": "hbm", "kernel": PHASE_KERNELS[dom], "phase": dom, "achieved": p["achieved_gbs"],
             "peak": peak, "unit": "GB/s", "frac": p["frac"],
@@ -563,7 +575,8 @@ def roofline(tm, out, args, peak, peak_kind, mma_peak=None):
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
             "bytes_model": "SURVEY.md 8(d) per-step model bytes per launch (fused kernels' compulsory "
                            "bytes alongside as fused_*); DESIGN.md section 6",
-            "frac_wall_share": p.get("wall_share_frac"), "phases": phases, "aggregate": agg}
+            "frac_wall_share": p.get("wall_share_frac"), "dominant_by": dom_by, "phases": phases,
+            "aggregate": agg}
 
 
 COARSE = {"auto": 0, "nd": 1, "fd": 3}   # HH_COARSE_AUTO / _ND / _FD (include/hh.h)

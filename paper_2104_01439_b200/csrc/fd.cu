@@ -420,6 +420,9 @@ constexpr int FD_BK = 16;
 #ifndef FD_3M
 #define FD_3M 1
 #endif
+#ifndef FD_MINB48
+#define FD_MINB48 2   // 48 x 48 tiles: 2 CTAs per SM (120 registers; 3 CTAs -> 96 registers + spills)
+#endif
 template <int BM, int BN, int WR, int WC>
 struct FDTile {
   static constexpr int NT = 32 * WR * WC;
@@ -431,7 +434,7 @@ struct FDTile {
 };
 
 template <int BM, int BN, int WR, int WC>
-__global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? 3 : 2)) k_fd_gemm(FDGemm g) {
+__global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MINB48 : 2)) k_fd_gemm(FDGemm g) {
   using T = FDTile<BM, BN, WR, WC>;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int i0 = (blockIdx.x / tiles_n) * BM, j0 = (blockIdx.x % tiles_n) * BN;
