@@ -230,7 +230,10 @@ def run_ours(args, rank, world, dev):
         timers = {"on": False, "acc": None, "flops": [0.0, 0.0], "kind": None}
 
         def step():
-            gp = hh.Problem.from_spec(spec, **slabkw)   # setup + coarse factorisation (inside the step)
+            kw = dict(slabkw)
+            if args.coarse_solver != "auto" and "coarse_solver" not in kw:
+                kw["coarse_solver"] = COARSE[args.coarse_solver]
+            gp = hh.Problem.from_spec(spec, **kw)   # setup + coarse factorisation (inside the step)
             if timers["on"]:
                 gp.reset_timers(True)
             x, r = gp.fgmres_solve(b_dev, o=hh.opts(restart=spec.restart, rtol=spec.rtol,
@@ -600,7 +603,7 @@ def main():
     ap.add_argument("--coarse", choices=["replicated", "dist"], default="replicated",
                     help="coarse factor of a slab-decomposed single solve (N > 1)")
     ap.add_argument("--coarse-solver", choices=["auto", "nd", "fd"], default="auto",
-                    help="sweep coarse solver (HH_COARSE_AUTO / _ND / _FD)")
+                    help="coarse solver (HH_COARSE_AUTO / _ND / _FD)")
     ap.add_argument("--check-every", type=int, default=1,
                     help="host reads the device convergence flags every this many iterations")
     ap.add_argument("--records", default=None, help="write the sweep's gathered per-sample records (JSONL)")
