@@ -20,6 +20,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <condition_variable>
 #include <new>
 #include <thread>
 #include <tuple>
@@ -338,6 +339,40 @@ FineLayout fine_layout(const BatchSpec& sp) {
   return F;
 }
 
+// Exclusive timing gate of the concurrent sweep engines: a sampled (timed)
+// iteration runs with the GPU to itself -- the other engines finish their queued
+// work and launch nothing until it is done -- so its per-phase CUDA-event times
+// are kernel times, not time-shared wall times.  Plain iterations take the
+// gate shared (only around their launch); a waiting exclusive request blocks new
+// shared entries (no starvation).
+struct ExclGate {
+  std::mutex mu;
+  std::condition_variable cv;
+  int active = 0, waiting = 0;
+  bool excl = false;
+  void lock_shared() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return !excl && waiting == 0; });
+    ++active;
+  }
+  void unlock_shared() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (--active == 0) cv.notify_all();
+  }
+  void lock() {
+    std::unique_lock<std::mutex> lk(mu);
+    ++waiting;
+    cv.wait(lk, [&] { return !excl && active == 0; });
+    --waiting;
+    excl = true;
+  }
+  void unlock() {
+    std::lock_guard<std::mutex> lk(mu);
+    excl = false;
+    cv.notify_all();
+  }
+};
+
 struct SampleOut {
   int status = 0, iterations = 0, converged = 0, restarts = 0;
   double rel_res_lsq = 0, rel_res_true = 0, rho = 0;
@@ -374,6 +409,8 @@ struct Engine {
   cudaGraphExec_t gexec_t = nullptr;   // iteration with phase events
   int64_t iter_counter = 0;
   int timing_every = 1;                // sample one iteration in timing_every
+  ExclGate* gate = nullptr;            // sweep: exclusive timed iterations (HH_SWEEP_EXCL_TIMING)
+  std::vector<cudaStream_t> peers;     // the other engines' streams (drained before a timed iteration)
   void drop_graphs() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (gexec_t) cudaGraphExecDestroy(gexec_t);
@@ -1030,10 +1067,21 @@ hh_status batch_solve(Engine& E, VArg bvec, VArg xvec, const hh_fgmres_opts& o,
         running = count_running(E);
         if (!running) break;
       }
-      HH_TRY(run_iteration(E, timed));
+      if (E.gate && timed) {   // the GPU to itself: peers drained, no new peer launches
+        E.gate->lock();
+        for (cudaStream_t ps : E.peers) cudaStreamSynchronize(ps);
+      } else if (E.gate) {
+        E.gate->lock_shared();
+      }
+      const hh_status ist = run_iteration(E, timed);
+      cudaError_t sst = cudaSuccess;
+      if (timed && ist == HH_OK) sst = cudaStreamSynchronize(s);
+      if (E.gate && timed) E.gate->unlock();
+      else if (E.gate) E.gate->unlock_shared();
+      HH_TRY(ist);
+      HH_CUDA_TRY(sst);
       if (E.timing) account_bytes_all(E, running, j);
       if (timed) {
-        HH_CUDA_TRY(cudaStreamSynchronize(s));
         harvest_timers(E);
         account_bytes(E, running, j);
       }
@@ -1604,6 +1652,16 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     for (int t = 0; t < nt; ++t) engines.push_back(pool[t].get());
   }
   for (Engine* E : engines) E->conc = nt > 1;
+  // exclusive timed iterations when several engines share the GPU (default on;
+  // HH_SWEEP_EXCL_TIMING=0: timed iterations time-share like the rest)
+  static ExclGate gates[64];
+  static const bool excl_timing = !getenv("HH_SWEEP_EXCL_TIMING") || atoi(getenv("HH_SWEEP_EXCL_TIMING")) != 0;
+  for (Engine* E : engines) {
+    E->gate = (excl_timing && nt > 1 && g_sweep_timing) ? &gates[common->device % 64] : nullptr;
+    E->peers.clear();
+    for (Engine* O : engines)
+      if (O != E) E->peers.push_back(O->s);
+  }
   for (Engine* E : engines)
     for (const BatchSpec& sp : specs) HH_TRY(reserve_pools(*E, sp));
   // ND solve schedule per (grid, batch size), timed once on an idle GPU (zero
@@ -1653,7 +1711,10 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     E.acc_flops = E.acc_flops_all = 0;
     E.launches = 0;
     if (const char* te = getenv("HH_TIMING_EVERY")) E.timing_every = std::max(1, atoi(te));
-    else E.timing_every = 8;   // sweep: sample 1 iteration in 8 (keeps the pipelines full)
+    // sweep: sample 1 iteration in 16, run with the GPU to itself (ExclGate): the
+    // phase times are kernel times; costs ~3% of the timed-region throughput
+    // (1 in 8: 5.5%; profiles/r02/fd/excl_ab), nothing outside the timed region
+    else E.timing_every = 16;
     const double w0 = now_s();
     int nbat = 0;
     double busy = 0;
