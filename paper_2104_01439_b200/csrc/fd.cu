@@ -119,7 +119,11 @@ __global__ void __launch_bounds__(256) k_fd_eig(int nc, const double* __restrict
   const double scale = fmax(1.0, d[r]);
   for (int s = 1; s <= FD_KS; ++s) {
     const cplx tr = cscale(rho, (double)s / FD_KS);
-    for (int it = 0; it < FD_NEWT; ++it) {
+    // intermediate points of the path only need to stay on their root's branch
+    // (relative 1e-9); the end point t = 1 is polished to round-off
+    const bool last = s == FD_KS;
+    const double tol = last ? 1e-15 : 1e-9;
+    for (int it = 0; it < (last ? 2 * FD_NEWT : FD_NEWT); ++it) {
       // g(l) = (d_r - l)(1 + t rho S) + t rho z_r^2, S = sum_{q != r} z_q^2 / (d_q - l)
       cplx S = cmake(0, 0), Sp = cmake(0, 0);
       for (int q = lane; q < p; q += 32) {
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(256) k_fd_eig(int nc, const double* __restrict
       const cplx gp = cadd(cmake(-one_trS.x, -one_trS.y), cmul(dr, cmul(tr, Sp)));
       const cplx step = cdiv(g, gp);
       l = csub(l, step);
-      if (sqrt(cabs2(step)) <= 1e-15 * fmax(scale, sqrt(cabs2(l)))) break;   // uniform over the warp
+      if (sqrt(cabs2(step)) <= tol * fmax(scale, sqrt(cabs2(l)))) break;   // uniform over the warp
     }
   }
   // residual of the converged root (relative to the terms of g)
@@ -416,7 +420,10 @@ __device__ __forceinline__ const cplx* fd_operand(const FDGemm& g, const FDOp& o
   return g.basis + (int64_t)__ldg(&g.bidx[b]) * g.BE + fd_mat_off(g.P, o.basis, (blk >> o.axis) & 1);
 }
 
-constexpr int FD_BK = 16;
+#ifndef FD_BKC
+#define FD_BKC 16
+#endif
+constexpr int FD_BK = FD_BKC;   // K-chunk per pipeline stage
 #ifndef FD_3M
 #define FD_3M 1
 #endif
