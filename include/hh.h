@@ -228,7 +228,12 @@ typedef struct {
 
 /* Sweep: for each 2D constant-k sample, set up, factor and solve with a unit
  * point source at the centre node (BASELINE configs[1]); common carries dim,
- * nu, omega, device, stream.  s, out: HOST arrays of n entries.  blocks. */
+ * nu, omega, device, stream and coarse_solver (HH_COARSE_AUTO: fast
+ * diagonalisation per batch where it applies, ND factor otherwise or after a
+ * failed FD validation; HH_COARSE_ND / HH_COARSE_FD force one; ND_DIST is
+ * rejected).  Samples are grouped by grid, ordered by shift strength and run in
+ * lockstep batches on several engine streams; results do not depend on the
+ * batching.  s, out: HOST arrays of n entries.  blocks. */
 hh_status hh_sweep(const hh_problem_desc* common, const hh_fgmres_opts* o,
                    const hh_sample* s, int32_t n, hh_sample_result* out);
 
