@@ -31,8 +31,15 @@ namespace {
 #ifndef FINE_DI_GLOBAL
 #define FINE_DI_GLOBAL 0   // 1: heterogeneous D^{-1} read through L1 instead of staged in smem (measured: no gain)
 #endif
-constexpr int TX = 32;   // tile width  (fine nodes along x, even)
-constexpr int TY = 16;   // tile height (even)
+#ifndef FINE_TX
+#define FINE_TX 32
+#endif
+#ifndef FINE_TY
+#define FINE_TY 16
+#endif
+constexpr int TX = FINE_TX;   // tile width  (fine nodes along x, even)
+constexpr int TY = FINE_TY;   // tile height (even)
+static_assert((TX / 2) * (TY / 2) <= 256, "the restriction takes one coarse node per thread");
 constexpr int NT = 256;  // threads per CTA
 
 struct Tile {
