@@ -119,15 +119,40 @@ class Clocks:
                 "reasons": reasons, "source": "nvml"}
 
 
-def rank_samples(rank, world):
-    """This rank's 1/world share of the whole sweep: samples sorted by (grid
-    size n, shift strength beta k^sigma, id) are dealt round-robin, so every
-    rank gets the same mix of grid sizes and (expected) iteration counts;
-    world = 1 is the full 3,520-sample sweep."""
+def rank_samples(rank, world, sharding="groups"):
+    """This rank's 1/world share of the whole sweep; world = 1 is the full
+    3,520-sample sweep.
+      roundrobin: samples sorted by (grid size n, shift strength beta k^sigma, id)
+        are dealt round-robin, so every rank gets the same mix of grid sizes and
+        (expected) iteration counts;
+      groups: grids with (n+1)^2 >= 2.4e6 / 110 (the node budget already cuts
+        their 110-sample groups into several batches on one GPU) are dealt
+        round-robin as above; every smaller grid's group stays WHOLE on one rank
+        (its lockstep batch keeps all 110 / 220 samples, as on one GPU), the
+        groups placed largest-first on the least-loaded rank (fine nodes)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"bad rank {rank} of {world}")
     order = sorted(sweep_samples(), key=lambda s: (s["n"], s["beta"] * s["k"] ** s["sigma"], s["id"]))
-    return [s for p, s in enumerate(order) if p % world == rank]
+    if sharding == "roundrobin" or world == 1:
+        return [s for p, s in enumerate(order) if p % world == rank]
+    if sharding != "groups":
+        raise ValueError(f"unknown sharding {sharding!r}")
+    split = 2.4e6 / 110
+    big = [s for s in order if (s["n"] + 1) ** 2 >= split]
+    mine = [s for p, s in enumerate(big) if p % world == rank]
+    load = [0.0] * world
+    for p, s in enumerate(big):
+        load[p % world] += (s["n"] + 1) ** 2
+    groups = {}
+    for s in order:
+        if (s["n"] + 1) ** 2 < split:
+            groups.setdefault(s["n"], []).append(s)
+    for n, g in sorted(groups.items(), key=lambda kv: (-len(kv[1]) * (kv[0] + 1) ** 2, kv[0])):
+        r = min(range(world), key=lambda q: (load[q], q))
+        load[r] += len(g) * (n + 1) ** 2
+        if r == rank:
+            mine.extend(g)
+    return mine
 
 
 def gather_records(res, world):
@@ -176,7 +201,7 @@ def run_ours(args, rank, world, dev):
     import paper_2104_01439_b200.hh as hh
     stream = torch.cuda.current_stream()
     if args.workload == "sweep":
-        samples = rank_samples(rank, world)
+        samples = rank_samples(rank, world, args.sharding)
         o = hh.opts(restart=100, rtol=1e-6, max_iters=500, check_every=args.check_every)
         gathered = {"recs": None}
 
@@ -192,7 +217,7 @@ def run_ours(args, rank, world, dev):
 
         wl = {"workload": "cfg1 shift sweep (BASELINE configs[1]), all 3,520 samples",
               "samples_per_rank": len(samples), "samples_total": len(sweep_samples()),
-              "sharding": "samples sorted by (n, beta k^sigma) dealt round-robin over ranks",
+              "sharding": args.sharding,
               "restart": 100, "rtol": 1e-6,
               "l2": "per-sample working sets are L2-resident; L2 flushed (512 MB write) between steps"}
     elif args.workload == "search":
@@ -604,6 +629,8 @@ def main():
                     help="coarse factor of a slab-decomposed single solve (N > 1)")
     ap.add_argument("--coarse-solver", choices=["auto", "nd", "fd"], default="auto",
                     help="coarse solver (HH_COARSE_AUTO / _ND / _FD)")
+    ap.add_argument("--sharding", choices=["roundrobin", "groups"], default="groups",
+                    help="sweep samples over ranks (see rank_samples)")
     ap.add_argument("--check-every", type=int, default=1,
                     help="host reads the device convergence flags every this many iterations")
     ap.add_argument("--records", default=None, help="write the sweep's gathered per-sample records (JSONL)")

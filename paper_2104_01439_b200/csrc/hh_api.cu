@@ -1572,10 +1572,10 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
   std::map<int, std::vector<int>> groups;
   for (int i = 0; i < n; ++i) groups[smp[i].n_cells].push_back(i);
   const char* es = getenv("HH_SWEEP_STREAMS");
-  // 3 engine streams: the same throughput as 4, 8 or 12 (1.62-1.65 s per sweep step with
-  // the FD coarse solve; 1 stream 1.82-2.02 s, 2 streams 1.68-1.72 s: profiles/r02/fd/ab)
-  // with the least time-sharing inflation of the per-launch phase timers
-  const int nstreams = std::max(1, es ? atoi(es) : 3);
+  // 6 engine streams: full sweep 1.51 s (3: 1.53, 8: 1.51; 2: 1.68-1.72, 1: 1.82-2.02 s),
+  // and the 1/N shards of a multi-GPU sweep need the extra concurrency most (one
+  // 8-way shard: 218 ms with 6 streams, 243 ms with 3; profiles/r02/shards)
+  const int nstreams = std::max(1, es ? atoi(es) : 6);
   const char* eb = getenv("HH_SWEEP_MAX_BATCH");
   const int maxB = std::max(1, eb ? atoi(eb) : 256);
   const char* en = getenv("HH_SWEEP_NODES");

@@ -13,22 +13,38 @@ from workloads import sweep_samples
 
 
 def test_shards_partition_the_sweep():
-    """Every N: the ranks' shares tile all 3,520 samples, sizes differ by at most
-    one, and every rank gets the same mix of grid sizes (strong scaling)."""
+    """Every N: the ranks' shares tile all 3,520 samples.  Round-robin: sizes
+    differ by at most one and every rank gets the same mix of grid sizes;
+    group-aware (default): small grids whole on one rank, big grids dealt evenly
+    (strong scaling either way)."""
     allids = sorted(s["id"] for s in sweep_samples())
     assert len(allids) == 3520
-    assert sorted(s["id"] for s in bench.rank_samples(0, 1)) == allids      # N = 1: the whole sweep
-    for world in (2, 3, 4, 8):
-        shares = [bench.rank_samples(r, world) for r in range(world)]
-        seen = sorted(s["id"] for sh in shares for s in sh)
-        assert seen == allids
-        sizes = [len(sh) for sh in shares]
-        assert max(sizes) - min(sizes) <= 1
-        # balance of the dominant cost (fine nodes): within 2% of the mean
-        work = [sum((s["n"] + 1) ** 2 for s in sh) for sh in shares]
-        assert max(work) <= 1.02 * sum(work) / world
+    for sh in ("roundrobin", "groups"):
+        assert sorted(s["id"] for s in bench.rank_samples(0, 1, sh)) == allids   # N = 1: the whole sweep
+        for world in (2, 3, 4, 8):
+            shares = [bench.rank_samples(r, world, sh) for r in range(world)]
+            seen = sorted(s["id"] for sh_ in shares for s in sh_)
+            assert seen == allids                                               # a partition
+            work = [sum((s["n"] + 1) ** 2 for s in x) for x in shares]
+            if sh == "roundrobin":
+                sizes = [len(x) for x in shares]
+                assert max(sizes) - min(sizes) <= 1
+                assert max(work) <= 1.02 * sum(work) / world      # fine nodes within 2% of the mean
+            else:
+                # grids below the split size stay whole on one rank; the big grids are
+                # dealt round-robin (equal counts per grid and rank, +-1)
+                split = 2.4e6 / 110
+                for n in sorted({s["n"] for s in sweep_samples()}):
+                    per = [sum(1 for s in x if s["n"] == n) for x in shares]
+                    if (n + 1) ** 2 < split:
+                        assert sorted(per)[-2] == 0, (n, per)         # one rank holds the group
+                    else:
+                        assert max(per) - min(per) <= 1, (n, per)
+                assert max(work) <= 1.10 * sum(work) / world
     with pytest.raises(ValueError):
         bench.rank_samples(2, 2)
+    with pytest.raises(ValueError):
+        bench.rank_samples(0, 2, "nope")
 
 
 def _free_port():
