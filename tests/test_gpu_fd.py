@@ -233,3 +233,20 @@ def test_fd_flops_are_accounted():
     gn.fgmres_solve(_dev(spec.rhs()))
     assert hh.coarse_flops(gn) == (0.0, 0.0)
     gn.close()
+
+
+def test_fd_sweep_equals_nd_sweep():
+    """hh_sweep with the FD coarse solve forced and with the ND factor forced on a
+    strided subset of cfg1 (every grid size class, both kh, weak and strong
+    shifts, two k sharing a grid -> two basis slots in one batch): the same
+    iteration counts (+-1: the coarse solves agree to ~1e-14) and true residuals."""
+    from workloads import sweep_samples
+    samples = sweep_samples()[::53]
+    fd = hh.sweep(samples, coarse_solver=hh.HH_COARSE_FD)
+    nd = hh.sweep(samples, coarse_solver=hh.HH_COARSE_ND)
+    for s, a, b in zip(samples, fd, nd):
+        assert a["status"] == 0 and b["status"] == 0, (s, a, b)
+        assert abs(a["iterations"] - b["iterations"]) <= 1, (s, a, b)
+        assert a["converged"] == b["converged"] == 1
+        if a["iterations"] == b["iterations"]:
+            assert abs(a["rel_res_true"] - b["rel_res_true"]) <= 1e-6 * b["rel_res_true"]
