@@ -441,7 +441,7 @@ struct FDTile {
 };
 
 template <int BM, int BN, int WR, int WC>
-__global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MINB48 : 2)) k_fd_gemm(FDGemm g) {
+__global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MINB48 : (BM == 40 ? 4 : 2))) k_fd_gemm(FDGemm g) {
   using T = FDTile<BM, BN, WR, WC>;
   const int tiles_n = (g.N + BN - 1) / BN;
   const int i0 = (blockIdx.x / tiles_n) * BM, j0 = (blockIdx.x % tiles_n) * BN;
@@ -564,24 +564,30 @@ hh_status fd_gemm_launch(const FDGemm& g, int B, cudaStream_t s) {
   HH_CUDA_TRY(cudaGetLastError());
   return HH_OK;
 }
-// tile choice: the least padded output area ceil(M/t) t x ceil(N/t) t over t = 32 / 48
-// (ties -> 32: more CTAs); measured per grid size on the sweep's batches
-// (scripts/probe_fd.py, profiles/r02/fd): 32 wins at P = 9..18, 51, 68, 101 and
-// 48 at P = 34, 134, where the area rule picks them; 64 x 64 tiles never won.
-// HH_FD_TILE = 32 / 48 / 64 forces one (A/B).
+// tile choice: the least padded output area ceil(M/t) t x ceil(N/t) t over t = 32 / 40 / 48
+// (ties -> the smaller tile: more CTAs); measured per grid size on the sweep's batches
+// (scripts/probe_fd.py, profiles/r02/fd): the area rule picks the fastest of 32 / 48 at
+// every size tried; 64 x 64 tiles never won.  40 x 40 tiles (5 warps of 8 x 40) are a
+// candidate only where a GEMM dimension is <= 40: cfg3's P = 33 mode products (coarse
+// 84.8 -> 78.9 us) and the sweep's P = 34 (56.8 -> 49.2 us); at P = 101 / 118 they lost
+// to 32 x 32 (112.9 -> 118.4, 107.9 -> 111.9 us; profiles/r02/fd/tile40).
+// HH_FD_TILE = 32 / 40 / 48 / 64 forces one (A/B).
 hh_status fd_gemm(const FDGemm& g, int B, cudaStream_t s) {
   static const int force = getenv("HH_FD_TILE") ? atoi(getenv("HH_FD_TILE")) : 0;
+  static const bool use40 = !getenv("HH_FD_TILE40") || atoi(getenv("HH_FD_TILE40")) != 0;
   (void)B;
-  const int tiles[2] = {32, 48};
+  const int tiles[3] = {32, 40, 48};
   int best = 0;
   int64_t ba = INT64_MAX;
-  for (int t = 0; t < 2; ++t) {
+  for (int t = 0; t < 3; ++t) {
+    if (tiles[t] == 40 && (!use40 || std::min(g.M, g.N) > 40)) continue;   // 40: only where a dimension <= 40
     const int64_t a = (int64_t)((g.M + tiles[t] - 1) / tiles[t]) * tiles[t] * (((g.N + tiles[t] - 1) / tiles[t]) * tiles[t]);
     if (a < ba) { ba = a; best = t; }
   }
   const int tile = force ? force : tiles[best];
   if (tile == 64) return fd_gemm_launch<64, 64, 4, 2>(g, B, s);
   if (tile == 48) return fd_gemm_launch<48, 48, 3, 2>(g, B, s);
+  if (tile == 40) return fd_gemm_launch<40, 40, 5, 1>(g, B, s);
   return fd_gemm_launch<32, 32, 2, 2>(g, B, s);
 }
 
