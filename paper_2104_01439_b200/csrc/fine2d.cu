@@ -370,6 +370,9 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
   double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
   const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9 = make_const9(kc, h, true);
+  // constant k: interior D = centre coefficient; its reciprocal (an FP64 division) is
+  // formed while the region loads are in flight, not after the barrier
+  const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);
   // f staged unscaled with cp.async (the Krylov scale fsc is applied where it is read)
   const double fsa = FINE_ASYNC ? fsc : 1.0;
   if (FINE_ASYNC) {
@@ -388,7 +391,6 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
   }
   __syncthreads();
   // the first step from u = 0 (pointwise) on the full region
-  const cplx di_int = HET ? cmake(0, 0) : cinv(c9.c0);   // constant k: interior D = centre coefficient
   FOR_REGION(t.R, {
     cplx v = cmake(0, 0);
     if (in) v = cscale(cmul(dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int), sF[si]), omega * fsa);
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
   double2* sE = reinterpret_cast<double2*>(sDi + (FINE_DI_GLOBAL ? 0 : S));   // HET only
   const cplx* dg = HET ? P.dinv + (int64_t)b * P.stride - vofs : nullptr;
   const Const9 c9e = make_const9(kc, h, true);
+  const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);   // formed under the region loads
   const double fsa = FINE_ASYNC ? fsc : 1.0;
   if (FINE_ASYNC) {
     load_region_async(sF, fg - vofs, t, n, rlo, rhi);
@@ -512,7 +515,6 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
     load_coef(sE, P.coef + b * P.coef_bs, t, n);
   }
   if (FINE_ASYNC) cp_async_wait_all();
-  const cplx di_int = HET ? cmake(0, 0) : cinv(c9e.c0);
   __syncthreads();
   // u + I ec on the full region (bilinear interpolation from the staged block)
   FOR_REGION(t.R, {
