@@ -193,6 +193,8 @@ __global__ void k_mdot_fin(KArgs A, int B, int pass) {
 }
 
 __device__ void givens_tail(const KArgs& A, int b, int j, double ssum);
+__device__ void givens_core(const KArgs& A, int b, int j, double ssum, cplx* Hcol, const double* csp,
+                            const cplx* snp);
 __device__ void update_tail(const KArgs& A, int b, int j, double ssum, int pass);
 
 // w' = w - sum_i (H_i vscale_i) V_i -> V[j+1] ; ||w'||^2 ; last block:
@@ -239,11 +241,37 @@ __global__ void __launch_bounds__(KT, 5) k_update(KArgs A, int pass) {
   double* dpart = A.dpart + (int64_t)b * gridDim.x;
   if (threadIdx.x == 0) dpart[blockIdx.x] = r.x;
   if (!last_block(A.counter + b)) return;
-  const double ssum = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;
-  if (threadIdx.x != 0) return;
-  A.counter[b] = 0u;
-  if (A.slabred) { A.red2[b] = ssum; return; }
-  update_tail(A, b, j, ssum, pass);
+  const double ssum = block_sum(cmake(grid_partial_sum(dpart), 0), sh).x;   // thread 0
+  // Tail (update_tail's decisions, then the Givens step) with H column j and
+  // the previous rotations staged in shared memory by the whole CTA: the
+  // rotation recurrence then runs on shared-memory operands instead of a chain
+  // of dependent L2 round trips (one per previous rotation).
+  __shared__ int go;
+  __shared__ double scs[KMAX_RESTART];
+  __shared__ cplx ssn[KMAX_RESTART];
+  if (threadIdx.x == 0) {
+    A.counter[b] = 0u;
+    int g = 0;
+    if (A.slabred) A.red2[b] = ssum;
+    else if (pass == 2) { A.reo[b] = 0; g = 1; }
+    else if (A.reorth == 2 || (A.reorth == 1 && ssum < 0.5 * A.wnorm2[b])) A.reo[b] = 1;   // second pass finishes the step
+    else { if (A.reorth) A.reo[b] = 0; g = 1; }
+    go = g;
+  }
+  __syncthreads();
+  if (!go) return;
+  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+  const cplx* y2 = A.y + (int64_t)b * A.ldv;
+  cplx* sH = cf;   // KMAX_CF >= j + 2
+  for (int q = threadIdx.x; q <= j; q += KT) sH[q] = pass == 2 ? cadd(Hcol[q], y2[q]) : Hcol[q];
+  for (int q = threadIdx.x; q < j; q += KT) {
+    scs[q] = A.cs[(int64_t)b * A.ldv + q];
+    ssn[q] = A.sn[(int64_t)b * A.ldv + q];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) givens_core(A, b, j, ssum, sH, scs, ssn);
+  __syncthreads();
+  for (int q = threadIdx.x; q <= j + 1; q += KT) Hcol[q] = sH[q];
 }
 
 // slabred: ||w'||^2 = sum over the entries, then the Givens tail
@@ -278,7 +306,14 @@ __device__ void update_tail(const KArgs& A, int b, int j, double ssum, int pass)
 
 // h_{j+1,j} = sqrt(ssum), vscale_{j+1}, Givens rotations on column j, status
 __device__ void givens_tail(const KArgs& A, int b, int j, double ssum) {
-  cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+  givens_core(A, b, j, ssum, A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh, A.cs + (int64_t)b * A.ldv,
+              A.sn + (int64_t)b * A.ldv);
+}
+
+// the Givens step on H column j at Hcol (global, or staged in shared memory by
+// the caller, which writes it back); previous rotations read from csp / snp
+__device__ void givens_core(const KArgs& A, int b, int j, double ssum, cplx* Hcol, const double* csp,
+                            const cplx* snp) {
   const double hn = sqrt(ssum);
   double* vsw = A.vscale + (int64_t)b * A.ldv;
   double* cs = A.cs + (int64_t)b * A.ldv;
@@ -288,8 +323,8 @@ __device__ void givens_tail(const KArgs& A, int b, int j, double ssum) {
   vsw[j + 1] = hn > 0 ? 1.0 / hn : 0.0;
   for (int i = 0; i < j; ++i) {       // previous rotations on column j
     const cplx hi0 = Hcol[i], hi1 = Hcol[i + 1];
-    const double c = cs[i];
-    const cplx s = sn[i];
+    const double c = csp[i];
+    const cplx s = snp[i];
     cplx a = cscale(hi0, c);
     cfma(a, s, hi1);
     cplx bb = cscale(hi1, c);
