@@ -477,10 +477,10 @@ int krylov_blocks(int64_t N) {
   return (int)std::max<int64_t>(1, std::max<int64_t>(a, (N + 2047) / 2048));
 }
 
-size_t ksmall_bytes(int B, int m) {
-  const size_t ldv = m + 1, ldh = m + 1;
+size_t ksmall_bytes(int B, int m, int nblk) {
+  const size_t ldv = m + 1, ldh = m + 1, ldg = (nblk + 31) / 32;
   auto r = [](size_t b) { return (b + 255) / 256 * 256; };
-  return r(B * ldv * 8) * 2 + r(B * ldv * 16) * 3 + r((size_t)B * m * ldh * 16) + r(B * 8) * 3 +
+  return r(B * ldg * 4) + r(B * ldv * 8) * 2 + r(B * ldv * 16) * 3 + r((size_t)B * m * ldh * 16) + r(B * 8) * 3 +
          r(B * 4) * 3 + r(16) + r(B * 4) * 2 + r(B * (ldv + 1) * 16) + r(B * 8) + r(B * 8) + r(B * 4) * 2 +
          r(16);
 }
@@ -526,7 +526,7 @@ hh_status reserve_pools(Engine& E, const BatchSpec& sp) {
   HH_TRY(E.cpart.ensure((size_t)B * nblk * (m + 2) * 16));
   HH_TRY(E.dpart.ensure((size_t)B * nblk * 8));
   HH_TRY(E.hist.ensure((size_t)B * HIST_LEN * 8));
-  HH_TRY(E.ksmall.ensure(ksmall_bytes(B, m)));
+  HH_TRY(E.ksmall.ensure(ksmall_bytes(B, m, nblk)));
   if (E.h_cap < B) {
     if (E.h_status) cudaFreeHost(E.h_status);
     E.h_status = nullptr;
@@ -701,6 +701,8 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   // (ksmall_bytes() below must mirror this layout)
+  const int ldg = (E.nblk + 31) / 32;   // k_mdot group counters (MD_GROUP = 32)
+  const size_t o_gc = carve((size_t)B * ldg * 4);
   const size_t o_vs = carve(B * ldv * 8), o_cs = carve(B * ldv * 8), o_sn = carve(B * ldv * 16),
                o_g = carve(B * ldv * 16), o_y = carve(B * ldv * 16), o_H = carve((size_t)B * m * ldh * 16),
                o_bn = carve(B * 8), o_res = carve(B * 8), o_rt = carve(B * 8), o_st = carve(B * 4),
@@ -727,6 +729,7 @@ hh_status batch_setup(Engine& E, const BatchSpec& sp) {
   A.cpart = E.cpart.as<cplx>(); A.ldp = m + 2;
   A.dpart = E.dpart.as<double>();
   A.counter = (unsigned*)(base + o_cnt);
+  A.gcounter = (unsigned*)(base + o_gc); A.ldg = ldg;
   E.jdev = (int*)(base + o_j);
   A.jdev = E.jdev;
   A.nblk = E.nblk;

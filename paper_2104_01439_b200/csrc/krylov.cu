@@ -57,6 +57,37 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return amLast;
 }
 
+// last_block for a counter shared by `total` CTAs
+__device__ __forceinline__ bool last_of(unsigned* counter, int total) {
+  __shared__ bool amLast;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) amLast = (atomicAdd(counter, 1u) == (unsigned)total - 1);
+  __syncthreads();
+  if (amLast) __threadfence();
+  return amLast;
+}
+
+// sum_r P[r * ld + q] for q = threadIdx.x < cnt (<= KT / 2), rows split over the
+// two thread halves (even / odd r), fixed order; sh: KT / 2 cplx of scratch
+__device__ __noinline__ cplx colsum(const cplx* P, int64_t ld, int rows, int cnt, cplx* sh) {
+  const int q = threadIdx.x % (KT / 2), half = threadIdx.x / (KT / 2);
+  cplx s0 = cmake(0, 0), s1 = cmake(0, 0);
+  if (q < cnt) {
+    int r = half;
+    for (; r + 2 < rows; r += 4) {
+      s0 = cadd(s0, P[(int64_t)r * ld + q]);
+      s1 = cadd(s1, P[(int64_t)(r + 2) * ld + q]);
+    }
+    if (r < rows) s0 = cadd(s0, P[(int64_t)r * ld + q]);
+  }
+  const cplx s = cadd(s0, s1);
+  __syncthreads();
+  if (half == 1) sh[q] = s;
+  __syncthreads();
+  return half == 0 ? cadd(s, sh[q]) : cmake(0, 0);   // valid in threads q < cnt
+}
+
 __device__ __forceinline__ void owned_view(const KArgs& A, int b, int64_t& off, int64_t& len) {
   const int2 sl = slab_of(A.slab, b, A.n);
   off = (int64_t)A.G * A.plane;
@@ -69,6 +100,7 @@ __device__ __forceinline__ void owned_view(const KArgs& A, int b, int64_t& off, 
 // flight (no serial tail loop); unit partials are combined in shared memory in
 // a fixed order (deterministic).
 constexpr int MD_UNITS = 1024;   // max units per CTA (nv <= 128, sub-chunks <= 8)
+constexpr int MD_GROUP = 32;     // CTAs per first-level group of the column sums
 // pass 2 (reorth): w = V[j+1] (the first pass's w'), result h2 -> y (folded into
 // H column j by the second update's tail); reorth = 1: ||w||^2 rides along as
 // the extra column nv of the partials (DGKS criterion).
@@ -144,33 +176,35 @@ __global__ void __launch_bounds__(KT, 4) k_mdot(KArgs A, int pass) {
     part[q] = acc;
   }
   if (wn && threadIdx.x == 0) part[nv] = cmake(wsum, 0);
-  if (last_block(A.counter + b)) {
-    // column sums over the CTAs: one warp per entry, lanes stride the CTAs, fixed-order shuffle
-    cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
-    const cplx* P0 = A.cpart + (int64_t)b * gridDim.x * A.ldp;
-    cplx* y = A.y + (int64_t)b * A.ldv;
-    for (int q = warp; q < nv + (wn ? 1 : 0); q += KT / 32) {
-      cplx s0 = cmake(0, 0), s1 = cmake(0, 0);
-      int k = lane;
-      for (; k + 32 < (int)gridDim.x; k += 64) {
-        s0 = cadd(s0, P0[(int64_t)k * A.ldp + q]);
-        s1 = cadd(s1, P0[(int64_t)(k + 32) * A.ldp + q]);
-      }
-      if (k < (int)gridDim.x) s0 = cadd(s0, P0[(int64_t)k * A.ldp + q]);
-      cplx s = cadd(s0, s1);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-      }
-      if (lane == 0) {
-        if (A.slabred) A.red[(int64_t)b * A.ldr + q] = s;
-        else if (q == nv) A.wnorm2[b] = s.x;
-        else if (pass == 2) y[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
-        else Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
-      }
-    }
+  // Column sums over the CTAs in two deterministic levels: the last CTA of each
+  // group of MD_GROUP CTAs folds the group's partial rows into the group's first
+  // row, the last group finisher folds the group rows.  Each finisher reads
+  // <= MD_GROUP (resp. ngroups) rows with coalesced, independent loads, so the
+  // serial tail of a launch is two short reductions instead of one CTA reading
+  // all nblk rows.
+  const int cnt = nv + (wn ? 1 : 0);
+  const int grp = blockIdx.x / MD_GROUP, ngrp = (gridDim.x + MD_GROUP - 1) / MD_GROUP;
+  const int r0 = grp * MD_GROUP, nr = min((int)gridDim.x, r0 + MD_GROUP) - r0;
+  cplx* P0 = A.cpart + (int64_t)b * gridDim.x * A.ldp;
+  if (!last_of(A.gcounter + (int64_t)b * A.ldg + grp, nr)) return;
+  cplx s = colsum(P0 + (int64_t)r0 * A.ldp, A.ldp, nr, cnt, usum);
+  if (ngrp > 1) {
+    if (threadIdx.x < cnt) P0[(int64_t)r0 * A.ldp + threadIdx.x] = s;
+    if (threadIdx.x == 0) A.gcounter[(int64_t)b * A.ldg + grp] = 0u;
+    if (!last_of(A.counter + b, ngrp)) return;
+    s = colsum(P0, (int64_t)MD_GROUP * A.ldp, ngrp, cnt, usum);
     if (threadIdx.x == 0) A.counter[b] = 0u;
+  } else if (threadIdx.x == 0) {
+    A.gcounter[(int64_t)b * A.ldg + grp] = 0u;
+  }
+  const int q = threadIdx.x;
+  if (q < cnt) {
+    cplx* Hcol = A.H + (int64_t)b * A.HB + (int64_t)j * A.ldh;
+    cplx* y = A.y + (int64_t)b * A.ldv;
+    if (A.slabred) A.red[(int64_t)b * A.ldr + q] = s;
+    else if (q == nv) A.wnorm2[b] = s.x;
+    else if (pass == 2) y[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
+    else Hcol[q] = cscale(s, A.vscale[(int64_t)b * A.ldv + q]);
   }
 }
 

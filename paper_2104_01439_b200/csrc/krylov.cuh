@@ -37,6 +37,7 @@ struct KArgs {
   cplx* cpart = nullptr; int ldp = 0;   // [B][nblk][ldp]
   double* dpart = nullptr;              // [B][nblk]
   unsigned* counter = nullptr;          // [B]
+  unsigned* gcounter = nullptr; int ldg = 0;   // [B][ldg] k_mdot group counters (ldg >= ceil(nblk / 32))
   const int* jdev = nullptr;
   int nblk = 1;
   double rtol = 1e-6;
