@@ -198,6 +198,67 @@ __device__ __forceinline__ cplx node_diag(const Tile& t, int gx, int gy, int n, 
     }                                                                          \
   }
 
+#ifndef FINE_PAIR
+#define FINE_PAIR 1   // constant k: a thread takes two vertically adjacent nodes (12 shared-memory loads, not 18)
+#endif
+// The region of halo `hal` in vertical node pairs (rows sy, sy + 1; the region
+// height TY + 2 hal is even); the body sees sx, sy, gx, gy, si of the lower node
+// and in0 / in1 (lower / upper node inside the domain).
+#define FOR_REGION2(hal, ...)                                                  \
+  {                                                                            \
+    const int _w = TX + 2 * (hal), _h = (TY + 2 * (hal)) / 2;                  \
+    const int _q = NT / _w, _r = NT - _q * _w;                                 \
+    int _x = threadIdx.x % _w, _y = threadIdx.x / _w;                          \
+    for (; _y < _h;) {                                                         \
+      const int sx = t.R - (hal) + _x, sy = t.R - (hal) + 2 * _y;              \
+      const int gx = t.gx(sx), gy = t.gy(sy);                                  \
+      const bool inx = gx >= 0 && gx <= n;                                     \
+      const bool in0 = inx && gy >= rlo && gy <= rhi;                          \
+      const bool in1 = inx && gy + 1 >= rlo && gy + 1 <= rhi;                  \
+      const int si = sy * t.SX + sx;                                           \
+      { __VA_ARGS__ }                                                          \
+      _x += _r; _y += _q;                                                      \
+      if (_x >= _w) { _x -= _w; ++_y; }                                        \
+    }                                                                          \
+  }
+
+// Constant k: rows of A x at the vertical pair (si, si + SX).  Both interior:
+// the 12 values of rows sy - 1 .. sy + 2 are read once and the sums are formed
+// in node_op's order (bit-identical results); otherwise node_op per node.
+template <bool EPS>
+__device__ __forceinline__ void node_op_pair(const cplx* __restrict__ X, int si, const Tile& t, int gx, int gy,
+                                             int n, double h, const double2* sE, double2 kc, const Const9& c9,
+                                             bool in0, bool in1, cplx& a0, cplx& a1) {
+  if (in0 && in1 && gx > 0 && gx < n && gy > 0 && gy + 1 < n) {
+    const int SX = t.SX;
+    const cplx* r0 = X + si - SX;
+    const cplx W0 = r0[-1], C0 = r0[0], E0 = r0[1];
+    const cplx W1 = X[si - 1], C1 = X[si], E1 = X[si + 1];
+    const cplx* r2 = X + si + SX;
+    const cplx W2 = r2[-1], C2 = r2[0], E2 = r2[1];
+    const cplx* r3 = r2 + SX;
+    const cplx W3 = r3[-1], C3 = r3[0], E3 = r3[1];
+    const cplx h1 = cmake(W1.x + E1.x, W1.y + E1.y);
+    {
+      const cplx e4 = cmake(h1.x + C0.x + C2.x, h1.y + C0.y + C2.y);
+      const cplx c4 = cmake(W0.x + E0.x + W2.x + E2.x, W0.y + E0.y + W2.y + E2.y);
+      a0 = cmul(c9.c0, C1);
+      cfma(a0, c9.c1, e4);
+      cfma(a0, c9.c2, c4);
+    }
+    {
+      const cplx e4 = cmake(W2.x + E2.x + C1.x + C3.x, W2.y + E2.y + C1.y + C3.y);
+      const cplx c4 = cmake(h1.x + W3.x + E3.x, h1.y + W3.y + E3.y);
+      a1 = cmul(c9.c0, C2);
+      cfma(a1, c9.c1, e4);
+      cfma(a1, c9.c2, c4);
+    }
+    return;
+  }
+  if (in0) a0 = node_op<false, EPS>(X, si, t, gx, gy, n, h, sE, kc, c9);
+  if (in1) a1 = node_op<false, EPS>(X, si + t.SX, t, gx, gy + 1, n, h, sE, kc, c9);
+}
+
 #ifndef FINE_ASYNC
 #define FINE_ASYNC 1   // 1: stage the smoothers' inputs with cp.async (all in flight at once, no registers)
 #endif
@@ -402,24 +463,42 @@ __global__ void __launch_bounds__(NT, HET && !FINE_DI_GLOBAL ? 3 : FINE_CONST_MI
   cplx* nxt = sB;
   for (int step = 2; step <= nu; ++step) {
     const int hal = t.R - step + 1;
-    FOR_REGION(hal, if (in) {
-      const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
+    auto jac = [&](int si, int gx, int gy, cplx ax) {
       const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
       cfma(v, cscale(di, omega), csub(cscale(sF[si], fsa), ax));
       nxt[si] = v;
-    })
+    };
+    if constexpr (!HET && FINE_PAIR) {
+      FOR_REGION2(hal, if (in0 || in1) {
+        cplx a0, a1;
+        node_op_pair<true>(cur, si, t, gx, gy, n, h, sE, kc, c9, in0, in1, a0, a1);
+        if (in0) jac(si, gx, gy, a0);
+        if (in1) jac(si + t.SX, gx, gy + 1, a1);
+      })
+    } else {
+      FOR_REGION(hal, if (in) jac(si, gx, gy, node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9));)
+    }
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
   // residual on halo 1 -> nxt ; u on the tile (owned rows) -> global
   cplx* ub = uo.at(b) - vofs;
-  FOR_REGION(1, if (in) {
-    const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9);
+  auto res = [&](int si, int sx, int sy, int gx, int gy, cplx ax) {
     nxt[si] = csub(cscale(sF[si], fsa), ax);
     if (sx >= t.R && sx < t.R + TX && sy >= t.R && sy < t.R + TY && gy < sl.y)
       ub[(int64_t)gy * (n + 1) + gx] = cur[si];
-  })
+  };
+  if constexpr (!HET && FINE_PAIR) {
+    FOR_REGION2(1, if (in0 || in1) {
+      cplx a0, a1;
+      node_op_pair<true>(cur, si, t, gx, gy, n, h, sE, kc, c9, in0, in1, a0, a1);
+      if (in0) res(si, sx, sy, gx, gy, a0);
+      if (in1) res(si + t.SX, sx, sy + 1, gx, gy + 1, a1);
+    })
+  } else {
+    FOR_REGION(1, if (in) res(si, sx, sy, gx, gy, node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9));)
+  }
   __syncthreads();
   // restriction I^T at coarse nodes (2I, 2J) inside the tile
   const int nc = n / 2;
@@ -550,24 +629,52 @@ __global__ void __launch_bounds__(NT, HET ? 3 : FINE_CONST_MINB) k_post2d(FineK 
   cplx* nxt = sB;
   for (int step = 1; step <= nu; ++step) {
     const int hal = t.R - step;
-    FOR_REGION(hal, if (in) {
-      const cplx ax = node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e);
+    auto jac = [&](int si, int gx, int gy, cplx ax) {
       const cplx di = dinv_at<HET>(sDi, dg, si, t, gx, gy, n, h, sE, kc, di_int);
       cplx v = cur[si];
       cfma(v, cscale(di, omega), csub(cscale(sF[si], fsa), ax));
       nxt[si] = v;
-    })
+    };
+    if constexpr (!HET && FINE_PAIR) {
+      FOR_REGION2(hal, if (in0 || in1) {
+        cplx a0, a1;
+        node_op_pair<true>(cur, si, t, gx, gy, n, h, sE, kc, c9e, in0, in1, a0, a1);
+        if (in0) jac(si, gx, gy, a0);
+        if (in1) jac(si + t.SX, gx, gy + 1, a1);
+      })
+    } else {
+      FOR_REGION(hal, if (in) jac(si, gx, gy, node_op<HET, true>(cur, si, t, gx, gy, n, h, sE, kc, c9e));)
+    }
     __syncthreads();
     cplx* tmp = cur; cur = nxt; nxt = tmp;
   }
   cplx* zb = zo.at(b) - vofs;
   cplx* wb = WITH_W ? wo.at(b) - vofs : nullptr;
   const Const9 c90 = make_const9(kc, h, false);
-  FOR_REGION(0, if (in && gy < sl.y) {
-    const int64_t gi = (int64_t)gy * (n + 1) + gx;
-    zb[gi] = cur[si];
-    if (WITH_W) wb[gi] = node_op<HET, false>(cur, si, t, gx, gy, n, h, sE, kc, c90);
-  })
+  if constexpr (!HET && FINE_PAIR) {
+    FOR_REGION2(0, {
+      const bool o0 = in0 && gy < sl.y, o1 = in1 && gy + 1 < sl.y;
+      if (o0 || o1) {
+        cplx a0, a1;
+        if (WITH_W) node_op_pair<false>(cur, si, t, gx, gy, n, h, sE, kc, c90, o0, o1, a0, a1);
+        const int64_t gi = (int64_t)gy * (n + 1) + gx;
+        if (o0) {
+          zb[gi] = cur[si];
+          if (WITH_W) wb[gi] = a0;
+        }
+        if (o1) {
+          zb[gi + n + 1] = cur[si + t.SX];
+          if (WITH_W) wb[gi + n + 1] = a1;
+        }
+      }
+    })
+  } else {
+    FOR_REGION(0, if (in && gy < sl.y) {
+      const int64_t gi = (int64_t)gy * (n + 1) + gx;
+      zb[gi] = cur[si];
+      if (WITH_W) wb[gi] = node_op<HET, false>(cur, si, t, gx, gy, n, h, sE, kc, c90);
+    })
+  }
 }
 
 // ------------------------------------------------------------ precomputed D^{-1}
