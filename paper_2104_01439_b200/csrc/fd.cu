@@ -482,6 +482,14 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
     for (int cb = 0; cb < T::CB; ++cb)
       re[rb][cb][0] = re[rb][cb][1] = im[rb][cb][0] = im[rb][cb][1] = t3[rb][cb][0] = t3[rb][cb][1] = 0.0;
   const int nk = (g.K + FD_BK - 1) / FD_BK;
+  // 8-row / 8-column fragment blocks wholly beyond M / N (tile padding) and
+  // k-steps wholly beyond K (the last chunk) are skipped: warp-uniform, and the
+  // skipped products are exact zeros or never stored, so results are unchanged
+  bool rbv[T::RB], cbv[T::CB];
+#pragma unroll
+  for (int rb = 0; rb < T::RB; ++rb) rbv[rb] = i0 + wr * T::WM + rb * 8 < g.M;
+#pragma unroll
+  for (int cb = 0; cb < T::CB; ++cb) cbv[cb] = j0 + wc * T::WN + cb * 8 < g.N;
   load_stage(0, 0);
   for (int kt = 0; kt < nk; ++kt) {
     if (kt + 1 < nk) {
@@ -493,8 +501,10 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
     __syncthreads();
     const cplx* As = sm + (kt & 1) * T::stage;
     const cplx* Bs = As + BM * T::SA;
+    const int kv = g.K - kt * FD_BK;   // valid k of this chunk (>= FD_BK except the last)
 #pragma unroll
     for (int ks = 0; ks < FD_BK / 4; ++ks) {
+      if (ks * 4 >= kv) break;
       const int k = ks * 4 + q;
       cplx av[T::RB], bv[T::CB];
 #pragma unroll
@@ -505,6 +515,7 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
       for (int rb = 0; rb < T::RB; ++rb)
 #pragma unroll
         for (int cb = 0; cb < T::CB; ++cb) {
+          if (!rbv[rb] || !cbv[cb]) continue;
           if (FD_3M) {
             dmma884(re[rb][cb][0], re[rb][cb][1], av[rb].x, bv[cb].x);                       // t1
             dmma884(im[rb][cb][0], im[rb][cb][1], av[rb].y, bv[cb].y);                       // t2
