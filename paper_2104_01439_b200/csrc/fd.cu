@@ -430,14 +430,21 @@ constexpr int FD_BK = FD_BKC;   // K-chunk per pipeline stage
 #ifndef FD_MINB48
 #define FD_MINB48 2   // 48 x 48 tiles: 2 CTAs per SM (120 registers; 3 CTAs -> 96 registers + spills)
 #endif
+#ifndef FD_ST48
+#define FD_ST48 2   // cp.async stages of the 48 x 48 tiles (3 = one barrier per K-chunk, two chunks in flight: measured slower, P = 134 coarse 111.8 -> 119.5 us)
+#endif
+#ifndef FD_ST32
+#define FD_ST32 2   // other tiles (3 stages of 16-k chunks would cost a resident CTA; FD_BKC=12 keeps 5: A/B below)
+#endif
 template <int BM, int BN, int WR, int WC>
 struct FDTile {
   static constexpr int NT = 32 * WR * WC;
-  static constexpr int SA = FD_BK + 4;   // cplx row stride of the A stage (conflict-free fragment loads)
+  static constexpr int ST = BM == 48 ? FD_ST48 : FD_ST32;
+  static constexpr int SA = (FD_BK % 8 == 4) ? FD_BK : FD_BK + 4;   // cplx row stride of the A stage: = 4 mod 8 (conflict-free fragment loads)
   static constexpr int SB = BN + 2;
   static constexpr int WM = BM / WR, WN = BN / WC, RB = WM / 8, CB = WN / 8;
   static constexpr size_t stage = (size_t)(BM * SA + FD_BK * SB);
-  static constexpr size_t smem = 2 * stage * sizeof(cplx);
+  static constexpr size_t smem = ST * stage * sizeof(cplx);
 };
 
 template <int BM, int BN, int WR, int WC>
@@ -491,15 +498,24 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
 #pragma unroll
   for (int cb = 0; cb < T::CB; ++cb) cbv[cb] = j0 + wc * T::WN + cb * 8 < g.N;
   load_stage(0, 0);
+  if (T::ST >= 3 && nk > 1) load_stage(1, FD_BK);
   for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_stage((kt + 1) & 1, (kt + 1) * FD_BK);
-      cp_wait<1>();
+    if (T::ST >= 3) {
+      // three stages: chunk kt + 2 goes to the buffer chunk kt - 1 was read from,
+      // free once every thread has passed this iteration's barrier
+      if (kt + 1 < nk) cp_wait<1>(); else cp_wait<0>();
+      __syncthreads();
+      if (kt + 2 < nk) load_stage((kt + 2) % 3, (kt + 2) * FD_BK);
     } else {
-      cp_wait<0>();
+      if (kt + 1 < nk) {
+        load_stage((kt + 1) & 1, (kt + 1) * FD_BK);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    const cplx* As = sm + (kt & 1) * T::stage;
+    const cplx* As = sm + (T::ST >= 3 ? kt % 3 : (kt & 1)) * T::stage;
     const cplx* Bs = As + BM * T::SA;
     const int kv = g.K - kt * FD_BK;   // valid k of this chunk (>= FD_BK except the last)
 #pragma unroll
@@ -528,7 +544,7 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
           }
         }
     }
-    __syncthreads();
+    if (T::ST < 3) __syncthreads();
   }
   cplx* C = g.C + ((int64_t)b * g.nblk + blk) * g.sblk + (int64_t)sl * g.ssl;
   const cplx* lamb = g.basis + (int64_t)__ldg(&g.bidx[b]) * g.BE;
