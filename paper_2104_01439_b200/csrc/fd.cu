@@ -599,19 +599,24 @@ hh_status fd_gemm_launch(const FDGemm& g, int B, cudaStream_t s) {
 // 84.8 -> 78.9 us) and the sweep's P = 34 (56.8 -> 49.2 us); at P = 101 / 118 they lost
 // to 32 x 32 (112.9 -> 118.4, 107.9 -> 111.9 us; profiles/r02/fd/tile40).
 // HH_FD_TILE = 32 / 40 / 48 / 64 forces one (A/B).
-hh_status fd_gemm(const FDGemm& g, int B, cudaStream_t s) {
+// the tile fd_gemm launches for an M x N output (HH_FD_TILE forces one)
+static int fd_tile_for(int M, int N) {
   static const int force = getenv("HH_FD_TILE") ? atoi(getenv("HH_FD_TILE")) : 0;
   static const bool use40 = !getenv("HH_FD_TILE40") || atoi(getenv("HH_FD_TILE40")) != 0;
-  (void)B;
+  if (force) return force;
   const int tiles[3] = {32, 40, 48};
   int best = 0;
   int64_t ba = INT64_MAX;
   for (int t = 0; t < 3; ++t) {
-    if (tiles[t] == 40 && (!use40 || std::min(g.M, g.N) > 40)) continue;   // 40: only where a dimension <= 40
-    const int64_t a = (int64_t)((g.M + tiles[t] - 1) / tiles[t]) * tiles[t] * (((g.N + tiles[t] - 1) / tiles[t]) * tiles[t]);
+    if (tiles[t] == 40 && (!use40 || std::min(M, N) > 40)) continue;   // 40: only where a dimension <= 40
+    const int64_t a = (int64_t)((M + tiles[t] - 1) / tiles[t]) * tiles[t] * (((N + tiles[t] - 1) / tiles[t]) * tiles[t]);
     if (a < ba) { ba = a; best = t; }
   }
-  const int tile = force ? force : tiles[best];
+  return tiles[best];
+}
+hh_status fd_gemm(const FDGemm& g, int B, cudaStream_t s) {
+  (void)B;
+  const int tile = fd_tile_for(g.M, g.N);
   if (tile == 64) return fd_gemm_launch<64, 64, 4, 2>(g, B, s);
   if (tile == 48) return fd_gemm_launch<48, 48, 3, 2>(g, B, s);
   if (tile == 40) return fd_gemm_launch<40, 40, 5, 1>(g, B, s);
@@ -621,6 +626,12 @@ hh_status fd_gemm(const FDGemm& g, int B, cudaStream_t s) {
 }  // namespace
 
 int fd_P(int nc) { return nc / 2 + 1; }
+// 2D: CTAs one sample adds to each k_fd_gemm launch, and the CTAs of that tile one SM holds
+void fd_gemm_ctas2d(int nc, int* per_sample, int* per_sm) {
+  const int P = fd_P(nc), t = fd_tile_for(P, P), tl = (P + t - 1) / t;
+  *per_sample = 4 * tl * tl;
+  *per_sm = t == 32 ? 5 : (t == 48 ? FD_MINB48 : (t == 40 ? 4 : 2));
+}
 int64_t fd_basis_entries(int nc) {
   const int64_t P = fd_P(nc);
   return 4 * P * P + 4 * P;

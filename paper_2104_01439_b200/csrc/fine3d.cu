@@ -847,15 +847,41 @@ static hh_status march3(const Level& L, const F3& P, int B, VArg x, VArg f, SArg
   const int ni = P.n - 1;   // interior nodes per side
   const int tx = (ni + MTX - 1) / MTX, ty = (ni + MTY - 1) / MTY;
   const int span = std::min(P.N1, P.maxloc + 2 * P.ext);
-  const int want = std::max(1, (4 * 148 + tx * ty * B - 1) / (tx * ty * B));
-  const int nzc = std::max(1, std::min(span, want));
-  const int zlen = (span + nzc - 1) / nzc;
-  const size_t sm = sizeof(MarchSmem);
-  const dim3 g(tx, ty, nzc * B);
   // register budget: 3 CTAs per SM (80 registers) or 2 (128); HH_3D_MINB selects,
   // default = the measured faster one
   static const int minb_env = getenv("HH_3D_MINB") ? atoi(getenv("HH_3D_MINB")) : 0;
   const int minb = minb_env ? minb_env : (L.het ? 2 : 3);   // spill-free budgets
+  // z-chunks per column of tiles: the count whose launch takes the fewest plane
+  // steps, rounds of resident CTAs (sms * minb slots) x (planes per chunk + the
+  // 3 planes a chunk stages before its first output), instead of ">= 4 CTAs per
+  // SM" (cfg3: 5 chunks = 640 CTAs = 1.44 rounds of 444 slots -> 3 chunks = 384
+  // CTAs in one round).  HH_3D_NZC forces a count, HH_3D_NZC_OLD=1 the old rule.
+  static const int nzc_env = getenv("HH_3D_NZC") ? atoi(getenv("HH_3D_NZC")) : 0;
+  static const bool nzc_old = getenv("HH_3D_NZC_OLD") && atoi(getenv("HH_3D_NZC_OLD")) != 0;
+  static const int sms = [] {
+    int d = 0, n = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0) n = 148;
+    return n;
+  }();
+  int nzc;
+  if (nzc_env > 0) {
+    nzc = std::min(span, nzc_env);
+  } else if (nzc_old) {
+    const int want = std::max(1, (4 * 148 + tx * ty * B - 1) / (tx * ty * B));
+    nzc = std::max(1, std::min(span, want));
+  } else {
+    const int64_t tiles = (int64_t)tx * ty * B, slots = (int64_t)sms * minb;
+    int64_t best = INT64_MAX;
+    nzc = 1;
+    for (int c = 1; c <= std::min(span, 32); ++c) {
+      const int64_t rounds = (tiles * c + slots - 1) / slots;
+      const int64_t cost = rounds * ((span + c - 1) / c + 3);
+      if (cost < best) { best = cost; nzc = c; }
+    }
+  }
+  const int zlen = (span + nzc - 1) / nzc;
+  const size_t sm = sizeof(MarchSmem);
+  const dim3 g(tx, ty, nzc * B);
   const int e = eps ? 1 : 0;
   if (L.het && minb == 2) {
     HH_CUDA_TRY(smem_attr((const void*)k_march3d<true, MODE, 2>, sm));

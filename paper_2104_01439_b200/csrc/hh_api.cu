@@ -1616,7 +1616,21 @@ static hh_status sweep_run(const hh_problem_desc* common, const hh_fgmres_opts* 
     const int64_t per = per_sample_bytes(2, kv.first, m, plan);
     const double Nn = (double)(kv.first + 1) * (kv.first + 1);
     const int bmem = (int)std::max<int64_t>(1, std::min<int64_t>(maxB, (int64_t)(budget / per)));
-    const int bmax = std::max(1, std::min(bmem, (int)(node_budget / Nn)));
+    int bmax = std::max(1, std::min(bmem, (int)(node_budget / Nn)));
+    // HH_SWEEP_FD_WAVE=1 (A/B): size FD batches to whole waves of the GEMM tiles -- a batch
+    // whose CTAs overshoot W full waves by less than 0.8 of a wave shrinks to W waves
+    static const bool fd_wave = getenv("HH_SWEEP_FD_WAVE") && atoi(getenv("HH_SWEEP_FD_WAVE")) != 0;
+    if (fd && fd_wave) {
+      int per_sample = 1, per_sm = 1, sms = 148;
+      fd_gemm_ctas2d(kv.first / 2, &per_sample, &per_sm);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, common->device);
+      const double slots = (double)sms * per_sm;
+      const int cnt0 = (int)gi.size(), nb0 = (cnt0 + bmax - 1) / bmax;
+      const int bact = (cnt0 + nb0 - 1) / nb0;   // the batches' actual size (the group is split evenly)
+      const double waves = bact * (double)per_sample / slots;
+      const int W = (int)waves;
+      if (W >= 1 && waves - W > 0.02 && waves - W < 0.8) bmax = std::max(1, (int)(W * slots / per_sample));
+    }
     const int cnt = (int)gi.size();
     const int nb = (cnt + bmax - 1) / bmax;
     for (int k = 0; k < nb; ++k) {

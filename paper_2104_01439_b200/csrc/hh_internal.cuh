@@ -167,6 +167,7 @@ hh_status nd_solve(const NDPlan* p, int B, const int* st, const cplx* F, cplx* w
 // fd_setup: flag[b] = 1 if the secular roots fail validation, 2 if the operator is
 // singular (both leave flag 0 untouched otherwise; the caller zeroes it).
 int fd_P(int nc);
+void fd_gemm_ctas2d(int nc, int* per_sample, int* per_sm);
 int64_t fd_basis_entries(int nc);
 int64_t fd_work_entries(int dim, int nc);
 int fd_solve_launches(int dim);
