@@ -274,6 +274,12 @@ __global__ void k_fd_check(int dim, int nc, const double2* __restrict__ kc, cons
 
 // ---------------------------------------------------------------- fold / unfold
 __device__ __forceinline__ cplx ldx(const cplx* p) { return __ldg(p); }
+// programmatic dependent launch inside the fold -> GEMM ... -> unfold chain (default on):
+// a kernel signals once its last input is read / its main loop is done, the next one
+// is launched while this one drains and blocks in fd_pdl_wait() until this one has
+// completed and flushed; both are no-ops for launches without the attribute
+__device__ __forceinline__ void fd_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void fd_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // 2D: rhs[y][x] (m x m) -> blocks [py*2+px][i][j] (P x P), i folded y, j folded x
 __global__ void k_fd_fold2(int nc, const int* __restrict__ st, VArg rhs, cplx* __restrict__ W) {
@@ -284,8 +290,10 @@ __global__ void k_fd_fold2(int nc, const int* __restrict__ st, VArg rhs, cplx* _
   if (idx >= P * P) return;
   const int i = idx / P, j = idx % P, i2 = nc - i, j2 = nc - j;
   const cplx* f = rhs.at(b);
+  fd_pdl_wait();
   const cplx a = ldx(&f[(int64_t)i * m + j]), bq = ldx(&f[(int64_t)i * m + j2]);
   const cplx c = ldx(&f[(int64_t)i2 * m + j]), d = ldx(&f[(int64_t)i2 * m + j2]);
+  fd_pdl_trigger();
   const bool xi = j < j2, yi = i < i2;   // false: centre line (no mirror)
   // fold along x
   const cplx sp0 = xi ? cadd(a, bq) : a, sm0 = xi ? csub(a, bq) : cmake(0, 0);   // row i
@@ -306,6 +314,7 @@ __global__ void k_fd_unfold2(int nc, const int* __restrict__ st, const cplx* __r
   const int i = idx / P, j = idx % P, i2 = nc - i, j2 = nc - j;
   const int64_t PP = (int64_t)P * P;
   const cplx* Wb = W + (int64_t)b * 4 * PP + idx;
+  fd_pdl_wait();
   const cplx z00 = Wb[0], z01 = Wb[PP], z10 = Wb[2 * PP], z11 = Wb[3 * PP];
   // unfold along y (P_y[i] +- Q_y[i]) then x
   const cplx r0p = cadd(z00, z10), r0m = cadd(z01, z11);   // row i : even-x part, odd-x part
@@ -497,6 +506,7 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
   for (int rb = 0; rb < T::RB; ++rb) rbv[rb] = i0 + wr * T::WM + rb * 8 < g.M;
 #pragma unroll
   for (int cb = 0; cb < T::CB; ++cb) cbv[cb] = j0 + wc * T::WN + cb * 8 < g.N;
+  fd_pdl_wait();
   load_stage(0, 0);
   if (T::ST >= 3 && nk > 1) load_stage(1, FD_BK);
   for (int kt = 0; kt < nk; ++kt) {
@@ -546,6 +556,7 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
     }
     if (T::ST < 3) __syncthreads();
   }
+  fd_pdl_trigger();
   cplx* C = g.C + ((int64_t)b * g.nblk + blk) * g.sblk + (int64_t)sl * g.ssl;
   const cplx* lamb = g.basis + (int64_t)__ldg(&g.bidx[b]) * g.BE;
   cplx shift = cmake(0, 0);
@@ -580,6 +591,27 @@ __global__ void __launch_bounds__(32 * WR * WC, BM == 32 ? 5 : (BM == 48 ? FD_MI
   }
 }
 
+// launch inside the FD chain: with programmatic stream serialisation (HH_FD_PDL=0 or
+// HH_NO_PDL=1: plain launches).  Measured (profiles/r02/fd_pdl): coarse phase per batch
+// iteration 28.1 -> 25.5 us (P = 9), 47.7 -> 46.8 (P = 34), 114.7 -> 111.3 (P = 101),
+// 112.5 -> 111.0 (P = 134); sweep 87-89 -> 84-85 us, 3.473-3.483 -> 3.483-3.490e9 it*DOF/s
+static const bool g_fd_pdl = !(getenv("HH_FD_PDL") && atoi(getenv("HH_FD_PDL")) == 0) && getenv("HH_NO_PDL") == nullptr;
+template <typename... Args>
+static hh_status fd_launch(void (*kern)(Args...), dim3 grid, int block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_fd_pdl ? 1 : 0;
+  HH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return HH_OK;
+}
+
 template <int BM, int BN, int WR, int WC>
 hh_status fd_gemm_launch(const FDGemm& g, int B, cudaStream_t s) {
   using T = FDTile<BM, BN, WR, WC>;
@@ -587,9 +619,7 @@ hh_status fd_gemm_launch(const FDGemm& g, int B, cudaStream_t s) {
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   const int64_t zc = (int64_t)B * g.nblk * g.nsl;
   if (zc > 65535) { hh_set_error("fd_solve: batch x blocks x slices = %lld > 65535", (long long)zc); return HH_E_CONFIG; }
-  k_fd_gemm<BM, BN, WR, WC><<<dim3(tiles, (unsigned)zc), T::NT, T::smem, s>>>(g);
-  HH_CUDA_TRY(cudaGetLastError());
-  return HH_OK;
+  return fd_launch(k_fd_gemm<BM, BN, WR, WC>, dim3(tiles, (unsigned)zc), T::NT, T::smem, s, g);
 }
 // tile choice: the least padded output area ceil(M/t) t x ceil(N/t) t over t = 32 / 40 / 48
 // (ties -> the smaller tile: more CTAs); measured per grid size on the sweep's batches
@@ -700,16 +730,14 @@ hh_status fd_solve(int dim, int nc, int B, const int* st, const cplx* basis, con
   auto bas = [&](int which, int axis) { FDOp o; o.p = nullptr; o.ld = P; o.basis = which; o.axis = axis; return o; };
   if (dim == 2) {
     const unsigned gx = (unsigned)((P * P + 255) / 256);
-    k_fd_fold2<<<dim3(gx, B), 256, 0, s>>>(nc, st, rhs, W0);
-    HH_CUDA_TRY(cudaGetLastError());
+    HH_TRY(fd_launch(k_fd_fold2, dim3(gx, B), 256, 0, s, nc, st, rhs, W0));
     g.M = g.N = g.K = P; g.ldc = P;
     // Y = V_y^T F V_x (/ D), X = V_y H V_x^T
     g.A = data(W0, P); g.B = bas(0, 0); g.C = W1; g.dmode = 0; HH_TRY(fd_gemm(g, B, s));
     g.A = bas(1, 1); g.B = data(W1, P); g.C = W0; g.dmode = 1; HH_TRY(fd_gemm(g, B, s));
     g.A = bas(0, 1); g.B = data(W0, P); g.C = W1; g.dmode = 0; HH_TRY(fd_gemm(g, B, s));
     g.A = data(W1, P); g.B = bas(1, 0); g.C = W0; HH_TRY(fd_gemm(g, B, s));
-    k_fd_unfold2<<<dim3(gx, B), 256, 0, s>>>(nc, st, W0, x);
-    HH_CUDA_TRY(cudaGetLastError());
+    HH_TRY(fd_launch(k_fd_unfold2, dim3(gx, B), 256, 0, s, nc, st, (const cplx*)W0, x));
     return HH_OK;
   }
   const unsigned gx = (unsigned)((PD + 255) / 256);
